@@ -1,0 +1,173 @@
+/*
+ * bilu.h -- C-ABI of the B200-native numeric phase of the Crout-type block ILU
+ * (BILU) of Bollhoefer, Schenk, Verbosio, "High Performance Block Incomplete LU
+ * Factorization", arXiv:1908.10169.
+ *
+ * What the library computes:
+ *   Given a sparse A, a symmetric permutation perm and a partition of the
+ *   permuted matrix Ã = A(perm, perm) into contiguous diagonal blocks, compute
+ *       Ã ≈ L · D^{-1} · U        ("Technically we compute A ≈ L D^{-1} U",
+ *                                    PAPER.md:772-773)
+ *   with L unit block-lower, U unit block-upper, D block diagonal holding the
+ *   explicit inverses of the pivot blocks, by the Crout
+ *   recurrence of Alg. 1 generalised to blocks: a row i of
+ *   block column K of L is dropped iff max_t |(l_iK l_KK^{-1})_t| <= tau, a column
+ *   j of block row K of U iff max_t |(u_KK^{-1} u_Kj)_t| <= tau (
+ *   max-abs norm: DESIGN.md reading R1).  Consecutive blocks are merged
+ *   ("progressive aggregation", Sec. 3.5) when
+ *   nu <= 1.2 mu or nu <= mu + 2(p+q), and p+q <= max_block.
+ *
+ * Storage of the factors (hybrid layout of Fig. 1),
+ * per final block K with rows/cols [s_K, e_K), b_K = e_K - s_K:
+ *   L : sorted kept row indices i >= e_K and one dense m_K x b_K panel, row-major
+ *   Ũ : sorted kept column indices j >= e_K and one dense b_K x c_K panel,
+ *       column-major, holding the UNSCALED rows Ũ = D^{-1} U (so U = D_K Ũ)
+ *   D : D_K = P_K^{-1}, b_K x b_K column-major (P_K = the pivot block)
+ *
+ * Ownership and errors:
+ *   - Every input pointer is BORROWED for the duration of the call only.
+ *   - The context owns all device memory (factors, arenas, workspaces).
+ *   - No function aborts or throws across the ABI; each returns a status.  On
+ *     failure bilu_last_error(ctx) (or bilu_last_error(NULL) for failures
+ *     before a context exists) holds a one-line reason.
+ *   - All entry points are synchronous with respect to the host unless noted.
+ */
+#ifndef BILU_H
+#define BILU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BILU_OK = 0,
+  BILU_ERR_ARG = 1,        /* NULL pointer, n < 1, unsorted/duplicate CSR,
+                              perm not a bijection, sum(block_sizes) != n,
+                              a block size < 1 or > max_block                   */
+  BILU_ERR_BREAKDOWN = 2,  /* exactly singular pivot block P_K (stats->breakdown_block) */
+  BILU_ERR_OOM = 3,        /* device allocation failed                          */
+  BILU_ERR_CUDA = 4,       /* CUDA runtime error                                */
+  BILU_ERR_NCCL = 5,       /* reserved for the multi-GPU path                   */
+  BILU_ERR_STATE = 6,      /* e.g. bilu_apply / bilu_export before bilu_factor  */
+  BILU_ERR_NOT_BUILT = 7   /* library compiled without a usable device          */
+} bilu_status;
+
+typedef struct bilu_ctx bilu_ctx;   /* opaque; owns all device state */
+
+typedef struct {
+  int32_t device;        /* CUDA device ordinal                                  */
+  int32_t max_block;     /* cap on merged block size, and on initial blocks (<=128; R9) */
+  int32_t aggregate;     /* 1 = progressive aggregation (Sec. 3.5), 0 = off      */
+  int32_t n_ctas;        /* persistent CTAs of the factor kernel (0 = auto)      */
+  double  near_rel;      /* decisions with |max/tau - 1| <= near_rel are logged  */
+  int64_t arena_hint;    /* initial factor arena, doubles (0 = auto); grows on overflow */
+  void   *stream;        /* cudaStream_t to run on (NULL = the legacy default stream) */
+  int32_t rank, world;   /* multi-GPU: this rank / ranks (world = 1 only, round 1) */
+  void   *nccl_comm;     /* ncclComm_t or NULL                                   */
+} bilu_options;
+
+/* Fills *opt with the defaults (device 0, max_block 128, aggregate 1, near_rel
+ * 1e-8, auto sizes, default stream, world 1). */
+void bilu_options_default(bilu_options *opt);
+
+typedef struct {
+  double  flops;          /* algorithmic flops of the executed structure */
+  double  bytes_min;      /* compulsory bytes: read Ã once, write L, Ũ, D + indices once */
+  double  t_factor_ms;    /* device time of the numeric phase (CUDA events)      */
+  double  t_merge_ms;     /* of which: progressive aggregation post-pass         */
+  int64_t nnz_L, nnz_U, nnz_D;   /* stored doubles of the final factors          */
+  int32_t n_blocks_init, n_blocks_final, n_merges;
+  int32_t breakdown_block;       /* original block id of a singular pivot, or -1 */
+  int32_t n_retries;             /* workspace regrow-and-retry rounds             */
+  int32_t n_kernel_launches;     /* kernels launched by the last bilu_factor      */
+  int64_t n_decisions;           /* drop/keep decisions taken                     */
+  int64_t n_near;                /* of which |max/tau - 1| <= near_rel            */
+  double  min_margin;            /* min |max/tau - 1| over all decisions (tau>0)  */
+} bilu_factor_stats;
+
+/*
+ * bilu_analyze -- symbolic phase (host preprocessing + device upload).
+ *   n            order of A (>= 1)
+ *   row_ptr      HOST, int64[n+1], CSR row offsets of A (0-based, row_ptr[0]=0)
+ *   col_idx      HOST, int32[nnz], strictly increasing within each row
+ *   val          HOST, double[nnz], values of A (may be NULL: set later with
+ *                bilu_set_values before bilu_factor)
+ *   perm         HOST, int32[n] or NULL (identity): Ã(i,j) = A(perm[i], perm[j])
+ *                (the caller's fill-reducing ordering)
+ *   block_sizes  HOST, int32[n_blocks], initial partition of Ã, sum = n,
+ *                each in [1, max_block] (the caller's initial blocking,
+ *                PAPER.md:923-965, 1171-1242)
+ *   opt          options or NULL (defaults)
+ *   out          receives the context (set to NULL on failure)
+ * Builds Ã in CSR and CSC on the device, the block adjacency graph and the
+ * initial dependency counts of the dataflow schedule.
+ */
+bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                         const double *val, const int32_t *perm,
+                         const int32_t *block_sizes, int32_t n_blocks,
+                         const bilu_options *opt, bilu_ctx **out);
+
+/*
+ * bilu_set_values -- replace the values of A (same pattern as at analyze time).
+ *   val          double[nnz] in A's original CSR order; HOST memory if
+ *                on_device == 0, DEVICE memory (same device) if on_device != 0.
+ *                Host memory should be pinned for an asynchronous copy.
+ */
+bilu_status bilu_set_values(bilu_ctx *h, const double *val, int32_t on_device);
+
+/*
+ * bilu_factor -- numeric phase: Crout block ILU with tau-dropping and, if
+ * enabled, progressive aggregation (PAPER.md:158-175, 205-228, 767-799,
+ * 1405-1453).  May be called again (new tau or new values); each call rebuilds
+ * the factors from scratch.
+ *   tau   drop tolerance >= 0 (0 keeps every row/column that is not exactly 0)
+ *   st    optional statistics (may be NULL)
+ * Returns BILU_ERR_BREAKDOWN (st->breakdown_block set) if a pivot block is
+ * exactly singular; diagonal perturbation (Sec. 3.6) is not applied.
+ */
+bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *st);
+
+/*
+ * bilu_apply -- y = M^{-1} x with M = Pᵀ-permuted L D^{-1} U, i.e. solves
+ * A y ≈ x through the factors of Ã (forward substitution with L, multiply by
+ * the D blocks, backward substitution with U).
+ *   x, y   DEVICE double[n] in A's ORIGINAL ordering; may not alias.
+ *   stream cudaStream_t or NULL (context stream).  Asynchronous on that stream.
+ */
+bilu_status bilu_apply(bilu_ctx *h, const double *x, double *y, void *stream);
+
+/*
+ * Host copy of the final factors (paper convention except U, which is exported
+ * unscaled as Ũ; U = D_K Ũ).  All arrays are malloc'd by the library and owned
+ * by the view; release with bilu_factor_view_free.
+ */
+typedef struct {
+  int32_t n, n_blocks;
+  int32_t *bstart;          /* n_blocks+1 */
+  int64_t *Lp;  int32_t *Li;  int64_t *Lvp; double *Lv;   /* rows, m x b row-major */
+  int64_t *Up;  int32_t *Ui;  int64_t *Uvp; double *Uv;   /* cols, b x c col-major */
+  int64_t *Dp;  double *Dv;                               /* b x b col-major */
+  int64_t n_near;           /* near-threshold decisions logged (<= cap)      */
+  int32_t *near_blk, *near_side, *near_idx, *near_keep;   /* original block id, 0=L row 1=U col */
+  double *near_margin;
+} bilu_factor_view;
+
+bilu_status bilu_export(bilu_ctx *h, bilu_factor_view *v);
+void bilu_factor_view_free(bilu_factor_view *v);
+
+/* Destroys the context and frees all device memory.  NULL-safe. */
+void bilu_destroy(bilu_ctx *h);
+
+const char *bilu_status_string(bilu_status s);
+const char *bilu_last_error(const bilu_ctx *h);
+
+/* Number of kernels the library launched since the context was created
+ * (evidence counter for benchmarks). */
+int64_t bilu_kernel_launches(const bilu_ctx *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BILU_H */

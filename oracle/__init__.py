@@ -1,0 +1,235 @@
+"""CPU oracle for the BILU numeric phase -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` leg may import this package.  The product path
+(``paper_1908_10169_b200``) never imports it and shares no code with it.
+
+The arithmetic lives in ``bilu_oracle.c`` (plain C, fp64 scalar loops, no BLAS);
+this module only builds it with gcc and marshals arguments (ctypes).  Each C
+function cites the PAPER.md passage it follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "bilu_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (building the checker is not using it)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "bilu_oracle.h"))
+    ):
+        tmp = _LIB + ".tmp%d" % os.getpid()
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c99", "-D_POSIX_C_SOURCE=199309L", "-shared", "-fPIC",
+             "-o", tmp, _SRC, "-lm"]
+        )
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Factor(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int32), ("nblk", ctypes.c_int32),
+        ("bstart", ctypes.POINTER(ctypes.c_int32)),
+        ("Lp", ctypes.POINTER(ctypes.c_int64)), ("Li", ctypes.POINTER(ctypes.c_int32)),
+        ("Lvp", ctypes.POINTER(ctypes.c_int64)), ("Lv", ctypes.POINTER(ctypes.c_double)),
+        ("Up", ctypes.POINTER(ctypes.c_int64)), ("Ui", ctypes.POINTER(ctypes.c_int32)),
+        ("Uvp", ctypes.POINTER(ctypes.c_int64)), ("Uv", ctypes.POINTER(ctypes.c_double)),
+        ("Dp", ctypes.POINTER(ctypes.c_int64)), ("Dv", ctypes.POINTER(ctypes.c_double)),
+        ("flops", ctypes.c_double), ("t_factor_s", ctypes.c_double),
+        ("n_merges", ctypes.c_int32), ("breakdown_block", ctypes.c_int32),
+        ("n_decisions", ctypes.c_int64), ("n_near", ctypes.c_int64),
+        ("min_margin", ctypes.c_double),
+    ]
+
+
+class _Override(ctypes.Structure):
+    _fields_ = [("blk", ctypes.c_int32), ("side", ctypes.c_int32),
+                ("idx", ctypes.c_int32), ("keep", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        lib.orc_bilu_factor.restype = ctypes.c_int
+        lib.orc_bilu_factor.argtypes = [
+            ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_int32, ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(_Factor),
+        ]
+        lib.orc_bilu_apply.restype = ctypes.c_int
+        lib.orc_bilu_apply.argtypes = [ctypes.POINTER(_Factor), ctypes.c_void_p, ctypes.c_void_p]
+        lib.orc_aggregate_test.restype = ctypes.c_int
+        lib.orc_aggregate_test.argtypes = [ctypes.c_int64] * 11
+        lib.orc_free.restype = None
+        lib.orc_free.argtypes = [ctypes.POINTER(_Factor)]
+        _lib = lib
+    return _lib
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+@dataclass
+class OracleFactor:
+    """Final (post-aggregation) factors in the permuted ordering.
+
+    Per final block K (rows/cols [bstart[K], bstart[K+1])):
+      L rows  Li[Lp[K]:Lp[K+1]]  panel Lv[Lvp[K]:Lvp[K+1]] (m x b row-major)
+      Ũ cols  Ui[Up[K]:Up[K+1]]  panel Uv[Uvp[K]:Uvp[K+1]] (b x c column-major)
+      D_K     Dv[Dp[K]:Dp[K+1]]  (b x b column-major), D_K = P_K^{-1}
+    """
+    n: int
+    bstart: np.ndarray
+    Lp: np.ndarray
+    Li: np.ndarray
+    Lvp: np.ndarray
+    Lv: np.ndarray
+    Up: np.ndarray
+    Ui: np.ndarray
+    Uvp: np.ndarray
+    Uv: np.ndarray
+    Dp: np.ndarray
+    Dv: np.ndarray
+    flops: float = 0.0
+    t_factor_s: float = 0.0
+    n_merges: int = 0
+    n_decisions: int = 0
+    n_near: int = 0
+    min_margin: float = float("inf")
+    _keep: object = field(default=None, repr=False)
+
+    @property
+    def nblk(self) -> int:
+        return len(self.bstart) - 1
+
+    def block(self, K: int):
+        s, e = int(self.bstart[K]), int(self.bstart[K + 1])
+        b = e - s
+        rows = self.Li[self.Lp[K]:self.Lp[K + 1]]
+        L = self.Lv[self.Lvp[K]:self.Lvp[K + 1]].reshape(len(rows), b)
+        cols = self.Ui[self.Up[K]:self.Up[K + 1]]
+        Ut = self.Uv[self.Uvp[K]:self.Uvp[K + 1]].reshape(len(cols), b).T
+        D = self.Dv[self.Dp[K]:self.Dp[K + 1]].reshape(b, b).T
+        return s, e, rows, L, cols, Ut, D
+
+
+def _np(ptr, count, dtype):
+    if count == 0:
+        return np.zeros(0, dtype=dtype)
+    return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True)
+
+
+def factor(indptr, indices, data, block_sizes, tau, aggregate=True, max_block=128,
+           overrides=None, near_rel=1e-8) -> OracleFactor:
+    """Run the oracle on an already-permuted CSR matrix (Ã)."""
+    lib = _load()
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    indices = np.ascontiguousarray(indices, dtype=np.int32)
+    data = np.ascontiguousarray(data, dtype=np.float64)
+    bsz = np.ascontiguousarray(block_sizes, dtype=np.int32)
+    n = len(indptr) - 1
+    ov = None
+    nov = 0
+    if overrides:
+        arr = (_Override * len(overrides))()
+        for i, (blk, side, idx, keep) in enumerate(overrides):
+            arr[i] = _Override(int(blk), int(side), int(idx), int(keep))
+        ov = ctypes.cast(arr, ctypes.c_void_p)
+        nov = len(overrides)
+    f = _Factor()
+    rc = lib.orc_bilu_factor(
+        n, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data,
+        len(bsz), bsz.ctypes.data, float(tau), int(bool(aggregate)), int(max_block),
+        ov, nov, float(near_rel), ctypes.byref(f))
+    if rc != 0:
+        bb = f.breakdown_block
+        lib.orc_free(ctypes.byref(f))
+        raise OracleError({1: "bad argument", 2: "breakdown in block %d" % bb,
+                           3: "out of memory"}.get(rc, "error %d" % rc))
+    nb = f.nblk
+    bstart = _np(f.bstart, nb + 1, np.int64)
+    Lp = _np(f.Lp, nb + 1, np.int64)
+    Lvp = _np(f.Lvp, nb + 1, np.int64)
+    Up = _np(f.Up, nb + 1, np.int64)
+    Uvp = _np(f.Uvp, nb + 1, np.int64)
+    Dp = _np(f.Dp, nb + 1, np.int64)
+    out = OracleFactor(
+        n=f.n, bstart=bstart, Lp=Lp, Li=_np(f.Li, int(Lp[-1]), np.int64), Lvp=Lvp,
+        Lv=_np(f.Lv, int(Lvp[-1]), np.float64), Up=Up, Ui=_np(f.Ui, int(Up[-1]), np.int64),
+        Uvp=Uvp, Uv=_np(f.Uv, int(Uvp[-1]), np.float64), Dp=Dp,
+        Dv=_np(f.Dv, int(Dp[-1]), np.float64), flops=f.flops, t_factor_s=f.t_factor_s,
+        n_merges=f.n_merges, n_decisions=f.n_decisions, n_near=f.n_near,
+        min_margin=f.min_margin)
+    lib.orc_free(ctypes.byref(f))
+    return out
+
+
+def _as_struct(fac: OracleFactor):
+    """Re-expose an OracleFactor to C (for orc_bilu_apply)."""
+    keep = {
+        "bstart": np.ascontiguousarray(fac.bstart, dtype=np.int32),
+        "Lp": np.ascontiguousarray(fac.Lp, dtype=np.int64),
+        "Li": np.ascontiguousarray(fac.Li, dtype=np.int32),
+        "Lvp": np.ascontiguousarray(fac.Lvp, dtype=np.int64),
+        "Lv": np.ascontiguousarray(fac.Lv, dtype=np.float64),
+        "Up": np.ascontiguousarray(fac.Up, dtype=np.int64),
+        "Ui": np.ascontiguousarray(fac.Ui, dtype=np.int32),
+        "Uvp": np.ascontiguousarray(fac.Uvp, dtype=np.int64),
+        "Uv": np.ascontiguousarray(fac.Uv, dtype=np.float64),
+        "Dp": np.ascontiguousarray(fac.Dp, dtype=np.int64),
+        "Dv": np.ascontiguousarray(fac.Dv, dtype=np.float64),
+    }
+    f = _Factor()
+    f.n = fac.n
+    f.nblk = fac.nblk
+    for k, arr in keep.items():
+        ctype = {np.int32: ctypes.c_int32, np.int64: ctypes.c_int64,
+                 np.float64: ctypes.c_double}[arr.dtype.type]
+        setattr(f, k, arr.ctypes.data_as(ctypes.POINTER(ctype)))
+    return f, keep
+
+
+def apply(fac: OracleFactor, x: np.ndarray) -> np.ndarray:
+    """y = (L P U)^{-1} x in the permuted ordering."""
+    lib = _load()
+    f, keep = _as_struct(fac)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros(fac.n, dtype=np.float64)
+    rc = lib.orc_bilu_apply(ctypes.byref(f), x.ctypes.data, y.ctypes.data)
+    if rc != 0:
+        raise OracleError("apply failed")
+    del keep
+    return y
+
+
+def aggregate_test(p, q, r, s, t, r2, s2, t2, u, v, max_block=128) -> bool:
+    return bool(_load().orc_aggregate_test(p, q, r, s, t, r2, s2, t2, u, v, max_block))
+
+
+def permute_csr(indptr, indices, data, perm):
+    """Ã = A(perm, perm) as sorted CSR (plain scipy; the oracle side of the input
+    permutation -- the CUDA path does its own inside bilu_analyze)."""
+    import scipy.sparse as sp
+    n = len(indptr) - 1
+    A = sp.csr_matrix((data, indices, indptr), shape=(n, n))
+    if perm is not None:
+        perm = np.asarray(perm)
+        A = A[perm][:, perm]
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    return A.indptr.astype(np.int64), A.indices.astype(np.int32), A.data.astype(np.float64)

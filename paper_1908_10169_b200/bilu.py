@@ -1,0 +1,250 @@
+"""Thin ctypes binding of libbilu.so (include/bilu.h): argument marshalling only.
+
+Every step of the numeric phase runs in the library's sm_100a kernels; there is
+no CPU fallback -- if the library or a CUDA device is missing, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbilu.so")
+
+STATUS = {0: "BILU_OK", 1: "BILU_ERR_ARG", 2: "BILU_ERR_BREAKDOWN", 3: "BILU_ERR_OOM",
+          4: "BILU_ERR_CUDA", 5: "BILU_ERR_NCCL", 6: "BILU_ERR_STATE", 7: "BILU_ERR_NOT_BUILT"}
+
+# every symbol include/bilu.h declares
+ABI_SYMBOLS = ["bilu_options_default", "bilu_analyze", "bilu_set_values", "bilu_factor",
+               "bilu_apply", "bilu_export", "bilu_factor_view_free", "bilu_destroy",
+               "bilu_status_string", "bilu_last_error", "bilu_kernel_launches"]
+
+
+class BiluError(RuntimeError):
+    def __init__(self, status, msg, breakdown_block=-1):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+        self.breakdown_block = breakdown_block
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("max_block", ctypes.c_int32),
+                ("aggregate", ctypes.c_int32), ("n_ctas", ctypes.c_int32),
+                ("near_rel", ctypes.c_double), ("arena_hint", ctypes.c_int64),
+                ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("nccl_comm", ctypes.c_void_p)]
+
+
+class FactorStats(ctypes.Structure):
+    _fields_ = [("flops", ctypes.c_double), ("bytes_min", ctypes.c_double),
+                ("t_factor_ms", ctypes.c_double), ("t_merge_ms", ctypes.c_double),
+                ("nnz_L", ctypes.c_int64), ("nnz_U", ctypes.c_int64), ("nnz_D", ctypes.c_int64),
+                ("n_blocks_init", ctypes.c_int32), ("n_blocks_final", ctypes.c_int32),
+                ("n_merges", ctypes.c_int32), ("breakdown_block", ctypes.c_int32),
+                ("n_retries", ctypes.c_int32), ("n_kernel_launches", ctypes.c_int32),
+                ("n_decisions", ctypes.c_int64), ("n_near", ctypes.c_int64),
+                ("min_margin", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class FactorView(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("n_blocks", ctypes.c_int32),
+                ("bstart", ctypes.POINTER(ctypes.c_int32)),
+                ("Lp", ctypes.POINTER(ctypes.c_int64)), ("Li", ctypes.POINTER(ctypes.c_int32)),
+                ("Lvp", ctypes.POINTER(ctypes.c_int64)), ("Lv", ctypes.POINTER(ctypes.c_double)),
+                ("Up", ctypes.POINTER(ctypes.c_int64)), ("Ui", ctypes.POINTER(ctypes.c_int32)),
+                ("Uvp", ctypes.POINTER(ctypes.c_int64)), ("Uv", ctypes.POINTER(ctypes.c_double)),
+                ("Dp", ctypes.POINTER(ctypes.c_int64)), ("Dv", ctypes.POINTER(ctypes.c_double)),
+                ("n_near", ctypes.c_int64),
+                ("near_blk", ctypes.POINTER(ctypes.c_int32)), ("near_side", ctypes.POINTER(ctypes.c_int32)),
+                ("near_idx", ctypes.POINTER(ctypes.c_int32)), ("near_keep", ctypes.POINTER(ctypes.c_int32)),
+                ("near_margin", ctypes.POINTER(ctypes.c_double))]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libbilu.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("libbilu.so not built (run __graft_entry__.build() or "
+                          "python paper_1908_10169_b200/build.py)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    lib.bilu_options_default.argtypes = [ctypes.POINTER(Options)]
+    lib.bilu_options_default.restype = None
+    lib.bilu_analyze.argtypes = [ctypes.c_int32, P, P, P, P, P, ctypes.c_int32,
+                                 ctypes.POINTER(Options), ctypes.POINTER(P)]
+    lib.bilu_analyze.restype = ctypes.c_int
+    lib.bilu_set_values.argtypes = [P, P, ctypes.c_int32]
+    lib.bilu_set_values.restype = ctypes.c_int
+    lib.bilu_factor.argtypes = [P, ctypes.c_double, ctypes.POINTER(FactorStats)]
+    lib.bilu_factor.restype = ctypes.c_int
+    lib.bilu_apply.argtypes = [P, P, P, P]
+    lib.bilu_apply.restype = ctypes.c_int
+    lib.bilu_export.argtypes = [P, ctypes.POINTER(FactorView)]
+    lib.bilu_export.restype = ctypes.c_int
+    lib.bilu_factor_view_free.argtypes = [ctypes.POINTER(FactorView)]
+    lib.bilu_factor_view_free.restype = None
+    lib.bilu_destroy.argtypes = [P]
+    lib.bilu_destroy.restype = None
+    lib.bilu_status_string.argtypes = [ctypes.c_int]
+    lib.bilu_status_string.restype = ctypes.c_char_p
+    lib.bilu_last_error.argtypes = [P]
+    lib.bilu_last_error.restype = ctypes.c_char_p
+    lib.bilu_kernel_launches.argtypes = [P]
+    lib.bilu_kernel_launches.restype = ctypes.c_int64
+    _lib = lib
+    return lib
+
+
+def default_options(**kw) -> Options:
+    lib = load_library()
+    o = Options()
+    lib.bilu_options_default(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def _arr(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+@dataclass
+class Factor:
+    """Host copy of the final factors (same layout as oracle.OracleFactor)."""
+    n: int
+    bstart: np.ndarray
+    Lp: np.ndarray
+    Li: np.ndarray
+    Lvp: np.ndarray
+    Lv: np.ndarray
+    Up: np.ndarray
+    Ui: np.ndarray
+    Uvp: np.ndarray
+    Uv: np.ndarray
+    Dp: np.ndarray
+    Dv: np.ndarray
+    near: np.ndarray  # rows (blk, side, idx, keep)
+    near_margin: np.ndarray
+
+    @property
+    def nblk(self):
+        return len(self.bstart) - 1
+
+    def block(self, K):
+        s, e = int(self.bstart[K]), int(self.bstart[K + 1])
+        b = e - s
+        rows = self.Li[self.Lp[K]:self.Lp[K + 1]]
+        L = self.Lv[self.Lvp[K]:self.Lvp[K + 1]].reshape(len(rows), b)
+        cols = self.Ui[self.Up[K]:self.Up[K + 1]]
+        Ut = self.Uv[self.Uvp[K]:self.Uvp[K + 1]].reshape(len(cols), b).T
+        D = self.Dv[self.Dp[K]:self.Dp[K + 1]].reshape(b, b).T
+        return s, e, rows, L, cols, Ut, D
+
+
+class BILU:
+    """bilu_analyze / bilu_set_values / bilu_factor / bilu_apply / bilu_export."""
+
+    def __init__(self, indptr, indices, data, block_sizes, perm=None, **opts):
+        self.lib = load_library()
+        self._keep = {}
+        self.indptr = _arr(indptr, np.int64)
+        self.indices = _arr(indices, np.int32)
+        self.n = len(self.indptr) - 1
+        self.nnz = int(self.indptr[-1])
+        bs = _arr(block_sizes, np.int32)
+        pm = None if perm is None else _arr(perm, np.int32)
+        vals = None if data is None else _arr(data, np.float64)
+        self.opt = default_options(**opts)
+        h = ctypes.c_void_p()
+        rc = self.lib.bilu_analyze(
+            self.n, self.indptr.ctypes.data, self.indices.ctypes.data,
+            None if vals is None else vals.ctypes.data,
+            None if pm is None else pm.ctypes.data, bs.ctypes.data, len(bs),
+            ctypes.byref(self.opt), ctypes.byref(h))
+        if rc != 0:
+            raise BiluError(rc, self.lib.bilu_last_error(None).decode())
+        self.h = h
+        self.stats = None
+
+    def _check(self, rc, bb=-1):
+        if rc != 0:
+            raise BiluError(rc, self.lib.bilu_last_error(self.h).decode(), bb)
+
+    def set_values(self, data=None, device_ptr=None):
+        if device_ptr is not None:
+            self._check(self.lib.bilu_set_values(self.h, ctypes.c_void_p(device_ptr), 1))
+        else:
+            vals = _arr(data, np.float64)
+            self._keep["vals"] = vals
+            self._check(self.lib.bilu_set_values(self.h, vals.ctypes.data, 0))
+
+    def factor(self, tau) -> dict:
+        st = FactorStats()
+        rc = self.lib.bilu_factor(self.h, float(tau), ctypes.byref(st))
+        self._check(rc, st.breakdown_block)
+        self.stats = st.as_dict()
+        return self.stats
+
+    def apply(self, x_ptr: int, y_ptr: int, stream: int = 0):
+        """y = M^{-1} x on DEVICE pointers (original ordering)."""
+        self._check(self.lib.bilu_apply(self.h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
+                                        ctypes.c_void_p(stream) if stream else None))
+
+    def apply_tensor(self, x):
+        """Convenience: torch CUDA tensor in, torch CUDA tensor out."""
+        import torch
+        x = x.contiguous()
+        y = torch.empty_like(x)
+        self.apply(x.data_ptr(), y.data_ptr())
+        return y
+
+    def export(self) -> Factor:
+        v = FactorView()
+        self._check(self.lib.bilu_export(self.h, ctypes.byref(v)))
+
+        def cp(ptr, cnt, dt):
+            if cnt == 0:
+                return np.zeros(0, dtype=dt)
+            return np.ctypeslib.as_array(ptr, shape=(cnt,)).astype(dt, copy=True)
+        nb = v.n_blocks
+        Lp = cp(v.Lp, nb + 1, np.int64)
+        Lvp = cp(v.Lvp, nb + 1, np.int64)
+        Up = cp(v.Up, nb + 1, np.int64)
+        Uvp = cp(v.Uvp, nb + 1, np.int64)
+        Dp = cp(v.Dp, nb + 1, np.int64)
+        nn = v.n_near
+        near = np.stack([cp(v.near_blk, nn, np.int64), cp(v.near_side, nn, np.int64),
+                         cp(v.near_idx, nn, np.int64), cp(v.near_keep, nn, np.int64)], axis=1) \
+            if nn else np.zeros((0, 4), dtype=np.int64)
+        out = Factor(n=v.n, bstart=cp(v.bstart, nb + 1, np.int64), Lp=Lp,
+                     Li=cp(v.Li, int(Lp[-1]), np.int64), Lvp=Lvp, Lv=cp(v.Lv, int(Lvp[-1]), np.float64),
+                     Up=Up, Ui=cp(v.Ui, int(Up[-1]), np.int64), Uvp=Uvp,
+                     Uv=cp(v.Uv, int(Uvp[-1]), np.float64), Dp=Dp, Dv=cp(v.Dv, int(Dp[-1]), np.float64),
+                     near=near, near_margin=cp(v.near_margin, nn, np.float64))
+        self.lib.bilu_factor_view_free(ctypes.byref(v))
+        return out
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.bilu_kernel_launches(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.bilu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

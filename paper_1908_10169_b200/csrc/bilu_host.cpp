@@ -1,0 +1,885 @@
+// bilu_host.cpp -- host orchestrator behind the C-ABI of include/bilu.h.
+//
+// bilu_analyze: validation, symmetric permutation Ã = A(perm, perm) (CSR and
+//   CSC), the block graph of sym(Ã) (static part of the dataflow schedule) and
+//   device upload.  (Host preprocessing is allowed by the task; the caller's
+//   ordering/blocking are inputs: PAPER.md:1541-1573.)
+// bilu_factor:  resets the device schedule state, launches the persistent
+//   factor kernel (bilu_factor.cu), regrows workspaces on overflow, runs the
+//   progressive-aggregation post-pass (bilu_merge.cu) and collects statistics.
+// bilu_apply:   level-free dataflow triangular solves (bilu_apply.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bilu.h"
+#include "bilu_internal.h"
+
+using namespace bilu;
+
+namespace bilu {
+extern "C" cudaError_t bilu_launch_factor(const DevFactor &F, int grid, cudaStream_t st);
+extern "C" cudaError_t bilu_factor_occupancy(int smem_bytes, int *blocks_per_sm);
+extern "C" cudaError_t bilu_launch_gather(double *dst, const double *src, const int64_t *map,
+                                          int64_t n, cudaStream_t st);
+extern "C" cudaError_t bilu_launch_permute(double *y, const double *x, const int32_t *perm,
+                                           int32_t n, int inverse, cudaStream_t st);
+extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_t st);
+extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
+                                        cudaStream_t st);
+extern "C" cudaError_t bilu_launch_apply(const ApplyArgs &A, int grid, int backward, cudaStream_t st);
+}  // namespace bilu
+
+// Final (post-aggregation) factor: per final block F, descriptors into the
+// L/U arenas of DevFactor and a final D arena.
+struct FinalFactor {
+  int nF = 0;
+  int32_t *bstart = nullptr;                      // [nF+1]
+  int64_t *Lrow_off = nullptr, *Lval_off = nullptr, *Ucol_off = nullptr, *Uval_off = nullptr;
+  int32_t *Lm = nullptr, *Uc = nullptr;
+  int64_t *D_off = nullptr;                       // [nF+1]
+  double *D = nullptr;
+  int64_t nnzL = 0, nnzU = 0, nnzD = 0, nidxL = 0, nidxU = 0;   // final factor sizes
+  int64_t usedLi = 0, usedLv = 0, usedUi = 0, usedUv = 0;       // arena prefixes in use
+  bool owns = false;                              // arrays allocated for merges
+};
+
+static thread_local std::string g_last_error;
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+struct bilu_ctx {
+  bilu_options opt;
+  cudaStream_t stream = nullptr;
+  int n = 0, N = 0;
+  int64_t nnz = 0;
+  std::string err;
+  int sms = 0;
+  int64_t launches = 0;
+  bool factored = false;
+  int max_b = 0;
+  // host copies
+  std::vector<int32_t> bstart, ready0;
+  std::vector<int64_t> D_off;
+  std::vector<int64_t> map_csr, map_csc;   // Ã entry -> original CSR entry
+  std::vector<int32_t> perm;
+  // device buffers (owned)
+  std::vector<void *> owned;
+  int32_t *d_bstart = nullptr, *d_block_of = nullptr;
+  int64_t *d_rp = nullptr, *d_cp = nullptr;
+  int32_t *d_ci = nullptr, *d_cr = nullptr;
+  double *d_val = nullptr, *d_cval = nullptr, *d_val_orig = nullptr;
+  int64_t *d_map_csr = nullptr, *d_map_csc = nullptr;
+  int32_t *d_adj_ptr = nullptr, *d_adj = nullptr, *d_pending0 = nullptr, *d_ready0 = nullptr;
+  int32_t *d_perm = nullptr;
+  int32_t nready0 = 0;
+  // dynamic
+  DevFactor F{};
+  int grid = 0;
+  int64_t cap_val = 0, cap_idx = 0, work_per_cta = 0;
+  int pool_lc = 0, pool_uc = 0, pool_succ = 0;
+  int64_t near_cap = 1 << 20;
+  // results
+  FinalFactor fin;
+  bilu_factor_stats last{};
+  // merge workspace
+  MergeArgs M{};
+  bool merge_alloc = false;
+  int64_t merge_work_ints = 0, merge_dwork = 0, fD_cap = 0;
+  double *d_mdwork = nullptr;
+  // apply structure (built lazily after each factorization)
+  bool apply_ready = false;
+  ApplyArgs AA{};
+  int32_t *d_fl_ptr = nullptr, *d_fl_rec = nullptr, *d_fs_ptr = nullptr, *d_fs = nullptr;
+  int32_t *d_bs_ptr = nullptr, *d_bs = nullptr, *d_cnt_f0 = nullptr, *d_cnt_b0 = nullptr;
+  int32_t *d_q_f0 = nullptr, *d_q_b0 = nullptr;
+  int32_t nq_f0 = 0, nq_b0 = 0;
+  unsigned long long nq_f0_ull = 0, nq_b0_ull = 0;
+  double *d_w = nullptr, *d_y = nullptr;
+};
+
+static void set_err(bilu_ctx *h, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  if (h) h->err = buf;
+}
+
+#define CUDA_TRY(h, x)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess) {                                                        \
+      set_err(h, "CUDA error %s at %s:%d", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return e_ == cudaErrorMemoryAllocation ? BILU_ERR_OOM : BILU_ERR_CUDA;         \
+    }                                                                               \
+  } while (0)
+
+template <typename T>
+static cudaError_t dalloc(bilu_ctx *h, T **p, size_t count) {
+  void *q = nullptr;
+  cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) return e;
+  h->owned.push_back(q);
+  *p = (T *)q;
+  return cudaSuccess;
+}
+template <typename T>
+static void dfree(bilu_ctx *h, T *&p) {
+  if (!p) return;
+  auto it = std::find(h->owned.begin(), h->owned.end(), (void *)p);
+  if (it != h->owned.end()) h->owned.erase(it);
+  cudaFree(p);
+  p = nullptr;
+}
+
+extern "C" void bilu_options_default(bilu_options *opt) {
+  if (!opt) return;
+  memset(opt, 0, sizeof(*opt));
+  opt->device = 0;
+  opt->max_block = 128;
+  opt->aggregate = 1;
+  opt->n_ctas = 0;
+  opt->near_rel = 1e-8;
+  opt->arena_hint = 0;
+  opt->stream = nullptr;
+  opt->rank = 0;
+  opt->world = 1;
+  opt->nccl_comm = nullptr;
+}
+
+extern "C" const char *bilu_status_string(bilu_status s) {
+  switch (s) {
+    case BILU_OK: return "ok";
+    case BILU_ERR_ARG: return "invalid argument";
+    case BILU_ERR_BREAKDOWN: return "breakdown: singular pivot block";
+    case BILU_ERR_OOM: return "out of device memory";
+    case BILU_ERR_CUDA: return "CUDA error";
+    case BILU_ERR_NCCL: return "NCCL error";
+    case BILU_ERR_STATE: return "invalid state";
+    case BILU_ERR_NOT_BUILT: return "no usable CUDA device";
+  }
+  return "unknown status";
+}
+
+extern "C" const char *bilu_last_error(const bilu_ctx *h) {
+  if (h) return h->err.c_str();
+  return g_last_error.c_str();
+}
+
+extern "C" int64_t bilu_kernel_launches(const bilu_ctx *h) { return h ? h->launches : 0; }
+
+// --------------------------------------------------------------- destroy
+extern "C" void bilu_destroy(bilu_ctx *h) {
+  if (!h) return;
+  if (h->opt.device >= 0) cudaSetDevice(h->opt.device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void *p : h->owned) cudaFree(p);
+  h->owned.clear();
+  delete h;
+}
+
+// --------------------------------------------------------------- analyze
+extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                                    const double *val, const int32_t *perm,
+                                    const int32_t *block_sizes, int32_t n_blocks,
+                                    const bilu_options *opt_in, bilu_ctx **out) {
+  if (!out) { set_err(nullptr, "bilu_analyze: out is NULL"); return BILU_ERR_ARG; }
+  *out = nullptr;
+  bilu_options opt;
+  if (opt_in) opt = *opt_in; else bilu_options_default(&opt);
+  if (n < 1 || !row_ptr || !col_idx || !block_sizes || n_blocks < 1) {
+    set_err(nullptr, "bilu_analyze: null pointer or empty problem (n=%d, n_blocks=%d)", n, n_blocks);
+    return BILU_ERR_ARG;
+  }
+  if (opt.max_block < 1 || opt.max_block > 128) {
+    set_err(nullptr, "bilu_analyze: max_block must be in [1,128] (got %d)", opt.max_block);
+    return BILU_ERR_ARG;
+  }
+  if (n_blocks >= (1 << 21)) {
+    set_err(nullptr, "bilu_analyze: at most 2^21-1 blocks supported (got %d)", n_blocks);
+    return BILU_ERR_ARG;
+  }
+  if (opt.world != 1) {
+    set_err(nullptr, "bilu_analyze: world > 1 is not supported by this build");
+    return BILU_ERR_ARG;
+  }
+  // ---- validate CSR
+  if (row_ptr[0] != 0) { set_err(nullptr, "bilu_analyze: row_ptr[0] != 0"); return BILU_ERR_ARG; }
+  for (int32_t i = 0; i < n; ++i) {
+    if (row_ptr[i + 1] < row_ptr[i]) { set_err(nullptr, "bilu_analyze: row_ptr decreases at row %d", i); return BILU_ERR_ARG; }
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      if (col_idx[p] < 0 || col_idx[p] >= n) { set_err(nullptr, "bilu_analyze: column index out of range in row %d", i); return BILU_ERR_ARG; }
+      if (p > row_ptr[i] && col_idx[p] <= col_idx[p - 1]) { set_err(nullptr, "bilu_analyze: row %d not strictly increasing (unsorted or duplicate)", i); return BILU_ERR_ARG; }
+    }
+  }
+  const int64_t nnz = row_ptr[n];
+  // ---- validate permutation
+  std::vector<int32_t> pm(n), ipm(n, -1);
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t p = perm ? perm[i] : i;
+    if (p < 0 || p >= n || ipm[p] != -1) { set_err(nullptr, "bilu_analyze: perm is not a bijection (position %d)", i); return BILU_ERR_ARG; }
+    pm[i] = p; ipm[p] = i;
+  }
+  // ---- validate partition
+  std::vector<int32_t> bstart(n_blocks + 1, 0);
+  int max_b = 0;
+  for (int32_t K = 0; K < n_blocks; ++K) {
+    if (block_sizes[K] < 1 || block_sizes[K] > opt.max_block) {
+      set_err(nullptr, "bilu_analyze: block %d has size %d outside [1, max_block=%d]", K, block_sizes[K], opt.max_block);
+      return BILU_ERR_ARG;
+    }
+    bstart[K + 1] = bstart[K] + block_sizes[K];
+    max_b = std::max(max_b, (int)block_sizes[K]);
+    if (bstart[K + 1] > n) break;
+  }
+  if (bstart[n_blocks] != n) { set_err(nullptr, "bilu_analyze: sum(block_sizes) != n"); return BILU_ERR_ARG; }
+
+  bilu_ctx *h = new bilu_ctx();
+  h->opt = opt;
+  h->n = n; h->N = n_blocks; h->nnz = nnz; h->max_b = max_b;
+  h->bstart = bstart;
+  h->perm = pm;
+  if (cudaSetDevice(opt.device) != cudaSuccess) {
+    set_err(h, "bilu_analyze: cannot use CUDA device %d", opt.device);
+    g_last_error = h->err;
+    delete h;
+    return BILU_ERR_NOT_BUILT;
+  }
+  h->stream = (cudaStream_t)opt.stream;
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, opt.device);
+
+  // ---- Ã = A(perm, perm), CSR (rows sorted)
+  std::vector<int64_t> rp(n + 1, 0);
+  for (int32_t i = 0; i < n; ++i) rp[i + 1] = rp[i] + (row_ptr[pm[i] + 1] - row_ptr[pm[i]]);
+  std::vector<int32_t> ci(nnz);
+  h->map_csr.resize(nnz);
+  {
+    std::vector<std::pair<int32_t, int64_t>> tmp;
+    for (int32_t i = 0; i < n; ++i) {
+      int32_t o = pm[i];
+      tmp.clear();
+      for (int64_t p = row_ptr[o]; p < row_ptr[o + 1]; ++p) tmp.emplace_back(ipm[col_idx[p]], p);
+      std::sort(tmp.begin(), tmp.end());
+      int64_t q = rp[i];
+      for (auto &t : tmp) { ci[q] = t.first; h->map_csr[q] = t.second; ++q; }
+    }
+  }
+  // ---- CSC of Ã (counting transpose; rows ascending within a column)
+  std::vector<int64_t> cp(n + 1, 0);
+  for (int64_t p = 0; p < nnz; ++p) cp[ci[p] + 1]++;
+  for (int32_t i = 0; i < n; ++i) cp[i + 1] += cp[i];
+  std::vector<int32_t> cr(nnz);
+  h->map_csc.resize(nnz);
+  {
+    std::vector<int64_t> fill(cp.begin(), cp.end() - 1);
+    for (int32_t i = 0; i < n; ++i)
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        int64_t q = fill[ci[p]]++;
+        cr[q] = i;
+        h->map_csc[q] = h->map_csr[p];
+      }
+  }
+  // ---- block graph of sym(Ã): successors > K and pending counts
+  std::vector<int32_t> block_of(n);
+  for (int32_t K = 0; K < n_blocks; ++K)
+    for (int32_t i = bstart[K]; i < bstart[K + 1]; ++i) block_of[i] = K;
+  std::vector<uint64_t> edges;
+  {
+    std::vector<int32_t> mark(n_blocks, -1);
+    for (int32_t I = 0; I < n_blocks; ++I) {
+      for (int32_t i = bstart[I]; i < bstart[I + 1]; ++i)
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+          int32_t J = block_of[ci[p]];
+          if (J == I || mark[J] == I) continue;
+          mark[J] = I;
+          int32_t a = std::min(I, J), b = std::max(I, J);
+          edges.push_back(((uint64_t)a << 32) | (uint32_t)b);
+        }
+    }
+    std::sort(edges.begin(), edges.end());
+    edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+  }
+  std::vector<int32_t> adj_ptr(n_blocks + 1, 0), adj(edges.size()), pending0(n_blocks, 0);
+  for (uint64_t eg : edges) { adj_ptr[(eg >> 32) + 1]++; pending0[(uint32_t)eg]++; }
+  for (int32_t K = 0; K < n_blocks; ++K) adj_ptr[K + 1] += adj_ptr[K];
+  for (size_t x = 0; x < edges.size(); ++x) adj[x] = (int32_t)(uint32_t)edges[x];  // sorted by (a, b)
+  for (int32_t K = 0; K < n_blocks; ++K) if (pending0[K] == 0) h->ready0.push_back(K);
+  h->nready0 = (int32_t)h->ready0.size();
+  h->D_off.assign(n_blocks + 1, 0);
+  for (int32_t K = 0; K < n_blocks; ++K) {
+    int64_t b = bstart[K + 1] - bstart[K];
+    h->D_off[K + 1] = h->D_off[K] + b * b;
+  }
+
+  // ---- device upload
+#define ALLOC(ptr, cnt) do { cudaError_t e_ = dalloc(h, &ptr, cnt); if (e_ != cudaSuccess) { set_err(h, "bilu_analyze: cudaMalloc failed (%s)", cudaGetErrorString(e_)); g_last_error = h->err; bilu_destroy(h); return BILU_ERR_OOM; } } while (0)
+#define H2D(dst, src, cnt) do { cudaError_t e_ = cudaMemcpy(dst, src, (cnt) * sizeof(*(src)), cudaMemcpyHostToDevice); if (e_ != cudaSuccess) { set_err(h, "bilu_analyze: copy failed (%s)", cudaGetErrorString(e_)); g_last_error = h->err; bilu_destroy(h); return BILU_ERR_CUDA; } } while (0)
+  ALLOC(h->d_bstart, n_blocks + 1); H2D(h->d_bstart, bstart.data(), n_blocks + 1);
+  ALLOC(h->d_block_of, n); H2D(h->d_block_of, block_of.data(), n);
+  ALLOC(h->d_rp, n + 1); H2D(h->d_rp, rp.data(), n + 1);
+  ALLOC(h->d_ci, nnz); H2D(h->d_ci, ci.data(), nnz);
+  ALLOC(h->d_cp, n + 1); H2D(h->d_cp, cp.data(), n + 1);
+  ALLOC(h->d_cr, nnz); H2D(h->d_cr, cr.data(), nnz);
+  ALLOC(h->d_map_csr, nnz); H2D(h->d_map_csr, h->map_csr.data(), nnz);
+  ALLOC(h->d_map_csc, nnz); H2D(h->d_map_csc, h->map_csc.data(), nnz);
+  ALLOC(h->d_val, nnz); ALLOC(h->d_cval, nnz); ALLOC(h->d_val_orig, nnz);
+  ALLOC(h->d_adj_ptr, n_blocks + 1); H2D(h->d_adj_ptr, adj_ptr.data(), n_blocks + 1);
+  ALLOC(h->d_adj, adj.size()); if (!adj.empty()) H2D(h->d_adj, adj.data(), adj.size());
+  ALLOC(h->d_pending0, n_blocks); H2D(h->d_pending0, pending0.data(), n_blocks);
+  ALLOC(h->d_ready0, std::max<int32_t>(h->nready0, 1));
+  if (h->nready0) H2D(h->d_ready0, h->ready0.data(), h->nready0);
+  ALLOC(h->d_perm, n); H2D(h->d_perm, pm.data(), n);
+  {
+    int64_t *d_Doff = nullptr;
+    ALLOC(d_Doff, n_blocks + 1); H2D(d_Doff, h->D_off.data(), n_blocks + 1);
+    h->F.D_off = d_Doff;
+  }
+#undef H2D
+
+  // ---- schedule state and factor descriptors (sizes independent of values)
+  DevFactor &F = h->F;
+  F.n = n; F.N = n_blocks;
+  F.bstart = h->d_bstart; F.block_of = h->d_block_of;
+  F.rp = h->d_rp; F.ci = h->d_ci; F.val = h->d_val;
+  F.cp = h->d_cp; F.cr = h->d_cr; F.cval = h->d_cval;
+  F.adj_ptr = h->d_adj_ptr; F.adj = h->d_adj;
+  ALLOC(F.pending, n_blocks);
+  ALLOC(F.queue, n_blocks);
+  ALLOC(F.ctrl, CTRL_COUNT);
+  ALLOC(F.Lrow_off, n_blocks); ALLOC(F.Lm, n_blocks); ALLOC(F.Lval_off, n_blocks);
+  ALLOC(F.Ucol_off, n_blocks); ALLOC(F.Uc, n_blocks); ALLOC(F.Uval_off, n_blocks);
+  ALLOC(F.D, h->D_off[n_blocks]);
+  ALLOC(F.blk_flops, n_blocks);
+  ALLOC(F.blk_ncand, 2 * (size_t)n_blocks);
+  ALLOC(F.lc.cnt, n_blocks); ALLOC(F.uc.cnt, n_blocks); ALLOC(F.succ.cnt, n_blocks);
+  ALLOC(F.lc.dir, (size_t)n_blocks * DIR_SLOTS);
+  ALLOC(F.uc.dir, (size_t)n_blocks * DIR_SLOTS);
+  ALLOC(F.succ.dir, (size_t)n_blocks * DIR_SLOTS);
+  ALLOC(F.near_i, 4 * (size_t)h->near_cap); ALLOC(F.near_m, (size_t)h->near_cap);
+  F.near_cap = h->near_cap;
+  F.lc.rec_ints = REC_INTS; F.uc.rec_ints = REC_INTS; F.succ.rec_ints = 1;
+  F.lc.ctrl_cursor = CTRL_POOL_LC; F.uc.ctrl_cursor = CTRL_POOL_UC; F.succ.ctrl_cursor = CTRL_POOL_SUCC;
+#undef ALLOC
+
+  // launch geometry: persistent CTAs, all co-resident
+  F.smem_bytes = 110 * 1024;
+  int per_sm = 0;
+  if (bilu_factor_occupancy(F.smem_bytes, &per_sm) != cudaSuccess || per_sm < 1) per_sm = 1;
+  h->grid = opt.n_ctas > 0 ? opt.n_ctas : h->sms * per_sm;
+
+  // initial capacities (grown on overflow)
+  h->cap_val = opt.arena_hint > 0 ? opt.arena_hint : std::max<int64_t>(16 * nnz, (int64_t)n * max_b * 4);
+  h->cap_idx = h->cap_val;
+  h->work_per_cta = 256 * 1024;
+  h->pool_lc = h->pool_uc = std::max(2 * n_blocks, 1024);
+  h->pool_succ = std::max(2 * n_blocks, 1024);
+
+  if (val) {
+    bilu_status st = bilu_set_values(h, val, 0);
+    if (st != BILU_OK) { g_last_error = h->err; bilu_destroy(h); return st; }
+  }
+  *out = h;
+  return BILU_OK;
+}
+
+// ------------------------------------------------------------ set values
+extern "C" bilu_status bilu_set_values(bilu_ctx *h, const double *val, int32_t on_device) {
+  if (!h || !val) { set_err(h, "bilu_set_values: null argument"); return BILU_ERR_ARG; }
+  cudaSetDevice(h->opt.device);
+  CUDA_TRY(h, cudaMemcpyAsync(h->d_val_orig, val, h->nnz * sizeof(double),
+                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, bilu_launch_gather(h->d_val, h->d_val_orig, h->d_map_csr, h->nnz, h->stream));
+  CUDA_TRY(h, bilu_launch_gather(h->d_cval, h->d_val_orig, h->d_map_csc, h->nnz, h->stream));
+  h->launches += 2;
+  h->factored = false;
+  return BILU_OK;
+}
+
+// ------------------------------------------------------------ capacities
+static bilu_status ensure_capacity(bilu_ctx *h) {
+  DevFactor &F = h->F;
+  if (F.cap_Lval != h->cap_val) {
+    dfree(h, F.Lval); dfree(h, F.Uval);
+    CUDA_TRY(h, dalloc(h, &F.Lval, h->cap_val));
+    CUDA_TRY(h, dalloc(h, &F.Uval, h->cap_val));
+    F.cap_Lval = F.cap_Uval = h->cap_val;
+  }
+  if (F.cap_Lidx != h->cap_idx) {
+    dfree(h, F.Lidx); dfree(h, F.Uidx);
+    CUDA_TRY(h, dalloc(h, &F.Lidx, h->cap_idx));
+    CUDA_TRY(h, dalloc(h, &F.Uidx, h->cap_idx));
+    F.cap_Lidx = F.cap_Uidx = h->cap_idx;
+  }
+  if (F.work_per_cta != h->work_per_cta) {
+    dfree(h, F.work);
+    CUDA_TRY(h, dalloc(h, &F.work, (size_t)h->work_per_cta * h->grid));
+    F.work_per_cta = h->work_per_cta;
+  }
+  if (F.lc.pool_cap != h->pool_lc) {
+    dfree(h, F.lc.pool);
+    CUDA_TRY(h, dalloc(h, &F.lc.pool, (size_t)h->pool_lc * CHUNK * REC_INTS));
+    F.lc.pool_cap = h->pool_lc;
+  }
+  if (F.uc.pool_cap != h->pool_uc) {
+    dfree(h, F.uc.pool);
+    CUDA_TRY(h, dalloc(h, &F.uc.pool, (size_t)h->pool_uc * CHUNK * REC_INTS));
+    F.uc.pool_cap = h->pool_uc;
+  }
+  if (F.succ.pool_cap != h->pool_succ) {
+    dfree(h, F.succ.pool);
+    CUDA_TRY(h, dalloc(h, &F.succ.pool, (size_t)h->pool_succ * CHUNK));
+    F.succ.pool_cap = h->pool_succ;
+  }
+  return BILU_OK;
+}
+
+static bilu_status reset_schedule(bilu_ctx *h) {
+  DevFactor &F = h->F;
+  cudaStream_t st = h->stream;
+  const size_t N = h->N;
+  CUDA_TRY(h, cudaMemcpyAsync(F.pending, h->d_pending0, N * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(h, cudaMemsetAsync(F.queue, 0xFF, N * sizeof(int32_t), st));
+  if (h->nready0)
+    CUDA_TRY(h, cudaMemcpyAsync(F.queue, h->d_ready0, h->nready0 * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(h, cudaMemsetAsync(F.ctrl, 0, CTRL_COUNT * sizeof(unsigned long long), st));
+  unsigned long long qh = (unsigned long long)h->nready0;
+  CUDA_TRY(h, cudaMemcpyAsync(F.ctrl + CTRL_QHEAD, &qh, sizeof(qh), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h, cudaMemsetAsync(F.lc.cnt, 0, N * sizeof(int), st));
+  CUDA_TRY(h, cudaMemsetAsync(F.uc.cnt, 0, N * sizeof(int), st));
+  CUDA_TRY(h, cudaMemsetAsync(F.succ.cnt, 0, N * sizeof(int), st));
+  CUDA_TRY(h, cudaMemsetAsync(F.lc.dir, 0xFF, N * DIR_SLOTS * sizeof(int), st));
+  CUDA_TRY(h, cudaMemsetAsync(F.uc.dir, 0xFF, N * DIR_SLOTS * sizeof(int), st));
+  CUDA_TRY(h, cudaMemsetAsync(F.succ.dir, 0xFF, N * DIR_SLOTS * sizeof(int), st));
+  return BILU_OK;
+}
+
+// ------------------------------------------------------------ finalize
+// Grows one arena to hold `need` elements, keeping the first `used` ones.
+template <typename T>
+static bilu_status grow_keep(bilu_ctx *h, T *&p, int64_t &cap, int64_t need, int64_t used) {
+  if (need <= cap) return BILU_OK;
+  int64_t nc = std::max<int64_t>(need + need / 4, 2 * cap);
+  T *q = nullptr;
+  CUDA_TRY(h, dalloc(h, &q, nc));
+  if (used > 0) CUDA_TRY(h, cudaMemcpyAsync(q, p, used * sizeof(T), cudaMemcpyDeviceToDevice, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  dfree(h, p);
+  p = q;
+  cap = nc;
+  return BILU_OK;
+}
+
+static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_factor_stats &S, int &launches) {
+  DevFactor &F = h->F;
+  FinalFactor &fin = h->fin;
+  const int N = h->N;
+  double fl;
+  memcpy(&fl, &ctrl[CTRL_FLOPS], sizeof(double));
+  S.flops = fl;
+  h->apply_ready = false;
+  if (!h->opt.aggregate) {
+    fin.nF = N;
+    fin.bstart = h->d_bstart;
+    fin.Lrow_off = F.Lrow_off; fin.Lval_off = F.Lval_off; fin.Lm = F.Lm;
+    fin.Ucol_off = F.Ucol_off; fin.Uval_off = F.Uval_off; fin.Uc = F.Uc;
+    fin.D_off = const_cast<int64_t *>(F.D_off); fin.D = F.D;
+    fin.nidxL = fin.usedLi = (int64_t)ctrl[CTRL_CUR_LIDX]; fin.nnzL = fin.usedLv = (int64_t)ctrl[CTRL_CUR_LVAL];
+    fin.nidxU = fin.usedUi = (int64_t)ctrl[CTRL_CUR_UIDX]; fin.nnzU = fin.usedUv = (int64_t)ctrl[CTRL_CUR_UVAL];
+    fin.nnzD = h->D_off[N];
+    S.n_blocks_final = N;
+    S.n_merges = 0;
+  } else {
+    MergeArgs &M = h->M;
+    if (!h->merge_alloc) {
+      CUDA_TRY(h, dalloc(h, &M.T, 4 * (size_t)N));
+      CUDA_TRY(h, dalloc(h, &M.first, (size_t)N + 1));
+      CUDA_TRY(h, dalloc(h, &M.nF, 1));
+      CUDA_TRY(h, dalloc(h, &M.fbstart, (size_t)N + 1));
+      CUDA_TRY(h, dalloc(h, &M.fLm, (size_t)N)); CUDA_TRY(h, dalloc(h, &M.fUc, (size_t)N));
+      CUDA_TRY(h, dalloc(h, &M.fLrow_off, (size_t)N)); CUDA_TRY(h, dalloc(h, &M.fLval_off, (size_t)N));
+      CUDA_TRY(h, dalloc(h, &M.fUcol_off, (size_t)N)); CUDA_TRY(h, dalloc(h, &M.fUval_off, (size_t)N));
+      CUDA_TRY(h, dalloc(h, &M.fD_off, (size_t)N + 1));
+      CUDA_TRY(h, dalloc(h, &M.tot, 16)); CUDA_TRY(h, dalloc(h, &M.flops, 1)); CUDA_TRY(h, dalloc(h, &M.ovf, 1));
+      h->merge_work_ints = 16384;
+      CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * h->grid));
+      h->fD_cap = std::max<int64_t>(h->D_off[N], 1);
+      CUDA_TRY(h, dalloc(h, &M.fD, h->fD_cap));
+      h->merge_alloc = true;
+    }
+    M.n = h->n; M.N = N; M.max_block = h->opt.max_block;
+    M.bstart = h->d_bstart;
+    M.Lrow_off = F.Lrow_off; M.Lm = F.Lm; M.Lval_off = F.Lval_off;
+    M.Ucol_off = F.Ucol_off; M.Uc = F.Uc; M.Uval_off = F.Uval_off;
+    M.D = F.D; M.D_off = F.D_off;
+    M.work_ints = h->merge_work_ints;
+    unsigned long long tot[16];
+    for (int attempt = 0;; ++attempt) {
+      M.Lidx = F.Lidx; M.Uidx = F.Uidx; M.Lval = F.Lval; M.Uval = F.Uval;
+      unsigned long long cur[4] = {ctrl[CTRL_CUR_LIDX], ctrl[CTRL_CUR_LVAL], ctrl[CTRL_CUR_UIDX], ctrl[CTRL_CUR_UVAL]};
+      CUDA_TRY(h, cudaMemcpyAsync(M.tot, cur, sizeof(cur), cudaMemcpyHostToDevice, h->stream));
+      CUDA_TRY(h, cudaMemsetAsync(M.ovf, 0, sizeof(int), h->stream));
+      CUDA_TRY(h, cudaMemsetAsync(M.flops, 0, sizeof(double), h->stream));
+      CUDA_TRY(h, bilu_merge_plan(M, h->grid, h->stream));
+      launches += 4;
+      int ovf = 0;
+      CUDA_TRY(h, cudaMemcpyAsync(tot, M.tot, sizeof(tot), cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(h, cudaMemcpyAsync(&ovf, M.ovf, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      if (!ovf) break;
+      if (attempt > 8) { set_err(h, "bilu_factor: merge workspace overflow"); return BILU_ERR_OOM; }
+      dfree(h, M.work);
+      h->merge_work_ints *= 4;
+      CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * h->grid));
+      M.work_ints = h->merge_work_ints;
+      S.n_retries++;
+    }
+    const int nF = (int)(N - (int64_t)tot[11]);
+    // arenas: merged panels are appended after the factor kernel's cursors
+    bilu_status bs;
+    if ((bs = grow_keep(h, F.Lidx, F.cap_Lidx, (int64_t)tot[4], (int64_t)ctrl[CTRL_CUR_LIDX])) != BILU_OK) return bs;
+    if ((bs = grow_keep(h, F.Lval, F.cap_Lval, (int64_t)tot[5], (int64_t)ctrl[CTRL_CUR_LVAL])) != BILU_OK) return bs;
+    if ((bs = grow_keep(h, F.Uidx, F.cap_Uidx, (int64_t)tot[6], (int64_t)ctrl[CTRL_CUR_UIDX])) != BILU_OK) return bs;
+    if ((bs = grow_keep(h, F.Uval, F.cap_Uval, (int64_t)tot[7], (int64_t)ctrl[CTRL_CUR_UVAL])) != BILU_OK) return bs;
+    h->cap_val = std::max(F.cap_Lval, F.cap_Uval); h->cap_idx = std::max(F.cap_Lidx, F.cap_Uidx);
+    F.cap_Lval = F.cap_Uval = h->cap_val; F.cap_Lidx = F.cap_Uidx = h->cap_idx;
+    if ((int64_t)tot[8] > h->fD_cap) {
+      dfree(h, M.fD);
+      h->fD_cap = (int64_t)tot[8] + (int64_t)tot[8] / 4;
+      CUDA_TRY(h, dalloc(h, &M.fD, h->fD_cap));
+    }
+    const int64_t need_dw = (int64_t)tot[9];
+    if (need_dw > h->merge_dwork) {
+      dfree(h, h->d_mdwork);
+      h->merge_dwork = need_dw;
+      CUDA_TRY(h, dalloc(h, &h->d_mdwork, (size_t)need_dw * h->grid));
+    }
+    M.Lidx = F.Lidx; M.Uidx = F.Uidx; M.Lval = F.Lval; M.Uval = F.Uval;
+    M.Lidx_out = F.Lidx; M.Uidx_out = F.Uidx; M.Lval_out = F.Lval; M.Uval_out = F.Uval;
+    CUDA_TRY(h, bilu_merge_arith(M, h->d_mdwork, std::max<int64_t>(h->merge_dwork, 1), h->grid, h->stream));
+    launches += 1;
+    double mfl = 0.0;
+    int ovf = 0;
+    CUDA_TRY(h, cudaMemcpyAsync(&mfl, M.flops, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(&ovf, M.ovf, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (ovf) { set_err(h, "bilu_factor: merge workspace overflow in arithmetic"); return BILU_ERR_OOM; }
+    S.flops += mfl;
+    fin.nF = nF;
+    fin.bstart = M.fbstart;
+    fin.Lrow_off = M.fLrow_off; fin.Lval_off = M.fLval_off; fin.Lm = M.fLm;
+    fin.Ucol_off = M.fUcol_off; fin.Uval_off = M.fUval_off; fin.Uc = M.fUc;
+    fin.D_off = M.fD_off; fin.D = M.fD;
+    fin.usedLi = (int64_t)tot[4]; fin.usedLv = (int64_t)tot[5];
+    fin.usedUi = (int64_t)tot[6]; fin.usedUv = (int64_t)tot[7];
+    fin.nnzD = (int64_t)tot[8];
+    fin.nnzL = (int64_t)tot[12]; fin.nnzU = (int64_t)tot[13];
+    fin.nidxL = (int64_t)tot[14]; fin.nidxU = (int64_t)tot[15];
+    S.n_blocks_final = nF;
+    S.n_merges = (int32_t)tot[11];
+  }
+  S.nnz_D = fin.nnzD;
+  S.nnz_L = fin.nnzL;
+  S.nnz_U = fin.nnzU;
+  S.bytes_min = 12.0 * (double)h->nnz + 4.0 * (h->n + 1) + 8.0 * (double)(fin.nnzL + fin.nnzU + fin.nnzD) +
+                4.0 * (double)(fin.nidxL + fin.nidxU);
+  return BILU_OK;
+}
+
+// ------------------------------------------------------------ factor
+extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *st_out) {
+  if (!h) { set_err(nullptr, "bilu_factor: null context"); return BILU_ERR_ARG; }
+  if (!(tau >= 0.0)) { set_err(h, "bilu_factor: tau must be >= 0"); return BILU_ERR_ARG; }
+  cudaSetDevice(h->opt.device);
+  DevFactor &F = h->F;
+  F.tau = tau;
+  F.near_rel = h->opt.near_rel;
+  bilu_factor_stats S{};
+  S.breakdown_block = -1;
+  S.n_blocks_init = h->N;
+  cudaEvent_t e0, e1, e2;
+  CUDA_TRY(h, cudaEventCreate(&e0)); CUDA_TRY(h, cudaEventCreate(&e1)); CUDA_TRY(h, cudaEventCreate(&e2));
+  h->factored = false;
+  int launches = 0;
+  unsigned long long ctrl[CTRL_COUNT];
+  for (int attempt = 0;; ++attempt) {
+    bilu_status bs = ensure_capacity(h);
+    if (bs != BILU_OK) return bs;
+    CUDA_TRY(h, cudaEventRecord(e0, h->stream));
+    bs = reset_schedule(h);
+    if (bs != BILU_OK) return bs;
+    CUDA_TRY(h, bilu_launch_factor(F, h->grid, h->stream));
+    launches = 1;
+    CUDA_TRY(h, cudaEventRecord(e1, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(ctrl, F.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    const int code = (int)ctrl[CTRL_ABORT];
+    if (code == DEV_OK) {
+      if (ctrl[CTRL_DONE] != (unsigned long long)h->N) {
+        set_err(h, "bilu_factor: schedule finished %llu of %d blocks", ctrl[CTRL_DONE], h->N);
+        return BILU_ERR_STATE;
+      }
+      break;
+    }
+    if (code == DEV_BREAKDOWN) {
+      S.breakdown_block = (int32_t)ctrl[CTRL_ERRBLK];
+      if (st_out) *st_out = S;
+      set_err(h, "bilu_factor: pivot block %d is exactly singular", S.breakdown_block);
+      return BILU_ERR_BREAKDOWN;
+    }
+    if (attempt >= 12) { set_err(h, "bilu_factor: workspace overflow persists (code %d)", code); return BILU_ERR_OOM; }
+    S.n_retries++;
+    switch (code) {
+      case DEV_OVF_ARENA: h->cap_val *= 2; h->cap_idx *= 2; break;
+      case DEV_OVF_WORK: h->work_per_cta *= 4; break;
+      case DEV_OVF_POOL: h->pool_lc *= 2; h->pool_uc *= 2; h->pool_succ *= 2; break;
+      default: set_err(h, "bilu_factor: device list overflow (code %d, block %llu)", code, ctrl[CTRL_ERRBLK]); return BILU_ERR_OOM;
+    }
+  }
+  h->launches += launches;
+  S.n_decisions = (int64_t)ctrl[CTRL_NDEC];
+  S.n_near = (int64_t)ctrl[CTRL_NEAR];
+  // ---- progressive aggregation post-pass + final factor descriptors
+  int mlaunch = 0;
+  bilu_status ms = finalize(h, ctrl, S, mlaunch);
+  if (ms != BILU_OK) return ms;
+  launches += mlaunch;
+  h->launches += mlaunch;
+  CUDA_TRY(h, cudaEventRecord(e2, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  float ms1 = 0.f, ms2 = 0.f;
+  cudaEventElapsedTime(&ms1, e0, e1);
+  cudaEventElapsedTime(&ms2, e1, e2);
+  S.t_factor_ms = ms1 + ms2;
+  S.t_merge_ms = ms2;
+  S.n_kernel_launches = launches;
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
+  h->factored = true;
+  h->last = S;
+  if (st_out) *st_out = S;
+  return BILU_OK;
+}
+
+// ------------------------------------------------------------ export
+extern "C" bilu_status bilu_export(bilu_ctx *h, bilu_factor_view *v) {
+  if (!h || !v) { set_err(h, "bilu_export: null argument"); return BILU_ERR_ARG; }
+  memset(v, 0, sizeof(*v));
+  if (!h->factored) { set_err(h, "bilu_export: no factorization"); return BILU_ERR_STATE; }
+  cudaSetDevice(h->opt.device);
+  const FinalFactor &fin = h->fin;
+  const int nF = fin.nF;
+  cudaStream_t st = h->stream;
+  std::vector<int32_t> fb(nF + 1), Lm(nF), Uc(nF), Li(fin.usedLi), Ui(fin.usedUi);
+  std::vector<int64_t> Lro(nF), Lvo(nF), Uco(nF), Uvo(nF), Doff(nF + 1);
+  std::vector<double> Lv(fin.usedLv), Uv(fin.usedUv), Dv(fin.nnzD);
+  CUDA_TRY(h, cudaMemcpyAsync(fb.data(), fin.bstart, (nF + 1) * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Lm.data(), fin.Lm, nF * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Uc.data(), fin.Uc, nF * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Lro.data(), fin.Lrow_off, nF * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Lvo.data(), fin.Lval_off, nF * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Uco.data(), fin.Ucol_off, nF * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Uvo.data(), fin.Uval_off, nF * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Doff.data(), fin.D_off, (nF + 1) * 8, cudaMemcpyDeviceToHost, st));
+  if (fin.usedLi) CUDA_TRY(h, cudaMemcpyAsync(Li.data(), h->F.Lidx, fin.usedLi * 4, cudaMemcpyDeviceToHost, st));
+  if (fin.usedUi) CUDA_TRY(h, cudaMemcpyAsync(Ui.data(), h->F.Uidx, fin.usedUi * 4, cudaMemcpyDeviceToHost, st));
+  if (fin.usedLv) CUDA_TRY(h, cudaMemcpyAsync(Lv.data(), h->F.Lval, fin.usedLv * 8, cudaMemcpyDeviceToHost, st));
+  if (fin.usedUv) CUDA_TRY(h, cudaMemcpyAsync(Uv.data(), h->F.Uval, fin.usedUv * 8, cudaMemcpyDeviceToHost, st));
+  if (fin.nnzD) CUDA_TRY(h, cudaMemcpyAsync(Dv.data(), fin.D, fin.nnzD * 8, cudaMemcpyDeviceToHost, st));
+  int64_t nnear = std::min<int64_t>(h->last.n_near, h->near_cap);
+  std::vector<int32_t> ni(4 * nnear);
+  std::vector<double> nm(nnear);
+  if (nnear) {
+    CUDA_TRY(h, cudaMemcpyAsync(ni.data(), h->F.near_i, 4 * nnear * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaMemcpyAsync(nm.data(), h->F.near_m, nnear * 8, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  v->n = h->n; v->n_blocks = nF;
+  v->bstart = (int32_t *)malloc(sizeof(int32_t) * (nF + 1));
+  v->Lp = (int64_t *)malloc(sizeof(int64_t) * (nF + 1));
+  v->Lvp = (int64_t *)malloc(sizeof(int64_t) * (nF + 1));
+  v->Up = (int64_t *)malloc(sizeof(int64_t) * (nF + 1));
+  v->Uvp = (int64_t *)malloc(sizeof(int64_t) * (nF + 1));
+  v->Dp = (int64_t *)malloc(sizeof(int64_t) * (nF + 1));
+  v->Lp[0] = v->Lvp[0] = v->Up[0] = v->Uvp[0] = v->Dp[0] = 0;
+  for (int F = 0; F < nF; ++F) {
+    int64_t b = fb[F + 1] - fb[F];
+    v->bstart[F] = fb[F];
+    v->Lp[F + 1] = v->Lp[F] + Lm[F];
+    v->Lvp[F + 1] = v->Lvp[F] + Lm[F] * b;
+    v->Up[F + 1] = v->Up[F] + Uc[F];
+    v->Uvp[F + 1] = v->Uvp[F] + Uc[F] * b;
+    v->Dp[F + 1] = v->Dp[F] + b * b;
+  }
+  v->bstart[nF] = fb[nF];
+  v->Li = (int32_t *)malloc(sizeof(int32_t) * std::max<int64_t>(v->Lp[nF], 1));
+  v->Lv = (double *)malloc(sizeof(double) * std::max<int64_t>(v->Lvp[nF], 1));
+  v->Ui = (int32_t *)malloc(sizeof(int32_t) * std::max<int64_t>(v->Up[nF], 1));
+  v->Uv = (double *)malloc(sizeof(double) * std::max<int64_t>(v->Uvp[nF], 1));
+  v->Dv = (double *)malloc(sizeof(double) * std::max<int64_t>(v->Dp[nF], 1));
+  for (int F = 0; F < nF; ++F) {
+    int64_t b = fb[F + 1] - fb[F];
+    if (Lm[F]) {
+      memcpy(v->Li + v->Lp[F], Li.data() + Lro[F], sizeof(int32_t) * Lm[F]);
+      memcpy(v->Lv + v->Lvp[F], Lv.data() + Lvo[F], sizeof(double) * Lm[F] * b);
+    }
+    if (Uc[F]) {
+      memcpy(v->Ui + v->Up[F], Ui.data() + Uco[F], sizeof(int32_t) * Uc[F]);
+      memcpy(v->Uv + v->Uvp[F], Uv.data() + Uvo[F], sizeof(double) * Uc[F] * b);
+    }
+    memcpy(v->Dv + v->Dp[F], Dv.data() + Doff[F], sizeof(double) * b * b);
+  }
+  v->n_near = nnear;
+  v->near_blk = (int32_t *)malloc(sizeof(int32_t) * std::max<int64_t>(nnear, 1));
+  v->near_side = (int32_t *)malloc(sizeof(int32_t) * std::max<int64_t>(nnear, 1));
+  v->near_idx = (int32_t *)malloc(sizeof(int32_t) * std::max<int64_t>(nnear, 1));
+  v->near_keep = (int32_t *)malloc(sizeof(int32_t) * std::max<int64_t>(nnear, 1));
+  v->near_margin = (double *)malloc(sizeof(double) * std::max<int64_t>(nnear, 1));
+  for (int64_t i = 0; i < nnear; ++i) {
+    v->near_blk[i] = ni[4 * i]; v->near_side[i] = ni[4 * i + 1];
+    v->near_idx[i] = ni[4 * i + 2]; v->near_keep[i] = ni[4 * i + 3];
+    v->near_margin[i] = nm[i];
+  }
+  return BILU_OK;
+}
+
+extern "C" void bilu_factor_view_free(bilu_factor_view *v) {
+  if (!v) return;
+  free(v->bstart); free(v->Lp); free(v->Li); free(v->Lvp); free(v->Lv);
+  free(v->Up); free(v->Ui); free(v->Uvp); free(v->Uv); free(v->Dp); free(v->Dv);
+  free(v->near_blk); free(v->near_side); free(v->near_idx); free(v->near_keep); free(v->near_margin);
+  memset(v, 0, sizeof(*v));
+}
+
+// ------------------------------------------------------------ apply
+// Dependency lists of the two sweeps, built once per factorization from the
+// final index lists (host side, like the schedule tables of bilu_analyze).
+static bilu_status build_apply(bilu_ctx *h) {
+  const FinalFactor &fin = h->fin;
+  const int nF = fin.nF, n = h->n;
+  cudaStream_t st = h->stream;
+  std::vector<int32_t> fb(nF + 1), Lm(nF), Uc(nF), Li(fin.usedLi), Ui(fin.usedUi);
+  std::vector<int64_t> Lro(nF), Uco(nF);
+  CUDA_TRY(h, cudaMemcpyAsync(fb.data(), fin.bstart, (nF + 1) * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Lm.data(), fin.Lm, nF * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Uc.data(), fin.Uc, nF * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Lro.data(), fin.Lrow_off, nF * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaMemcpyAsync(Uco.data(), fin.Ucol_off, nF * 8, cudaMemcpyDeviceToHost, st));
+  if (fin.usedLi) CUDA_TRY(h, cudaMemcpyAsync(Li.data(), h->F.Lidx, fin.usedLi * 4, cudaMemcpyDeviceToHost, st));
+  if (fin.usedUi) CUDA_TRY(h, cudaMemcpyAsync(Ui.data(), h->F.Uidx, fin.usedUi * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  std::vector<int32_t> fbo(n);
+  for (int F = 0; F < nF; ++F) for (int i = fb[F]; i < fb[F + 1]; ++i) fbo[i] = F;
+  // forward: target T pulls (J, r0, r1) for every J with L rows in T
+  std::vector<int32_t> fl_cnt(nF + 1, 0), fs_ptr(nF + 1, 0), bs_cnt(nF + 1, 0), cnt_b(nF, 0);
+  for (int J = 0; J < nF; ++J) {
+    const int32_t *r = Li.data() + Lro[J];
+    for (int p = 0; p < Lm[J]; ++p) if (p == 0 || fbo[r[p]] != fbo[r[p - 1]]) { fl_cnt[fbo[r[p]] + 1]++; fs_ptr[J + 1]++; }
+    const int32_t *c = Ui.data() + Uco[J];
+    for (int q = 0; q < Uc[J]; ++q) if (q == 0 || fbo[c[q]] != fbo[c[q - 1]]) { bs_cnt[fbo[c[q]] + 1]++; cnt_b[J]++; }
+  }
+  std::vector<int32_t> fl_ptr(nF + 1, 0), bs_ptr(nF + 1, 0), cnt_f(nF, 0);
+  for (int F = 0; F < nF; ++F) {
+    fl_ptr[F + 1] = fl_ptr[F] + fl_cnt[F + 1];
+    bs_ptr[F + 1] = bs_ptr[F] + bs_cnt[F + 1];
+    fs_ptr[F + 1] += fs_ptr[F];
+    cnt_f[F] = fl_cnt[F + 1];
+  }
+  std::vector<int32_t> fl_rec(3 * (size_t)fl_ptr[nF] + 3), fs(fs_ptr[nF] + 1), bs(bs_ptr[nF] + 1);
+  std::vector<int32_t> flf(fl_ptr.begin(), fl_ptr.end() - 1), bsf(bs_ptr.begin(), bs_ptr.end() - 1);
+  for (int J = 0; J < nF; ++J) {
+    const int32_t *r = Li.data() + Lro[J];
+    int xs = fs_ptr[J];
+    for (int p = 0; p < Lm[J];) {
+      int T = fbo[r[p]], p1 = p;
+      while (p1 < Lm[J] && fbo[r[p1]] == T) ++p1;
+      int x = flf[T]++;
+      fl_rec[3 * x] = J; fl_rec[3 * x + 1] = p; fl_rec[3 * x + 2] = p1;
+      fs[xs++] = T;
+      p = p1;
+    }
+    const int32_t *c = Ui.data() + Uco[J];
+    for (int q = 0; q < Uc[J];) {
+      int T = fbo[c[q]], q1 = q;
+      while (q1 < Uc[J] && fbo[c[q1]] == T) ++q1;
+      bs[bsf[T]++] = J;
+      q = q1;
+    }
+  }
+  std::vector<int32_t> qf, qb;
+  for (int F = 0; F < nF; ++F) if (cnt_f[F] == 0) qf.push_back(F);
+  for (int F = nF - 1; F >= 0; --F) if (cnt_b[F] == 0) qb.push_back(F);
+  dfree(h, h->d_fl_ptr); dfree(h, h->d_fl_rec); dfree(h, h->d_fs_ptr); dfree(h, h->d_fs);
+  dfree(h, h->d_bs_ptr); dfree(h, h->d_bs); dfree(h, h->d_cnt_f0); dfree(h, h->d_cnt_b0);
+  dfree(h, h->d_q_f0); dfree(h, h->d_q_b0);
+  auto up = [&](int32_t *&d, const std::vector<int32_t> &v) -> bilu_status {
+    CUDA_TRY(h, dalloc(h, &d, std::max<size_t>(v.size(), 1)));
+    if (!v.empty()) CUDA_TRY(h, cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+    return BILU_OK;
+  };
+  bilu_status bs_;
+  if ((bs_ = up(h->d_fl_ptr, fl_ptr)) || (bs_ = up(h->d_fl_rec, fl_rec)) || (bs_ = up(h->d_fs_ptr, fs_ptr)) ||
+      (bs_ = up(h->d_fs, fs)) || (bs_ = up(h->d_bs_ptr, bs_ptr)) || (bs_ = up(h->d_bs, bs)) ||
+      (bs_ = up(h->d_cnt_f0, cnt_f)) || (bs_ = up(h->d_cnt_b0, cnt_b)) || (bs_ = up(h->d_q_f0, qf)) ||
+      (bs_ = up(h->d_q_b0, qb)))
+    return bs_;
+  h->nq_f0 = (int32_t)qf.size(); h->nq_b0 = (int32_t)qb.size();
+  h->nq_f0_ull = (unsigned long long)h->nq_f0; h->nq_b0_ull = (unsigned long long)h->nq_b0;
+  ApplyArgs &A = h->AA;
+  if (!A.cnt) {
+    CUDA_TRY(h, dalloc(h, &A.cnt, (size_t)h->N));
+    CUDA_TRY(h, dalloc(h, &A.queue, (size_t)h->N));
+    CUDA_TRY(h, dalloc(h, &A.ctrl, 4));
+    CUDA_TRY(h, dalloc(h, &h->d_w, (size_t)n));
+    CUDA_TRY(h, dalloc(h, &h->d_y, (size_t)n));
+  }
+  A.n = n; A.nF = nF;
+  A.fbstart = fin.bstart;
+  A.Lrow_off = fin.Lrow_off; A.Lval_off = fin.Lval_off; A.Ucol_off = fin.Ucol_off; A.Uval_off = fin.Uval_off;
+  A.D_off = fin.D_off; A.Lm = fin.Lm; A.Uc = fin.Uc;
+  A.Lidx = h->F.Lidx; A.Uidx = h->F.Uidx; A.Lval = h->F.Lval; A.Uval = h->F.Uval; A.D = fin.D;
+  A.fl_ptr = h->d_fl_ptr; A.fl_rec = h->d_fl_rec; A.fs_ptr = h->d_fs_ptr; A.fs = h->d_fs;
+  A.bs_ptr = h->d_bs_ptr; A.bs = h->d_bs;
+  A.w = h->d_w; A.y = h->d_y;
+  h->apply_ready = true;
+  return BILU_OK;
+}
+
+extern "C" bilu_status bilu_apply(bilu_ctx *h, const double *x, double *y, void *stream) {
+  if (!h || !x || !y) { set_err(h, "bilu_apply: null argument"); return BILU_ERR_ARG; }
+  if (x == y) { set_err(h, "bilu_apply: x and y may not alias"); return BILU_ERR_ARG; }
+  if (!h->factored) { set_err(h, "bilu_apply: no factorization"); return BILU_ERR_STATE; }
+  cudaSetDevice(h->opt.device);
+  if (!h->apply_ready) { bilu_status s = build_apply(h); if (s != BILU_OK) return s; }
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  ApplyArgs &A = h->AA;
+  const int nF = h->fin.nF;
+  const int grid = std::max(1, std::min(nF, h->sms * 8));
+  CUDA_TRY(h, bilu_launch_permute(h->d_w, x, h->d_perm, h->n, 0, st));
+  for (int pass = 0; pass < 2; ++pass) {
+    const int32_t *cnt0 = pass ? h->d_cnt_b0 : h->d_cnt_f0;
+    const int32_t *q0 = pass ? h->d_q_b0 : h->d_q_f0;
+    const int nq = pass ? h->nq_b0 : h->nq_f0;
+    CUDA_TRY(h, cudaMemcpyAsync(A.cnt, cnt0, nF * 4, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(h, cudaMemsetAsync(A.queue, 0xFF, nF * 4, st));
+    if (nq) CUDA_TRY(h, cudaMemcpyAsync(A.queue, q0, nq * 4, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(h, cudaMemsetAsync(A.ctrl, 0, 4 * sizeof(unsigned long long), st));
+    CUDA_TRY(h, cudaMemcpyAsync(A.ctrl, pass ? &h->nq_b0_ull : &h->nq_f0_ull, sizeof(unsigned long long),
+                                cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, bilu_launch_apply(A, grid, pass, st));
+  }
+  CUDA_TRY(h, bilu_launch_permute(y, h->d_y, h->d_perm, h->n, 1, st));
+  h->launches += 4;
+  return BILU_OK;
+}

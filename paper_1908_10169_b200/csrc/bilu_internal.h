@@ -1,0 +1,132 @@
+// bilu_internal.h -- shared between the host orchestrator (bilu_host.cpp) and
+// the sm_100a kernels (bilu_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <stdint.h>
+
+namespace bilu {
+
+// Records of the per-target contributor lists (replace the paper's
+// L_head/L_list/L_first linked lists).  8 x int32.
+//   Lc(T) entry: J has Ũ columns in T: {J, c0, c1, lrs, lre, 0, 0, 0}
+//       c0..c1  = positions of J's kept columns inside T
+//       lrs     = first position of J's kept rows >= s_T
+//       lre     = first position of J's kept rows >= e_T
+//   Uc(T) entry: J has L rows in T:    {J, r0, r1, cus, 0, 0, 0, 0}
+//       r0..r1  = positions of J's kept rows inside T
+//       cus     = first position of J's kept columns >= e_T
+constexpr int REC_INTS = 8;
+constexpr int CHUNK = 32;        // records per chunk of a chunked list
+constexpr int DIR_SLOTS = 32;    // chunks per target -> 1024 records max
+
+// error codes raised on the device (ctrl[CTRL_ABORT])
+enum : int {
+  DEV_OK = 0,
+  DEV_BREAKDOWN = 1,
+  DEV_OVF_ARENA = 2,
+  DEV_OVF_LIST = 3,
+  DEV_OVF_WORK = 4,
+  DEV_OVF_POOL = 5,
+};
+
+// control block indices (int64 each)
+enum : int {
+  CTRL_QHEAD = 0,
+  CTRL_QTAIL,
+  CTRL_ABORT,
+  CTRL_ERRBLK,
+  CTRL_CUR_LIDX,
+  CTRL_CUR_LVAL,
+  CTRL_CUR_UIDX,
+  CTRL_CUR_UVAL,
+  CTRL_POOL_LC,
+  CTRL_POOL_UC,
+  CTRL_POOL_SUCC,
+  CTRL_NEAR,
+  CTRL_DONE,
+  CTRL_NDEC,
+  CTRL_FLOPS,
+  CTRL_COUNT = 16
+};
+
+struct ChunkList {
+  int *cnt;        // [N]   records appended per target
+  int *dir;        // [N * DIR_SLOTS] chunk ids (-1 = none, -2 = overflow)
+  int *pool;       // [pool_cap * CHUNK * rec_ints]
+  int pool_cap;    // chunks
+  int rec_ints;
+  int ctrl_cursor; // index into ctrl of the pool cursor
+};
+
+struct DevFactor {
+  // problem
+  int32_t n, N;
+  const int32_t *bstart;     // [N+1]
+  const int32_t *block_of;   // [n]
+  // Ã, CSR and CSC
+  const int64_t *rp; const int32_t *ci; const double *val;
+  const int64_t *cp; const int32_t *cr; const double *cval;
+  // static schedule: block adjacency of sym(Ã), successors > J
+  const int32_t *adj_ptr; const int32_t *adj;
+  int32_t *pending;          // [N]
+  int32_t *queue;            // [N]
+  unsigned long long *ctrl;  // [CTRL_COUNT]
+  // factors (per original block)
+  int64_t *Lrow_off; int32_t *Lm; int64_t *Lval_off;
+  int64_t *Ucol_off; int32_t *Uc; int64_t *Uval_off;
+  const int64_t *D_off;      // static prefix of b^2
+  int32_t *Lidx; double *Lval; int64_t cap_Lidx, cap_Lval;
+  int32_t *Uidx; double *Uval; int64_t cap_Uidx, cap_Uval;
+  double *D;
+  double *blk_flops;         // [N]
+  int32_t *blk_ncand;        // [2N] candidate rows / cols
+  // lists
+  ChunkList lc, uc, succ;
+  // near-threshold log
+  int32_t *near_i; double *near_m; int64_t near_cap;
+  // per-CTA global workspace
+  double *work; int64_t work_per_cta;   // doubles per CTA
+  int smem_bytes;
+  double tau, near_rel;
+};
+
+struct MergeArgs {
+  int n, N, max_block;
+  const int32_t *bstart;
+  const int64_t *Lrow_off; const int32_t *Lm; const int64_t *Lval_off;
+  const int64_t *Ucol_off; const int32_t *Uc; const int64_t *Uval_off;
+  const int32_t *Lidx; const int32_t *Uidx;
+  const double *Lval; const double *Uval; const double *D; const int64_t *D_off;
+  // outputs / workspace
+  uint32_t *T;            // [4N] test bitmasks, bit d-1 <=> merge(a = k-d, k)
+  int32_t *first;         // [N+1] first original block of each final block
+  int32_t *nF;            // [1]
+  int32_t *fbstart;       // [N+1]
+  int32_t *fLm, *fUc;     // [N]
+  int64_t *fLrow_off, *fLval_off, *fUcol_off, *fUval_off, *fD_off;  // [N] / [N+1]
+  unsigned long long *tot;  // [16] cursors and maxima
+  int32_t *Lidx_out; double *Lval_out; int32_t *Uidx_out; double *Uval_out;
+  double *fD;
+  int *work; int64_t work_ints;  // per-CTA workspace (ints)
+  double *flops;          // [1]
+  int *ovf;               // [1]
+};
+
+// Apply (forward/backward block triangular solves) -- dataflow over final blocks.
+struct ApplyArgs {
+  int n, nF;
+  const int32_t *fbstart;
+  const int64_t *Lrow_off, *Lval_off, *Ucol_off, *Uval_off, *D_off;
+  const int32_t *Lm, *Uc;
+  const int32_t *Lidx, *Uidx;
+  const double *Lval, *Uval, *D;
+  // forward pull lists: for target T, records (J, r0, r1) at fl_ptr[T]..fl_ptr[T+1]
+  const int32_t *fl_ptr, *fl_rec;
+  const int32_t *fs_ptr, *fs;     // forward successors of J
+  const int32_t *bs_ptr, *bs;     // backward successors of T (blocks with U cols in T)
+  int32_t *cnt;                   // [nF] working counters
+  int32_t *queue;                 // [nF]
+  unsigned long long *ctrl;       // [4]: qhead, qtail
+  double *w, *y;                  // permuted work vectors
+};
+
+}  // namespace bilu

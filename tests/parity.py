@@ -1,0 +1,61 @@
+"""Parity comparison between the CUDA factors and the oracle's (test helper).
+
+SURVEY.md 8(c) reading 14: "relative 1e-10" is checked normwise per stored
+object: each L row, each Ũ column and each D block,
+    max|g - o| <= tol * max|o|   (over that row / column / block).
+Patterns must be identical (near-threshold decisions are replayed in the oracle
+before comparing, reading 15).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def compare_factors(g, o, tol=1e-10):
+    """Return a dict of discrepancies (empty problems list == parity)."""
+    problems = []
+    if g.nblk != o.nblk or not np.array_equal(np.asarray(g.bstart), np.asarray(o.bstart)):
+        problems.append("partition differs: %d vs %d blocks" % (g.nblk, o.nblk))
+        return {"problems": problems, "max_rel": np.inf}
+    worst = 0.0
+    for K in range(o.nblk):
+        s, e, gr, gL, gc, gU, gD = g.block(K)
+        _, _, orr, oL, oc, oU, oD = o.block(K)
+        if not np.array_equal(gr, orr):
+            problems.append("block %d: L row pattern differs (%d vs %d rows)" % (K, len(gr), len(orr)))
+            continue
+        if not np.array_equal(gc, oc):
+            problems.append("block %d: U col pattern differs (%d vs %d cols)" % (K, len(gc), len(oc)))
+            continue
+        for a, b_ in ((gL, oL), (gU.T, oU.T)):
+            if a.size:
+                den = np.maximum(np.abs(b_).max(axis=1), 1e-300)
+                rel = (np.abs(a - b_).max(axis=1) / den).max()
+                worst = max(worst, rel)
+        if gD.size:
+            rel = np.abs(gD - oD).max() / max(np.abs(oD).max(), 1e-300)
+            worst = max(worst, rel)
+    if worst > tol:
+        problems.append("max normwise relative difference %.3e > %.1e" % (worst, tol))
+    return {"problems": problems, "max_rel": worst}
+
+
+def overrides_from_near(near):
+    """GPU near-threshold decisions -> oracle override list (blk, side, idx, keep)."""
+    return [tuple(int(x) for x in row) for row in np.asarray(near)]
+
+
+def dense_LPU(f, n):
+    """Dense L, P (= D^{-1} blocks), U of a factor (small n only; test helper)."""
+    L = np.eye(n)
+    U = np.eye(n)
+    P = np.zeros((n, n))
+    for K in range(f.nblk):
+        s, e, rows, Lp, cols, Ut, D = f.block(K)
+        if len(rows):
+            L[np.asarray(rows)[:, None], np.arange(s, e)[None, :]] = Lp
+        Pk = np.linalg.inv(D)
+        P[s:e, s:e] = Pk
+        if len(cols):
+            U[np.arange(s, e)[:, None], np.asarray(cols)[None, :]] = D @ Ut
+    return L, P, U
