@@ -1,0 +1,284 @@
+#!/usr/bin/env python
+"""Benchmark of the BILU numeric phase (BASELINE.json metric) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+
+A step is one bilu_factor (the whole hot path: scatter, Schur updates, pivot
+inverses, scaling/dropping, progressive aggregation) of the configs[1] matrix
+(3D 7-pt convection-diffusion 64^3, ND ordering, tau = 1e-3), inputs resident in
+HBM.  value = factorizations per second over all ranks (N>1: independent
+replicas, weak scaling); ms_per_step = device time of one factorization (CUDA
+events on the library's stream, max over ranks).  `e2e` repeats the step through
+the C-ABI with the matrix values copied from pinned HOST memory every step.
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BILU numeric factor time & FP64 GFLOP/s (fraction of FP64 peak), 1-8 B200"
+FP64_PEAK_TFLOPS = 37.2     # measured: DMMA m8n8k4 microbenchmark (profiles/r01_fp64_peak.md)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def make_problem(name):
+    from inputs.configs import make_config
+    return make_config(name)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_init(n_gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if n_gpus > 0 else "gloo")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, world):
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the CPU oracle as it stands, on the box's host cores."""
+    import oracle
+    if rank != 0:
+        return
+    P = make_problem(args.config)
+    ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
+    times = []
+    for i in range(args.warmup + args.steps):
+        f = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, aggregate=True)
+        if i >= args.warmup:
+            times.append(f.t_factor_s)
+    t = float(np.mean(times))
+    val = 1.0 / t
+    out = {"metric": METRIC, "value": val, "unit": "factorizations/s", "impl": "reference",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic",
+           "config": {"workload": args.config + " (BASELINE.json configs[1])", "n": P.n, "nnz": P.nnz,
+                      "tau": P.tau, "blocks_init": int(len(P.block_sizes)), "aggregate": True},
+           "gflops": f.flops / t / 1e9, "flops_per_factorization": f.flops,
+           "cpu_baseline": {"value": val, "unit": "factorizations/s", "cores": 1, "kind": "oracle",
+                            "sample": "full %s factorization per step (plain C scalar oracle, 1 thread)" % args.config},
+           "e2e": {"value": val, "unit": "factorizations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(P, budget_s=30.0):
+    import oracle
+    ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
+    times = []
+    t_start = time.time()
+    flops = 0.0
+    while not times or (time.time() - t_start < budget_s * 0.4 and len(times) < 3):
+        f = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, aggregate=True)
+        times.append(f.t_factor_s)
+        flops = f.flops
+    t = float(np.mean(times))
+    return {"value": 1.0 / t, "unit": "factorizations/s", "cores": 1, "kind": "oracle",
+            "sample": "%d full %s factorization(s), plain C scalar oracle, 1 thread; %.2f s each, %.3g flops"
+                      % (len(times), P.name, t, flops)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank, world, local = dist_init(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    from paper_1908_10169_b200 import BILU
+    from paper_1908_10169_b200.build import build
+    torch.cuda.set_device(local)
+    if rank == 0:
+        build()
+    barrier(world)
+
+    P = make_problem(args.config)
+    g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm, device=local)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2 (126 MB)
+
+    for _ in range(args.warmup):
+        st = g.factor(P.tau)
+    torch.cuda.synchronize()
+
+    # ---------------- device-timed steps (inputs resident in HBM)
+    clk = ClockSampler(local)
+    clk.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    step_ms, kern_ms, launches = [], [], 0
+    flops = 0.0
+    for _ in range(args.steps):
+        flush.zero_()                                  # L2 flush between timed iterations
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = g.factor(P.tau)
+        e1.record()
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        kern_ms.append(st["t_factor_ms"] - st["t_merge_ms"])
+        launches += int(st["n_kernel_launches"])
+        flops = st["flops"]
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = clk.stop()
+    t_step = allreduce_max(float(np.sum(step_ms)), world) / args.steps
+    t_kern = allreduce_max(float(np.mean(kern_ms)), world)
+    value = world / (t_step * 1e-3)
+
+    # ---------------- e2e through the C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        vals_pinned = torch.from_numpy(np.ascontiguousarray(P.data)).pin_memory()
+        host_ptr = vals_pinned.data_ptr()
+        import ctypes
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            g.lib.bilu_set_values(g.h, ctypes.c_void_p(host_ptr), 0)
+            g.factor(P.tau)                          # ends with its device->host status read
+        torch.cuda.synchronize()
+        t_e2e = allreduce_max((time.perf_counter() - t0) / args.steps, world)
+        e2e = {"value": world / t_e2e, "unit": "factorizations/s",
+               "h2d_bytes_per_step": int(P.nnz * 8),
+               "d2h_bytes_per_step": int(16 * 8 + (16 * 8 + 4 + 8 + 4 if g.opt.aggregate else 0)),
+               "ms_per_step": t_e2e * 1e3}
+
+    if rank == 0:
+        hbm_peak, hbm_src = load_peaks()
+        achieved_tf = st["flops"] / (t_kern * 1e-3) / 1e12
+        out = {
+            "metric": METRIC, "value": value, "unit": "factorizations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.config + " (BASELINE.json configs[1]): 3D 7-pt conv-diff 64^3, "
+                                   "geometric ND, tau=1e-3, initial blocks <=8, aggregation on, max_block 128",
+                       "n": P.n, "nnz": P.nnz, "tau": P.tau, "blocks_init": int(len(P.block_sizes)),
+                       "blocks_final": int(st["n_blocks_final"]), "merges": int(st["n_merges"]),
+                       "parallelism": "replicas x%d" % world if world > 1 else "single GPU",
+                       "l2": "flushed between timed steps (256 MB write)"},
+            "gflops": world * flops / (t_step * 1e-3) / 1e9,
+            "flops_per_factorization": flops,
+            "fp64_peak_fraction": (flops / (t_step * 1e-3) / 1e12) / FP64_PEAK_TFLOPS,
+            "nnz_factors": int(st["nnz_L"] + st["nnz_U"] + st["nnz_D"]),
+            "roofline": {"bound": "tensor", "kernel": "factor_kernel (persistent, all of a-1..a-8)",
+                         "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": None,
+                         "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_fp64_peak.md)",
+                         "kernel_ms": t_kern,
+                         "hbm": {"achieved_gbs": st["bytes_min"] / (t_kern * 1e-3) / 1e9,
+                                 "peak_gbs": hbm_peak, "peak_source": hbm_src}},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if e2e:
+            out["e2e"] = e2e
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(P)
+        print(json.dumps(out), flush=True)
+    g.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -139,9 +139,12 @@ bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *st);
 bilu_status bilu_apply(bilu_ctx *h, const double *x, double *y, void *stream);
 
 /*
- * Host copy of the final factors (paper convention except U, which is exported
- * unscaled as Ũ; U = D_K Ũ).  All arrays are malloc'd by the library and owned
- * by the view; release with bilu_factor_view_free.
+ * bilu_export -- HOST copy of the final factors in the hybrid layout of Fig. 1
+ * (PAPER.md:220-228): per final block the sorted kept L rows + dense panel, the
+ * sorted kept U columns + dense panel of Ũ (U = D_K Ũ), and D_K; plus the log of
+ * near-threshold drop decisions (|max/tau - 1| <= near_rel) for decision replay.
+ * All arrays are malloc'd by the library and owned by the view; release them
+ * with bilu_factor_view_free.  BILU_ERR_STATE before a successful bilu_factor.
  */
 typedef struct {
   int32_t n, n_blocks;

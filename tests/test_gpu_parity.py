@@ -1,0 +1,220 @@
+"""CUDA path (through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE north_star):
+  - kept/dropped pattern identical after replaying the GPU's near-threshold
+    decisions (|max/tau - 1| <= 1e-8) in the oracle,
+  - factor values within 1e-10 normwise per L row / Ũ column / D block,
+  - preconditioned GMRES(30) iteration counts to 1e-8 within +-1.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle
+from harness.gmres import gmres
+from inputs.configs import config1, config2, config3, dense_to_csr, random_dd
+from tests.parity import compare_factors, dense_LPU, overrides_from_near
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_1908_10169_b200.build import build
+    build()
+
+
+def run_pair(ip, ix, dv, bs, tau, agg=True, perm=None, max_block=128, **kw):
+    from paper_1908_10169_b200 import BILU
+    g = BILU(ip, ix, dv, bs, perm=perm, aggregate=int(agg), max_block=max_block, **kw)
+    st = g.factor(tau)
+    gf = g.export()
+    if perm is not None:
+        pip, pix, pdv = oracle.permute_csr(ip, ix, dv, perm)
+    else:
+        pip, pix, pdv = ip, ix, dv
+    of = oracle.factor(pip, pix, pdv, bs, tau, aggregate=agg, max_block=max_block,
+                       overrides=overrides_from_near(gf.near))
+    return g, st, gf, of
+
+
+def assert_parity(gf, of, tol=TOL):
+    r = compare_factors(gf, of, tol)
+    assert not r["problems"], r["problems"][:5]
+    return r
+
+
+def partition(n, rng, maxb):
+    out = []
+    while sum(out) < n:
+        out.append(int(min(rng.integers(1, maxb + 1), n - sum(out))))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("tau", [0.0, 1e-3, 3e-2])
+@pytest.mark.parametrize("agg", [False, True])
+def test_random_small(seed, tau, agg):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(30, 260))
+    A = random_dd(n, float(rng.uniform(0.02, 0.2)), 500 + seed, dominance=float(rng.uniform(1.05, 2.0)))
+    ip, ix, dv = dense_to_csr(A)
+    bs = partition(n, rng, int(rng.integers(1, 17)))
+    g, st, gf, of = run_pair(ip, ix, dv, bs, tau, agg)
+    assert_parity(gf, of)
+    if agg:
+        assert st["n_blocks_final"] == of.nblk
+    g.close()
+
+
+def test_edge_single_unknown():
+    g, st, gf, of = run_pair([0, 1], [0], [3.0], [1], 1e-2)
+    assert_parity(gf, of)
+    np.testing.assert_allclose(gf.Dv, [1 / 3.0])
+
+
+def test_edge_one_block_of_max_size():
+    A = random_dd(128, 0.3, 1)
+    ip, ix, dv = dense_to_csr(A)
+    g, st, gf, of = run_pair(ip, ix, dv, [128], 1e-2)
+    assert_parity(gf, of)
+    np.testing.assert_allclose(gf.block(0)[6], np.linalg.inv(A), rtol=1e-9, atol=1e-13)
+
+
+def test_edge_scalar_blocks_and_large_blocks_mixed():
+    A = random_dd(300, 0.05, 2, dominance=1.2)
+    ip, ix, dv = dense_to_csr(A)
+    bs = np.array([1] * 50 + [64, 64] + [2] * 61)
+    assert bs.sum() == 300
+    g, st, gf, of = run_pair(ip, ix, dv, bs, 1e-3)
+    assert_parity(gf, of)
+
+
+def test_edge_tau_infinite_block_jacobi():
+    A = random_dd(100, 0.1, 3)
+    ip, ix, dv = dense_to_csr(A)
+    g, st, gf, of = run_pair(ip, ix, dv, [10] * 10, 1e300, agg=False)
+    assert len(gf.Li) == 0 and len(gf.Ui) == 0
+    assert_parity(gf, of)
+
+
+def test_edge_identity():
+    n = 64
+    ip = np.arange(n + 1)
+    g, st, gf, of = run_pair(ip, np.arange(n), np.ones(n), [8] * 8, 1e-2, agg=True)
+    assert_parity(gf, of)
+
+
+def test_breakdown_reports_block():
+    from paper_1908_10169_b200 import BILU, BiluError
+    A = np.array([[4.0, 1, 0, 0], [1, 4, 0, 0], [0, 0, 1, 1], [0, 0, 1, 1]])
+    ip, ix, dv = dense_to_csr(A)
+    g = BILU(ip, ix, dv, [2, 2], aggregate=0)
+    with pytest.raises(BiluError) as ei:
+        g.factor(0.0)
+    assert ei.value.status == 2 and ei.value.breakdown_block == 1
+
+
+def test_near_threshold_decision_is_logged_and_replayed():
+    """l_21 = 0.02 / 2 = 0.01 = tau exactly: a tie (dropped, R2) with margin 0."""
+    A = np.array([[2.0, 0.0], [0.02, 1.0]])
+    ip, ix, dv = dense_to_csr(A)
+    g, st, gf, of = run_pair(ip, ix, dv, [1, 1], 0.01, agg=False)
+    assert st["n_near"] == 1 and gf.near.shape == (1, 4)
+    assert tuple(gf.near[0]) == (0, 0, 1, 0)
+    assert_parity(gf, of)
+
+
+def test_refactor_new_values_and_tau():
+    A = random_dd(150, 0.08, 4)
+    ip, ix, dv = dense_to_csr(A)
+    bs = [5] * 30
+    from paper_1908_10169_b200 import BILU
+    g = BILU(ip, ix, dv, bs)
+    g.factor(1e-2)
+    dv2 = dv * np.random.default_rng(0).uniform(0.9, 1.1, len(dv))
+    g.set_values(dv2)
+    g.factor(3e-3)
+    gf = g.export()
+    of = oracle.factor(ip, ix, dv2, bs, 3e-3, overrides=overrides_from_near(gf.near))
+    assert_parity(gf, of)
+
+
+def test_apply_matches_oracle_apply():
+    import torch
+    A = random_dd(200, 0.05, 5)
+    ip, ix, dv = dense_to_csr(A)
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(200)
+    g, st, gf, of = run_pair(ip, ix, dv, [4] * 50, 1e-2, perm=perm)
+    x = rng.standard_normal(200)
+    y = g.apply_tensor(torch.tensor(x, device="cuda")).cpu().numpy()
+    yo_p = oracle.apply(of, x[perm])
+    yo = np.empty(200); yo[perm] = yo_p
+    np.testing.assert_allclose(y, yo, rtol=1e-11, atol=1e-13 * np.abs(yo).max())
+    # and it inverts L P U in the original ordering
+    L, P, U = dense_LPU(of, 200)
+    M = np.zeros((200, 200)); M[np.ix_(perm, perm)] = L @ P @ U
+    np.testing.assert_allclose(M @ y, x, atol=1e-10 * np.abs(x).max())
+
+
+def _gmres_counts(prob, g, of):
+    import torch
+    A = sp.csr_matrix((prob.data, prob.indices, prob.indptr), shape=(prob.n, prob.n))
+    perm = prob.perm
+    b = np.ones(prob.n)
+
+    def m_gpu(v):
+        return g.apply_tensor(torch.tensor(v, device="cuda")).cpu().numpy()
+
+    def m_orc(v):
+        y = oracle.apply(of, v[perm])
+        out = np.empty_like(y); out[perm] = y
+        return out
+    _, it_g, ok_g, _ = gmres(A.dot, b, precond=m_gpu, restart=30, tol=1e-8)
+    _, it_o, ok_o, _ = gmres(A.dot, b, precond=m_orc, restart=30, tol=1e-8)
+    return it_g, ok_g, it_o, ok_o
+
+
+def test_c1_full_parity_and_gmres():
+    P = config1()
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert_parity(gf, of)
+    it_g, ok_g, it_o, ok_o = _gmres_counts(P, g, of)
+    assert ok_g and ok_o and abs(it_g - it_o) <= 1
+
+
+def test_c2_reduced_parity():
+    P = config2(N=24, leaf=128)
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert_parity(gf, of)
+
+
+def test_c2_full_parity_and_gmres():
+    """BASELINE configs[1] at full size, in the bench.py launch configuration."""
+    P = config2()
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert st["n_blocks_init"] == 33111
+    assert_parity(gf, of)
+    assert st["n_merges"] == of.n_merges
+    it_g, ok_g, it_o, ok_o = _gmres_counts(P, g, of)
+    assert ok_g and ok_o and abs(it_g - it_o) <= 1
+
+
+def test_c3_reduced_parity_nodal_blocks():
+    P = config3(N=10)
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert_parity(gf, of)
+
+
+def test_small_max_block_merges():
+    A = random_dd(400, 0.02, 6, dominance=1.3)
+    ip, ix, dv = dense_to_csr(A)
+    g, st, gf, of = run_pair(ip, ix, dv, [2] * 200, 1e-3, True, max_block=16)
+    assert_parity(gf, of)
+    assert np.diff(gf.bstart).max() <= 16

@@ -1,0 +1,312 @@
+"""Pins of the CPU oracle to things other than itself (run without a GPU).
+
+Each test names what fixes the expected value: a worked example of the paper /
+SPEC, a closed form, a library routine, a mathematical identity, or a literal
+transcription of Alg. 1 on tiny inputs.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import oracle
+from inputs.configs import dense_to_csr, random_dd
+from tests.parity import dense_LPU
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def fac(A, bs, tau, agg=False, max_block=128):
+    ip, ix, dv = dense_to_csr(A)
+    return oracle.factor(ip, ix, dv, bs, tau, aggregate=agg, max_block=max_block)
+
+
+def random_partition(n, rng, maxb=8):
+    out = []
+    while sum(out) < n:
+        out.append(int(min(rng.integers(1, maxb + 1), n - sum(out))))
+    return out
+
+
+# ------------------------------------------------------------ worked examples
+def test_spec_2x2_worked_example():
+    """[[2,1],[1,2]], tau=0 -> L=[[1,0],[.5,1]], pivots diag(2,1.5), U=[[1,.5],[0,1]]."""
+    g = json.load(open(os.path.join(GOLD, "spec_2x2.json")))
+    A = np.array(g["A"])
+    f = fac(A, g["block_sizes"], g["tau"])
+    L, P, U = dense_LPU(f, 2)
+    np.testing.assert_allclose(L, g["L"], atol=1e-15)
+    np.testing.assert_allclose(P, g["pivots"], atol=1e-15)
+    np.testing.assert_allclose(U, g["U"], atol=1e-15)
+    # D stores the inverted pivots
+    np.testing.assert_allclose(f.block(1)[6], [[1 / 1.5]], atol=1e-15)
+
+
+def test_spec_forced_merge_gives_inverse():
+    """merging the two scalar blocks of [[2,1],[1,2]] gives one 2x2 block, D = A^{-1}."""
+    A = np.array([[2.0, 1.0], [1.0, 2.0]])
+    f = fac(A, [1, 1], 0.0, agg=True)
+    assert f.nblk == 1 and f.n_merges == 1
+    np.testing.assert_allclose(f.block(0)[6], np.linalg.inv(A), atol=1e-15)
+
+
+def test_aggregate_test_worked_examples():
+    g = json.load(open(os.path.join(GOLD, "aggregate_test.json")))
+    for c in g["cases"]:
+        p, q, r, s, t, r2, s2, t2, u, v = c["args"]
+        mu = p * (p + r + s + r2 + s2) + q * (q + t + t2)
+        nu = (p + q) * (p + q + u + v)
+        assert (mu, nu) == (c["mu"], c["nu"])
+        assert oracle.aggregate_test(*c["args"]) == c["merge"]
+    # max_block caps the merge (R9)
+    assert oracle.aggregate_test(1, 1, 0, 0, 0, 0, 0, 0, 0, 0, max_block=2)
+    assert not oracle.aggregate_test(1, 1, 0, 0, 0, 0, 0, 0, 0, 0, max_block=1)
+
+
+def test_identity_chain_merges_to_one_block():
+    """SPEC.md:396 / PAPER.md:1436-1440: decoupled scalars merge step by step into one block."""
+    f = fac(np.eye(4), [1, 1, 1, 1], 1e-2, agg=True)
+    assert f.nblk == 1 and f.n_merges == 3
+    np.testing.assert_allclose(f.block(0)[6], np.eye(4), atol=0)
+
+
+# ------------------------------------------------------------ closed forms
+@pytest.mark.parametrize("seed", range(6))
+def test_tau0_is_exact_block_LDU(seed):
+    """tau = 0 keeps every nonzero row: L P U = A to rounding (BASELINE north_star)."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(10, 80))
+    A = random_dd(n, 0.15, seed)
+    bs = random_partition(n, rng)
+    f = fac(A, bs, 0.0)
+    L, P, U = dense_LPU(f, n)
+    assert np.abs(L @ P @ U - A).max() <= 1e-12 * np.abs(A).max()
+
+
+def test_tau0_matches_scipy_lu_without_pivoting():
+    """Library routine: a column-diagonally-dominant matrix needs no row swaps in
+    LAPACK getrf, so A = L_s U_s with L_s unit lower; the scalar BILU at tau=0 gives
+    the same L, pivots diag(U_s) and unit U = diag(U_s)^{-1} U_s."""
+    A = random_dd(30, 0.3, 7).T.copy()            # column dominant
+    Pm, Ls, Us = sla.lu(A)
+    assert np.array_equal(Pm, np.eye(30))
+    f = fac(A, [1] * 30, 0.0)
+    L, P, U = dense_LPU(f, 30)
+    np.testing.assert_allclose(L, Ls, atol=1e-13)
+    np.testing.assert_allclose(np.diag(P), np.diag(Us), rtol=1e-13)
+    np.testing.assert_allclose(U, np.diag(1 / np.diag(Us)) @ Us, atol=1e-13)
+
+
+def test_tridiagonal_thomas_closed_form():
+    """No fill on a tridiagonal matrix: p_1 = a_11, p_i = a_ii - a_{i,i-1} a_{i-1,i} / p_{i-1},
+    l_{i,i-1} = a_{i,i-1}/p_{i-1}, Ũ_{i-1,i} = a_{i-1,i} (ILU(0)-pattern results are exact)."""
+    rng = np.random.default_rng(3)
+    n = 50
+    sub, sup = rng.uniform(-1, 1, n - 1), rng.uniform(-1, 1, n - 1)
+    dia = 3.0 + rng.uniform(0, 1, n)
+    A = np.diag(dia) + np.diag(sub, -1) + np.diag(sup, 1)
+    f = fac(A, [1] * n, 1e-6)
+    p = np.zeros(n)
+    p[0] = dia[0]
+    for i in range(1, n):
+        p[i] = dia[i] - sub[i - 1] * sup[i - 1] / p[i - 1]
+    for K in range(n):
+        s, e, rows, L, cols, Ut, D = f.block(K)
+        np.testing.assert_allclose(D, [[1 / p[K]]], rtol=1e-14)
+        if K < n - 1:
+            assert list(rows) == [K + 1] and list(cols) == [K + 1]
+            np.testing.assert_allclose(L[0, 0], sub[K] / p[K], rtol=1e-14)
+            np.testing.assert_allclose(Ut[0, 0], sup[K], rtol=1e-14)
+
+
+def test_block_tridiagonal_aligned_partition_is_exact():
+    """Block Thomas: P_1 = A_11, P_i = A_ii - A_{i,i-1} P_{i-1}^{-1} A_{i-1,i}; fill stays
+    inside the dense diagonal blocks, so BILU with tau=0 reproduces it."""
+    rng = np.random.default_rng(5)
+    bs = [3, 5, 2, 4, 6]
+    st = np.concatenate([[0], np.cumsum(bs)])
+    n = st[-1]
+    A = np.zeros((n, n))
+    for i in range(len(bs)):
+        A[st[i]:st[i + 1], st[i]:st[i + 1]] = rng.standard_normal((bs[i], bs[i])) + 8 * np.eye(bs[i])
+        if i:
+            A[st[i]:st[i + 1], st[i - 1]:st[i]] = rng.standard_normal((bs[i], bs[i - 1]))
+            A[st[i - 1]:st[i], st[i]:st[i + 1]] = rng.standard_normal((bs[i - 1], bs[i]))
+    f = fac(A, bs, 0.0)
+    Pprev = None
+    for i in range(len(bs)):
+        Aii = A[st[i]:st[i + 1], st[i]:st[i + 1]]
+        if i == 0:
+            Pi = Aii
+        else:
+            Pi = Aii - A[st[i]:st[i + 1], st[i - 1]:st[i]] @ np.linalg.solve(Pprev, A[st[i - 1]:st[i], st[i]:st[i + 1]])
+        np.testing.assert_allclose(np.linalg.inv(f.block(i)[6]), Pi, rtol=1e-12, atol=1e-12)
+        Pprev = Pi
+
+
+def test_tau_infinite_is_block_jacobi():
+    """tau = 1e300 drops every off-diagonal row/col: L = U = I, D_K = Ã_KK^{-1}."""
+    A = random_dd(40, 0.2, 11)
+    bs = [3, 5, 2, 4, 6, 1, 3, 8, 4, 4]
+    f = fac(A, bs, 1e300)
+    st = np.concatenate([[0], np.cumsum(bs)])
+    assert len(f.Li) == 0 and len(f.Ui) == 0
+    for K in range(len(bs)):
+        np.testing.assert_allclose(f.block(K)[6], np.linalg.inv(A[st[K]:st[K + 1], st[K]:st[K + 1]]),
+                                   rtol=1e-12, atol=1e-14)
+
+
+def test_single_block_is_the_inverse():
+    A = random_dd(17, 0.5, 2)
+    f = fac(A, [17], 0.3)
+    np.testing.assert_allclose(f.block(0)[6], np.linalg.inv(A), rtol=1e-12, atol=1e-14)
+
+
+# ------------------------------------------------------- residual characterisation
+def residual_check(A, f, tau, slack=1e-12):
+    """R = A - L P U vanishes on every kept position and on the diagonal blocks; a
+    dropped L row / U column equals the unscaled dropped entries and its scaled form
+    is <= tau; a kept one is > tau.  These equations
+    determine the factors uniquely, given the partition."""
+    n = A.shape[0]
+    L, P, U = dense_LPU(f, n)
+    R = A - L @ P @ U
+    scale = np.abs(A).max()
+    for K in range(f.nblk):
+        s, e, rows, Lp, cols, Ut, D = f.block(K)
+        assert np.abs(R[s:e, s:e]).max() <= slack * scale
+        kept = set(int(r) for r in rows)
+        for i in range(e, n):
+            Ri = R[i, s:e]
+            if i in kept:
+                assert np.abs(Ri).max() <= slack * scale
+                assert np.abs(L[i, s:e]).max() > tau
+            else:
+                assert np.abs(Ri @ D).max() <= tau * (1 + 1e-10) + slack
+        keptc = set(int(c) for c in cols)
+        for j in range(e, n):
+            Rj = R[s:e, j]
+            if j in keptc:
+                assert np.abs(Rj).max() <= slack * scale
+                assert np.abs(D @ Ut[:, list(cols).index(j)]).max() > tau
+            else:
+                assert np.abs(D @ Rj).max() <= tau * (1 + 1e-10) + slack
+
+
+@pytest.mark.parametrize("seed,tau", [(0, 1e-3), (1, 1e-2), (2, 5e-2), (3, 0.3), (4, 0.0)])
+def test_residual_characterisation(seed, tau):
+    rng = np.random.default_rng(100 + seed)
+    n = 60
+    A = random_dd(n, 0.12, 100 + seed, dominance=1.3)
+    bs = random_partition(n, rng)
+    f = fac(A, bs, tau)
+    residual_check(A, f, tau)
+
+
+def test_residual_characterisation_scalar_tridiag_plus_fill():
+    A = random_dd(45, 0.08, 42, dominance=1.1)
+    f = fac(A, [1] * 45, 2e-2)
+    residual_check(A, f, 2e-2)
+
+
+# ------------------------------------------------------------ aggregation identity
+@pytest.mark.parametrize("seed,tau", [(0, 1e-3), (1, 1e-2), (2, 0.0)])
+def test_merge_leaves_operator_unchanged(seed, tau):
+    """merging k-1 and k rewrites L D^{-1} U without changing it,
+    so L P U with aggregation equals L P U without (and the merged diagonal blocks are
+    the inverses of the merged pivots)."""
+    rng = np.random.default_rng(200 + seed)
+    n = 70
+    A = random_dd(n, 0.1, 200 + seed)
+    bs = random_partition(n, rng, maxb=4)
+    f0 = fac(A, bs, tau, agg=False)
+    f1 = fac(A, bs, tau, agg=True)
+    assert f1.n_merges > 0
+    L0, P0, U0 = dense_LPU(f0, n)
+    L1, P1, U1 = dense_LPU(f1, n)
+    assert np.abs(L0 @ P0 @ U0 - L1 @ P1 @ U1).max() <= 1e-12 * np.abs(A).max()
+    # unit triangularity of the merged factors
+    for K in range(f1.nblk):
+        s, e, rows, Lp, cols, Ut, D = f1.block(K)
+        assert np.all(np.asarray(rows) >= e) and np.all(np.asarray(cols) >= e)
+
+
+def test_merge_sizes_respect_max_block():
+    A = random_dd(120, 0.3, 9)
+    f = fac(A, [4] * 30, 1e-3, agg=True, max_block=16)
+    assert np.diff(f.bstart).max() <= 16
+
+
+# ------------------------------------------------------------ Alg. 1 transcription
+def crout_ilu_alg1(A, tau):
+    """Literal transcription of Alg. 1, dense loops, n <= 60.
+    Returns L (unit lower, scaled) and U (upper, unscaled incl. the diagonal)."""
+    n = A.shape[0]
+    L = np.zeros((n, n))
+    U = np.zeros((n, n))
+    for k in range(n):
+        l = A[:, k].copy()                      # l_ik <- a_ik, i >= k
+        l[:k] = 0.0
+        for j in range(k):
+            if U[j, k] != 0.0:
+                for i in range(k, n):
+                    if L[i, j] != 0.0:
+                        l[i] -= L[i, j] * U[j, k]
+        u = A[k, :].copy()                      # u_ki <- a_ki, i >= k
+        u[:k] = 0.0
+        for j in range(k):
+            if L[k, j] != 0.0:
+                for i in range(k, n):
+                    if U[j, i] != 0.0:
+                        u[i] -= L[k, j] * U[j, i]
+        lkk = l[k]
+        for i in range(k + 1, n):               # drop |l_ik| <= tau |l_kk|, then scale
+            if abs(l[i]) <= tau * abs(lkk):
+                l[i] = 0.0
+        L[k:, k] = l[k:] / lkk
+        for i in range(k + 1, n):               # drop |u_ki| <= tau |u_kk|
+            if abs(u[i]) <= tau * abs(u[k]):
+                u[i] = 0.0
+        U[k, k:] = u[k:]
+    return L, U
+
+
+@pytest.mark.parametrize("seed,tau", [(0, 1e-2), (1, 5e-2), (2, 1e-3)])
+def test_scalar_partition_is_alg1(seed, tau):
+    """BILU(---) reduces to the scalar Crout ILU."""
+    A = random_dd(40, 0.12, 300 + seed, dominance=1.2)
+    Lr, Ur = crout_ilu_alg1(A, tau)
+    f = fac(A, [1] * 40, tau)
+    L, P, U = dense_LPU(f, 40)
+    np.testing.assert_allclose(L, Lr, atol=1e-12)
+    np.testing.assert_allclose(P @ U, Ur, atol=1e-12)
+
+
+# ------------------------------------------------------------ apply
+def test_apply_solves_LPU():
+    A = random_dd(50, 0.1, 77)
+    bs = [5] * 10
+    for agg in (False, True):
+        f = fac(A, bs, 1e-2, agg=agg)
+        L, P, U = dense_LPU(f, 50)
+        x = np.random.default_rng(1).standard_normal(50)
+        y = oracle.apply(f, x)
+        np.testing.assert_allclose(L @ P @ U @ y, x, atol=1e-12 * np.abs(x).max())
+
+
+def test_breakdown_is_reported():
+    A = np.array([[1.0, 1.0, 0.0], [1.0, 1.0, 0.0], [0.0, 0.0, 1.0]])
+    with pytest.raises(oracle.OracleError, match="breakdown in block 0"):
+        fac(A, [2, 1], 0.0)
+
+
+def test_decision_override_replays():
+    """Decision replay (SURVEY.md 8(c) reading 15): a forced keep of a dropped row."""
+    A = np.array([[2.0, 0.0], [0.02, 1.0]])
+    f = fac(A, [1, 1], 0.01)                     # l = 0.01 == tau -> dropped (ties drop, R2)
+    assert len(f.Li) == 0 and f.n_near == 1 and f.min_margin == 0.0
+    ip, ix, dv = dense_to_csr(A)
+    g = oracle.factor(ip, ix, dv, [1, 1], 0.01, aggregate=False, overrides=[(0, 0, 1, 1)])
+    assert list(g.Li) == [1]
