@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbilu.so")
+LIB_PATH = os.environ.get("BILU_LIB", os.path.join(_HERE, "libbilu.so"))
 
 STATUS = {0: "BILU_OK", 1: "BILU_ERR_ARG", 2: "BILU_ERR_BREAKDOWN", 3: "BILU_ERR_OOM",
           4: "BILU_ERR_CUDA", 5: "BILU_ERR_NCCL", 6: "BILU_ERR_STATE", 7: "BILU_ERR_NOT_BUILT"}

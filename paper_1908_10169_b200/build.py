@@ -10,6 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbilu.so")
+LIB_PROF = os.path.join(HERE, "libbilu_prof.so")   # diagnostic build with per-phase clock64 counters
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["bilu_factor.cu", "bilu_merge.cu", "bilu_apply.cu", "bilu_util.cu"]
@@ -22,10 +23,11 @@ def _newest_source() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_source():
-        return LIB
-    objdir = os.path.join(HERE, "build")
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    lib = LIB_PROF if profile else LIB
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= _newest_source():
+        return lib
+    objdir = os.path.join(HERE, "build_prof" if profile else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for f in CU_SOURCES:
@@ -34,6 +36,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, f), "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
+        if profile:
+            cmd.insert(1, "-DBILU_PROFILE")
         subprocess.check_call(cmd)
         objs.append(o)
     for f in CPP_SOURCES:
@@ -41,11 +45,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.check_call(["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-I/usr/local/cuda/include",
                                "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, f), "-o", o])
         objs.append(o)
-    tmp = LIB + ".tmp%d" % os.getpid()
+    tmp = lib + ".tmp%d" % os.getpid()
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv))

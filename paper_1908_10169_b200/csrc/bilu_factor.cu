@@ -28,8 +28,38 @@
 
 namespace bilu {
 
-constexpr int NT = 256;
+#ifndef BILU_NT
+#define BILU_NT 512
+#endif
+constexpr int NT = BILU_NT;
 constexpr int NW = NT / 32;
+
+// progress markers for the host-side deadlock watchdog (BILU_DEBUG_TIMEOUT)
+#define DBGP(i) do { if (threadIdx.x == 0 && F.dbg) { F.dbg[4 * blockIdx.x + 1] = (i); } } while (0)
+#define DBGK(k) do { if (threadIdx.x == 0 && F.dbg) { F.dbg[4 * blockIdx.x] = (k); F.dbg[4 * blockIdx.x + 1] = 0; \
+  F.dbg[4 * blockIdx.x + 2]++; } } while (0)
+#ifdef BILU_PROFILE
+__device__ unsigned long long g_prof[32];
+__device__ unsigned long long *g_blkprof;   // [N * 16]: t0, t1 (globaltimer ns), phase cycles, sizes
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
+}
+#define PROF_T0 long long _pt = clock64(); if (threadIdx.x == 0 && g_blkprof) g_blkprof[32 * (size_t)K] = gtimer();
+#define PROF(i) do { DBGP(i); if (threadIdx.x == 0) { long long _n = clock64(); atomicAdd(&g_prof[i], (unsigned long long)(_n - _pt)); \
+  if (g_blkprof) g_blkprof[32 * (size_t)K + 1 + (i)] = (unsigned long long)(_n - _pt); _pt = _n; } } while (0)
+#define SUBP(i) do { if (threadIdx.x == 0 && g_blkprof) { long long _n2 = clock64(); \
+  g_blkprof[32 * (size_t)K + 16 + (i)] += (unsigned long long)(_n2 - _sp); _sp = _n2; } } while (0)
+#define SUBP_T0 long long _sp = clock64();
+#define PROF_END(a, b_, c, d) do { if (threadIdx.x == 0 && g_blkprof) { g_blkprof[32 * (size_t)K + 10] = gtimer(); \
+  g_blkprof[32 * (size_t)K + 11] = (a); g_blkprof[32 * (size_t)K + 12] = (b_); g_blkprof[32 * (size_t)K + 13] = (c); \
+  g_blkprof[32 * (size_t)K + 14] = (d); g_blkprof[32 * (size_t)K + 15] = blockIdx.x; } } while (0)
+#else
+#define PROF_END(a, b_, c, d) do {} while (0)
+#define SUBP(i) do {} while (0)
+#define SUBP_T0
+#define PROF_T0
+#define PROF(i) DBGP(i)
+#endif
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ int ld_vol(const int *p) { return *(const volatile int *)p; }
@@ -39,10 +69,10 @@ __device__ __forceinline__ unsigned long long ld_vol64(const unsigned long long 
 __device__ __forceinline__ void st_vol(int *p, int v) { *(volatile int *)p = v; }
 
 __device__ __forceinline__ void raise_abort(const DevFactor &F, int code, int blk) {
-  if (atomicCAS(&F.ctrl[CTRL_ABORT], 0ull, (unsigned long long)code) == 0ull)
-    atomicExch(&F.ctrl[CTRL_ERRBLK], (unsigned long long)blk);
+  if (atomicCAS(&F.ctrl[CS * CTRL_ABORT], 0ull, (unsigned long long)code) == 0ull)
+    atomicExch(&F.ctrl[CS * CTRL_ERRBLK], (unsigned long long)blk);
 }
-__device__ __forceinline__ bool aborted(const DevFactor &F) { return ld_vol64(&F.ctrl[CTRL_ABORT]) != 0ull; }
+__device__ __forceinline__ bool aborted(const DevFactor &F) { return ld_vol64(&F.ctrl[CS * CTRL_ABORT]) != 0ull; }
 
 // first position p in a[lo, hi) with a[p] >= key
 __device__ __forceinline__ int lbound(const int *a, int lo, int hi, int key) {
@@ -146,7 +176,7 @@ __device__ bool list_append(const DevFactor &F, const ChunkList &L, int T, const
   int *dptr = &L.dir[(size_t)T * DIR_SLOTS + slot];
   int id;
   if (idx % CHUNK == 0) {
-    unsigned long long c = atomicAdd(&F.ctrl[L.ctrl_cursor], 1ull);
+    unsigned long long c = atomicAdd(&F.ctrl[CS * L.ctrl_cursor], 1ull);
     if (c >= (unsigned long long)L.pool_cap) {
       atomicExch(dptr, -2);
       raise_abort(F, DEV_OVF_POOL, T);
@@ -169,19 +199,19 @@ __device__ bool list_append(const DevFactor &F, const ChunkList &L, int T, const
 
 // ------------------------------------------------------ per-block allocator
 struct Bump {
-  unsigned char *sbase; int sused, scap;
-  double *gbase; int64_t gused, gcap;
+  unsigned char *sbase; int sused, stop, scap;     // shared: bottom (persistent) / top (scratch)
+  double *gbase; int64_t gused, gtop, gcap;        // global spill region, same scheme (doubles)
   bool ovf;
 };
 __device__ __forceinline__ void *balloc(Bump &A, int64_t bytes) {
   bytes = (bytes + 15) & ~int64_t(15);
-  if (A.sused + bytes <= A.scap) {
+  if (A.sused + bytes <= A.stop) {
     void *p = A.sbase + A.sused;
     A.sused += (int)bytes;
     return p;
   }
   int64_t d = bytes / 8;
-  if (A.gused + d <= A.gcap) {
+  if (A.gused + d <= A.gtop) {
     void *p = A.gbase + A.gused;
     A.gused += d;
     return p;
@@ -189,343 +219,573 @@ __device__ __forceinline__ void *balloc(Bump &A, int64_t bytes) {
   A.ovf = true;
   return A.gbase;  // caller checks ovf
 }
+__device__ __forceinline__ void *balloc_top(Bump &A, int64_t bytes) {
+  bytes = (bytes + 15) & ~int64_t(15);
+  if (A.stop - bytes >= A.sused) {
+    A.stop -= (int)bytes;
+    return A.sbase + A.stop;
+  }
+  int64_t d = bytes / 8;
+  if (A.gtop - d >= A.gused) {
+    A.gtop -= d;
+    return A.gbase + A.gtop;
+  }
+  A.ovf = true;
+  return A.gbase;
+}
 
 // --------------------------------------------------------------- the kernel
 struct Shared {
   int K;
-  int misc[8];
   int tmp[NW + 1];
   int piv;
   double pivd;
+  int cnt[4];
   unsigned long long off[4];
 };
 
-__device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned char *smem) {
+// per-contributor descriptor kept in shared memory while block K is processed
+struct Contrib {
+  int J, bJ;
+  int n_items;        // L side: rows >= s_K of L_J; U side: cols >= e_K of Ũ_J
+  int n_cand_skip;    // L side: rows of the suffix that lie inside K (not candidates)
+  int ncol;           // L side: Ũ_J columns inside K;  U side: L_J rows inside K
+  int item_off;       // prefix over n_items
+  int64_t rows;       // L side: Lidx offset of the first row >= s_K; U side: of row r0
+  int64_t lval;       // matching Lval offset
+  int64_t cols;       // L side: Uidx offset of column c0;  U side: of the first col >= e_K
+  int64_t uval;       // matching Uval offset
+};
+
+// ---- open-addressing hash set of row (or column) indices -> dense buffer slot
+__device__ __forceinline__ unsigned hslot(int key, unsigned mask) {
+  return ((unsigned)key * 0x9E3779B1u) >> 7 & mask;
+}
+__device__ __forceinline__ void hinsert(int *keys, unsigned mask, int key) {
+  unsigned h = hslot(key, mask);
+  while (true) {
+    int old = atomicCAS(&keys[h], -1, key);
+    if (old == -1 || old == key) return;
+    h = (h + 1) & mask;
+  }
+}
+__device__ __forceinline__ int hlookup(const int *keys, const int *vals, unsigned mask, int key) {
+  unsigned h = hslot(key, mask);
+  while (keys[h] != key) h = (h + 1) & mask;
+  return vals[h];
+}
+
+// rank sort of distinct keys: out[rank(x)] = x (n small; thread per element)
+__device__ void cta_rank_sort(const int *keys, int n, int *out) {
+  for (int x = threadIdx.x; x < n; x += NT) {
+    const int k = keys[x];
+    int r = 0;
+    for (int y = 0; y < n; ++y) r += keys[y] < k;
+    out[r] = x;
+  }
+  __syncthreads();
+}
+
+// Load the contributor list of one side into shared descriptors, sorted by J.
+// side 0 (Lc: J has Ũ columns in K): items = rows of L_J >= s_K
+// side 1 (Uc: J has L rows in K):    items = cols of Ũ_J >= e_K
+__device__ int load_contribs(const DevFactor &F, const ChunkList &L, int K, int side, Contrib *C, int *ord,
+                             int *tmp_keys, Shared &S) {
+  const int tid = threadIdx.x;
+  const int nc = __ldcg(&L.cnt[K]);
+  for (int x = tid; x < nc; x += NT) {
+    const int *r = list_rec(L, K, x);
+    const int J = __ldcg(r);
+    tmp_keys[x] = J;
+    Contrib c;
+    c.J = J;
+    const int sJ = F.bstart[J];
+    c.bJ = F.bstart[J + 1] - sJ;
+    const int64_t lro = __ldcg(&F.Lrow_off[J]), lvo = __ldcg(&F.Lval_off[J]);
+    const int64_t uco = __ldcg(&F.Ucol_off[J]), uvo = __ldcg(&F.Uval_off[J]);
+    if (side == 0) {
+      const int c0 = __ldcg(r + 1), c1 = __ldcg(r + 2), lrs = __ldcg(r + 3), lre = __ldcg(r + 4);
+      const int mJ = __ldcg(&F.Lm[J]);
+      c.n_items = mJ - lrs;
+      c.n_cand_skip = lre - lrs;
+      c.ncol = c1 - c0;
+      c.rows = lro + lrs;
+      c.lval = lvo + (int64_t)lrs * c.bJ;
+      c.cols = uco + c0;
+      c.uval = uvo + (int64_t)c0 * c.bJ;
+    } else {
+      const int r0 = __ldcg(r + 1), r1 = __ldcg(r + 2), cus = __ldcg(r + 3);
+      const int cJ = __ldcg(&F.Uc[J]);
+      c.n_items = cJ - cus;
+      c.n_cand_skip = 0;
+      c.ncol = r1 - r0;
+      c.rows = lro + r0;
+      c.lval = lvo + (int64_t)r0 * c.bJ;
+      c.cols = uco + cus;
+      c.uval = uvo + (int64_t)cus * c.bJ;
+    }
+    C[nc + x] = c;  // staging copy (second half), permuted below
+  }
+  __syncthreads();
+  // ascending J (R13): rank sort (J distinct within one list)
+  for (int x = tid; x < nc; x += NT) {
+    const int k = tmp_keys[x];
+    int rk = 0;
+    for (int y = 0; y < nc; ++y) rk += tmp_keys[y] < k;
+    C[rk] = C[nc + x];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int x = 0; x < nc; ++x) { C[x].item_off = acc; acc += C[x].n_items; }
+    S.cnt[side] = acc;
+  }
+  __syncthreads();
+  (void)ord;
+  return nc;
+}
+
+__device__ __forceinline__ int contrib_of(const Contrib *C, int nc, int t) {
+  int lo = 0, hi = nc - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (C[mid].item_off <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+
+// ------------------------------------------------ bulk async copies (TMA engine)
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ bool is_smem(const void *p) { return __isShared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// key -> buffer line of the candidate set of one side.  Two representations:
+//  * bitmap (range of keys [e, e + 32*words) small enough for shared memory): bit per
+//    key, per-word prefix counts; lines are in ascending key order
+//  * pos map (fallback for wide ranges): per-CTA global array, last writer wins
+struct LineMap {
+  const unsigned *bm; const int *pre; int words;   // bitmap path
+  const int *pos;                                   // pos-map path (bm == nullptr)
+  int e, base;
+  __device__ __forceinline__ int operator()(int key) const {
+    if (bm) {
+      const int r = key - e, w = r >> 5;
+      return base + pre[w] + __popc(bm[w] & ((1u << (r & 31)) - 1u));
+    }
+    return pos[key];
+  }
+};
+
+// One side of block K (SIDE 0: block column of L incl. the pivot block; SIDE 1:
+// block row of U):
+//   a-3  candidate set: keys >= e_K of Ã's block column (resp. row) and of every
+//        contributor's kept L rows (resp. Ũ columns)
+//   a-4  dense buffer W (SIDE 0: (b + nR) x b row-major, rows 0..b-1 = the pivot
+//        block; SIDE 1: nC columns of b), Ã's entries scattered in ("load the
+//        associated scalar sparse columns of A into block column buffer")
+//   a-5  W -= L_J Ũ_J for every contributor J in ascending J (R13) -- "gather ... GEMM
+//        ... scatter": one thread per item (a row of L_J >= s_K,
+//        resp. a column of Ũ_J >= e_K), the next contributor's operands prefetched
+//        into registers while the current one is applied.
+template <int SIDE>
+__device__ bool side_update(const DevFactor &F, int K, int s, int e, int b, Contrib *C, int nc, int T,
+                            int64_t a0, int64_t ae, int64_t a1, Bump &A, Shared &S, double **Wout,
+                            int **lineOf_out, int *n_out, double &flops) {
+  const int tid = threadIdx.x;
+  const int32_t *arc = SIDE == 0 ? F.AL_rc : F.AU_rc;
+  const double *aval = SIDE == 0 ? F.AL_val : F.AU_val;
+  const int32_t *cidx = SIDE == 0 ? F.Lidx : F.Uidx;     // index list of the item side
+  const int nA = (int)(a1 - ae);                           // Ã entries that are candidates
+  SUBP_T0
+  // -- range of candidate keys: max over Ã's keys and every contributor's last key
+  if (tid == 0) S.cnt[2] = e - 1;
+  __syncthreads();
+  {
+    int mx = e - 1;
+    for (int64_t p = ae + tid; p < a1; p += NT) mx = max(mx, arc[p] >> 7);
+    for (int a = tid; a < nc; a += NT)
+      if (C[a].n_items > C[a].n_cand_skip) mx = max(mx, cidx[(SIDE == 0 ? C[a].rows : C[a].cols) + C[a].n_items - 1]);
+    atomicMax(&S.cnt[2], mx);
+  }
+  __syncthreads();
+  const int hi = S.cnt[2];
+  const int words = (hi - e + 1 + 31) >> 5;
+  const int base = SIDE == 0 ? b : 0;            // buffer line of the first candidate
+  LineMap M;
+  M.e = e; M.base = base; M.bm = nullptr; M.pre = nullptr; M.words = words;
+  M.pos = F.posmap + (size_t)blockIdx.x * F.n;
+  int nU = 0;
+  unsigned *bm = nullptr;
+  int *pre = nullptr;
+  if (words <= 8192) {
+    // ---- bitmap path: dedup by atomicOr in shared memory, sorted for free
+    bm = (unsigned *)balloc_top(A, (int64_t)(words + 1) * 4);
+    pre = (int *)balloc_top(A, (int64_t)(words + 1) * 4);
+    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
+    for (int w = tid; w < words; w += NT) bm[w] = 0u;
+    __syncthreads();
+    for (int64_t p = ae + tid; p < a1; p += NT) {
+      const int r = (arc[p] >> 7) - e;
+      atomicOr(&bm[r >> 5], 1u << (r & 31));
+    }
+    {
+      int a = 0;
+      for (int t = tid; t < T; t += NT) {
+        while (a + 1 < nc && C[a + 1].item_off <= t) ++a;
+        const int i = t - C[a].item_off;
+        if (i < C[a].n_cand_skip) continue;                // rows inside K (pivot block)
+        const int r = cidx[(SIDE == 0 ? C[a].rows : C[a].cols) + i] - e;
+        atomicOr(&bm[r >> 5], 1u << (r & 31));
+      }
+    }
+    __syncthreads();
+    for (int w = tid; w < words; w += NT) pre[w] = __popc(bm[w]);
+    __syncthreads();
+    nU = cta_scan(pre, words, S.tmp);
+    M.bm = bm; M.pre = pre;
+  } else {
+    // ---- pos-map path: every occurrence writes its id, the surviving writer appends
+    const int occ = nA + T;
+    int *pos = F.posmap + (size_t)blockIdx.x * F.n;
+    {
+      int a = 0;
+      for (int o = tid; o < occ; o += NT) {
+        int key;
+        if (o < nA) key = arc[ae + o] >> 7;
+        else {
+          const int t = o - nA;
+          while (a + 1 < nc && C[a + 1].item_off <= t) ++a;
+          const int i = t - C[a].item_off;
+          if (i < C[a].n_cand_skip) continue;
+          key = cidx[(SIDE == 0 ? C[a].rows : C[a].cols) + i];
+        }
+        pos[key] = o;
+      }
+    }
+    if (tid == 0) S.cnt[2] = 0;
+    __syncthreads();
+    int *uniq = (int *)balloc_top(A, (int64_t)(occ + 1) * 4);
+    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
+    {
+      int a = 0;
+      for (int o = tid; o < occ; o += NT) {
+        int key;
+        if (o < nA) key = arc[ae + o] >> 7;
+        else {
+          const int t = o - nA;
+          while (a + 1 < nc && C[a + 1].item_off <= t) ++a;
+          const int i = t - C[a].item_off;
+          if (i < C[a].n_cand_skip) continue;
+          key = cidx[(SIDE == 0 ? C[a].rows : C[a].cols) + i];
+        }
+        if (pos[key] == o) uniq[atomicAdd(&S.cnt[2], 1)] = key;
+      }
+    }
+    __syncthreads();
+    nU = S.cnt[2];
+    for (int x = tid; x < nU; x += NT) pos[uniq[x]] = base + x;
+    __syncthreads();
+    // keep uniq (it becomes lineOf below)
+    pre = uniq;
+  }
+  SUBP(8 * SIDE + 0);
+  const int nW = base + nU;
+  double *W = (double *)balloc(A, (int64_t)nW * b * 8);
+  int *lineOf = (int *)balloc(A, (int64_t)(nW + 1) * 4);
+  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
+  for (int x = tid; x < base; x += NT) lineOf[x] = s + x;
+  if (M.bm) {
+    for (int w = tid; w < words; w += NT) {
+      unsigned m = bm[w];
+      int at = base + pre[w];
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        lineOf[at++] = e + (w << 5) + bit;
+        m &= m - 1;
+      }
+    }
+  } else {
+    for (int x = tid; x < nU; x += NT) lineOf[base + x] = pre[x];
+  }
+  for (int x = tid; x < nW * b; x += NT) W[x] = 0.0;
+  __syncthreads();
+  // -- a-4: scatter Ã
+  for (int64_t p = a0 + tid; p < a1; p += NT) {
+    const int rc = arc[p], key = rc >> 7;
+    const int w = (SIDE == 0 && key < e) ? key - s : M(key);
+    W[(int64_t)w * b + (rc & 127)] = aval[p];
+  }
+  __syncthreads();
+  SUBP(8 * SIDE + 1);
+  // -- a-5: every (contributor, item) pair in parallel; contributions are added into
+  //    the shared buffer atomically, so their order is unspecified (exact in exact
+  //    arithmetic, R13; differences are rounding only)
+  {
+    int a = 0;
+#pragma unroll 2
+    for (int t = tid; t < T; t += NT) {
+      while (a + 1 < nc && C[a + 1].item_off <= t) ++a;
+      const Contrib &c = C[a];
+      const int i = t - c.item_off, bJ = c.bJ, ncol = c.ncol;
+      const int key = cidx[(SIDE == 0 ? c.rows : c.cols) + i];
+      const int ln = (SIDE == 0 && key < e) ? key - s : M(key);
+      const double *vi = (SIDE == 0 ? F.Lval + c.lval : F.Uval + c.uval) + (int64_t)i * bJ;
+      const double *sm = SIDE == 0 ? F.Uval + c.uval : F.Lval + c.lval;
+      const int32_t *sidx = SIDE == 0 ? F.Uidx + c.cols : F.Lidx + c.rows;
+      double *wl = W + (int64_t)ln * b;
+      if (bJ <= 16) {
+        double v[16];
+#pragma unroll
+        for (int t2 = 0; t2 < 16; ++t2) v[t2] = t2 < bJ ? vi[t2] : 0.0;
+        for (int q = 0; q < ncol; ++q) {
+          const double *u = sm + (int64_t)q * bJ;
+          double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+          for (int t2 = 0; t2 < 16; t2 += 2) {
+            if (t2 < bJ) acc0 = fma(v[t2], u[t2], acc0);
+            if (t2 + 1 < bJ) acc1 = fma(v[t2 + 1], u[t2 + 1], acc1);
+          }
+          atomicAdd(&wl[sidx[q] - s], -(acc0 + acc1));
+        }
+      } else {
+        for (int q = 0; q < ncol; ++q) {
+          const double *u = sm + (int64_t)q * bJ;
+          double acc = 0.0;
+          for (int t2 = 0; t2 < bJ; ++t2) acc = fma(vi[t2], u[t2], acc);
+          atomicAdd(&wl[sidx[q] - s], -acc);
+        }
+      }
+    }
+  }
+  for (int a = 0; a < nc; ++a) flops += 2.0 * C[a].bJ * (double)C[a].n_items * (double)C[a].ncol;
+  __syncthreads();
+  SUBP(8 * SIDE + 2);
+  A.stop = A.scap; A.gtop = A.gcap;                 // release the bitmap / scratch
+  __syncthreads();
+  *Wout = W;
+  *lineOf_out = lineOf;
+  *n_out = nU;
+  return true;
+}
+
+__device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned char *smem, uint64_t *mbar,
+                              unsigned &mphase) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
   Bump A;
-  A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes;
-  A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta;
+  A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes;
+  A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
   A.ovf = false;
   double flops = 0.0;
+  PROF_T0
+#define OVF_CHECK() do { if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; } } while (0)
 
   // ---------------- a-2: contributor lists (Lc: J with Ũ cols in K; Uc: J with L rows in K)
-  const int nLc = __ldcg(&F.lc.cnt[K]);
-  const int nUc = __ldcg(&F.uc.cnt[K]);
-  int *lrec = (int *)balloc(A, (int64_t)nLc * REC_INTS * 4);
-  int *urec = (int *)balloc(A, (int64_t)nUc * REC_INTS * 4);
-  int mL = 1; while (mL < nLc) mL <<= 1;
-  int mU = 1; while (mU < nUc) mU <<= 1;
-  int *lkey = (int *)balloc(A, (int64_t)mL * 4);
-  int *ukey = (int *)balloc(A, (int64_t)mU * 4);
-  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
-  for (int i = tid; i < nLc * REC_INTS; i += NT) {
-    const int *r = list_rec(F.lc, K, i / REC_INTS);
-    lrec[i] = __ldcg(r + (i % REC_INTS));
-  }
-  for (int i = tid; i < nUc * REC_INTS; i += NT) {
-    const int *r = list_rec(F.uc, K, i / REC_INTS);
-    urec[i] = __ldcg(r + (i % REC_INTS));
-  }
-  __syncthreads();
-  // deterministic ascending-J order (R13): key = J << 10 | record index
-  for (int i = tid; i < mL; i += NT) lkey[i] = i < nLc ? (lrec[i * REC_INTS] << 10) | i : INT_MAX;
-  for (int i = tid; i < mU; i += NT) ukey[i] = i < nUc ? (urec[i * REC_INTS] << 10) | i : INT_MAX;
-  __syncthreads();
-  if (mL > 1) cta_bitonic(lkey, mL);
-  if (mU > 1) cta_bitonic(ukey, mU);
+  const int nLc0 = __ldcg(&F.lc.cnt[K]), nUc0 = __ldcg(&F.uc.cnt[K]);
+  Contrib *CL = (Contrib *)balloc(A, (int64_t)2 * nLc0 * sizeof(Contrib));
+  Contrib *CU = (Contrib *)balloc(A, (int64_t)2 * nUc0 * sizeof(Contrib));
+  int *tkeys = (int *)balloc(A, (int64_t)(nLc0 > nUc0 ? nLc0 : nUc0) * 4);
+  OVF_CHECK();
+  const int nLc = load_contribs(F, F.lc, K, 0, CL, nullptr, tkeys, S);
+  const int nUc = load_contribs(F, F.uc, K, 1, CU, nullptr, tkeys, S);
+  const int TL = S.cnt[0], TU = S.cnt[1];
+  const int64_t aL0 = F.AL_ptr[K], aLe = F.AL_ge[K], aL1 = F.AL_ptr[K + 1];
+  const int64_t aU0 = F.AU_ptr[K], aU1 = F.AU_ptr[K + 1];
+  PROF(1);
 
-  // ---------------- a-3: candidate rows R_K (>= e) and columns C_K (>= e)
-  // item counts: b columns of Ã + nLc contributors (rows), b rows of Ã + nUc (cols)
-  int *rcnt = (int *)balloc(A, (int64_t)(b + nLc + 1) * 4);
-  int *ccnt = (int *)balloc(A, (int64_t)(b + nUc + 1) * 4);
-  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
-  for (int i = tid; i < b + nLc; i += NT) {
-    if (i < b) {
-      int c = s + i;
-      int64_t lo = F.cp[c], hi = F.cp[c + 1];
-      int64_t p = lo, q = hi;  // first entry with row >= e
-      while (p < q) { int64_t mid = (p + q) >> 1; if (F.cr[mid] < e) p = mid + 1; else q = mid; }
-      rcnt[i] = (int)(hi - p);
-    } else {
-      const int *r = lrec + (i - b) * REC_INTS;
-      int J = r[0];
-      rcnt[i] = __ldcg(&F.Lm[J]) - r[4];
-    }
-  }
-  for (int i = tid; i < b + nUc; i += NT) {
-    if (i < b) {
-      int rr = s + i;
-      int64_t lo = F.rp[rr], hi = F.rp[rr + 1];
-      int64_t p = lo, q = hi;
-      while (p < q) { int64_t mid = (p + q) >> 1; if (F.ci[mid] < e) p = mid + 1; else q = mid; }
-      ccnt[i] = (int)(hi - p);
-    } else {
-      const int *r = urec + (i - b) * REC_INTS;
-      int J = r[0];
-      ccnt[i] = __ldcg(&F.Uc[J]) - r[3];
-    }
-  }
-  __syncthreads();
-  const int totR = cta_scan(rcnt, b + nLc, S.tmp);
-  const int totC = cta_scan(ccnt, b + nUc, S.tmp);
-  // candidate buffers (+flags), power-of-two capacity
-  int pR = 1; while (pR < totR) pR <<= 1;
-  int pC = 1; while (pC < totC) pC <<= 1;
-  const int saved = A.sused; const int64_t gsaved = A.gused;
-  int *candR = (int *)balloc(A, (int64_t)pR * 4);
-  int *flagR = (int *)balloc(A, (int64_t)pR * 4);
-  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
-  // warp per item copy
-  for (int it = wid; it < b + nLc; it += NW) {
-    int off = rcnt[it];
-    if (it < b) {
-      int c = s + it;
-      int64_t hi = F.cp[c + 1];
-      int n_it = (it + 1 < b + nLc ? rcnt[it + 1] : totR) - off;
-      int64_t lo = hi - n_it;
-      for (int64_t p = lo + lane; p < hi; p += 32) candR[off + (p - lo)] = F.cr[p];
-    } else {
-      const int *r = lrec + (it - b) * REC_INTS;
-      int J = r[0];
-      int n_it = (it + 1 < b + nLc ? rcnt[it + 1] : totR) - off;
-      const int *rows = F.Lidx + __ldcg(&F.Lrow_off[J]) + r[4];
-      for (int p = lane; p < n_it; p += 32) candR[off + p] = __ldcg(rows + p);
-    }
-  }
-  __syncthreads();
-  const int nR = cta_sort_unique(candR, totR, flagR, S.tmp);
-  // release the temporary part of the allocation, keep R (same address unless
-  // the candidates spilled to global memory and R now fits in shared memory)
-  A.sused = saved; A.gused = gsaved;
-  int *R = (int *)balloc(A, (int64_t)nR * 4);
-  if (R != candR) {
-    for (int i = threadIdx.x; i < nR; i += NT) R[i] = candR[i];
-    __syncthreads();
-  }
-  const int saved2 = A.sused; const int64_t gsaved2 = A.gused;
-  int *candC = (int *)balloc(A, (int64_t)pC * 4);
-  int *flagC = (int *)balloc(A, (int64_t)pC * 4);
-  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
-  for (int it = wid; it < b + nUc; it += NW) {
-    int off = ccnt[it];
-    int n_it = (it + 1 < b + nUc ? ccnt[it + 1] : totC) - off;
-    if (it < b) {
-      int rr = s + it;
-      int64_t hi = F.rp[rr + 1];
-      int64_t lo = hi - n_it;
-      for (int64_t p = lo + lane; p < hi; p += 32) candC[off + (p - lo)] = F.ci[p];
-    } else {
-      const int *r = urec + (it - b) * REC_INTS;
-      int J = r[0];
-      const int *cols = F.Uidx + __ldcg(&F.Ucol_off[J]) + r[3];
-      for (int p = lane; p < n_it; p += 32) candC[off + p] = __ldcg(cols + p);
-    }
-  }
-  __syncthreads();
-  const int nC = cta_sort_unique(candC, totC, flagC, S.tmp);
-  A.sused = saved2; A.gused = gsaved2;
-  int *C = (int *)balloc(A, (int64_t)nC * 4);
-  if (C != candC) {
-    for (int i = threadIdx.x; i < nC; i += NT) C[i] = candC[i];
-    __syncthreads();
-  }
-
-  // ---------------- a-4: dense buffers, scatter Ã
-  // W_L: (b + nR) x b row-major (rows: the b diagonal rows, then R);  W_U: nC x b (column j contiguous)
-  double *WL = (double *)balloc(A, (int64_t)(b + nR) * b * 8);
-  double *WU = (double *)balloc(A, (int64_t)nC * b * 8);
-  double *P = (double *)balloc(A, (int64_t)b * b * 8);
-  int *keepR = (int *)balloc(A, (int64_t)(nR + 1) * 4);
-  int *keepC = (int *)balloc(A, (int64_t)(nC + 1) * 4);
-  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
-  for (int i = tid; i < (b + nR) * b; i += NT) WL[i] = 0.0;
-  for (int i = tid; i < nC * b; i += NT) WU[i] = 0.0;
-  __syncthreads();
-  for (int it = wid; it < b; it += NW) {
-    int c = s + it;
-    int64_t lo = F.cp[c], hi = F.cp[c + 1];
-    for (int64_t p = lo + lane; p < hi; p += 32) {
-      int row = F.cr[p];
-      if (row < s) continue;
-      int w = row < e ? row - s : b + lbound(R, 0, nR, row);
-      WL[(int64_t)w * b + it] = F.cval[p];
-    }
-    int rr = s + it;
-    lo = F.rp[rr]; hi = F.rp[rr + 1];
-    for (int64_t p = lo + lane; p < hi; p += 32) {
-      int col = F.ci[p];
-      if (col < e) continue;
-      WU[(int64_t)lbound(C, 0, nC, col) * b + it] = F.val[p];
-    }
-  }
-  __syncthreads();
-
-  // ---------------- a-5: Schur updates, L side (and diagonal block)
-  //   W_L[rows(L_J) >= s, cols(Ũ_J) in K] -= L_J[rows >= s, :] * Ũ_J[:, cols in K]
-  const int mark = A.sused; const int64_t gmark = A.gused;
-  for (int a = 0; a < nLc; ++a) {
-    const int *r = lrec + (lkey[a] & 1023) * REC_INTS;
-    const int J = r[0], c0 = r[1], c1 = r[2], lrs = r[3];
-    const int bJ = F.bstart[J + 1] - F.bstart[J];
-    const int mJ = __ldcg(&F.Lm[J]);
-    const int nrow = mJ - lrs, ncol = c1 - c0;
-    if (nrow <= 0 || ncol <= 0) continue;
-    A.sused = mark; A.gused = gmark;
-    double *sL = (double *)balloc(A, (int64_t)nrow * bJ * 8);
-    double *sU = (double *)balloc(A, (int64_t)ncol * bJ * 8);
-    int *wrow = (int *)balloc(A, (int64_t)nrow * 4);
-    int *wcol = (int *)balloc(A, (int64_t)ncol * 4);
-    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
-    const double *gL = F.Lval + __ldcg(&F.Lval_off[J]) + (int64_t)lrs * bJ;
-    const double *gU = F.Uval + __ldcg(&F.Uval_off[J]) + (int64_t)c0 * bJ;
-    const int *grow = F.Lidx + __ldcg(&F.Lrow_off[J]) + lrs;
-    const int *gcol = F.Uidx + __ldcg(&F.Ucol_off[J]) + c0;
-    for (int i = tid; i < nrow * bJ; i += NT) sL[i] = __ldcg(gL + i);
-    for (int i = tid; i < ncol * bJ; i += NT) sU[i] = __ldcg(gU + i);
-    for (int i = tid; i < nrow; i += NT) {
-      int row = __ldcg(grow + i);
-      wrow[i] = row < e ? row - s : b + lbound(R, 0, nR, row);
-    }
-    for (int i = tid; i < ncol; i += NT) wcol[i] = __ldcg(gcol + i) - s;
-    __syncthreads();
-    for (int it = tid; it < nrow * ncol; it += NT) {
-      int p = it / ncol, q = it - p * ncol;
-      const double *l = sL + (int64_t)p * bJ, *u = sU + (int64_t)q * bJ;
-      double acc = 0.0;
-      for (int t = 0; t < bJ; ++t) acc = fma(l[t], u[t], acc);
-      WL[(int64_t)wrow[p] * b + wcol[q]] -= acc;
-    }
-    flops += 2.0 * bJ * (double)nrow * (double)ncol;
-    __syncthreads();
-  }
-  // ---------------- a-5: Schur updates, U side
-  //   W_U[rows(L_J) in K, cols(Ũ_J) >= e] -= L_J[rows in K, :] * Ũ_J[:, cols >= e]
-  for (int a = 0; a < nUc; ++a) {
-    const int *r = urec + (ukey[a] & 1023) * REC_INTS;
-    const int J = r[0], r0 = r[1], r1 = r[2], cus = r[3];
-    const int bJ = F.bstart[J + 1] - F.bstart[J];
-    const int cJ = __ldcg(&F.Uc[J]);
-    const int nrow = r1 - r0, ncol = cJ - cus;
-    if (nrow <= 0 || ncol <= 0) continue;
-    A.sused = mark; A.gused = gmark;
-    double *sL = (double *)balloc(A, (int64_t)nrow * bJ * 8);
-    double *sU = (double *)balloc(A, (int64_t)ncol * bJ * 8);
-    int *wrow = (int *)balloc(A, (int64_t)nrow * 4);
-    int *wcol = (int *)balloc(A, (int64_t)ncol * 4);
-    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
-    const double *gL = F.Lval + __ldcg(&F.Lval_off[J]) + (int64_t)r0 * bJ;
-    const double *gU = F.Uval + __ldcg(&F.Uval_off[J]) + (int64_t)cus * bJ;
-    const int *grow = F.Lidx + __ldcg(&F.Lrow_off[J]) + r0;
-    const int *gcol = F.Uidx + __ldcg(&F.Ucol_off[J]) + cus;
-    for (int i = tid; i < nrow * bJ; i += NT) sL[i] = __ldcg(gL + i);
-    for (int i = tid; i < ncol * bJ; i += NT) sU[i] = __ldcg(gU + i);
-    for (int i = tid; i < nrow; i += NT) wrow[i] = __ldcg(grow + i) - s;
-    for (int i = tid; i < ncol; i += NT) wcol[i] = lbound(C, 0, nC, __ldcg(gcol + i));
-    __syncthreads();
-    for (int it = tid; it < nrow * ncol; it += NT) {
-      int q = it / nrow, p = it - q * nrow;
-      const double *l = sL + (int64_t)p * bJ, *u = sU + (int64_t)q * bJ;
-      double acc = 0.0;
-      for (int t = 0; t < bJ; ++t) acc = fma(l[t], u[t], acc);
-      WU[(int64_t)wcol[q] * b + wrow[p]] -= acc;
-    }
-    flops += 2.0 * bJ * (double)nrow * (double)ncol;
-    __syncthreads();
-  }
-  A.sused = mark; A.gused = gmark;
+  // ---------------- a-3 / a-4 / a-5 for both sides
+  double *WL, *WU;
+  int *rowOf, *colOf;
+  int nR, nC;
+  if (!side_update<0>(F, K, s, e, b, CL, nLc, TL, aL0, aLe, aL1, A, S, &WL, &rowOf, &nR, flops)) return;
+  PROF(2);
+  PROF(3);
+  if (!side_update<1>(F, K, s, e, b, CU, nUc, TU, aU0, aU0, aU1, A, S, &WU, &colOf, &nC, flops)) return;
+  PROF(4);
 
   // ---------------- a-6: D_K = P_K^{-1}, Gauss-Jordan with partial pivoting (column-major P)
+  double *P = (double *)balloc(A, (int64_t)b * b * 8);
+  int *ipiv = (int *)balloc(A, (int64_t)b * 4);
+  double *fcol = (double *)balloc(A, (int64_t)b * 8);
+  OVF_CHECK();
   for (int i = tid; i < b * b; i += NT) {
     int rr = i % b, cc = i / b;
     P[i] = WL[(int64_t)rr * b + cc];
   }
-  int *ipiv = (int *)balloc(A, (int64_t)b * 4);
-  double *fcol = (double *)balloc(A, (int64_t)b * 8);
-  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
   __syncthreads();
   bool singular = false;
-  for (int k = 0; k < b; ++k) {
+  if (b <= 32) {
+    // one warp: lane j owns column j; no CTA barriers
     if (wid == 0) {
-      double best = -1.0; int bi = k;
-      for (int i = k + lane; i < b; i += 32) {
-        double v = fabs(P[i + (int64_t)k * b]);
-        if (v > best) { best = v; bi = i; }
-      }
+      for (int k = 0; k < b; ++k) {
+        double best = -1.0; int bi = k;
+        if (k + lane < b) { best = fabs(P[k + lane + k * b]); bi = k + lane; }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double ob = __shfl_down_sync(0xffffffffu, best, o);
-        int oi = __shfl_down_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        for (int o = 16; o > 0; o >>= 1) {
+          double ob = __shfl_down_sync(0xffffffffu, best, o);
+          int oi = __shfl_down_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        best = __shfl_sync(0xffffffffu, best, 0);
+        bi = __shfl_sync(0xffffffffu, bi, 0);
+        if (best == 0.0) { singular = true; break; }
+        if (lane == 0) ipiv[k] = bi;
+        if (lane < b && bi != k) {
+          double t = P[k + lane * b]; P[k + lane * b] = P[bi + lane * b]; P[bi + lane * b] = t;
+        }
+        __syncwarp();
+        const double d = 1.0 / P[k + k * b];
+        if (lane < b) fcol[lane] = P[lane + k * b];
+        __syncwarp();
+        if (lane < b) {
+          const int j = lane;
+          const double pr = (j == k) ? d : P[k + j * b] * d;
+          for (int i = 0; i < b; ++i) {
+            if (i == k) continue;
+            const double base = (j == k) ? 0.0 : P[i + j * b];
+            P[i + j * b] = base - fcol[i] * pr;
+          }
+          P[k + j * b] = pr;
+        }
+        __syncwarp();
       }
-      if (lane == 0) { S.piv = bi; S.pivd = best; ipiv[k] = bi; }
+      if (!singular) {
+        for (int k = b - 1; k >= 0; --k) {
+          const int pv = ipiv[k];
+          if (pv != k && lane < b) {
+            double t = P[lane + k * b]; P[lane + k * b] = P[lane + pv * b]; P[lane + pv * b] = t;
+          }
+          __syncwarp();
+        }
+      }
+      if (lane == 0) S.piv = singular ? 1 : 0;
     }
     __syncthreads();
-    if (S.pivd == 0.0) { singular = true; break; }
-    const int pv = S.piv;
-    if (pv != k)
-      for (int j = tid; j < b; j += NT) {
-        double t = P[k + (int64_t)j * b]; P[k + (int64_t)j * b] = P[pv + (int64_t)j * b]; P[pv + (int64_t)j * b] = t;
+    singular = S.piv != 0;
+  } else {
+    for (int k = 0; k < b; ++k) {
+      if (wid == 0) {
+        double best = -1.0; int bi = k;
+        for (int i = k + lane; i < b; i += 32) {
+          double v = fabs(P[i + (int64_t)k * b]);
+          if (v > best) { best = v; bi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          double ob = __shfl_down_sync(0xffffffffu, best, o);
+          int oi = __shfl_down_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) { S.piv = bi; S.pivd = best; ipiv[k] = bi; }
       }
-    __syncthreads();
-    const double d = 1.0 / P[k + (int64_t)k * b];
-    __syncthreads();
-    if (tid == 0) P[k + (int64_t)k * b] = 1.0;
-    __syncthreads();
-    for (int j = tid; j < b; j += NT) P[k + (int64_t)j * b] *= d;
-    for (int i = tid; i < b; i += NT) fcol[i] = (i == k) ? 0.0 : P[i + (int64_t)k * b];
-    __syncthreads();
-    for (int it = tid; it < b * b; it += NT) {
-      int i = it % b, j = it / b;
-      if (i == k) continue;
-      double base = (j == k) ? 0.0 : P[i + (int64_t)j * b];
-      P[i + (int64_t)j * b] = base - fcol[i] * P[k + (int64_t)j * b];
+      __syncthreads();
+      if (S.pivd == 0.0) { singular = true; break; }
+      const int pv = S.piv;
+      if (pv != k)
+        for (int j = tid; j < b; j += NT) {
+          double t = P[k + (int64_t)j * b]; P[k + (int64_t)j * b] = P[pv + (int64_t)j * b]; P[pv + (int64_t)j * b] = t;
+        }
+      __syncthreads();
+      const double d = 1.0 / P[k + (int64_t)k * b];
+      for (int i = tid; i < b; i += NT) fcol[i] = P[i + (int64_t)k * b];
+      __syncthreads();
+      for (int it = tid; it < b * b; it += NT) {
+        const int i = it % b, j = it / b;
+        const double pr = (j == k) ? d : P[k + (int64_t)j * b] * d;
+        if (i == k) continue;
+        const double base = (j == k) ? 0.0 : P[i + (int64_t)j * b];
+        P[i + (int64_t)j * b] = base - fcol[i] * pr;
+      }
+      __syncthreads();
+      for (int j = tid; j < b; j += NT) P[k + (int64_t)j * b] = (j == k) ? d : P[k + (int64_t)j * b] * d;
+      __syncthreads();
     }
-    __syncthreads();
+    if (!singular) {
+      for (int k = b - 1; k >= 0; --k) {
+        const int pv = ipiv[k];
+        if (pv != k)
+          for (int i = tid; i < b; i += NT) {
+            double t = P[i + (int64_t)k * b]; P[i + (int64_t)k * b] = P[i + (int64_t)pv * b]; P[i + (int64_t)pv * b] = t;
+          }
+        __syncthreads();
+      }
+    }
   }
   if (singular) {
     if (tid == 0) raise_abort(F, DEV_BREAKDOWN, K);
     return;
-  }
-  // undo the row interchanges as column interchanges, in reverse order
-  for (int k = b - 1; k >= 0; --k) {
-    int pv = ipiv[k];
-    if (pv != k)
-      for (int i = tid; i < b; i += NT) {
-        double t = P[i + (int64_t)k * b]; P[i + (int64_t)k * b] = P[i + (int64_t)pv * b]; P[i + (int64_t)pv * b] = t;
-      }
-    __syncthreads();
   }
   {
     double *Dg = F.D + F.D_off[K];
     for (int i = tid; i < b * b; i += NT) Dg[i] = P[i];
   }
   flops += 2.0 * b * b * (double)b + 2.0 * b * b * (double)(nR + nC);
+  PROF(5);
 
-  // ---------------- a-7/a-8: scale, drop, compact -- L rows
+  // ---------------- a-7/a-8: scale, drop (R1-R3), compact
+  // L rows: l = w D_K, kept iff max|l| > tau; the scaled row overwrites W_L's row
   const double tau = F.tau;
+  int *keepR = (int *)balloc(A, (int64_t)(nR + 1) * 4);
+  int *keepC = (int *)balloc(A, (int64_t)(nC + 1) * 4);
+  OVF_CHECK();
   for (int i = tid; i < nR; i += NT) {
-    const double *w = WL + (int64_t)(b + i) * b;
+    double *w = WL + (int64_t)(b + i) * b;
     double mx = 0.0;
-    for (int c = 0; c < b; ++c) {
-      double acc = 0.0;
-      for (int t = 0; t < b; ++t) acc = fma(w[t], P[t + (int64_t)c * b], acc);
-      mx = fmax(mx, fabs(acc));
+    if (b <= 16) {
+      double l[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        if (c < b) {
+          double acc = 0.0;
+          for (int t = 0; t < b; ++t) acc = fma(w[t], P[t + c * b], acc);
+          l[c] = acc;
+          mx = fmax(mx, fabs(acc));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) if (c < b) w[c] = l[c];
+    } else {
+      for (int c = 0; c < b; ++c) {
+        double acc = 0.0;
+        for (int t = 0; t < b; ++t) acc = fma(w[t], P[t + (int64_t)c * b], acc);
+        mx = fmax(mx, fabs(acc));
+      }
     }
-    int keep = mx > tau;
+    const int keep = mx > tau;
     keepR[i] = keep;
     if (tau > 0.0) {
       double margin = fabs(mx / tau - 1.0);
       if (margin <= F.near_rel) {
-        unsigned long long slot = atomicAdd(&F.ctrl[CTRL_NEAR], 1ull);
+        unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_NEAR], 1ull);
         if (slot < (unsigned long long)F.near_cap) {
           F.near_i[4 * slot] = K; F.near_i[4 * slot + 1] = 0;
-          F.near_i[4 * slot + 2] = R[i]; F.near_i[4 * slot + 3] = keep;
+          F.near_i[4 * slot + 2] = rowOf[b + i]; F.near_i[4 * slot + 3] = keep;
           F.near_m[slot] = margin;
         }
       }
     }
   }
+  // U cols: u = D_K z, kept iff max|u| > tau; Ũ stores z (unscaled)
   for (int j = tid; j < nC; j += NT) {
     const double *z = WU + (int64_t)j * b;
     double mx = 0.0;
@@ -534,32 +794,81 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
       for (int t = 0; t < b; ++t) acc = fma(P[rr + (int64_t)t * b], z[t], acc);
       mx = fmax(mx, fabs(acc));
     }
-    int keep = mx > tau;
+    const int keep = mx > tau;
     keepC[j] = keep;
     if (tau > 0.0) {
       double margin = fabs(mx / tau - 1.0);
       if (margin <= F.near_rel) {
-        unsigned long long slot = atomicAdd(&F.ctrl[CTRL_NEAR], 1ull);
+        unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_NEAR], 1ull);
         if (slot < (unsigned long long)F.near_cap) {
           F.near_i[4 * slot] = K; F.near_i[4 * slot + 1] = 1;
-          F.near_i[4 * slot + 2] = C[j]; F.near_i[4 * slot + 3] = keep;
+          F.near_i[4 * slot + 2] = colOf[j]; F.near_i[4 * slot + 3] = keep;
           F.near_m[slot] = margin;
         }
       }
     }
   }
   __syncthreads();
-  const int mK = cta_scan(keepR, nR, S.tmp);   // keepR -> exclusive positions
+  const int mK = cta_scan(keepR, nR, S.tmp);
   const int cK = cta_scan(keepC, nC, S.tmp);
-  keepR[nR] = mK;   // sentinel so keep(i) = keepR[i+1] > keepR[i]
-  keepC[nC] = cK;
+  if (tid == 0) { keepR[nR] = mK; keepC[nC] = cK; }
+  // kept rows / cols (buffer indices), then sorted by matrix index
+  int *kr = (int *)balloc(A, (int64_t)(mK + 1) * 4);
+  int *krow = (int *)balloc(A, (int64_t)(mK + 1) * 4);
+  int *kc = (int *)balloc(A, (int64_t)(cK + 1) * 4);
+  int *kcol = (int *)balloc(A, (int64_t)(cK + 1) * 4);
+  int *R = (int *)balloc(A, (int64_t)(mK + 1) * 4);     // sorted kept rows
+  int *Cs = (int *)balloc(A, (int64_t)(cK + 1) * 4);    // sorted kept cols
+  int *ordR = (int *)balloc(A, (int64_t)(mK + 1) * 4);
+  int *ordC = (int *)balloc(A, (int64_t)(cK + 1) * 4);
+  OVF_CHECK();
+  __syncthreads();
+  for (int i = tid; i < nR; i += NT)
+    if (keepR[i + 1] > keepR[i]) { kr[keepR[i]] = b + i; krow[keepR[i]] = rowOf[b + i]; }
+  for (int j = tid; j < nC; j += NT)
+    if (keepC[j + 1] > keepC[j]) { kc[keepC[j]] = j; kcol[keepC[j]] = colOf[j]; }
+  __syncthreads();
+  if (mK <= 1024) cta_rank_sort(krow, mK, ordR);
+  else {
+    // large: bitonic on (row << 0) keys carrying positions via a second pass
+    for (int x = tid; x < mK; x += NT) R[x] = krow[x];
+    __syncthreads();
+    int m2 = 1; while (m2 < mK) m2 <<= 1;
+    int *tmpk = (int *)balloc(A, (int64_t)m2 * 4);
+    OVF_CHECK();
+    for (int x = tid; x < m2; x += NT) tmpk[x] = x < mK ? R[x] : INT_MAX;
+    __syncthreads();
+    cta_bitonic(tmpk, m2);
+    for (int x = tid; x < mK; x += NT) {
+      const int r = lbound(tmpk, 0, mK, krow[x]);
+      ordR[r] = x;
+    }
+    __syncthreads();
+  }
+  if (cK <= 1024) cta_rank_sort(kcol, cK, ordC);
+  else {
+    int m2 = 1; while (m2 < cK) m2 <<= 1;
+    int *tmpk = (int *)balloc(A, (int64_t)m2 * 4);
+    OVF_CHECK();
+    for (int x = tid; x < m2; x += NT) tmpk[x] = x < cK ? kcol[x] : INT_MAX;
+    __syncthreads();
+    cta_bitonic(tmpk, m2);
+    for (int x = tid; x < cK; x += NT) ordC[lbound(tmpk, 0, cK, kcol[x])] = x;
+    __syncthreads();
+  }
+  for (int x = tid; x < mK; x += NT) R[x] = krow[ordR[x]];
+  for (int x = tid; x < cK; x += NT) Cs[x] = kcol[ordC[x]];
   if (tid == 0) {
-    unsigned long long oi = atomicAdd(&F.ctrl[CTRL_CUR_LIDX], (unsigned long long)mK);
-    unsigned long long ov = atomicAdd(&F.ctrl[CTRL_CUR_LVAL], (unsigned long long)mK * b);
-    unsigned long long ui = atomicAdd(&F.ctrl[CTRL_CUR_UIDX], (unsigned long long)cK);
-    unsigned long long uv = atomicAdd(&F.ctrl[CTRL_CUR_UVAL], (unsigned long long)cK * b);
-    S.off[0] = oi; S.off[1] = ov; S.off[2] = ui; S.off[3] = uv;
-    atomicAdd(&F.ctrl[CTRL_NDEC], (unsigned long long)(nR + nC));
+    // 128-byte aligned slices: no L1 line is ever shared by two blocks' panels
+    const unsigned long long mi = ((unsigned long long)mK + 31) & ~31ull;
+    const unsigned long long mv = ((unsigned long long)mK * b + 15) & ~15ull;
+    const unsigned long long ci = ((unsigned long long)cK + 31) & ~31ull;
+    const unsigned long long cv = ((unsigned long long)cK * b + 15) & ~15ull;
+    S.off[0] = atomicAdd(&F.ctrl[CS * CTRL_CUR_LIDX], mi);
+    S.off[1] = atomicAdd(&F.ctrl[CS * CTRL_CUR_LVAL], mv);
+    S.off[2] = atomicAdd(&F.ctrl[CS * CTRL_CUR_UIDX], ci);
+    S.off[3] = atomicAdd(&F.ctrl[CS * CTRL_CUR_UVAL], cv);
+    atomicAdd(&F.ctrl[CS * CTRL_NDEC], (unsigned long long)(nR + nC));
   }
   __syncthreads();
   if (S.off[0] + mK > (unsigned long long)F.cap_Lidx || S.off[1] + (unsigned long long)mK * b > (unsigned long long)F.cap_Lval ||
@@ -568,53 +877,37 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     return;
   }
   const int64_t oLi = (int64_t)S.off[0], oLv = (int64_t)S.off[1], oUi = (int64_t)S.off[2], oUv = (int64_t)S.off[3];
-  // kept row/col lists in shared memory for registration (R / C compacted in place)
-  for (int i = tid; i < nR; i += NT)
-    if (keepR[i + 1] > keepR[i]) F.Lidx[oLi + keepR[i]] = R[i];
-  for (int it = tid; it < nR * b; it += NT) {
-    int i = it / b, c = it - i * b;
-    if (keepR[i + 1] > keepR[i]) {
-      const double *w = WL + (int64_t)(b + i) * b;
+  for (int x = tid; x < mK; x += NT) F.Lidx[oLi + x] = R[x];
+  for (int it = tid; it < mK * b; it += NT) {
+    const int x = it / b, c = it - x * b;
+    if (b <= 16) {
+      F.Lval[oLv + it] = WL[(int64_t)kr[ordR[x]] * b + c];
+    } else {
+      const double *w = WL + (int64_t)kr[ordR[x]] * b;
       double acc = 0.0;
       for (int t = 0; t < b; ++t) acc = fma(w[t], P[t + (int64_t)c * b], acc);
-      F.Lval[oLv + (int64_t)keepR[i] * b + c] = acc;
+      F.Lval[oLv + it] = acc;
     }
   }
-  for (int j = tid; j < nC; j += NT)
-    if (keepC[j + 1] > keepC[j]) F.Uidx[oUi + keepC[j]] = C[j];
-  for (int it = tid; it < nC * b; it += NT) {
-    int j = it / b;
-    if (keepC[j + 1] > keepC[j]) F.Uval[oUv + (int64_t)keepC[j] * b + (it - j * b)] = WU[it];
-  }
-  __syncthreads();
-  // compact R -> kept rows, C -> kept cols (chunked in place)
-  for (int base = 0; base < nR; base += NT) {
-    int i = base + tid; int v = 0, pos = -1;
-    if (i < nR && keepR[i + 1] > keepR[i]) { v = R[i]; pos = keepR[i]; }
-    __syncthreads();
-    if (pos >= 0) R[pos] = v;
-    __syncthreads();
-  }
-  for (int base = 0; base < nC; base += NT) {
-    int j = base + tid; int v = 0, pos = -1;
-    if (j < nC && keepC[j + 1] > keepC[j]) { v = C[j]; pos = keepC[j]; }
-    __syncthreads();
-    if (pos >= 0) C[pos] = v;
-    __syncthreads();
+  for (int x = tid; x < cK; x += NT) F.Uidx[oUi + x] = Cs[x];
+  for (int it = tid; it < cK * b; it += NT) {
+    const int x = it / b;
+    F.Uval[oUv + it] = WU[(int64_t)kc[ordC[x]] * b + (it - x * b)];
   }
   if (tid == 0) {
     F.Lrow_off[K] = oLi; F.Lm[K] = mK; F.Lval_off[K] = oLv;
     F.Ucol_off[K] = oUi; F.Uc[K] = cK; F.Uval_off[K] = oUv;
     F.blk_ncand[2 * K] = nR; F.blk_ncand[2 * K + 1] = nC;
   }
+  __syncthreads();
+  PROF(6);
 
   // ---------------- a-2 (producer side): register K with the blocks it feeds,
   // and the chain edges of the readiness rule.
-  // run starts of kept rows / cols by target block
-  int *rrun = keepR;  // reuse: run flags -> positions
+  int *rrun = keepR;  // reuse
   int *crun = keepC;
   for (int i = tid; i < mK; i += NT) rrun[i] = (i == 0 || F.block_of[R[i]] != F.block_of[R[i - 1]]) ? 1 : 0;
-  for (int j = tid; j < cK; j += NT) crun[j] = (j == 0 || F.block_of[C[j]] != F.block_of[C[j - 1]]) ? 1 : 0;
+  for (int j = tid; j < cK; j += NT) crun[j] = (j == 0 || F.block_of[Cs[j]] != F.block_of[Cs[j - 1]]) ? 1 : 0;
   __syncthreads();
   const int nRr = cta_scan(rrun, mK, S.tmp);
   const int nCr = cta_scan(crun, cK, S.tmp);
@@ -623,27 +916,23 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   int pN = 1; while (pN < nRr + nCr) pN <<= 1;
   int *nb = (int *)balloc(A, (int64_t)pN * 4);
   int *nbf = (int *)balloc(A, (int64_t)pN * 4);
-  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
-  for (int i = tid; i < mK; i += NT) {
-    bool st = (i == 0) || F.block_of[R[i]] != F.block_of[R[i - 1]];
-    if (st) rstart[rrun[i]] = i;
-  }
-  for (int j = tid; j < cK; j += NT) {
-    bool st = (j == 0) || F.block_of[C[j]] != F.block_of[C[j - 1]];
-    if (st) cstart[crun[j]] = j;
-  }
+  OVF_CHECK();
+  for (int i = tid; i < mK; i += NT)
+    if (i == 0 || F.block_of[R[i]] != F.block_of[R[i - 1]]) rstart[rrun[i]] = i;
+  for (int j = tid; j < cK; j += NT)
+    if (j == 0 || F.block_of[Cs[j]] != F.block_of[Cs[j - 1]]) cstart[crun[j]] = j;
   if (tid == 0) { rstart[nRr] = mK; cstart[nCr] = cK; }
   __syncthreads();
   for (int x = tid; x < nRr; x += NT) {
     const int r0 = rstart[x], r1 = rstart[x + 1];
     const int T = F.block_of[R[r0]];
-    int rec[REC_INTS] = {K, r0, r1, lbound(C, 0, cK, F.bstart[T + 1]), 0, 0, 0, 0};
+    int rec[REC_INTS] = {K, r0, r1, lbound(Cs, 0, cK, F.bstart[T + 1]), 0, 0, 0, 0};
     list_append(F, F.uc, T, rec);
     nb[x] = T;
   }
   for (int x = tid; x < nCr; x += NT) {
     const int c0 = cstart[x], c1 = cstart[x + 1];
-    const int T = F.block_of[C[c0]];
+    const int T = F.block_of[Cs[c0]];
     int rec[REC_INTS] = {K, c0, c1, lbound(R, 0, mK, F.bstart[T]), lbound(R, 0, mK, F.bstart[T + 1]), 0, 0, 0};
     list_append(F, F.lc, T, rec);
     nb[nRr + x] = T;
@@ -656,9 +945,10 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     int rec1 = nb[x + 1];
     list_append(F, F.succ, nb[x], &rec1);
   }
-  if (tid == 0) { F.blk_flops[K] = flops; atomicAdd((double *)&F.ctrl[CTRL_FLOPS], flops); }
+  if (tid == 0) { F.blk_flops[K] = flops; atomicAdd((double *)&F.ctrl[CS * CTRL_FLOPS], flops); }
   __threadfence();
   __syncthreads();
+  PROF(7);
 
   // ---------------- a-1: release successors (static adjacency of Ã + chain edges)
   const int a0 = F.adj_ptr[K], a1 = F.adj_ptr[K + 1];
@@ -666,36 +956,55 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   for (int x = tid; x < (a1 - a0) + nS; x += NT) {
     int T = x < (a1 - a0) ? F.adj[a0 + x] : __ldcg(list_rec(F.succ, K, x - (a1 - a0)));
     if (atomicSub(&F.pending[T], 1) == 1) {
-      unsigned long long slot = atomicAdd(&F.ctrl[CTRL_QHEAD], 1ull);
+      unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
       __threadfence();
       st_vol(&F.queue[slot], T);
     }
   }
-  if (tid == 0) atomicAdd(&F.ctrl[CTRL_DONE], 1ull);
+  if (tid == 0) atomicAdd(&F.ctrl[CS * CTRL_DONE], 1ull);
+  PROF(8);
+  PROF_END(nLc, nUc, nR, nC);
+#undef OVF_CHECK
 }
 
-__global__ void __launch_bounds__(NT) factor_kernel(DevFactor F) {
-  extern __shared__ __align__(16) unsigned char smem[];
+__global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Shared S;
+  __shared__ __align__(8) uint64_t s_mbar;
+  unsigned mphase = 0;
+  if (threadIdx.x == 0) mbar_init(&s_mbar, 1);
+  __syncthreads();
   while (true) {
     if (threadIdx.x == 0) {
+#ifdef BILU_PROFILE
+      long long _w0 = clock64();
+#endif
       int K = -1;
-      unsigned long long idx = aborted(F) ? ~0ull : atomicAdd(&F.ctrl[CTRL_QTAIL], 1ull);
+      unsigned long long idx = aborted(F) ? ~0ull : atomicAdd(&F.ctrl[CS * CTRL_QTAIL], 1ull);
       if (idx < (unsigned long long)F.N) {
+        unsigned ns = 32, polls = 0;
         while (true) {
           K = ld_vol(&F.queue[idx]);
           if (K >= 0) break;
-          if (aborted(F)) { K = -1; break; }
-          __nanosleep(32);
+          if ((++polls & 15u) == 0 && aborted(F)) { K = -1; break; }
+          __nanosleep(ns);
+          if (ns < 256) ns <<= 1;
         }
       }
       S.K = K;
+#ifdef BILU_PROFILE
+      atomicAdd(&g_prof[0], (unsigned long long)(clock64() - _w0));
+      if (K >= 0) atomicAdd(&g_prof[31], 1ull);
+#endif
     }
     __syncthreads();
     const int K = S.K;
     if (K < 0) break;
+    DBGK(K);
     __threadfence();
-    process_block(F, K, S, smem);
+    // order the bulk (async-proxy) reads of other blocks' panels after the acquire
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    process_block(F, K, S, smem, &s_mbar, mphase);
     __syncthreads();
   }
 }
@@ -704,6 +1013,13 @@ __global__ void __launch_bounds__(NT) factor_kernel(DevFactor F) {
 extern "C" cudaError_t bilu_launch_factor(const DevFactor &F, int grid, cudaStream_t st) {
   cudaError_t err = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F.smem_bytes);
   if (err != cudaSuccess) return err;
+  // shared memory carve-out just large enough for the CTAs of one SM; the rest stays L1
+  // (the Schur updates read contributor panels through L1)
+  {
+    int carve = 50;
+    if (const char *cv = getenv("BILU_CARVEOUT")) carve = atoi(cv);
+    cudaFuncSetAttribute(factor_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+  }
   factor_kernel<<<grid, NT, F.smem_bytes, st>>>(F);
   return cudaGetLastError();
 }
@@ -715,3 +1031,24 @@ extern "C" cudaError_t bilu_factor_occupancy(int smem_bytes, int *blocks_per_sm)
 }
 
 }  // namespace bilu
+
+namespace bilu {
+extern "C" int bilu_prof_set_blk(unsigned long long *dev_ptr) {
+#ifdef BILU_PROFILE
+  return cudaMemcpyToSymbol(g_blkprof, &dev_ptr, sizeof(dev_ptr)) == cudaSuccess;
+#else
+  (void)dev_ptr;
+  return 0;
+#endif
+}
+extern "C" int bilu_prof_read(unsigned long long *out, int reset) {
+#ifdef BILU_PROFILE
+  cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 32);
+  if (reset) { unsigned long long z[32] = {0}; cudaMemcpyToSymbol(g_prof, z, sizeof(z)); }
+  return 1;
+#else
+  (void)out; (void)reset;
+  return 0;
+#endif
+}
+}

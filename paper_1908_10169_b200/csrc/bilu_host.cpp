@@ -18,6 +18,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <ctime>
+#include <unistd.h>
 
 #include "../../include/bilu.h"
 #include "bilu_internal.h"
@@ -71,18 +73,22 @@ struct bilu_ctx {
   // host copies
   std::vector<int32_t> bstart, ready0;
   std::vector<int64_t> D_off;
-  std::vector<int64_t> map_csr, map_csc;   // Ã entry -> original CSR entry
+  std::vector<int64_t> map_csr;            // Ã entry -> original CSR entry
   std::vector<int32_t> perm;
   // device buffers (owned)
   std::vector<void *> owned;
   int32_t *d_bstart = nullptr, *d_block_of = nullptr;
-  int64_t *d_rp = nullptr, *d_cp = nullptr;
-  int32_t *d_ci = nullptr, *d_cr = nullptr;
-  double *d_val = nullptr, *d_cval = nullptr, *d_val_orig = nullptr;
-  int64_t *d_map_csr = nullptr, *d_map_csc = nullptr;
+  double *d_val_orig = nullptr;
+  int64_t *d_AL_ptr = nullptr, *d_AL_ge = nullptr, *d_AU_ptr = nullptr;
+  int32_t *d_AL_rc = nullptr, *d_AU_rc = nullptr;
+  double *d_AL_val = nullptr, *d_AU_val = nullptr;
+  int64_t *d_AL_map = nullptr, *d_AU_map = nullptr;
+  int64_t nAL = 0, nAU = 0;
   int32_t *d_adj_ptr = nullptr, *d_adj = nullptr, *d_pending0 = nullptr, *d_ready0 = nullptr;
   int32_t *d_perm = nullptr;
   int32_t nready0 = 0;
+  unsigned long long nready0_ull = 0;
+  unsigned long long ctrl_full[CTRL_COUNT * CS];
   // dynamic
   DevFactor F{};
   int grid = 0;
@@ -97,6 +103,7 @@ struct bilu_ctx {
   bool merge_alloc = false;
   int64_t merge_work_ints = 0, merge_dwork = 0, fD_cap = 0;
   double *d_mdwork = nullptr;
+  volatile int *dbg_host = nullptr;
   // apply structure (built lazily after each factorization)
   bool apply_ready = false;
   ApplyArgs AA{};
@@ -208,6 +215,7 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     set_err(nullptr, "bilu_analyze: max_block must be in [1,128] (got %d)", opt.max_block);
     return BILU_ERR_ARG;
   }
+  if (n >= (1 << 24)) { set_err(nullptr, "bilu_analyze: n must be < 2^24 (got %d)", n); return BILU_ERR_ARG; }
   if (n_blocks >= (1 << 21)) {
     set_err(nullptr, "bilu_analyze: at most 2^21-1 blocks supported (got %d)", n_blocks);
     return BILU_ERR_ARG;
@@ -277,21 +285,6 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
       for (auto &t : tmp) { ci[q] = t.first; h->map_csr[q] = t.second; ++q; }
     }
   }
-  // ---- CSC of Ã (counting transpose; rows ascending within a column)
-  std::vector<int64_t> cp(n + 1, 0);
-  for (int64_t p = 0; p < nnz; ++p) cp[ci[p] + 1]++;
-  for (int32_t i = 0; i < n; ++i) cp[i + 1] += cp[i];
-  std::vector<int32_t> cr(nnz);
-  h->map_csc.resize(nnz);
-  {
-    std::vector<int64_t> fill(cp.begin(), cp.end() - 1);
-    for (int32_t i = 0; i < n; ++i)
-      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-        int64_t q = fill[ci[p]]++;
-        cr[q] = i;
-        h->map_csc[q] = h->map_csr[p];
-      }
-  }
   // ---- block graph of sym(Ã): successors > K and pending counts
   std::vector<int32_t> block_of(n);
   for (int32_t K = 0; K < n_blocks; ++K)
@@ -312,12 +305,59 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     std::sort(edges.begin(), edges.end());
     edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
   }
+  // ---- per-block lists of Ã's entries: AL (block column K, rows >= s_K, sorted by
+  // (row, col)) and AU (block row K, cols >= e_K, sorted by (col, row)); values are
+  // gathered into this order by bilu_set_values.
+  std::vector<int64_t> AL_ptr(n_blocks + 1, 0), AL_ge(n_blocks, 0), AU_ptr(n_blocks + 1, 0);
+  std::vector<int32_t> AL_rc, AU_rc;
+  std::vector<int64_t> AL_map, AU_map;
+  AL_rc.reserve(nnz); AL_map.reserve(nnz); AU_rc.reserve(nnz); AU_map.reserve(nnz);
+  {
+    // bucket every entry (i, j) by its owning block: block(j) <= block(i) -> AL of block(j), else AU of block(i)
+    std::vector<int64_t> cntL(n_blocks + 1, 0), cntU(n_blocks + 1, 0);
+    for (int32_t i = 0; i < n; ++i)
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t bi = block_of[i], bj = block_of[ci[p]];
+        if (bj <= bi) cntL[bj + 1]++; else cntU[bi + 1]++;
+      }
+    for (int32_t K = 0; K < n_blocks; ++K) { cntL[K + 1] += cntL[K]; cntU[K + 1] += cntU[K]; }
+    AL_ptr = cntL; AU_ptr = cntU;
+    AL_rc.assign(cntL[n_blocks], 0); AL_map.assign(cntL[n_blocks], 0);
+    AU_rc.assign(cntU[n_blocks], 0); AU_map.assign(cntU[n_blocks], 0);
+    std::vector<int64_t> fl(cntL.begin(), cntL.end() - 1), fu(cntU.begin(), cntU.end() - 1);
+    // rows ascending, and within a row columns ascending -> AL sorted by (row, col)
+    for (int32_t i = 0; i < n; ++i)
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t j = ci[p], bi = block_of[i], bj = block_of[j];
+        if (bj <= bi) {
+          const int64_t q = fl[bj]++;
+          AL_rc[q] = (i << 7) | (j - bstart[bj]);
+          AL_map[q] = h->map_csr[p];
+        } else {
+          const int64_t q = fu[bi]++;
+          AU_rc[q] = (j << 7) | (i - bstart[bi]);
+          AU_map[q] = h->map_csr[p];
+        }
+      }
+    // AU: sort each block's list by (col, row)
+    for (int32_t K = 0; K < n_blocks; ++K) {
+      std::vector<std::pair<int32_t, int64_t>> tmp;
+      for (int64_t q = AU_ptr[K]; q < AU_ptr[K + 1]; ++q) tmp.emplace_back(AU_rc[q], AU_map[q]);
+      std::sort(tmp.begin(), tmp.end());
+      for (size_t x = 0; x < tmp.size(); ++x) { AU_rc[AU_ptr[K] + x] = tmp[x].first; AU_map[AU_ptr[K] + x] = tmp[x].second; }
+      int64_t q = AL_ptr[K];
+      while (q < AL_ptr[K + 1] && (AL_rc[q] >> 7) < bstart[K + 1]) ++q;
+      AL_ge[K] = q;
+    }
+  }
+  h->nAL = AL_ptr[n_blocks]; h->nAU = AU_ptr[n_blocks];
   std::vector<int32_t> adj_ptr(n_blocks + 1, 0), adj(edges.size()), pending0(n_blocks, 0);
   for (uint64_t eg : edges) { adj_ptr[(eg >> 32) + 1]++; pending0[(uint32_t)eg]++; }
   for (int32_t K = 0; K < n_blocks; ++K) adj_ptr[K + 1] += adj_ptr[K];
   for (size_t x = 0; x < edges.size(); ++x) adj[x] = (int32_t)(uint32_t)edges[x];  // sorted by (a, b)
   for (int32_t K = 0; K < n_blocks; ++K) if (pending0[K] == 0) h->ready0.push_back(K);
   h->nready0 = (int32_t)h->ready0.size();
+  h->nready0_ull = (unsigned long long)h->nready0;
   h->D_off.assign(n_blocks + 1, 0);
   for (int32_t K = 0; K < n_blocks; ++K) {
     int64_t b = bstart[K + 1] - bstart[K];
@@ -329,13 +369,14 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
 #define H2D(dst, src, cnt) do { cudaError_t e_ = cudaMemcpy(dst, src, (cnt) * sizeof(*(src)), cudaMemcpyHostToDevice); if (e_ != cudaSuccess) { set_err(h, "bilu_analyze: copy failed (%s)", cudaGetErrorString(e_)); g_last_error = h->err; bilu_destroy(h); return BILU_ERR_CUDA; } } while (0)
   ALLOC(h->d_bstart, n_blocks + 1); H2D(h->d_bstart, bstart.data(), n_blocks + 1);
   ALLOC(h->d_block_of, n); H2D(h->d_block_of, block_of.data(), n);
-  ALLOC(h->d_rp, n + 1); H2D(h->d_rp, rp.data(), n + 1);
-  ALLOC(h->d_ci, nnz); H2D(h->d_ci, ci.data(), nnz);
-  ALLOC(h->d_cp, n + 1); H2D(h->d_cp, cp.data(), n + 1);
-  ALLOC(h->d_cr, nnz); H2D(h->d_cr, cr.data(), nnz);
-  ALLOC(h->d_map_csr, nnz); H2D(h->d_map_csr, h->map_csr.data(), nnz);
-  ALLOC(h->d_map_csc, nnz); H2D(h->d_map_csc, h->map_csc.data(), nnz);
-  ALLOC(h->d_val, nnz); ALLOC(h->d_cval, nnz); ALLOC(h->d_val_orig, nnz);
+  ALLOC(h->d_AL_ptr, n_blocks + 1); H2D(h->d_AL_ptr, AL_ptr.data(), n_blocks + 1);
+  ALLOC(h->d_AL_ge, n_blocks); H2D(h->d_AL_ge, AL_ge.data(), n_blocks);
+  ALLOC(h->d_AU_ptr, n_blocks + 1); H2D(h->d_AU_ptr, AU_ptr.data(), n_blocks + 1);
+  ALLOC(h->d_AL_rc, h->nAL); if (h->nAL) H2D(h->d_AL_rc, AL_rc.data(), h->nAL);
+  ALLOC(h->d_AU_rc, h->nAU); if (h->nAU) H2D(h->d_AU_rc, AU_rc.data(), h->nAU);
+  ALLOC(h->d_AL_map, h->nAL); if (h->nAL) H2D(h->d_AL_map, AL_map.data(), h->nAL);
+  ALLOC(h->d_AU_map, h->nAU); if (h->nAU) H2D(h->d_AU_map, AU_map.data(), h->nAU);
+  ALLOC(h->d_AL_val, h->nAL); ALLOC(h->d_AU_val, h->nAU); ALLOC(h->d_val_orig, nnz);
   ALLOC(h->d_adj_ptr, n_blocks + 1); H2D(h->d_adj_ptr, adj_ptr.data(), n_blocks + 1);
   ALLOC(h->d_adj, adj.size()); if (!adj.empty()) H2D(h->d_adj, adj.data(), adj.size());
   ALLOC(h->d_pending0, n_blocks); H2D(h->d_pending0, pending0.data(), n_blocks);
@@ -353,12 +394,12 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   DevFactor &F = h->F;
   F.n = n; F.N = n_blocks;
   F.bstart = h->d_bstart; F.block_of = h->d_block_of;
-  F.rp = h->d_rp; F.ci = h->d_ci; F.val = h->d_val;
-  F.cp = h->d_cp; F.cr = h->d_cr; F.cval = h->d_cval;
+  F.AL_ptr = h->d_AL_ptr; F.AL_ge = h->d_AL_ge; F.AL_rc = h->d_AL_rc; F.AL_val = h->d_AL_val;
+  F.AU_ptr = h->d_AU_ptr; F.AU_rc = h->d_AU_rc; F.AU_val = h->d_AU_val;
   F.adj_ptr = h->d_adj_ptr; F.adj = h->d_adj;
   ALLOC(F.pending, n_blocks);
   ALLOC(F.queue, n_blocks);
-  ALLOC(F.ctrl, CTRL_COUNT);
+  ALLOC(F.ctrl, CTRL_COUNT * CS);
   ALLOC(F.Lrow_off, n_blocks); ALLOC(F.Lm, n_blocks); ALLOC(F.Lval_off, n_blocks);
   ALLOC(F.Ucol_off, n_blocks); ALLOC(F.Uc, n_blocks); ALLOC(F.Uval_off, n_blocks);
   ALLOC(F.D, h->D_off[n_blocks]);
@@ -376,8 +417,11 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
 
   // launch geometry: persistent CTAs, all co-resident
   F.smem_bytes = 110 * 1024;
+  if (const char *sk = getenv("BILU_SMEM_KB")) F.smem_bytes = std::max(16, std::min(220, atoi(sk))) * 1024;
   int per_sm = 0;
   if (bilu_factor_occupancy(F.smem_bytes, &per_sm) != cudaSuccess || per_sm < 1) per_sm = 1;
+  per_sm = 1;   // one CTA per SM: the rest of the unified L1/shared array caches panels
+  if (const char *cp = getenv("BILU_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(cp)));
   h->grid = opt.n_ctas > 0 ? opt.n_ctas : h->sms * per_sm;
 
   // initial capacities (grown on overflow)
@@ -401,8 +445,8 @@ extern "C" bilu_status bilu_set_values(bilu_ctx *h, const double *val, int32_t o
   cudaSetDevice(h->opt.device);
   CUDA_TRY(h, cudaMemcpyAsync(h->d_val_orig, val, h->nnz * sizeof(double),
                               on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
-  CUDA_TRY(h, bilu_launch_gather(h->d_val, h->d_val_orig, h->d_map_csr, h->nnz, h->stream));
-  CUDA_TRY(h, bilu_launch_gather(h->d_cval, h->d_val_orig, h->d_map_csc, h->nnz, h->stream));
+  if (h->nAL) CUDA_TRY(h, bilu_launch_gather(h->d_AL_val, h->d_val_orig, h->d_AL_map, h->nAL, h->stream));
+  if (h->nAU) CUDA_TRY(h, bilu_launch_gather(h->d_AU_val, h->d_val_orig, h->d_AU_map, h->nAU, h->stream));
   h->launches += 2;
   h->factored = false;
   return BILU_OK;
@@ -423,6 +467,7 @@ static bilu_status ensure_capacity(bilu_ctx *h) {
     CUDA_TRY(h, dalloc(h, &F.Uidx, h->cap_idx));
     F.cap_Lidx = F.cap_Uidx = h->cap_idx;
   }
+  if (!F.posmap) CUDA_TRY(h, dalloc(h, &F.posmap, (size_t)h->grid * h->n));
   if (F.work_per_cta != h->work_per_cta) {
     dfree(h, F.work);
     CUDA_TRY(h, dalloc(h, &F.work, (size_t)h->work_per_cta * h->grid));
@@ -454,9 +499,9 @@ static bilu_status reset_schedule(bilu_ctx *h) {
   CUDA_TRY(h, cudaMemsetAsync(F.queue, 0xFF, N * sizeof(int32_t), st));
   if (h->nready0)
     CUDA_TRY(h, cudaMemcpyAsync(F.queue, h->d_ready0, h->nready0 * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-  CUDA_TRY(h, cudaMemsetAsync(F.ctrl, 0, CTRL_COUNT * sizeof(unsigned long long), st));
-  unsigned long long qh = (unsigned long long)h->nready0;
-  CUDA_TRY(h, cudaMemcpyAsync(F.ctrl + CTRL_QHEAD, &qh, sizeof(qh), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h, cudaMemsetAsync(F.ctrl, 0, CTRL_COUNT * CS * sizeof(unsigned long long), st));
+  CUDA_TRY(h, cudaMemcpyAsync(F.ctrl + CS * CTRL_QHEAD, &h->nready0_ull, sizeof(unsigned long long),
+                              cudaMemcpyHostToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(F.lc.cnt, 0, N * sizeof(int), st));
   CUDA_TRY(h, cudaMemsetAsync(F.uc.cnt, 0, N * sizeof(int), st));
   CUDA_TRY(h, cudaMemsetAsync(F.succ.cnt, 0, N * sizeof(int), st));
@@ -620,11 +665,35 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
     CUDA_TRY(h, cudaEventRecord(e0, h->stream));
     bs = reset_schedule(h);
     if (bs != BILU_OK) return bs;
+    const char *dbg_env = getenv("BILU_DEBUG_TIMEOUT");
+    if (dbg_env && !F.dbg) {
+      void *hp = nullptr, *dp = nullptr;
+      CUDA_TRY(h, cudaHostAlloc(&hp, 4 * sizeof(int) * h->grid, cudaHostAllocMapped));
+      memset(hp, 0, 4 * sizeof(int) * h->grid);
+      CUDA_TRY(h, cudaHostGetDevicePointer(&dp, hp, 0));
+      F.dbg = (volatile int *)dp;
+      h->dbg_host = (volatile int *)hp;
+    }
     CUDA_TRY(h, bilu_launch_factor(F, h->grid, h->stream));
     launches = 1;
+    if (dbg_env) {
+      const double limit = atof(dbg_env);
+      const double t_start = (double)clock() / CLOCKS_PER_SEC;
+      while (cudaStreamQuery(h->stream) == cudaErrorNotReady) {
+        if ((double)clock() / CLOCKS_PER_SEC - t_start > limit) {
+          fprintf(stderr, "bilu watchdog: factor kernel still running after %.0f s; CTA progress (K, phase, blocks done):\n", limit);
+          for (int c = 0; c < h->grid; ++c)
+            if (h->dbg_host[4 * c + 2])
+              fprintf(stderr, "  cta %3d: K=%d phase=%d done=%d\n", c, h->dbg_host[4 * c], h->dbg_host[4 * c + 1], h->dbg_host[4 * c + 2]);
+          fflush(stderr);
+          _exit(3);
+        }
+      }
+    }
     CUDA_TRY(h, cudaEventRecord(e1, h->stream));
-    CUDA_TRY(h, cudaMemcpyAsync(ctrl, F.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(h->ctrl_full, F.ctrl, sizeof(h->ctrl_full), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    for (int i = 0; i < CTRL_COUNT; ++i) ctrl[i] = h->ctrl_full[CS * i];
     const int code = (int)ctrl[CTRL_ABORT];
     if (code == DEV_OK) {
       if (ctrl[CTRL_DONE] != (unsigned long long)h->N) {

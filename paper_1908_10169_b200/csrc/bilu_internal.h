@@ -47,6 +47,7 @@ enum : int {
   CTRL_FLOPS,
   CTRL_COUNT = 16
 };
+constexpr int CS = 16;   // ctrl stride: every control word on its own 128-byte line
 
 struct ChunkList {
   int *cnt;        // [N]   records appended per target
@@ -62,14 +63,16 @@ struct DevFactor {
   int32_t n, N;
   const int32_t *bstart;     // [N+1]
   const int32_t *block_of;   // [n]
-  // Ã, CSR and CSC
-  const int64_t *rp; const int32_t *ci; const double *val;
-  const int64_t *cp; const int32_t *cr; const double *cval;
+  // Ã per block: AL = entries of block column K with row >= s_K (sorted by row),
+  // packed rc = row << 7 | (col - s_K); AU = entries of block row K with col >= e_K,
+  // rc = col << 7 | (row - s_K).  AL_ge[K] = first AL entry with row >= e_K.
+  const int64_t *AL_ptr; const int64_t *AL_ge; const int32_t *AL_rc; const double *AL_val;
+  const int64_t *AU_ptr; const int32_t *AU_rc; const double *AU_val;
   // static schedule: block adjacency of sym(Ã), successors > J
   const int32_t *adj_ptr; const int32_t *adj;
   int32_t *pending;          // [N]
   int32_t *queue;            // [N]
-  unsigned long long *ctrl;  // [CTRL_COUNT]
+  unsigned long long *ctrl;  // [CTRL_COUNT * CS]
   // factors (per original block)
   int64_t *Lrow_off; int32_t *Lm; int64_t *Lval_off;
   int64_t *Ucol_off; int32_t *Uc; int64_t *Uval_off;
@@ -85,6 +88,8 @@ struct DevFactor {
   int32_t *near_i; double *near_m; int64_t near_cap;
   // per-CTA global workspace
   double *work; int64_t work_per_cta;   // doubles per CTA
+  int *posmap;                          // [grid * n] index -> occurrence / buffer line
+  volatile int *dbg;                    // mapped host memory for the deadlock watchdog (or NULL)
   int smem_bytes;
   double tau, near_rel;
 };
