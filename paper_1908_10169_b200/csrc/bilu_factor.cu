@@ -91,19 +91,17 @@ __device__ __forceinline__ int lbound_cg(const int *a, int lo, int hi, int key) 
 }
 
 // exclusive scan of a[0..n) in place (any memory), returns the total. CTA-wide.
+// Each warp owns a contiguous chunk and walks it in coalesced 32-element tiles
+// (no shared-memory bank conflicts): pass 1 sums, pass 2 scans with the carry.
 __device__ int cta_scan(int *a, int n, int *s_tmp /* >= NW+1 ints */) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int per = (n + NT - 1) / NT;
-  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  const int chunk = ((n + NW - 1) / NW + 31) & ~31;
+  const int lo = min(n, wid * chunk), hi = min(n, lo + chunk);
   int sum = 0;
-  for (int i = lo; i < hi; ++i) sum += a[i];
-  int x = sum;
+  for (int i = lo + lane; i < hi; i += 32) sum += a[i];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_tmp[wid] = x;
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) s_tmp[wid] = sum;
   __syncthreads();
   if (tid == 0) {
     int acc = 0;
@@ -111,9 +109,20 @@ __device__ int cta_scan(int *a, int n, int *s_tmp /* >= NW+1 ints */) {
     s_tmp[NW] = acc;
   }
   __syncthreads();
-  int run = s_tmp[wid] + x - sum;
-  for (int i = lo; i < hi; ++i) { int t = a[i]; a[i] = run; run += t; }
-  int total = s_tmp[NW];
+  int carry = s_tmp[wid];
+  for (int base = lo; base < hi; base += 32) {
+    const int i = base + lane;
+    const int v = i < hi ? a[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (i < hi) a[i] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  const int total = s_tmp[NW];
   __syncthreads();
   return total;
 }
@@ -450,12 +459,22 @@ __device__ bool side_update(const DevFactor &F, int K, int s, int e, int b, Cont
     }
     {
       int a = 0;
-      for (int t = tid; t < T; t += NT) {
-        while (a + 1 < nc && C[a + 1].item_off <= t) ++a;
-        const int i = t - C[a].item_off;
-        if (i < C[a].n_cand_skip) continue;                // rows inside K (pivot block)
-        const int r = cidx[(SIDE == 0 ? C[a].rows : C[a].cols) + i] - e;
-        atomicOr(&bm[r >> 5], 1u << (r & 31));
+      for (int t0 = tid; t0 < T; t0 += 4 * NT) {
+        int r4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u * NT;
+          r4[u] = -1;
+          if (t < T) {
+            while (a + 1 < nc && C[a + 1].item_off <= t) ++a;
+            const int i = t - C[a].item_off;
+            if (i >= C[a].n_cand_skip)                       // rows inside K are the pivot block
+              r4[u] = cidx[(SIDE == 0 ? C[a].rows : C[a].cols) + i] - e;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (r4[u] >= 0) atomicOr(&bm[r4[u] >> 5], 1u << (r4[u] & 31));
       }
     }
     __syncthreads();
@@ -634,51 +653,64 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   }
   __syncthreads();
   bool singular = false;
-  if (b <= 32) {
-    // one warp: lane j owns column j; no CTA barriers
+  if (b <= 8) {
+    // one warp, lane j holds column j of P_K in registers; pivot search by the lane
+    // that owns column k, broadcasts by shuffles (pivoting inside
+    // the block only; ties -> lowest row, R6)
     if (wid == 0) {
-      for (int k = 0; k < b; ++k) {
-        double best = -1.0; int bi = k;
-        if (k + lane < b) { best = fabs(P[k + lane + k * b]); bi = k + lane; }
+      double col[8];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          double ob = __shfl_down_sync(0xffffffffu, best, o);
-          int oi = __shfl_down_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      for (int i = 0; i < 8; ++i) col[i] = (lane < b && i < b) ? P[i + lane * b] : 0.0;
+      int piv_of[8];
+      bool sing = false;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < b && !sing) {
+          // argmax_{i >= k} |a_ik| on lane k
+          int bi = k; double best = -1.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) if (i >= k && i < b) { const double v = fabs(col[i]); if (v > best) { best = v; bi = i; } }
+          bi = __shfl_sync(0xffffffffu, bi, k);
+          best = __shfl_sync(0xffffffffu, best, k);
+          if (best == 0.0) { sing = true; }
+          else {
+            piv_of[k] = bi;
+            // swap rows k and bi in every column
+            double ck = 0.0, cb = 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { if (i == k) ck = col[i]; if (i == bi) cb = col[i]; }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { if (i == k) col[i] = cb; else if (i == bi) col[i] = ck; }
+            // f_i = a_ik (column k, lane k), d = 1 / a_kk
+            double f[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = __shfl_sync(0xffffffffu, col[i], k);
+            const double d = 1.0 / f[k];
+            const double pr = (lane == k) ? d : col[k] * d;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i != k) col[i] = ((lane == k) ? 0.0 : col[i]) - f[i] * pr;
+            col[k] = pr;
+          }
         }
-        best = __shfl_sync(0xffffffffu, best, 0);
-        bi = __shfl_sync(0xffffffffu, bi, 0);
-        if (best == 0.0) { singular = true; break; }
-        if (lane == 0) ipiv[k] = bi;
-        if (lane < b && bi != k) {
-          double t = P[k + lane * b]; P[k + lane * b] = P[bi + lane * b]; P[bi + lane * b] = t;
+      }
+      if (!sing) {
+        // undo the row interchanges as column interchanges, in reverse order
+#pragma unroll
+        for (int k = 7; k >= 0; --k) {
+          if (k < b) {
+            const int pv = piv_of[k];
+            const int partner = (lane == k) ? pv : (lane == pv ? k : lane);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) col[i] = __shfl_sync(0xffffffffu, col[i], partner);
+          }
         }
-        __syncwarp();
-        const double d = 1.0 / P[k + k * b];
-        if (lane < b) fcol[lane] = P[lane + k * b];
-        __syncwarp();
         if (lane < b) {
-          const int j = lane;
-          const double pr = (j == k) ? d : P[k + j * b] * d;
-          for (int i = 0; i < b; ++i) {
-            if (i == k) continue;
-            const double base = (j == k) ? 0.0 : P[i + j * b];
-            P[i + j * b] = base - fcol[i] * pr;
-          }
-          P[k + j * b] = pr;
-        }
-        __syncwarp();
-      }
-      if (!singular) {
-        for (int k = b - 1; k >= 0; --k) {
-          const int pv = ipiv[k];
-          if (pv != k && lane < b) {
-            double t = P[lane + k * b]; P[lane + k * b] = P[lane + pv * b]; P[lane + pv * b] = t;
-          }
-          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) if (i < b) P[i + lane * b] = col[i];
         }
       }
-      if (lane == 0) S.piv = singular ? 1 : 0;
+      if (lane == 0) S.piv = sing ? 1 : 0;
     }
     __syncthreads();
     singular = S.piv != 0;

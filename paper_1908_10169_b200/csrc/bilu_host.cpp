@@ -651,6 +651,7 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
   DevFactor &F = h->F;
   F.tau = tau;
   F.near_rel = h->opt.near_rel;
+  F.exp = getenv("BILU_EXP") ? atoi(getenv("BILU_EXP")) : 0;
   bilu_factor_stats S{};
   S.breakdown_block = -1;
   S.n_blocks_init = h->N;

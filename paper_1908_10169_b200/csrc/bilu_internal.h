@@ -92,6 +92,7 @@ struct DevFactor {
   volatile int *dbg;                    // mapped host memory for the deadlock watchdog (or NULL)
   int smem_bytes;
   double tau, near_rel;
+  int exp;                              // experiment switches (diagnostics only)
 };
 
 struct MergeArgs {

@@ -278,38 +278,99 @@ __global__ void __launch_bounds__(MT) merge_count_kernel(MergeArgs M) {
 
 // descriptors: singletons keep their arena slices; merged blocks are appended
 // after the factor kernel's cursors (tot[0..3] on entry).  One CTA.
-__global__ void merge_offsets_kernel(MergeArgs M) {
-  if (threadIdx.x != 0) return;
+// block-wide exclusive scan of NV 64-bit values per thread (1024 threads)
+template <int NV>
+__device__ void block_scan_ull(unsigned long long (&v)[NV], unsigned long long (&tot)[NV]) {
+  __shared__ unsigned long long sw[NV][32];
+  __shared__ unsigned long long st[NV];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    unsigned long long x = v[j];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[j][wid] = x;
+    v[j] = x - v[j];   // exclusive within the warp
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      unsigned long long x = lane < nw ? sw[j][lane] : 0ull, x0 = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane < nw) sw[j][lane] = x - x0;
+      if (lane == 31) st[j] = x;      // total (nw <= 32)
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NV; ++j) { v[j] += sw[j][wid]; tot[j] = st[j]; }
+  __syncthreads();
+}
+
+// descriptors: singletons keep their arena slices; merged blocks are appended after
+// the factor kernel's cursors (tot[0..3] on entry).  One CTA of 1024 threads, each
+// owning a contiguous range of final blocks.
+__global__ void __launch_bounds__(1024) merge_offsets_kernel(MergeArgs M) {
   const int nF = *M.nF;
-  unsigned long long cLi = M.tot[0], cLv = M.tot[1], cUi = M.tot[2], cUv = M.tot[3];
-  unsigned long long cD = 0, maxws = 0, nL = 0, nU = 0, iL = 0, iU = 0;
-  long long nmerged = 0;
-  for (int F = 0; F < nF; ++F) {
+  const int per = (nF + blockDim.x - 1) / blockDim.x;
+  const int lo = min(nF, (int)threadIdx.x * per), hi = min(nF, lo + per);
+  // per-thread sums: D, Li, Lv, Ui, Uv (merged only), nL, nU, iL, iU, nmerged
+  unsigned long long v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long maxws = 0;
+  for (int F = lo; F < hi; ++F) {
     const int a = M.first[F], k = M.first[F + 1] - 1;
-    const long long P = M.bstart[k + 1] - M.bstart[a];
+    const unsigned long long P = M.bstart[k + 1] - M.bstart[a];
+    const unsigned long long u = M.fLm[F], w = M.fUc[F];
+    v[0] += P * P;
+    if (a != k) {
+      v[1] += u; v[2] += u * P; v[3] += w; v[4] += w * P; v[9] += 1;
+      const unsigned long long ws = 6ull * P * P + (u + w) * P + 64;
+      if (ws > maxws) maxws = ws;
+    }
+    v[5] += u * P; v[6] += w * P; v[7] += u; v[8] += w;
+  }
+  unsigned long long tot[10];
+  block_scan_ull<10>(v, tot);
+  unsigned long long cD = v[0], cLi = M.tot[0] + v[1], cLv = M.tot[1] + v[2], cUi = M.tot[2] + v[3],
+                     cUv = M.tot[3] + v[4];
+  for (int F = lo; F < hi; ++F) {
+    const int a = M.first[F], k = M.first[F + 1] - 1;
+    const unsigned long long P = M.bstart[k + 1] - M.bstart[a];
     M.fD_off[F] = (int64_t)cD;
     cD += P * P;
-    nL += (unsigned long long)M.fLm[F] * P; iL += M.fLm[F];
-    nU += (unsigned long long)M.fUc[F] * P; iU += M.fUc[F];
     if (a == k) {
       M.fLrow_off[F] = M.Lrow_off[k]; M.fLval_off[F] = M.Lval_off[k];
       M.fUcol_off[F] = M.Ucol_off[k]; M.fUval_off[F] = M.Uval_off[k];
     } else {
-      const long long u = M.fLm[F], v = M.fUc[F];
+      const unsigned long long u = M.fLm[F], w = M.fUc[F];
       M.fLrow_off[F] = (int64_t)cLi; cLi += u;
       M.fLval_off[F] = (int64_t)cLv; cLv += u * P;
-      M.fUcol_off[F] = (int64_t)cUi; cUi += v;
-      M.fUval_off[F] = (int64_t)cUv; cUv += v * P;
-      unsigned long long ws = 6ull * P * P + (unsigned long long)(u + v) * P + 64;
-      if (ws > maxws) maxws = ws;
-      ++nmerged;
+      M.fUcol_off[F] = (int64_t)cUi; cUi += w;
+      M.fUval_off[F] = (int64_t)cUv; cUv += w * P;
     }
   }
-  M.fD_off[nF] = (int64_t)cD;
-  M.tot[4] = cLi; M.tot[5] = cLv; M.tot[6] = cUi; M.tot[7] = cUv;
-  M.tot[8] = cD; M.tot[9] = maxws; M.tot[10] = (unsigned long long)nmerged;
-  M.tot[11] = (unsigned long long)(M.N - nF);
-  M.tot[12] = nL; M.tot[13] = nU; M.tot[14] = iL; M.tot[15] = iU;
+  // max workspace: reduce
+  __shared__ unsigned long long smax;
+  if (threadIdx.x == 0) smax = 0;
+  __syncthreads();
+  atomicMax(&smax, maxws);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    M.fD_off[nF] = (int64_t)tot[0];
+    M.tot[4] = M.tot[0] + tot[1]; M.tot[5] = M.tot[1] + tot[2];
+    M.tot[6] = M.tot[2] + tot[3]; M.tot[7] = M.tot[3] + tot[4];
+    M.tot[8] = tot[0]; M.tot[9] = smax; M.tot[10] = tot[9];
+    M.tot[11] = (unsigned long long)(M.N - nF);
+    M.tot[12] = tot[5]; M.tot[13] = tot[6]; M.tot[14] = tot[7]; M.tot[15] = tot[8];
+  }
 }
 
 // ---------------------------------------------------------------- M4: arithmetic
@@ -483,7 +544,7 @@ extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_
   merge_test_kernel<<<grid, MT, smem, st>>>(M);
   merge_scan_kernel<<<1, 256, 0, st>>>(M);
   merge_count_kernel<<<grid, MT, 1024 * 4, st>>>(M);
-  merge_offsets_kernel<<<1, 32, 0, st>>>(M);
+  merge_offsets_kernel<<<1, 1024, 0, st>>>(M);
   return cudaGetLastError();
 }
 
