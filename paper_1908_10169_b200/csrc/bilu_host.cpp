@@ -34,6 +34,8 @@ extern "C" cudaError_t bilu_launch_gather(double *dst, const double *src, const 
 extern "C" cudaError_t bilu_launch_permute(double *y, const double *x, const int32_t *perm,
                                            int32_t n, int inverse, cudaStream_t st);
 extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_t st);
+extern "C" int bilu_merge_plan_launches();
+extern "C" int bilu_merge_nchunks(int N);
 extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
                                         cudaStream_t st);
 extern "C" cudaError_t bilu_launch_apply(const ApplyArgs &A, int grid, int backward, cudaStream_t st);
@@ -558,6 +560,30 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       CUDA_TRY(h, dalloc(h, &M.fUcol_off, (size_t)N)); CUDA_TRY(h, dalloc(h, &M.fUval_off, (size_t)N));
       CUDA_TRY(h, dalloc(h, &M.fD_off, (size_t)N + 1));
       CUDA_TRY(h, dalloc(h, &M.tot, 16)); CUDA_TRY(h, dalloc(h, &M.flops, 1)); CUDA_TRY(h, dalloc(h, &M.ovf, 1));
+      // test windows: W_k = largest W <= 127 with s_k - s_{k-W} + q_k <= max_block
+      {
+        std::vector<int64_t> wofs(N);
+        int64_t acc = 0;
+        const std::vector<int32_t> &bs = h->bstart;
+        for (int k = 0; k < N; ++k) {
+          int W = 0;
+          if (k > 0) {
+            const int sk = bs[k], q = bs[k + 1] - sk;
+            while (k - 1 - W >= 0 && (sk - bs[k - 1 - W]) + q <= h->opt.max_block && W < 127) ++W;
+          }
+          wofs[k] = acc;
+          acc += W + 1;
+        }
+        int64_t *d_wofs = nullptr;
+        CUDA_TRY(h, dalloc(h, &d_wofs, (size_t)N));
+        CUDA_TRY(h, cudaMemcpy(d_wofs, wofs.data(), N * sizeof(int64_t), cudaMemcpyHostToDevice));
+        M.wofs = d_wofs;
+        CUDA_TRY(h, dalloc(h, &M.UV, 2 * (size_t)std::max<int64_t>(acc, 1)));
+        const int nch = bilu_merge_nchunks(N);
+        CUDA_TRY(h, dalloc(h, &M.chunkmap, (size_t)std::max(nch, 1) * 128));
+        CUDA_TRY(h, dalloc(h, &M.chunkstart, (size_t)std::max(nch, 1)));
+        CUDA_TRY(h, dalloc(h, &M.flag, (size_t)N));
+      }
       h->merge_work_ints = 16384;
       CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * h->grid));
       h->fD_cap = std::max<int64_t>(h->D_off[N], 1);
@@ -578,7 +604,7 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       CUDA_TRY(h, cudaMemsetAsync(M.ovf, 0, sizeof(int), h->stream));
       CUDA_TRY(h, cudaMemsetAsync(M.flops, 0, sizeof(double), h->stream));
       CUDA_TRY(h, bilu_merge_plan(M, h->grid, h->stream));
-      launches += 4;
+      launches += bilu_merge_plan_launches();
       int ovf = 0;
       CUDA_TRY(h, cudaMemcpyAsync(tot, M.tot, sizeof(tot), cudaMemcpyDeviceToHost, h->stream));
       CUDA_TRY(h, cudaMemcpyAsync(&ovf, M.ovf, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -605,7 +631,8 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       h->fD_cap = (int64_t)tot[8] + (int64_t)tot[8] / 4;
       CUDA_TRY(h, dalloc(h, &M.fD, h->fD_cap));
     }
-    const int64_t need_dw = (int64_t)tot[9];
+    // per-CTA dense L_aa, U_aa of runs wider than the shared-memory tile
+    const int64_t need_dw = 2 * (int64_t)h->opt.max_block * h->opt.max_block;
     if (need_dw > h->merge_dwork) {
       dfree(h, h->d_mdwork);
       h->merge_dwork = need_dw;
@@ -613,14 +640,25 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
     }
     M.Lidx = F.Lidx; M.Uidx = F.Uidx; M.Lval = F.Lval; M.Uval = F.Uval;
     M.Lidx_out = F.Lidx; M.Uidx_out = F.Uidx; M.Lval_out = F.Lval; M.Uval_out = F.Uval;
-    CUDA_TRY(h, bilu_merge_arith(M, h->d_mdwork, std::max<int64_t>(h->merge_dwork, 1), h->grid, h->stream));
-    launches += 1;
     double mfl = 0.0;
-    int ovf = 0;
-    CUDA_TRY(h, cudaMemcpyAsync(&mfl, M.flops, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(h, cudaMemcpyAsync(&ovf, M.ovf, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-    if (ovf) { set_err(h, "bilu_factor: merge workspace overflow in arithmetic"); return BILU_ERR_OOM; }
+    for (int attempt = 0;; ++attempt) {
+      int ovf = 0;
+      CUDA_TRY(h, cudaMemsetAsync(M.ovf, 0, sizeof(int), h->stream));
+      CUDA_TRY(h, cudaMemsetAsync(M.flops, 0, sizeof(double), h->stream));
+      CUDA_TRY(h, bilu_merge_arith(M, h->d_mdwork, h->merge_dwork, h->grid, h->stream));
+      launches += 1;
+      CUDA_TRY(h, cudaMemcpyAsync(&mfl, M.flops, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(h, cudaMemcpyAsync(&ovf, M.ovf, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      if (!ovf) break;
+      if (ovf == 2) { set_err(h, "bilu_factor: merged union size differs from the aggregation test"); return BILU_ERR_STATE; }
+      if (attempt > 8) { set_err(h, "bilu_factor: merge workspace overflow in arithmetic"); return BILU_ERR_OOM; }
+      dfree(h, M.work);
+      h->merge_work_ints *= 4;
+      CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * h->grid));
+      M.work_ints = h->merge_work_ints;
+      S.n_retries++;
+    }
     S.flops += mfl;
     fin.nF = nF;
     fin.bstart = M.fbstart;

@@ -104,6 +104,11 @@ struct MergeArgs {
   const double *Lval; const double *Uval; const double *D; const int64_t *D_off;
   // outputs / workspace
   uint32_t *T;            // [4N] test bitmasks, bit d-1 <=> merge(a = k-d, k)
+  const int64_t *wofs;    // [N] offsets of the per-block windows (W_k + 1 entries each)
+  int32_t *UV;            // [2 * sum(W_k + 1)] union sizes u(d), v(d) of the test
+  uint8_t *chunkmap;      // [nchunks * 128] scan state maps
+  uint8_t *chunkstart;    // [nchunks]
+  int32_t *flag;          // [N] run-start flags
   int32_t *first;         // [N+1] first original block of each final block
   int32_t *nF;            // [1]
   int32_t *fbstart;       // [N+1]

@@ -6,12 +6,17 @@
 // the merge happens during or after the factorization;
 // the decisions only depend on index sets ("checking the union of nonzero index
 // sets ignoring any cancellations").  The sequential scan of
-// the paper is made parallel by evaluating the test for every (aggregate start
-// a, block k) pair that max_block allows (merge_test_kernel), after which the
-// scan itself is a walk over bitmasks (merge_scan_kernel).  The merged factors
-// of a whole run a..k are then formed in closed form (merge_arith_kernel):
-//   L^ = L_{>,agg} L_aa^{-1},  Ũ^ = L_aa Ũ_{agg,>},  D^ = U_aa^{-1} D_agg L_aa^{-1}
-// which is the paper's pairwise update applied k-a times (DESIGN.md derives it).
+// the paper is made parallel in three steps:
+//   merge_test_kernel   the test of Sec. 3.5 for every (aggregate start a = k-d,
+//                       block k) pair that max_block allows -> bitmask T[k] and
+//                       the union sizes u(d), v(d)
+//   merge_scan_kernel   the paper's left-to-right scan as a composition of
+//                       per-chunk state maps (state = distance to the run start)
+//   merge_offsets_kernel descriptors and arena offsets of the final blocks
+//   merge_arith_kernel  the merged factors of each run a..k, formed with block
+//                       triangular solves over the member blocks:
+//     D^ = U_aa^{-1} D_agg L_aa^{-1},  L^ = L_{>,agg} L_aa^{-1},  Ũ^ = L_aa Ũ_{agg,>}
+//   (the paper's pairwise update applied k-a times; DESIGN.md derives it).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <climits>
@@ -22,13 +27,18 @@ namespace bilu {
 
 constexpr int MT = 256;
 constexpr int MW = MT / 32;
-
-// MergeArgs: see bilu_internal.h
+constexpr int TEST_T = 128;            // threads of merge_test_kernel
+constexpr int TEST_STAGE = 6144;       // list elements staged in shared memory per side
+constexpr int SCAN_CHUNK = 256;        // blocks per chunk of the parallel scan
+constexpr int ARITH_KEYS = 4096;       // union keys sorted in shared memory
+constexpr int ARITH_PSMEM = 64;        // runs with P <= this keep L_aa, U_aa in shared memory
 
 // ----------------------------------------------------------- CTA helpers
+template <int NTH>
 __device__ int m_scan(int *a, int n, int *s_tmp) {
+  constexpr int NWp = NTH / 32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int per = (n + MT - 1) / MT;
+  const int per = (n + NTH - 1) / NTH;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
   int sum = 0;
   for (int i = lo; i < hi; ++i) sum += a[i];
@@ -42,13 +52,13 @@ __device__ int m_scan(int *a, int n, int *s_tmp) {
   __syncthreads();
   if (tid == 0) {
     int acc = 0;
-    for (int w = 0; w < MW; ++w) { int t = s_tmp[w]; s_tmp[w] = acc; acc += t; }
-    s_tmp[MW] = acc;
+    for (int w = 0; w < NWp; ++w) { int t = s_tmp[w]; s_tmp[w] = acc; acc += t; }
+    s_tmp[NWp] = acc;
   }
   __syncthreads();
   int run = s_tmp[wid] + x - sum;
   for (int i = lo; i < hi; ++i) { int t = a[i]; a[i] = run; run += t; }
-  int total = s_tmp[MW];
+  int total = s_tmp[NWp];
   __syncthreads();
   return total;
 }
@@ -75,9 +85,13 @@ __device__ __forceinline__ int m_lbound(const int *a, int lo, int hi, int key) {
   }
   return lo;
 }
+__device__ __forceinline__ bool m_contains(const int *a, int n, int key) {
+  int p = m_lbound(a, 0, n, key);
+  return p < n && a[p] == key;
+}
 
 // the test of Sec. 3.5: mu = p(p+r+s+r'+s') + q(q+t+t'), nu = (p+q)(p+q+u+v);
-// merge iff nu <= 1.2 mu (exactly: 5 nu <= 6 mu) or nu <= mu + 2(p+q); p+q <= max_block
+// merge iff nu <= 1.2 mu (exactly: 5 nu <= 6 mu, R10) or nu <= mu + 2(p+q); p+q <= max_block
 __device__ __forceinline__ bool agg_test(long long p, long long q, long long r, long long s, long long t,
                                          long long r2, long long s2, long long t2, long long u, long long v,
                                          long long max_block) {
@@ -87,198 +101,185 @@ __device__ __forceinline__ bool agg_test(long long p, long long q, long long r, 
   return (5 * nu <= 6 * mu) || (nu <= mu + 2 * (p + q));
 }
 
+// window of block k: the largest W with s_k - s_{k-W} + q <= max_block (W <= 127)
+__device__ __forceinline__ int merge_window(const int32_t *bstart, int k, int max_block) {
+  const int s_k = bstart[k], q = bstart[k + 1] - s_k;
+  int W = 0;
+  while (k - 1 - W >= 0 && (s_k - bstart[k - 1 - W]) + q <= max_block && W < 127) ++W;
+  return W;
+}
+
 // ---------------------------------------------------------------- M1: test
-// For block k and every candidate start a = k-d (d = 1..W), compute r,s,u (rows)
-// and r',s',v (cols) of the aggregate (a..k-1) against k from the histogram of
-// dmin(x) = distance k-j of the closest member j whose kept set contains x.
-__device__ void count_side(const MergeArgs &M, int k, int W, bool rows, int *keys, int cap,
-                           int *hist /* 3*(W+2) */, int *cnt /* W+2 */, int *s_tmp, int &t_out) {
+// One side (rows of L or columns of Ũ) of block k: the lists l_d = kept indices
+// >= s_k of member k-d (d = 0..W).  For the aggregate a..k-1 with a = k-d:
+//   r(d) = |∪_{1..d} l_d' ∩ block k|, s(d) = |∪_{1..d} l_d' ∩ [e_k, n)|,
+//   u(d) = |l_0 ∪ (∪_{1..d} l_d' ∩ [e_k, n))|, t = |l_0|.
+// An element of l_d is counted at d iff it is in none of l_1..l_{d-1}.
+struct TestSide {
+  int t;
+  int r[128], s[128], u[128];   // cumulative, index d (0 unused)
+};
+
+__device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *stage, int *s_len, int *s_off,
+                          const int **s_ptr, TestSide &R, int *s_tmp) {
   const int tid = threadIdx.x;
   const int s_k = M.bstart[k], e_k = M.bstart[k + 1];
   const int32_t *idx = rows ? M.Lidx : M.Uidx;
   const int64_t *off = rows ? M.Lrow_off : M.Ucol_off;
   const int32_t *len = rows ? M.Lm : M.Uc;
-  // members j = k-W .. k (d = k - j); suffix >= s_k
-  for (int d = tid; d <= W; d += MT) {
-    int j = k - d;
+  for (int d = tid; d <= W; d += TEST_T) {
+    const int j = k - d;
     const int32_t *L = idx + off[j];
-    int m = len[j];
-    int p0 = 0, p1 = m;
-    while (p0 < p1) { int mid = (p0 + p1) >> 1; if (L[mid] < s_k) p0 = mid + 1; else p1 = mid; }
-    cnt[d] = m - p0;
+    const int m = len[j];
+    const int p0 = m_lbound(L, 0, m, s_k);
+    s_len[d] = m - p0;
+    s_ptr[d] = L + p0;
   }
-  for (int i = tid; i < 3 * (W + 2); i += MT) hist[i] = 0;
+  for (int d = tid; d < 128; d += TEST_T) { R.r[d] = 0; R.s[d] = 0; R.u[d] = 0; }
   __syncthreads();
-  t_out = cnt[0];
-  int total = m_scan(cnt, W + 1, s_tmp);
-  { int pw0 = 1; while (pw0 < total) pw0 <<= 1;
-    if (pw0 > cap) { if (tid == 0) atomicExch(M.ovf, 1); return; } }
-  for (int d = 0; d <= W; ++d) {
-    int j = k - d;
-    const int32_t *L = idx + off[j];
-    int m = len[j];
-    int c = (d < W ? cnt[d + 1] : total) - cnt[d];
-    for (int i = tid; i < c; i += MT) keys[cnt[d] + i] = (L[m - c + i] << 8) | d;
+  if (tid == 0) {
+    int acc = 0;
+    for (int d = 0; d <= W; ++d) { s_off[d] = acc; acc += s_len[d]; }
+    s_off[W + 1] = acc;
+    R.t = s_len[0];
   }
-  int pw = 1; while (pw < total) pw <<= 1;
-  for (int i = total + tid; i < pw; i += MT) keys[i] = INT_MAX;
   __syncthreads();
-  if (pw > 1) m_bitonic(keys, pw);
-  for (int i = tid; i < total; i += MT) {
-    int key = keys[i], x = key >> 8, d = key & 255;
-    if (i > 0 && (keys[i - 1] >> 8) == x) continue;   // not the first of its value
-    bool inK = (d == 0);
-    int dmin = d;
-    if (inK) dmin = (i + 1 < total && (keys[i + 1] >> 8) == x) ? (keys[i + 1] & 255) : -1;
-    if (x < e_k) {                       // inside block k: r (d >= 1 always here)
-      atomicAdd(&hist[dmin], 1);
-    } else {
-      if (dmin > 0) atomicAdd(&hist[(W + 2) + dmin], 1);           // s
-      atomicAdd(&hist[2 * (W + 2) + (inK ? 1 : dmin)], 1);         // u
+  const int total = s_off[W + 1];
+  const bool staged = total <= TEST_STAGE;
+  if (staged) {
+    for (int d = 0; d <= W; ++d) {
+      const int *src = s_ptr[d];
+      int *dst = stage + s_off[d];
+      for (int i = tid; i < s_len[d]; i += TEST_T) dst[i] = src[i];
+    }
+    __syncthreads();
+    for (int d = tid; d <= W; d += TEST_T) s_ptr[d] = stage + s_off[d];
+    __syncthreads();
+  }
+  for (int x = s_len[0] + tid; x < total; x += TEST_T) {
+    // list of element x: last d with s_off[d] <= x
+    int lo = 1, hi = W;
+    while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= x) lo = mid; else hi = mid - 1; }
+    const int d = lo;
+    const int key = s_ptr[d][x - s_off[d]];
+    bool first = true;
+    for (int d2 = 1; d2 < d && first; ++d2) first = !m_contains(s_ptr[d2], s_len[d2], key);
+    if (!first) continue;
+    if (key < e_k) atomicAdd(&R.r[d], 1);
+    else {
+      atomicAdd(&R.s[d], 1);
+      if (!m_contains(s_ptr[0], s_len[0], key)) atomicAdd(&R.u[d], 1);
     }
   }
   __syncthreads();
   if (tid == 0) {
-    for (int d = 1; d <= W; ++d) {
-      hist[d] += hist[d - 1];
-      hist[(W + 2) + d] += hist[(W + 2) + d - 1];
-      hist[2 * (W + 2) + d] += hist[2 * (W + 2) + d - 1];
-    }
+    int r = 0, s = 0, u = R.t;
+    for (int d = 1; d <= W; ++d) { r += R.r[d]; s += R.s[d]; u += R.u[d]; R.r[d] = r; R.s[d] = s; R.u[d] = u; }
   }
   __syncthreads();
+  (void)s_tmp;
 }
 
-__global__ void __launch_bounds__(MT) merge_test_kernel(MergeArgs M) {
-  extern __shared__ int msm[];
-  __shared__ int s_tmp[MW + 1];
+__global__ void __launch_bounds__(TEST_T) merge_test_kernel(MergeArgs M) {
+  __shared__ int stage[TEST_STAGE];
+  __shared__ int s_len[129], s_off[130];
+  __shared__ const int *s_ptr[129];
+  __shared__ TestSide SR, SC;
+  __shared__ uint32_t s_mask[4];
+  __shared__ int s_tmp[8];
   const int tid = threadIdx.x;
-  const int cap = (int)M.work_ints;
-  int *keys = M.work + (size_t)blockIdx.x * M.work_ints;
-  int *hr = msm;              // 3 * 130
-  int *hc = msm + 3 * 130;    // 3 * 130
-  int *cnt = msm + 6 * 130;   // 130
   for (int k = blockIdx.x; k < M.N; k += gridDim.x) {
-    uint32_t mask[4] = {0, 0, 0, 0};
-    if (k > 0) {
+    if (tid < 4) s_mask[tid] = 0u;
+    const int W = k > 0 ? merge_window(M.bstart, k, M.max_block) : 0;
+    __syncthreads();
+    if (W > 0) {
+      test_side(M, k, W, true, stage, s_len, s_off, s_ptr, SR, s_tmp);
+      test_side(M, k, W, false, stage, s_len, s_off, s_ptr, SC, s_tmp);
       const int s_k = M.bstart[k], q = M.bstart[k + 1] - s_k;
-      int W = 0;
-      while (k - 1 - W >= 0 && (s_k - M.bstart[k - 1 - W]) + q <= M.max_block && W < 127) ++W;
-      if (W > 0) {
-        int t = 0, t2 = 0;
-        count_side(M, k, W, true, keys, cap, hr, cnt, s_tmp, t);
-        __syncthreads();
-        count_side(M, k, W, false, keys, cap, hc, cnt, s_tmp, t2);
-        __syncthreads();
-        if (tid == 0) {
-          for (int d = 1; d <= W; ++d) {
-            long long p = s_k - M.bstart[k - d];
-            long long r = hr[d], s = hr[(W + 2) + d], u = hr[2 * (W + 2) + d];
-            long long r2 = hc[d], s2 = hc[(W + 2) + d], v = hc[2 * (W + 2) + d];
-            if (agg_test(p, q, r, s, t, r2, s2, t2, u, v, M.max_block)) mask[(d - 1) >> 5] |= 1u << ((d - 1) & 31);
-          }
-        }
+      int32_t *uv = M.UV + 2 * M.wofs[k];
+      for (int d = 1 + tid; d <= W; d += TEST_T) {
+        const long long p = s_k - M.bstart[k - d];
+        if (agg_test(p, q, SR.r[d], SR.s[d], SR.t, SC.r[d], SC.s[d], SC.t, SR.u[d], SC.u[d], M.max_block))
+          atomicOr(&s_mask[(d - 1) >> 5], 1u << ((d - 1) & 31));
+        uv[2 * d] = SR.u[d];
+        uv[2 * d + 1] = SC.u[d];
       }
     }
-    if (tid == 0) for (int w = 0; w < 4; ++w) M.T[4 * (size_t)k + w] = mask[w];
+    __syncthreads();
+    if (tid < 4) M.T[4 * (size_t)k + tid] = s_mask[tid];
     __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------- M2: scan
 // The paper's order: after block k is finished, merge it into the aggregate
-// that ends at k-1 iff the test passes.
-__global__ void merge_scan_kernel(MergeArgs M) {
-  __shared__ uint32_t sT[4 * 1024];
-  int a = 0, nF = 0;
-  if (threadIdx.x == 0) { M.first[0] = 0; nF = 1; }
-  for (int base = 0; base < M.N; base += 1024) {
-    int cnt = min(1024, M.N - base);
-    for (int i = threadIdx.x; i < 4 * cnt; i += blockDim.x) sT[i] = M.T[4 * (size_t)base + i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int i = (base == 0 ? 1 : 0); i < cnt; ++i) {
-        int k = base + i;
-        int d = k - a;
-        bool merge = d >= 1 && d <= 128 && ((sT[4 * i + ((d - 1) >> 5)] >> ((d - 1) & 31)) & 1u);
-        if (!merge) { a = k; M.first[nF++] = k; }
-      }
-    }
-    __syncthreads();
+// that ends at k-1 iff the test passes.  State before block
+// k: d = (k-1) - a, a = start of the current run; k merges iff bit d of T[k] is set
+// (then d' = d+1, else d' = 0).  Chunks of SCAN_CHUNK blocks map every start state
+// (0..127) to an end state in parallel; one thread composes the chunk maps; every
+// chunk is then replayed from its true start state.
+__global__ void __launch_bounds__(128) merge_chunkmap_kernel(MergeArgs M) {
+  const int c = blockIdx.x, st0 = threadIdx.x;
+  const int k0 = 1 + c * SCAN_CHUNK, k1 = min(M.N, k0 + SCAN_CHUNK);
+  int d = st0;
+  for (int k = k0; k < k1; ++k) {
+    const uint32_t w = __ldg(&M.T[4 * (size_t)k + (d >> 5)]);
+    d = (d < 127 && ((w >> (d & 31)) & 1u)) ? d + 1 : 0;
   }
-  if (threadIdx.x == 0) { M.first[nF] = M.N; *M.nF = nF; }
+  M.chunkmap[(size_t)c * 128 + st0] = (uint8_t)d;
 }
 
-// --------------------------------------------------- M3: union sizes, descriptors
-// union of the members' kept indices >= e_k (rows of L^ / cols of Ũ^)
-__device__ int gather_union(const MergeArgs &M, int a, int k, bool rows, int *keys, int cap, int *cnt, int *s_tmp,
-                            int *flags) {
+__global__ void __launch_bounds__(1024) merge_scan_kernel(MergeArgs M, int nchunks) {
+  __shared__ int s_tmp[33];
   const int tid = threadIdx.x;
-  const int e_k = M.bstart[k + 1];
-  const int32_t *idx = rows ? M.Lidx : M.Uidx;
-  const int64_t *off = rows ? M.Lrow_off : M.Ucol_off;
-  const int32_t *len = rows ? M.Lm : M.Uc;
-  const int nm = k - a + 1;
-  for (int x = tid; x < nm; x += MT) {
-    int j = a + x;
-    const int32_t *L = idx + off[j];
-    int m = len[j];
-    int p0 = 0, p1 = m;
-    while (p0 < p1) { int mid = (p0 + p1) >> 1; if (L[mid] < e_k) p0 = mid + 1; else p1 = mid; }
-    cnt[x] = m - p0;
+  // compose the chunk maps (sequential over chunks, one thread)
+  if (tid == 0) {
+    int d = 0;
+    for (int c = 0; c < nchunks; ++c) { M.chunkstart[c] = (uint8_t)d; d = M.chunkmap[(size_t)c * 128 + d]; }
   }
   __syncthreads();
-  int total = m_scan(cnt, nm, s_tmp);
-  int pw = 1; while (pw < total) pw <<= 1;
-  if (2 * pw > cap) { if (tid == 0) atomicExch(M.ovf, 1); return -1; }
-  for (int x = 0; x < nm; ++x) {
-    int j = a + x;
-    const int32_t *L = idx + off[j];
-    int m = len[j];
-    int c = (x + 1 < nm ? cnt[x + 1] : total) - cnt[x];
-    for (int i = tid; i < c; i += MT) keys[cnt[x] + i] = L[m - c + i];
-  }
-  for (int i = total + tid; i < pw; i += MT) keys[i] = INT_MAX;
-  __syncthreads();
-  if (pw > 1) m_bitonic(keys, pw);
-  for (int i = tid; i < total; i += MT) flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
-  __syncthreads();
-  int u = m_scan(flags, total, s_tmp);
-  for (int base = 0; base < total; base += MT) {
-    int i = base + tid; int v = 0, pos = -1;
-    if (i < total) { v = keys[i]; int nxt = i + 1 < total ? flags[i + 1] : u; if (nxt > flags[i]) pos = flags[i]; }
-    __syncthreads();
-    if (pos >= 0) keys[pos] = v;
-    __syncthreads();
-  }
-  return u;
-}
-
-__global__ void __launch_bounds__(MT) merge_count_kernel(MergeArgs M) {
-  extern __shared__ int msm[];
-  __shared__ int s_tmp[MW + 1];
-  const int nF = *M.nF;
-  int *keys = M.work + (size_t)blockIdx.x * M.work_ints;
-  const int cap = (int)M.work_ints;
-  int *cnt = msm;
-  for (int F = blockIdx.x; F < nF; F += gridDim.x) {
-    const int a = M.first[F], k = M.first[F + 1] - 1;
-    if (threadIdx.x == 0) M.fbstart[F] = M.bstart[a];
-    if (a == k) {
-      if (threadIdx.x == 0) { M.fLm[F] = M.Lm[k]; M.fUc[F] = M.Uc[k]; }
-      continue;
+  // replay: flag[k] = 1 iff a run starts at k
+  int *flag = M.flag;
+  if (tid == 0) flag[0] = 1;
+  for (int c = tid; c < nchunks; c += blockDim.x) {
+    const int k0 = 1 + c * SCAN_CHUNK, k1 = min(M.N, k0 + SCAN_CHUNK);
+    int d = M.chunkstart[c];
+    for (int k = k0; k < k1; ++k) {
+      const uint32_t w = M.T[4 * (size_t)k + (d >> 5)];
+      const bool merge = d < 127 && ((w >> (d & 31)) & 1u);
+      flag[k] = merge ? 0 : 1;
+      d = merge ? d + 1 : 0;
     }
-    int u = gather_union(M, a, k, true, keys, cap, cnt, s_tmp, keys + cap / 2);
-    __syncthreads();
-    int v = gather_union(M, a, k, false, keys, cap, cnt, s_tmp, keys + cap / 2);
-    if (threadIdx.x == 0) { M.fLm[F] = u; M.fUc[F] = v; }
-    __syncthreads();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) M.fbstart[nF] = M.n;
+  __syncthreads();
+  // exclusive scan of the flags -> run ids; first[run] = k
+  const int N = M.N;
+  const int per = (N + 1023) / 1024;
+  const int lo = min(N, tid * per), hi = min(N, lo + per);
+  int sum = 0;
+  for (int i = lo; i < hi; ++i) sum += flag[i];
+  const int lane = tid & 31, wid = tid >> 5;
+  int x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_tmp[wid] = x;
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int w = 0; w < 32; ++w) { int t = s_tmp[w]; s_tmp[w] = acc; acc += t; }
+    s_tmp[32] = acc;
+  }
+  __syncthreads();
+  int run = s_tmp[wid] + x - sum;
+  for (int i = lo; i < hi; ++i)
+    if (flag[i]) M.first[run++] = i;
+  if (tid == 0) { M.first[s_tmp[32]] = N; *M.nF = s_tmp[32]; }
 }
 
-// descriptors: singletons keep their arena slices; merged blocks are appended
-// after the factor kernel's cursors (tot[0..3] on entry).  One CTA.
-// block-wide exclusive scan of NV 64-bit values per thread (1024 threads)
+// --------------------------------------------------- M3: descriptors, offsets
 template <int NV>
 __device__ void block_scan_ull(unsigned long long (&v)[NV], unsigned long long (&tot)[NV]) {
   __shared__ unsigned long long sw[NV][32];
@@ -315,26 +316,28 @@ __device__ void block_scan_ull(unsigned long long (&v)[NV], unsigned long long (
   __syncthreads();
 }
 
-// descriptors: singletons keep their arena slices; merged blocks are appended after
-// the factor kernel's cursors (tot[0..3] on entry).  One CTA of 1024 threads, each
-// owning a contiguous range of final blocks.
+// Singletons keep their arena slices; merged blocks are appended after the factor
+// kernel's cursors (tot[0..3] on entry).  Union sizes of merged runs a..k come
+// from the test: u(k-a), v(k-a) of block k.  One CTA of 1024 threads.
 __global__ void __launch_bounds__(1024) merge_offsets_kernel(MergeArgs M) {
   const int nF = *M.nF;
   const int per = (nF + blockDim.x - 1) / blockDim.x;
   const int lo = min(nF, (int)threadIdx.x * per), hi = min(nF, lo + per);
   // per-thread sums: D, Li, Lv, Ui, Uv (merged only), nL, nU, iL, iU, nmerged
   unsigned long long v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  unsigned long long maxws = 0;
   for (int F = lo; F < hi; ++F) {
     const int a = M.first[F], k = M.first[F + 1] - 1;
     const unsigned long long P = M.bstart[k + 1] - M.bstart[a];
-    const unsigned long long u = M.fLm[F], w = M.fUc[F];
-    v[0] += P * P;
-    if (a != k) {
-      v[1] += u; v[2] += u * P; v[3] += w; v[4] += w * P; v[9] += 1;
-      const unsigned long long ws = 6ull * P * P + (u + w) * P + 64;
-      if (ws > maxws) maxws = ws;
+    unsigned long long u, w;
+    if (a == k) { u = M.Lm[k]; w = M.Uc[k]; }
+    else {
+      const int32_t *uv = M.UV + 2 * (M.wofs[k] + (k - a));
+      u = uv[0]; w = uv[1];
     }
+    M.fbstart[F] = M.bstart[a];
+    M.fLm[F] = (int32_t)u; M.fUc[F] = (int32_t)w;
+    v[0] += P * P;
+    if (a != k) { v[1] += u; v[2] += u * P; v[3] += w; v[4] += w * P; v[9] += k - a; }
     v[5] += u * P; v[6] += w * P; v[7] += u; v[8] += w;
   }
   unsigned long long tot[10];
@@ -357,37 +360,77 @@ __global__ void __launch_bounds__(1024) merge_offsets_kernel(MergeArgs M) {
       M.fUval_off[F] = (int64_t)cUv; cUv += w * P;
     }
   }
-  // max workspace: reduce
-  __shared__ unsigned long long smax;
-  if (threadIdx.x == 0) smax = 0;
-  __syncthreads();
-  atomicMax(&smax, maxws);
-  __syncthreads();
   if (threadIdx.x == 0) {
+    M.fbstart[nF] = M.n;
     M.fD_off[nF] = (int64_t)tot[0];
     M.tot[4] = M.tot[0] + tot[1]; M.tot[5] = M.tot[1] + tot[2];
     M.tot[6] = M.tot[2] + tot[3]; M.tot[7] = M.tot[3] + tot[4];
-    M.tot[8] = tot[0]; M.tot[9] = smax; M.tot[10] = tot[9];
-    M.tot[11] = (unsigned long long)(M.N - nF);
+    M.tot[8] = tot[0]; M.tot[9] = 0; M.tot[10] = 0;
+    M.tot[11] = tot[9];
     M.tot[12] = tot[5]; M.tot[13] = tot[6]; M.tot[14] = tot[7]; M.tot[15] = tot[8];
   }
 }
 
 // ---------------------------------------------------------------- M4: arithmetic
-// per merged run a..k (P = e_k - s_a <= max_block):
-//   L_aa (unit lower), U_aa = D_j Ũ_j inside the run (unit upper), D_agg = diag(D_j)
-//   D^ = U_aa^{-1} D_agg L_aa^{-1};  L^ = L_{>,agg} L_aa^{-1};  Ũ^ = L_aa Ũ_{agg,>}
-// Work buffers in global memory (per CTA): Laa, Uaa, Linv, Uinv, T1 (P x P each,
-// row-major), Lg (u x P), Ug (v x P).
+// Sorted union of the members' kept indices >= e_k, written to out[0..u).
+// Returns the number of distinct keys (must equal the test's union size).
+__device__ int build_union(const MergeArgs &M, int a, int k, bool rows, int *keys, int *flags, int cap,
+                           int *s_cnt, int *s_tmp, int *out) {
+  const int tid = threadIdx.x;
+  const int e_k = M.bstart[k + 1];
+  const int32_t *idx = rows ? M.Lidx : M.Uidx;
+  const int64_t *off = rows ? M.Lrow_off : M.Ucol_off;
+  const int32_t *len = rows ? M.Lm : M.Uc;
+  const int nm = k - a + 1;
+  for (int x = tid; x < nm; x += MT) {
+    const int j = a + x;
+    const int32_t *L = idx + off[j];
+    const int m = len[j];
+    s_cnt[x] = m - m_lbound(L, 0, m, e_k);
+  }
+  __syncthreads();
+  const int total = m_scan<MT>(s_cnt, nm, s_tmp);
+  int pw = 1; while (pw < total) pw <<= 1;
+  if (pw > cap) return -1;
+  for (int x = 0; x < nm; ++x) {
+    const int j = a + x;
+    const int32_t *L = idx + off[j];
+    const int m = len[j];
+    const int c = (x + 1 < nm ? s_cnt[x + 1] : total) - s_cnt[x];
+    for (int i = tid; i < c; i += MT) keys[s_cnt[x] + i] = L[m - c + i];
+  }
+  for (int i = total + tid; i < pw; i += MT) keys[i] = INT_MAX;
+  __syncthreads();
+  if (pw > 1) m_bitonic(keys, pw);
+  for (int i = tid; i < total; i += MT) flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+  __syncthreads();
+  const int u = m_scan<MT>(flags, total, s_tmp);
+  for (int i = tid; i < total; i += MT) {
+    const int nxt = i + 1 < total ? flags[i + 1] : u;
+    if (nxt > flags[i]) out[flags[i]] = keys[i];
+  }
+  __syncthreads();
+  return u;
+}
+
+// per merged run a..k (P = e_k - s_a <= max_block), member blocks j with offsets
+// o_j = s_j - s_a:
+//   L_aa (unit lower, identity member diagonal blocks), U_aa = D_j Ũ_j inside the run
+//   D^: X L_aa = D_agg, then U_aa D^ = X        (member-block back/forward steps)
+//   L^: L^ L_aa = L_{>,agg}                       (in place in the output panel)
+//   Ũ^: Ũ^ = L_aa Ũ_{agg,>}                       (in place, members last to first)
 __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dwork, int64_t dwork_per_cta) {
-  extern __shared__ int msm[];
+  extern __shared__ __align__(16) unsigned char msm_raw[];
+  double *sLU = (double *)msm_raw;                                   // 2 * 64^2 doubles
+  int *skeys = (int *)(msm_raw + 2 * ARITH_PSMEM * ARITH_PSMEM * 8);   // ARITH_KEYS
+  int *sflags = skeys + ARITH_KEYS;                                  // ARITH_KEYS
   __shared__ int s_tmp[MW + 1];
+  __shared__ int s_cnt[130];
+  __shared__ int s_mo[130];       // member offsets o_j, j = a..k+1
   const int tid = threadIdx.x;
   const int nF = *M.nF;
-  int *keys = M.work + (size_t)blockIdx.x * M.work_ints;
-  const int cap = (int)M.work_ints;
-  int *cnt = msm;
-  double *base = dwork + (size_t)blockIdx.x * dwork_per_cta;
+  double *gbase = dwork + (size_t)blockIdx.x * dwork_per_cta;
+  int *gkeys = M.work + (size_t)blockIdx.x * M.work_ints;
   double flops = 0.0;
   for (int F = blockIdx.x; F < nF; F += gridDim.x) {
     const int a = M.first[F], k = M.first[F + 1] - 1;
@@ -399,158 +442,179 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
       for (int i = tid; i < P * P; i += MT) Dout[i] = Din[i];
       continue;
     }
-    double *Laa = base, *Uaa = Laa + P * P, *Linv = Uaa + P * P, *Uinv = Linv + P * P, *T1 = Uinv + P * P;
-    double *Lg = T1 + P * P;
-    const int u = M.fLm[F], v = M.fUc[F];
-    double *Ug = Lg + (size_t)u * P;
+    const int nm = k - a + 1;
+    for (int x = tid; x <= nm; x += MT) s_mo[x] = M.bstart[a + x] - sa;
+    double *Laa, *Uaa;
+    if (P <= ARITH_PSMEM) { Laa = sLU; Uaa = sLU + P * P; }
+    else { Laa = gbase; Uaa = gbase + (size_t)P * P; }
     for (int i = tid; i < P * P; i += MT) {
-      int r = i / P, c = i % P;
+      const int r = i / P, c = i - r * P;
       Laa[i] = (r == c) ? 1.0 : 0.0;
       Uaa[i] = (r == c) ? 1.0 : 0.0;
+      // X = D_agg (block diagonal), column-major in the output
+      Dout[i] = 0.0;
     }
-    for (int i = tid; i < (u + v) * P; i += MT) Lg[i] = 0.0;
     __syncthreads();
-    // L_aa and U_aa from the members' rows / cols inside the run
-    for (int j = a; j <= k; ++j) {
-      const int sj = M.bstart[j], ej = M.bstart[j + 1], bj = ej - sj;
+    // L_aa, U_aa and D_agg from the members
+    for (int x = 0; x < nm; ++x) {
+      const int j = a + x;
+      const int oj = s_mo[x], bj = s_mo[x + 1] - oj;
       const int32_t *rows = M.Lidx + M.Lrow_off[j];
       const double *Lv = M.Lval + M.Lval_off[j];
       const int mj = M.Lm[j];
       for (int it = tid; it < mj * bj; it += MT) {
-        int p = it / bj, t = it % bj;
-        int x = rows[p];
-        if (x < ek) Laa[(size_t)(x - sa) * P + (sj - sa) + t] = Lv[it];
+        const int p = it / bj, t = it - p * bj;
+        const int xr = rows[p];
+        if (xr < ek) Laa[(size_t)(xr - sa) * P + oj + t] = Lv[it];
       }
       const int32_t *cols = M.Uidx + M.Ucol_off[j];
       const double *Uv = M.Uval + M.Uval_off[j];
       const double *Dj = M.D + M.D_off[j];
       const int cj = M.Uc[j];
       for (int it = tid; it < cj * bj; it += MT) {
-        int q = it / bj, r = it % bj;
-        int y = cols[q];
+        const int q = it / bj, r = it - q * bj;
+        const int y = cols[q];
         if (y < ek) {
           double acc = 0.0;
           for (int t = 0; t < bj; ++t) acc = fma(Dj[r + (size_t)t * bj], Uv[(size_t)q * bj + t], acc);
-          Uaa[(size_t)(sj - sa + r) * P + (y - sa)] = acc;
+          Uaa[(size_t)(oj + r) * P + (y - sa)] = acc;
         }
+      }
+      for (int it = tid; it < bj * bj; it += MT) {
+        const int r = it % bj, c = it / bj;
+        Dout[(size_t)(oj + c) * P + oj + r] = Dj[it];
       }
     }
     __syncthreads();
-    // unit triangular inverses, one column per thread
-    for (int c = tid; c < P; c += MT) {
-      for (int i = 0; i < P; ++i) {
-        double x;
-        if (i < c) x = 0.0;
-        else if (i == c) x = 1.0;
-        else {
+    // D^: X L_aa = D_agg, members last to first: X[:, c in m] -= X[:, later] L_aa[later, c]
+    for (int x = nm - 1; x >= 0; --x) {
+      const int om = s_mo[x], bm = s_mo[x + 1] - om, e = s_mo[x + 1];
+      for (int it = tid; it < P * bm; it += MT) {
+        const int i = it % P, c = om + it / P;
+        double acc = 0.0;
+        for (int t = e; t < P; ++t) acc = fma(Dout[(size_t)t * P + i], Laa[(size_t)t * P + c], acc);
+        Dout[(size_t)c * P + i] -= acc;
+      }
+      __syncthreads();
+    }
+    // U_aa D^ = X, members last to first: D^[r in m, :] -= U_aa[r, later] D^[later, :]
+    for (int x = nm - 1; x >= 0; --x) {
+      const int om = s_mo[x], bm = s_mo[x + 1] - om, e = s_mo[x + 1];
+      for (int it = tid; it < P * bm; it += MT) {
+        const int r = om + it % bm, c = it / bm;
+        double acc = 0.0;
+        for (int t = e; t < P; ++t) acc = fma(Uaa[(size_t)r * P + t], Dout[(size_t)c * P + t], acc);
+        Dout[(size_t)c * P + r] -= acc;
+      }
+      __syncthreads();
+    }
+    // ---- L^ rows
+    const int u = M.fLm[F], v = M.fUc[F];
+    {
+      int *R = M.Lidx_out + M.fLrow_off[F];
+      const bool sm = true;
+      int cap = ARITH_KEYS;
+      int *kb = skeys, *fb = sflags;
+      int uu = build_union(M, a, k, true, kb, fb, cap, s_cnt, s_tmp, R);
+      if (uu < 0) {
+        (void)sm;
+        uu = build_union(M, a, k, true, gkeys, gkeys + M.work_ints / 2, (int)(M.work_ints / 2), s_cnt, s_tmp, R);
+      }
+      if (uu != u) { if (tid == 0) atomicExch(M.ovf, uu < 0 ? 1 : 2); return; }
+      double *Lout = M.Lval_out + M.fLval_off[F];
+      for (int i = tid; i < u * P; i += MT) Lout[i] = 0.0;
+      __syncthreads();
+      for (int x = 0; x < nm; ++x) {
+        const int j = a + x;
+        const int oj = s_mo[x], bj = s_mo[x + 1] - oj;
+        const int32_t *rows = M.Lidx + M.Lrow_off[j];
+        const double *Lv = M.Lval + M.Lval_off[j];
+        const int mj = M.Lm[j];
+        for (int it = tid; it < mj * bj; it += MT) {
+          const int p = it / bj, t = it - p * bj;
+          const int xr = rows[p];
+          if (xr >= ek) Lout[(size_t)m_lbound(R, 0, u, xr) * P + oj + t] = Lv[it];
+        }
+      }
+      __syncthreads();
+      for (int x = nm - 1; x >= 0; --x) {
+        const int om = s_mo[x], bm = s_mo[x + 1] - om, e = s_mo[x + 1];
+        if (e < P) {
+          for (int it = tid; it < u * bm; it += MT) {
+            const int i = it / bm, c = om + it % bm;
+            double *row = Lout + (size_t)i * P;
+            double acc = 0.0;
+            for (int t = e; t < P; ++t) acc = fma(row[t], Laa[(size_t)t * P + c], acc);
+            row[c] -= acc;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // ---- Ũ^ columns
+    {
+      int *Cc = M.Uidx_out + M.fUcol_off[F];
+      int vv = build_union(M, a, k, false, skeys, sflags, ARITH_KEYS, s_cnt, s_tmp, Cc);
+      if (vv < 0) vv = build_union(M, a, k, false, gkeys, gkeys + M.work_ints / 2, (int)(M.work_ints / 2), s_cnt, s_tmp, Cc);
+      if (vv != v) { if (tid == 0) atomicExch(M.ovf, vv < 0 ? 1 : 2); return; }
+      double *Uout = M.Uval_out + M.fUval_off[F];
+      for (int i = tid; i < v * P; i += MT) Uout[i] = 0.0;
+      __syncthreads();
+      for (int x = 0; x < nm; ++x) {
+        const int j = a + x;
+        const int oj = s_mo[x], bj = s_mo[x + 1] - oj;
+        const int32_t *cols = M.Uidx + M.Ucol_off[j];
+        const double *Uv = M.Uval + M.Uval_off[j];
+        const int cj = M.Uc[j];
+        for (int it = tid; it < cj * bj; it += MT) {
+          const int q = it / bj, t = it - q * bj;
+          const int y = cols[q];
+          if (y >= ek) Uout[(size_t)m_lbound(Cc, 0, v, y) * P + oj + t] = Uv[it];
+        }
+      }
+      __syncthreads();
+      // rows r of member m: Ũ^[r, y] += L_aa[r, earlier] Ũ_g[earlier, y]
+      for (int x = nm - 1; x >= 1; --x) {
+        const int om = s_mo[x], bm = s_mo[x + 1] - om;
+        for (int it = tid; it < v * bm; it += MT) {
+          const int y = it / bm, r = om + it % bm;
+          double *col = Uout + (size_t)y * P;
+          const double *lr = Laa + (size_t)r * P;
           double acc = 0.0;
-          for (int t = c; t < i; ++t) acc = fma(Laa[(size_t)i * P + t], Linv[(size_t)t * P + c], acc);
-          x = -acc;
+          for (int t = 0; t < om; ++t) acc = fma(lr[t], col[t], acc);
+          col[r] += acc;
         }
-        Linv[(size_t)i * P + c] = x;
-      }
-      for (int i = P - 1; i >= 0; --i) {
-        double x;
-        if (i > c) x = 0.0;
-        else if (i == c) x = 1.0;
-        else {
-          double acc = 0.0;
-          for (int t = i + 1; t <= c; ++t) acc = fma(Uaa[(size_t)i * P + t], Uinv[(size_t)t * P + c], acc);
-          x = -acc;
-        }
-        Uinv[(size_t)i * P + c] = x;
+        __syncthreads();
       }
     }
-    __syncthreads();
-    // T1 = D_agg Linv
-    for (int it = tid; it < P * P; it += MT) {
-      int r = it / P, c = it % P;
-      int j = a;
-      while (M.bstart[j + 1] - sa <= r) ++j;
-      const int sj = M.bstart[j] - sa, bj = M.bstart[j + 1] - M.bstart[j];
-      const double *Dj = M.D + M.D_off[j];
-      double acc = 0.0;
-      for (int t = 0; t < bj; ++t) acc = fma(Dj[(r - sj) + (size_t)t * bj], Linv[(size_t)(sj + t) * P + c], acc);
-      T1[it] = acc;
-    }
-    __syncthreads();
-    // D^ = Uinv T1, stored column-major
-    for (int it = tid; it < P * P; it += MT) {
-      int c = it / P, r = it % P;
-      double acc = 0.0;
-      for (int t = r; t < P; ++t) acc = fma(Uinv[(size_t)r * P + t], T1[(size_t)t * P + c], acc);
-      Dout[it] = acc;
-    }
-    // union rows / cols (recomputed; same as merge_count_kernel)
-    int uu = gather_union(M, a, k, true, keys, cap, cnt, s_tmp, keys + cap / 2);
-    if (uu < 0) return;
-    for (int i = tid; i < uu; i += MT) M.Lidx_out[M.fLrow_off[F] + i] = keys[i];
-    __syncthreads();
-    for (int j = a; j <= k; ++j) {
-      const int sj = M.bstart[j], bj = M.bstart[j + 1] - sj;
-      const int32_t *rows = M.Lidx + M.Lrow_off[j];
-      const double *Lv = M.Lval + M.Lval_off[j];
-      const int mj = M.Lm[j];
-      for (int it = tid; it < mj * bj; it += MT) {
-        int p = it / bj, t = it % bj;
-        int x = rows[p];
-        if (x >= ek) Lg[(size_t)m_lbound(keys, 0, uu, x) * P + (sj - sa) + t] = Lv[it];
-      }
-    }
-    __syncthreads();
-    double *Lout = M.Lval_out + M.fLval_off[F];
-    for (int it = tid; it < uu * P; it += MT) {
-      int x = it / P, c = it % P;
-      double acc = 0.0;
-      for (int t = c; t < P; ++t) acc = fma(Lg[(size_t)x * P + t], Linv[(size_t)t * P + c], acc);
-      Lout[it] = acc;
-    }
-    __syncthreads();
-    int vv = gather_union(M, a, k, false, keys, cap, cnt, s_tmp, keys + cap / 2);
-    if (vv < 0) return;
-    for (int i = tid; i < vv; i += MT) M.Uidx_out[M.fUcol_off[F] + i] = keys[i];
-    __syncthreads();
-    for (int j = a; j <= k; ++j) {
-      const int sj = M.bstart[j], bj = M.bstart[j + 1] - sj;
-      const int32_t *cols = M.Uidx + M.Ucol_off[j];
-      const double *Uv = M.Uval + M.Uval_off[j];
-      const int cj = M.Uc[j];
-      for (int it = tid; it < cj * bj; it += MT) {
-        int q = it / bj, t = it % bj;
-        int y = cols[q];
-        if (y >= ek) Ug[(size_t)m_lbound(keys, 0, vv, y) * P + (sj - sa) + t] = Uv[it];
-      }
-    }
-    __syncthreads();
-    double *Uout = M.Uval_out + M.fUval_off[F];
-    for (int it = tid; it < vv * P; it += MT) {
-      int y = it / P, r = it % P;
-      double acc = 0.0;
-      for (int t = 0; t <= r; ++t) acc = fma(Laa[(size_t)r * P + t], Ug[(size_t)y * P + t], acc);
-      Uout[it] = acc;
-    }
-    __syncthreads();
     if (tid == 0) {
-      double Pd = P;
-      flops += 2.0 * Pd * Pd * Pd / 3.0 + 2.0 * Pd * Pd * Pd / 2.0 + Pd * Pd * Pd + (double)(uu + vv) * Pd * Pd;
+      const double Pd = P;
+      flops += 2.0 * Pd * Pd * Pd / 3.0 + 2.0 * Pd * Pd * Pd / 2.0 + Pd * Pd * Pd + (double)(u + v) * Pd * Pd;
     }
+    __syncthreads();
   }
   if (tid == 0 && flops > 0.0) atomicAdd(M.flops, flops);
 }
 
 // ----------------------------------------------------------------- launchers
 extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_t st) {
-  const int smem = 7 * 130 * 4;
-  merge_test_kernel<<<grid, MT, smem, st>>>(M);
-  merge_scan_kernel<<<1, 256, 0, st>>>(M);
-  merge_count_kernel<<<grid, MT, 1024 * 4, st>>>(M);
+  const int nchunks = M.N > 1 ? (M.N - 1 + SCAN_CHUNK - 1) / SCAN_CHUNK : 0;
+  merge_test_kernel<<<grid * 8, TEST_T, 0, st>>>(M);
+  if (nchunks > 0) merge_chunkmap_kernel<<<nchunks, 128, 0, st>>>(M);
+  merge_scan_kernel<<<1, 1024, 0, st>>>(M, nchunks);
   merge_offsets_kernel<<<1, 1024, 0, st>>>(M);
   return cudaGetLastError();
 }
 
+extern "C" int bilu_merge_plan_launches() { return 4; }
+extern "C" int bilu_merge_nchunks(int N) { return N > 1 ? (N - 1 + SCAN_CHUNK - 1) / SCAN_CHUNK : 0; }
+
 extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
                                         cudaStream_t st) {
-  merge_arith_kernel<<<grid, MT, 1024 * 4, st>>>(M, dwork, dwork_per_cta);
+  const int smem = 2 * ARITH_PSMEM * ARITH_PSMEM * 8 + 2 * ARITH_KEYS * 4;
+  cudaError_t e = cudaFuncSetAttribute(merge_arith_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  merge_arith_kernel<<<grid, MT, smem, st>>>(M, dwork, dwork_per_cta);
   return cudaGetLastError();
 }
 
