@@ -170,6 +170,18 @@ const char *bilu_last_error(const bilu_ctx *h);
  * (evidence counter for benchmarks). */
 int64_t bilu_kernel_launches(const bilu_ctx *h);
 
+/* ---- diagnostics (tests and microbenchmarks; not needed by users) ----
+ * bilu_diag_dgemm -- the library's CTA-level FP64 tensor-core GEMM (DMMA
+ * m8n8k4, used for the Schur-update products PAPER.md:371-374 and the merged
+ * panels PAPER.md:1348-1387) on its own: for b = 0..batch-1 (one CTA each)
+ *     C_b = alpha * A_b * B_b + beta * C_b,   A_b = A + b*sa (M x K), B_b = B + b*sb
+ *     (K x N), C_b = C + b*sc (M x N); element (i, j) of X at X[i*xrs + j*xcs].
+ * All pointers DEVICE memory; asynchronous on `stream` (NULL = default stream).
+ * Returns 0, 1 (bad argument) or 4 (launch error). */
+int bilu_diag_dgemm(int M, int N, int K, double alpha, const double *A, int64_t ars, int64_t acs,
+                    const double *B, int64_t brs, int64_t bcs, double beta, double *C, int64_t crs,
+                    int64_t ccs, int batch, int64_t sa, int64_t sb, int64_t sc, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

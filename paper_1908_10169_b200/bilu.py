@@ -20,7 +20,7 @@ STATUS = {0: "BILU_OK", 1: "BILU_ERR_ARG", 2: "BILU_ERR_BREAKDOWN", 3: "BILU_ERR
 # every symbol include/bilu.h declares
 ABI_SYMBOLS = ["bilu_options_default", "bilu_analyze", "bilu_set_values", "bilu_factor",
                "bilu_apply", "bilu_export", "bilu_factor_view_free", "bilu_destroy",
-               "bilu_status_string", "bilu_last_error", "bilu_kernel_launches"]
+               "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm"]
 
 
 class BiluError(RuntimeError):
@@ -102,6 +102,10 @@ def load_library():
     lib.bilu_last_error.restype = ctypes.c_char_p
     lib.bilu_kernel_launches.argtypes = [P]
     lib.bilu_kernel_launches.restype = ctypes.c_int64
+    I64, D = ctypes.c_int64, ctypes.c_double
+    lib.bilu_diag_dgemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, D, P, I64, I64, P, I64, I64, D, P,
+                                    I64, I64, ctypes.c_int, I64, I64, I64, P]
+    lib.bilu_diag_dgemm.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -248,3 +252,17 @@ class BILU:
             self.close()
         except Exception:
             pass
+
+
+def diag_dgemm(A, B, C, alpha=1.0, beta=0.0, stream=0):
+    """C[b] = alpha A[b] B[b] + beta C[b] with the library's DMMA CTA GEMM (one CTA per
+    batch entry).  A, B, C: CUDA float64 tensors of shape (batch, M, K), (batch, K, N),
+    (batch, M, N), any strides.  Diagnostics only (tests, microbenchmarks)."""
+    lib = load_library()
+    bt, M, K = A.shape
+    N = B.shape[2]
+    rc = lib.bilu_diag_dgemm(M, N, K, alpha, A.data_ptr(), A.stride(1), A.stride(2), B.data_ptr(), B.stride(1),
+                             B.stride(2), beta, C.data_ptr(), C.stride(1), C.stride(2), bt, A.stride(0),
+                             B.stride(0), C.stride(0), ctypes.c_void_p(stream))
+    if rc != 0:
+        raise BiluError(rc, "bilu_diag_dgemm failed")

@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["bilu_factor.cu", "bilu_merge.cu", "bilu_apply.cu", "bilu_util.cu"]
 CPP_SOURCES = ["bilu_host.cpp"]
-HEADERS = ["bilu_internal.h", os.path.join("..", "..", "include", "bilu.h")]
+HEADERS = ["bilu_internal.h", "dgemm_cta.cuh", os.path.join("..", "..", "include", "bilu.h")]
 
 
 def _newest_source() -> float:

@@ -45,6 +45,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
 }
 #define PROF_T0 long long _pt = clock64(); if (threadIdx.x == 0 && g_blkprof) g_blkprof[32 * (size_t)K] = gtimer();
+#define PROF_T0C long long _pt = clock64();
 #define PROF(i) do { DBGP(i); if (threadIdx.x == 0) { long long _n = clock64(); atomicAdd(&g_prof[i], (unsigned long long)(_n - _pt)); \
   if (g_blkprof) g_blkprof[32 * (size_t)K + 1 + (i)] = (unsigned long long)(_n - _pt); _pt = _n; } } while (0)
 #define SUBP(i) do { if (threadIdx.x == 0 && g_blkprof) { long long _n2 = clock64(); \
@@ -58,6 +59,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define SUBP(i) do {} while (0)
 #define SUBP_T0
 #define PROF_T0
+#define PROF_T0C
 #define PROF(i) DBGP(i)
 #endif
 
@@ -211,10 +213,11 @@ struct Bump {
   unsigned char *sbase; int sused, stop, scap;     // shared: bottom (persistent) / top (scratch)
   double *gbase; int64_t gused, gtop, gcap;        // global spill region, same scheme (doubles)
   bool ovf;
+  bool bottom_global;                              // persistent allocations in global memory only
 };
 __device__ __forceinline__ void *balloc(Bump &A, int64_t bytes) {
   bytes = (bytes + 15) & ~int64_t(15);
-  if (A.sused + bytes <= A.stop) {
+  if (!A.bottom_global && A.sused + bytes <= A.stop) {
     void *p = A.sbase + A.sused;
     A.sused += (int)bytes;
     return p;
@@ -405,6 +408,25 @@ struct LineMap {
   }
 };
 
+// state of one side of block K after a-3/a-4
+struct SideState {
+  double *W;       // dense buffer, line-major (lines x b)
+  int *lineOf;     // line -> matrix index
+  int nU;          // candidate lines (excl. the pivot block)
+  bool sorted;     // lines in ascending index order (bitmap path)
+  LineMap M;
+  const unsigned *gbm; const int *gpre;   // global copies of the bitmap map (split blocks)
+};
+
+// a split heavy block (see process_block)
+struct HeavyCtx {
+  int K, nc[2], T[2], np[2];
+  int left;                 // parts not yet completed
+  const Contrib *C[2];
+  SideState R[2];
+  double flops;
+};
+
 // One side of block K (SIDE 0: block column of L incl. the pivot block; SIDE 1:
 // block row of U):
 //   a-3  candidate set: keys >= e_K of Ã's block column (resp. row) and of every
@@ -417,9 +439,8 @@ struct LineMap {
 //        resp. a column of Ũ_J >= e_K), the next contributor's operands prefetched
 //        into registers while the current one is applied.
 template <int SIDE>
-__device__ bool side_update(const DevFactor &F, int K, int s, int e, int b, Contrib *C, int nc, int T,
-                            int64_t a0, int64_t ae, int64_t a1, Bump &A, Shared &S, double **Wout,
-                            int **lineOf_out, int *n_out, double &flops) {
+__device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, const Contrib *C, int nc, int T,
+                             int64_t a0, int64_t ae, int64_t a1, Bump &A, Shared &S, SideState &R) {
   const int tid = threadIdx.x;
   const int32_t *arc = SIDE == 0 ? F.AL_rc : F.AU_rc;
   const double *aval = SIDE == 0 ? F.AL_val : F.AU_val;
@@ -482,6 +503,13 @@ __device__ bool side_update(const DevFactor &F, int K, int s, int e, int b, Cont
     __syncthreads();
     nU = cta_scan(pre, words, S.tmp);
     M.bm = bm; M.pre = pre;
+    if (A.bottom_global) {   // a split block: the helpers need the map in global memory
+      unsigned *gbm = (unsigned *)balloc(A, (int64_t)(words + 1) * 4);
+      int *gpre = (int *)balloc(A, (int64_t)(words + 1) * 4);
+      if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
+      for (int w = tid; w < words; w += NT) { gbm[w] = bm[w]; gpre[w] = pre[w]; }
+      R.gbm = gbm; R.gpre = gpre;
+    }
   } else {
     // ---- pos-map path: every occurrence writes its id, the surviving writer appends
     const int occ = nA + T;
@@ -556,66 +584,89 @@ __device__ bool side_update(const DevFactor &F, int K, int s, int e, int b, Cont
   }
   __syncthreads();
   SUBP(8 * SIDE + 1);
-  // -- a-5: every (contributor, item) pair in parallel; contributions are added into
-  //    the shared buffer atomically, so their order is unspecified (exact in exact
-  //    arithmetic, R13; differences are rounding only)
-  {
-    int a = 0;
-#pragma unroll 2
-    for (int t = tid; t < T; t += NT) {
-      while (a + 1 < nc && C[a + 1].item_off <= t) ++a;
-      const Contrib &c = C[a];
-      const int i = t - c.item_off, bJ = c.bJ, ncol = c.ncol;
-      const int key = cidx[(SIDE == 0 ? c.rows : c.cols) + i];
-      const int ln = (SIDE == 0 && key < e) ? key - s : M(key);
-      const double *vi = (SIDE == 0 ? F.Lval + c.lval : F.Uval + c.uval) + (int64_t)i * bJ;
-      const double *sm = SIDE == 0 ? F.Uval + c.uval : F.Lval + c.lval;
-      const int32_t *sidx = SIDE == 0 ? F.Uidx + c.cols : F.Lidx + c.rows;
-      double *wl = W + (int64_t)ln * b;
-      if (bJ <= 16) {
-        double v[16];
-#pragma unroll
-        for (int t2 = 0; t2 < 16; ++t2) v[t2] = t2 < bJ ? vi[t2] : 0.0;
-        for (int q = 0; q < ncol; ++q) {
-          const double *u = sm + (int64_t)q * bJ;
-          double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-          for (int t2 = 0; t2 < 16; t2 += 2) {
-            if (t2 < bJ) acc0 = fma(v[t2], u[t2], acc0);
-            if (t2 + 1 < bJ) acc1 = fma(v[t2 + 1], u[t2 + 1], acc1);
-          }
-          atomicAdd(&wl[sidx[q] - s], -(acc0 + acc1));
-        }
-      } else {
-        for (int q = 0; q < ncol; ++q) {
-          const double *u = sm + (int64_t)q * bJ;
-          double acc = 0.0;
-          for (int t2 = 0; t2 < bJ; ++t2) acc = fma(vi[t2], u[t2], acc);
-          atomicAdd(&wl[sidx[q] - s], -acc);
-        }
-      }
-    }
-  }
-  for (int a = 0; a < nc; ++a) flops += 2.0 * C[a].bJ * (double)C[a].n_items * (double)C[a].ncol;
-  __syncthreads();
-  SUBP(8 * SIDE + 2);
-  A.stop = A.scap; A.gtop = A.gcap;                 // release the bitmap / scratch
-  __syncthreads();
-  *Wout = W;
-  *lineOf_out = lineOf;
-  *n_out = nU;
+  R.W = W; R.lineOf = lineOf; R.nU = nU; R.M = M;
+  R.sorted = M.bm != nullptr;   // bitmap path: lines in ascending key order
   return true;
 }
 
+// a-5 for the items [t0, t1) of one side: W -= L_J Ũ_J, "gather ... GEMM ... scatter"
+// (Fig. 2): one thread per item (a row of L_J >= s_K, resp. a column of
+// Ũ_J >= e_K); contributions are added atomically (shared-memory W) or with native
+// global fp64 reductions (GLOBAL: W of a split heavy block), so the summation order is
+// unspecified (exact in exact arithmetic, R13; differences are rounding only).
+__device__ __forceinline__ void red_add_f64(double *p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+template <int SIDE, bool GLOBAL>
+__device__ void side_items(const DevFactor &F, int s, int e, const Contrib *C, int nc, int t0, int t1, int b,
+                           const LineMap &M, double *W) {
+  const int32_t *cidx = SIDE == 0 ? F.Lidx : F.Uidx;
+  int a = contrib_of(C, nc, min(t0 + (int)threadIdx.x, t1 - 1));
+#pragma unroll 2
+  for (int t = t0 + threadIdx.x; t < t1; t += NT) {
+    while (a + 1 < nc && C[a + 1].item_off <= t) ++a;
+    const Contrib &c = C[a];
+    const int i = t - c.item_off, bJ = c.bJ, ncol = c.ncol;
+    const int key = cidx[(SIDE == 0 ? c.rows : c.cols) + i];
+    const int ln = (SIDE == 0 && key < e) ? key - s : M(key);
+    const double *vi = (SIDE == 0 ? F.Lval + c.lval : F.Uval + c.uval) + (int64_t)i * bJ;
+    const double *sm = SIDE == 0 ? F.Uval + c.uval : F.Lval + c.lval;
+    const int32_t *sidx = SIDE == 0 ? F.Uidx + c.cols : F.Lidx + c.rows;
+    double *wl = W + (int64_t)ln * b;
+    if (bJ <= 16) {
+      double v[16];
+#pragma unroll
+      for (int t2 = 0; t2 < 16; ++t2) v[t2] = t2 < bJ ? vi[t2] : 0.0;
+      for (int q = 0; q < ncol; ++q) {
+        const double *u = sm + (int64_t)q * bJ;
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int t2 = 0; t2 < 16; t2 += 2) {
+          if (t2 < bJ) acc0 = fma(v[t2], u[t2], acc0);
+          if (t2 + 1 < bJ) acc1 = fma(v[t2 + 1], u[t2 + 1], acc1);
+        }
+        if (GLOBAL) red_add_f64(&wl[sidx[q] - s], -(acc0 + acc1));
+        else atomicAdd(&wl[sidx[q] - s], -(acc0 + acc1));
+      }
+    } else {
+      for (int q = 0; q < ncol; ++q) {
+        const double *u = sm + (int64_t)q * bJ;
+        double acc = 0.0;
+        for (int t2 = 0; t2 < bJ; ++t2) acc = fma(vi[t2], u[t2], acc);
+        if (GLOBAL) red_add_f64(&wl[sidx[q] - s], -acc);
+        else atomicAdd(&wl[sidx[q] - s], -acc);
+      }
+    }
+  }
+}
+
+__device__ double side_flops(const Contrib *C, int nc) {
+  double f = 0.0;
+  for (int a = 0; a < nc; ++a) f += 2.0 * C[a].bJ * (double)C[a].n_items * (double)C[a].ncol;
+  return f;
+}
+
+// ---------------------------------------------------------- split heavy blocks
+// A block whose Schur-update item count is large is processed as several tasks of the
+// dataflow queue: the owner CTA builds the candidate sets and a global-memory W
+// (a-2..a-4) and publishes a HeavyCtx; "part" tasks apply disjoint item ranges with
+// native global fp64 reductions (a-5) on any idle CTA; the CTA that completes the last
+// part runs a-6..a-1 (finish_block).  Same values as the one-CTA path up to the
+// summation order (R13).
+constexpr int ITEMS_PER_PART = 1024;
+constexpr int MAX_PARTS = 32;          // per block (both sides)
+
+__device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
+                             const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops);
+
 __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned char *smem, uint64_t *mbar,
                               unsigned &mphase) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x;
   const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
   Bump A;
   A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes;
   A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
-  A.ovf = false;
-  double flops = 0.0;
+  A.ovf = false; A.bottom_global = false;
   PROF_T0
 #define OVF_CHECK() do { if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; } } while (0)
 
@@ -630,18 +681,150 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   const int TL = S.cnt[0], TU = S.cnt[1];
   const int64_t aL0 = F.AL_ptr[K], aLe = F.AL_ge[K], aL1 = F.AL_ptr[K + 1];
   const int64_t aU0 = F.AU_ptr[K], aU1 = F.AU_ptr[K + 1];
+  const double flops = side_flops(CL, nLc) + side_flops(CU, nUc);
   PROF(1);
 
-  // ---------------- a-3 / a-4 / a-5 for both sides
-  double *WL, *WU;
-  int *rowOf, *colOf;
-  int nR, nC;
-  if (!side_update<0>(F, K, s, e, b, CL, nLc, TL, aL0, aLe, aL1, A, S, &WL, &rowOf, &nR, flops)) return;
-  PROF(2);
-  PROF(3);
-  if (!side_update<1>(F, K, s, e, b, CU, nUc, TU, aU0, aU0, aU1, A, S, &WU, &colOf, &nC, flops)) return;
-  PROF(4);
+  // ---------------- split decision: heavy blocks take their buffers from the global pool
+  // split only when CTAs are idle (tickets taken but not yet filled)
+  if (tid == 0) {
+    const long long idle = (long long)ld_vol64(&F.ctrl[CS * CTRL_QTAIL]) - (long long)ld_vol64(&F.ctrl[CS * CTRL_QHEAD]);
+    S.cnt[3] = (F.heavy_T > 0 && TL + TU >= F.heavy_T && idle >= F.heavy_idle) ? 1 : 0;
+  }
+  __syncthreads();
+  const bool heavy = S.cnt[3] != 0;
+  if (heavy) {
+    const int64_t nAL = aL1 - aLe, nAU = aU1;
+    const int64_t lines = (int64_t)b + nAL + TL + 1, cols = nAU - aU0 + TU + 1;
+    const int64_t need = (lines + cols) * (b + 1) + 2 * 8200 + 64 +
+                         (int64_t)(nLc + nUc) * (int64_t)(sizeof(Contrib) / 8) + 64;
+    if (tid == 0) {
+      unsigned long long o = atomicAdd(&F.ctrl[CS * CTRL_HPOOL], (unsigned long long)need);
+      S.off[0] = o;
+    }
+    __syncthreads();
+    if (S.off[0] + need > (unsigned long long)F.hpool_cap) { if (tid == 0) raise_abort(F, DEV_OVF_HPOOL, K); return; }
+    A.gbase = F.hpool + S.off[0]; A.gused = 0; A.gcap = need; A.gtop = need;
+    A.bottom_global = true;   // W and line maps in the pool (read by the helpers); scratch stays in shared memory
+  }
 
+  // ---------------- a-3 / a-4 for both sides
+  SideState RL, RU;
+  if (!side_prepare<0>(F, K, s, e, b, CL, nLc, TL, aL0, aLe, aL1, A, S, RL)) return;
+  PROF(2);
+  if (!side_prepare<1>(F, K, s, e, b, CU, nUc, TU, aU0, aU0, aU1, A, S, RU)) return;
+  PROF(3);
+
+  if (heavy && RL.sorted && RU.sorted) {
+    // publish the context and the part tasks; this CTA is free afterwards
+#ifdef BILU_PROFILE
+    if (tid == 0 && g_blkprof) { g_blkprof[32 * (size_t)K + 19] = gtimer(); g_blkprof[32 * (size_t)K + 20] = ~0ull; }
+#endif
+    Contrib *gCL = (Contrib *)balloc(A, (int64_t)nLc * sizeof(Contrib));
+    Contrib *gCU = (Contrib *)balloc(A, (int64_t)nUc * sizeof(Contrib));
+    OVF_CHECK();
+    for (int x = tid; x < nLc; x += NT) gCL[x] = CL[x];
+    for (int x = tid; x < nUc; x += NT) gCU[x] = CU[x];
+    const int pL = min(MAX_PARTS / 2, (TL + ITEMS_PER_PART - 1) / ITEMS_PER_PART);
+    const int pU = min(MAX_PARTS / 2, (TU + ITEMS_PER_PART - 1) / ITEMS_PER_PART);
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned long long h = atomicAdd(&F.ctrl[CS * CTRL_HCTX], 1ull);
+      if (h >= (unsigned long long)F.hctx_cap) { raise_abort(F, DEV_OVF_HPOOL, K); S.off[1] = ~0ull; }
+      else {
+        HeavyCtx &X = F.hctx[h];
+        X.K = K; X.nc[0] = nLc; X.nc[1] = nUc; X.T[0] = TL; X.T[1] = TU; X.np[0] = pL; X.np[1] = pU;
+        X.C[0] = gCL; X.C[1] = gCU; X.R[0] = RL; X.R[1] = RU; X.flops = flops;
+        X.R[0].M.bm = RL.gbm; X.R[0].M.pre = RL.gpre; X.R[1].M.bm = RU.gbm; X.R[1].M.pre = RU.gpre;
+        X.left = pL + pU;
+        __threadfence();
+        const unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], (unsigned long long)(pL + pU));
+        if (slot + pL + pU > (unsigned long long)F.qcap) raise_abort(F, DEV_OVF_HPOOL, K);
+        else
+          for (int p = 0; p < pL + pU; ++p) st_vol(&F.queue[slot + p], F.N + (int)h * MAX_PARTS + p);
+        S.off[1] = h;
+      }
+    }
+    __syncthreads();
+    return;
+  }
+
+  // ---------------- a-5, this CTA: every (contributor, item) pair
+  if (heavy) {
+    side_items<0, true>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
+    side_items<1, true>(F, s, e, CU, nUc, 0, TU, b, RU.M, RU.W);
+  } else {
+    side_items<0, false>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
+    side_items<1, false>(F, s, e, CU, nUc, 0, TU, b, RU.M, RU.W);
+  }
+  __syncthreads();
+  PROF(4);
+  if (heavy) {   // scratch of the finish phase from this CTA's own shared memory / workspace
+    A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes; A.bottom_global = false;
+    A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
+  } else {
+    A.stop = A.scap; A.gtop = A.gcap;   // release the bitmaps / scratch
+  }
+  finish_block(F, K, S, A, RL.W, RU.W, RL.lineOf, RU.lineOf, RL.nU, RU.nU, RL.sorted, RU.sorted, flops);
+#undef OVF_CHECK
+}
+
+// one part task: items of one side of a split heavy block; the CTA that completes the
+// last part finishes the block
+__device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char *smem) {
+  const int tid = threadIdx.x;
+  const int h = (task - F.N) / MAX_PARTS, p = (task - F.N) % MAX_PARTS;
+  HeavyCtx &X = F.hctx[h];
+  const int K = X.K;
+  const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
+  const int side = p < X.np[0] ? 0 : 1;
+  const int pp = side == 0 ? p : p - X.np[0], np = X.np[side], T = X.T[side];
+  const int per = (T + np - 1) / np;
+  const int t0 = min(T, pp * per), t1 = min(T, t0 + per);
+  const SideState &R = X.R[side];
+  // the contributor descriptors of this side, staged in shared memory
+  Contrib *C = (Contrib *)smem;
+  const int nc = X.nc[side];
+  const bool cs = (int64_t)nc * (int64_t)sizeof(Contrib) <= (int64_t)F.smem_bytes;
+  if (cs) for (int x = tid; x < nc; x += NT) C[x] = X.C[side][x];
+  __syncthreads();
+#ifdef BILU_PROFILE
+  if (tid == 0 && g_blkprof) {
+    const unsigned long long t = gtimer();
+    atomicMin(&g_blkprof[32 * (size_t)K + 20], t);            // first part start (buffer zeroed: use ~0 init)
+    atomicAdd(&g_blkprof[32 * (size_t)K + 22], 1ull);
+  }
+  long long _pc0 = clock64();
+#endif
+  if (side == 0) side_items<0, true>(F, s, e, cs ? C : X.C[0], nc, t0, t1, b, R.M, R.W);
+  else side_items<1, true>(F, s, e, cs ? C : X.C[1], nc, t0, t1, b, R.M, R.W);
+#ifdef BILU_PROFILE
+  __syncthreads();
+  if (tid == 0 && g_blkprof) {
+    atomicMax(&g_blkprof[32 * (size_t)K + 21], gtimer());     // last part end
+    atomicAdd(&g_blkprof[32 * (size_t)K + 23], (unsigned long long)(clock64() - _pc0));   // part cycles
+  }
+#endif
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) S.piv = atomicSub(&X.left, 1);
+  __syncthreads();
+  if (S.piv != 1) return;
+  __threadfence();
+  Bump A;
+  A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes;
+  A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
+  A.ovf = false; A.bottom_global = false;
+  finish_block(F, K, S, A, X.R[0].W, X.R[1].W, X.R[0].lineOf, X.R[1].lineOf, X.R[0].nU, X.R[1].nU, true, true,
+               X.flops);
+}
+
+// a-6 .. a-1 of block K once W_L (pivot block + candidate rows) and W_U are complete
+__device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
+                             const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
+  PROF_T0C
+#define OVF_CHECK() do { if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; } } while (0)
   // ---------------- a-6: D_K = P_K^{-1}, Gauss-Jordan with partial pivoting (column-major P)
   double *P = (double *)balloc(A, (int64_t)b * b * 8);
   int *ipiv = (int *)balloc(A, (int64_t)b * 4);
@@ -860,7 +1043,10 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   for (int j = tid; j < nC; j += NT)
     if (keepC[j + 1] > keepC[j]) { kc[keepC[j]] = j; kcol[keepC[j]] = colOf[j]; }
   __syncthreads();
-  if (mK <= 1024) cta_rank_sort(krow, mK, ordR);
+  if (sortedR) {
+    for (int x = tid; x < mK; x += NT) ordR[x] = x;
+    __syncthreads();
+  } else if (mK <= 1024) cta_rank_sort(krow, mK, ordR);
   else {
     // large: bitonic on (row << 0) keys carrying positions via a second pass
     for (int x = tid; x < mK; x += NT) R[x] = krow[x];
@@ -877,7 +1063,10 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     }
     __syncthreads();
   }
-  if (cK <= 1024) cta_rank_sort(kcol, cK, ordC);
+  if (sortedC) {
+    for (int x = tid; x < cK; x += NT) ordC[x] = x;
+    __syncthreads();
+  } else if (cK <= 1024) cta_rank_sort(kcol, cK, ordC);
   else {
     int m2 = 1; while (m2 < cK) m2 <<= 1;
     int *tmpk = (int *)balloc(A, (int64_t)m2 * 4);
@@ -995,7 +1184,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   }
   if (tid == 0) atomicAdd(&F.ctrl[CS * CTRL_DONE], 1ull);
   PROF(8);
-  PROF_END(nLc, nUc, nR, nC);
+  PROF_END(0, 0, nR, nC);
 #undef OVF_CHECK
 }
 
@@ -1013,12 +1202,13 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
 #endif
       int K = -1;
       unsigned long long idx = aborted(F) ? ~0ull : atomicAdd(&F.ctrl[CS * CTRL_QTAIL], 1ull);
-      if (idx < (unsigned long long)F.N) {
+      if (idx < (unsigned long long)F.qcap) {
         unsigned ns = 32, polls = 0;
         while (true) {
           K = ld_vol(&F.queue[idx]);
           if (K >= 0) break;
-          if ((++polls & 15u) == 0 && aborted(F)) { K = -1; break; }
+          if ((++polls & 15u) == 0 &&
+              (aborted(F) || ld_vol64(&F.ctrl[CS * CTRL_DONE]) >= (unsigned long long)F.N)) { K = -1; break; }
           __nanosleep(ns);
           if (ns < 256) ns <<= 1;
         }
@@ -1036,7 +1226,8 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
     __threadfence();
     // order the bulk (async-proxy) reads of other blocks' panels after the acquire
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    process_block(F, K, S, smem, &s_mbar, mphase);
+    if (K < F.N) process_block(F, K, S, smem, &s_mbar, mphase);
+    else run_part(F, K, S, smem);
     __syncthreads();
   }
 }
@@ -1055,6 +1246,9 @@ extern "C" cudaError_t bilu_launch_factor(const DevFactor &F, int grid, cudaStre
   factor_kernel<<<grid, NT, F.smem_bytes, st>>>(F);
   return cudaGetLastError();
 }
+
+extern "C" int bilu_heavyctx_size() { return (int)sizeof(HeavyCtx); }
+extern "C" int bilu_max_parts() { return MAX_PARTS; }
 
 extern "C" cudaError_t bilu_factor_occupancy(int smem_bytes, int *blocks_per_sm) {
   cudaError_t err = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);

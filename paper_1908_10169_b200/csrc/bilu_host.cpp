@@ -35,6 +35,8 @@ extern "C" cudaError_t bilu_launch_permute(double *y, const double *x, const int
                                            int32_t n, int inverse, cudaStream_t st);
 extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_t st);
 extern "C" int bilu_merge_plan_launches();
+extern "C" int bilu_heavyctx_size();
+extern "C" int bilu_max_parts();
 extern "C" int bilu_merge_nchunks(int N);
 extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
                                         cudaStream_t st);
@@ -94,7 +96,7 @@ struct bilu_ctx {
   // dynamic
   DevFactor F{};
   int grid = 0;
-  int64_t cap_val = 0, cap_idx = 0, work_per_cta = 0;
+  int64_t cap_val = 0, cap_idx = 0, work_per_cta = 0, hpool_cap = 0;
   int pool_lc = 0, pool_uc = 0, pool_succ = 0;
   int64_t near_cap = 1 << 20;
   // results
@@ -400,7 +402,22 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   F.AU_ptr = h->d_AU_ptr; F.AU_rc = h->d_AU_rc; F.AU_val = h->d_AU_val;
   F.adj_ptr = h->d_adj_ptr; F.adj = h->d_adj;
   ALLOC(F.pending, n_blocks);
-  ALLOC(F.queue, n_blocks);
+  // heavy-block splitting: contexts, part tasks in the queue
+  F.hctx_cap = std::max<int64_t>(256, n_blocks / 4);
+  F.qcap = (int64_t)n_blocks + F.hctx_cap * bilu_max_parts();
+  ALLOC(F.queue, F.qcap);
+  {
+    void *hc = nullptr;
+    if (cudaMalloc(&hc, (size_t)F.hctx_cap * bilu_heavyctx_size()) != cudaSuccess) {
+      set_err(nullptr, "bilu_analyze: out of device memory"); bilu_destroy(h); return BILU_ERR_OOM;
+    }
+    h->owned.push_back(hc);
+    F.hctx = (HeavyCtx *)hc;
+  }
+  F.heavy_T = 2048;
+  if (const char *ht = getenv("BILU_HEAVY_T")) F.heavy_T = atoi(ht);
+  F.heavy_idle = 8;
+  if (const char *hi = getenv("BILU_HEAVY_IDLE")) F.heavy_idle = atoi(hi);
   ALLOC(F.ctrl, CTRL_COUNT * CS);
   ALLOC(F.Lrow_off, n_blocks); ALLOC(F.Lm, n_blocks); ALLOC(F.Lval_off, n_blocks);
   ALLOC(F.Ucol_off, n_blocks); ALLOC(F.Uc, n_blocks); ALLOC(F.Uval_off, n_blocks);
@@ -430,6 +447,7 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   h->cap_val = opt.arena_hint > 0 ? opt.arena_hint : std::max<int64_t>(16 * nnz, (int64_t)n * max_b * 4);
   h->cap_idx = h->cap_val;
   h->work_per_cta = 256 * 1024;
+  h->hpool_cap = std::max<int64_t>(1 << 22, 8 * nnz);
   h->pool_lc = h->pool_uc = std::max(2 * n_blocks, 1024);
   h->pool_succ = std::max(2 * n_blocks, 1024);
 
@@ -470,6 +488,11 @@ static bilu_status ensure_capacity(bilu_ctx *h) {
     F.cap_Lidx = F.cap_Uidx = h->cap_idx;
   }
   if (!F.posmap) CUDA_TRY(h, dalloc(h, &F.posmap, (size_t)h->grid * h->n));
+  if (F.hpool_cap != h->hpool_cap) {
+    dfree(h, F.hpool);
+    CUDA_TRY(h, dalloc(h, &F.hpool, (size_t)h->hpool_cap));
+    F.hpool_cap = h->hpool_cap;
+  }
   if (F.work_per_cta != h->work_per_cta) {
     dfree(h, F.work);
     CUDA_TRY(h, dalloc(h, &F.work, (size_t)h->work_per_cta * h->grid));
@@ -498,7 +521,7 @@ static bilu_status reset_schedule(bilu_ctx *h) {
   cudaStream_t st = h->stream;
   const size_t N = h->N;
   CUDA_TRY(h, cudaMemcpyAsync(F.pending, h->d_pending0, N * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-  CUDA_TRY(h, cudaMemsetAsync(F.queue, 0xFF, N * sizeof(int32_t), st));
+  CUDA_TRY(h, cudaMemsetAsync(F.queue, 0xFF, F.qcap * sizeof(int32_t), st));
   if (h->nready0)
     CUDA_TRY(h, cudaMemcpyAsync(F.queue, h->d_ready0, h->nready0 * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(F.ctrl, 0, CTRL_COUNT * CS * sizeof(unsigned long long), st));
@@ -585,7 +608,7 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
         CUDA_TRY(h, dalloc(h, &M.flag, (size_t)N));
       }
       h->merge_work_ints = 16384;
-      CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * h->grid));
+      CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * 2 * h->sms));
       h->fD_cap = std::max<int64_t>(h->D_off[N], 1);
       CUDA_TRY(h, dalloc(h, &M.fD, h->fD_cap));
       h->merge_alloc = true;
@@ -613,7 +636,7 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       if (attempt > 8) { set_err(h, "bilu_factor: merge workspace overflow"); return BILU_ERR_OOM; }
       dfree(h, M.work);
       h->merge_work_ints *= 4;
-      CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * h->grid));
+      CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * 2 * h->sms));
       M.work_ints = h->merge_work_ints;
       S.n_retries++;
     }
@@ -632,11 +655,12 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       CUDA_TRY(h, dalloc(h, &M.fD, h->fD_cap));
     }
     // per-CTA dense L_aa, U_aa of runs wider than the shared-memory tile
-    const int64_t need_dw = 2 * (int64_t)h->opt.max_block * h->opt.max_block;
+    const int64_t need_dw = 3 * (int64_t)h->opt.max_block * h->opt.max_block + (int64_t)tot[9];
+    const int mgrid = 2 * h->sms;
     if (need_dw > h->merge_dwork) {
       dfree(h, h->d_mdwork);
       h->merge_dwork = need_dw;
-      CUDA_TRY(h, dalloc(h, &h->d_mdwork, (size_t)need_dw * h->grid));
+      CUDA_TRY(h, dalloc(h, &h->d_mdwork, (size_t)need_dw * mgrid));
     }
     M.Lidx = F.Lidx; M.Uidx = F.Uidx; M.Lval = F.Lval; M.Uval = F.Uval;
     M.Lidx_out = F.Lidx; M.Uidx_out = F.Uidx; M.Lval_out = F.Lval; M.Uval_out = F.Uval;
@@ -645,7 +669,7 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       int ovf = 0;
       CUDA_TRY(h, cudaMemsetAsync(M.ovf, 0, sizeof(int), h->stream));
       CUDA_TRY(h, cudaMemsetAsync(M.flops, 0, sizeof(double), h->stream));
-      CUDA_TRY(h, bilu_merge_arith(M, h->d_mdwork, h->merge_dwork, h->grid, h->stream));
+      CUDA_TRY(h, bilu_merge_arith(M, h->d_mdwork, h->merge_dwork, mgrid, h->stream));
       launches += 1;
       CUDA_TRY(h, cudaMemcpyAsync(&mfl, M.flops, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
       CUDA_TRY(h, cudaMemcpyAsync(&ovf, M.ovf, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -655,7 +679,7 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       if (attempt > 8) { set_err(h, "bilu_factor: merge workspace overflow in arithmetic"); return BILU_ERR_OOM; }
       dfree(h, M.work);
       h->merge_work_ints *= 4;
-      CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * h->grid));
+      CUDA_TRY(h, dalloc(h, &M.work, (size_t)h->merge_work_ints * 2 * h->sms));
       M.work_ints = h->merge_work_ints;
       S.n_retries++;
     }
@@ -753,6 +777,10 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
       case DEV_OVF_ARENA: h->cap_val *= 2; h->cap_idx *= 2; break;
       case DEV_OVF_WORK: h->work_per_cta *= 4; break;
       case DEV_OVF_POOL: h->pool_lc *= 2; h->pool_uc *= 2; h->pool_succ *= 2; break;
+      case DEV_OVF_HPOOL:
+        if (ctrl[CTRL_HCTX] >= (unsigned long long)F.hctx_cap) F.heavy_T *= 2;   // fewer, larger splits
+        h->hpool_cap = std::max<int64_t>(h->hpool_cap, (int64_t)ctrl[CTRL_HPOOL] + (int64_t)ctrl[CTRL_HPOOL] / 4);
+        break;
       default: set_err(h, "bilu_factor: device list overflow (code %d, block %llu)", code, ctrl[CTRL_ERRBLK]); return BILU_ERR_OOM;
     }
   }

@@ -26,6 +26,7 @@ enum : int {
   DEV_OVF_LIST = 3,
   DEV_OVF_WORK = 4,
   DEV_OVF_POOL = 5,
+  DEV_OVF_HPOOL = 6,     // heavy-block pool, context table or task queue
 };
 
 // control block indices (int64 each)
@@ -45,7 +46,9 @@ enum : int {
   CTRL_DONE,
   CTRL_NDEC,
   CTRL_FLOPS,
-  CTRL_COUNT = 16
+  CTRL_HPOOL,      // doubles used in the heavy-block pool
+  CTRL_HCTX,       // heavy contexts used
+  CTRL_COUNT = 24
 };
 constexpr int CS = 16;   // ctrl stride: every control word on its own 128-byte line
 
@@ -57,6 +60,8 @@ struct ChunkList {
   int rec_ints;
   int ctrl_cursor; // index into ctrl of the pool cursor
 };
+
+struct HeavyCtx;   // bilu_factor.cu
 
 struct DevFactor {
   // problem
@@ -71,7 +76,8 @@ struct DevFactor {
   // static schedule: block adjacency of sym(Ã), successors > J
   const int32_t *adj_ptr; const int32_t *adj;
   int32_t *pending;          // [N]
-  int32_t *queue;            // [N]
+  int32_t *queue;            // [qcap]: block ids (< N) and part tasks (>= N) of split heavy blocks
+  int64_t qcap;
   unsigned long long *ctrl;  // [CTRL_COUNT * CS]
   // factors (per original block)
   int64_t *Lrow_off; int32_t *Lm; int64_t *Lval_off;
@@ -90,6 +96,11 @@ struct DevFactor {
   double *work; int64_t work_per_cta;   // doubles per CTA
   int *posmap;                          // [grid * n] index -> occurrence / buffer line
   volatile int *dbg;                    // mapped host memory for the deadlock watchdog (or NULL)
+  // split heavy blocks
+  HeavyCtx *hctx; int64_t hctx_cap;
+  double *hpool; int64_t hpool_cap;     // doubles
+  int heavy_T;                          // item count from which a block is split (0 = never)
+  int heavy_idle;                       // ... if at least this many CTAs are idle
   int smem_bytes;
   double tau, near_rel;
   int exp;                              // experiment switches (diagnostics only)

@@ -22,6 +22,7 @@
 #include <climits>
 
 #include "bilu_internal.h"
+#include "dgemm_cta.cuh"
 
 namespace bilu {
 
@@ -325,6 +326,7 @@ __global__ void __launch_bounds__(1024) merge_offsets_kernel(MergeArgs M) {
   const int lo = min(nF, (int)threadIdx.x * per), hi = min(nF, lo + per);
   // per-thread sums: D, Li, Lv, Ui, Uv (merged only), nL, nU, iL, iU, nmerged
   unsigned long long v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long maxws = 0;
   for (int F = lo; F < hi; ++F) {
     const int a = M.first[F], k = M.first[F + 1] - 1;
     const unsigned long long P = M.bstart[k + 1] - M.bstart[a];
@@ -337,7 +339,11 @@ __global__ void __launch_bounds__(1024) merge_offsets_kernel(MergeArgs M) {
     M.fbstart[F] = M.bstart[a];
     M.fLm[F] = (int32_t)u; M.fUc[F] = (int32_t)w;
     v[0] += P * P;
-    if (a != k) { v[1] += u; v[2] += u * P; v[3] += w; v[4] += w * P; v[9] += k - a; }
+    if (a != k) {
+      v[1] += u; v[2] += u * P; v[3] += w; v[4] += w * P; v[9] += k - a;
+      const unsigned long long ws = (u > w ? u : w) * P;
+      if (ws > maxws) maxws = ws;
+    }
     v[5] += u * P; v[6] += w * P; v[7] += u; v[8] += w;
   }
   unsigned long long tot[10];
@@ -360,12 +366,17 @@ __global__ void __launch_bounds__(1024) merge_offsets_kernel(MergeArgs M) {
       M.fUval_off[F] = (int64_t)cUv; cUv += w * P;
     }
   }
+  __shared__ unsigned long long smax;
+  if (threadIdx.x == 0) smax = 0;
+  __syncthreads();
+  atomicMax(&smax, maxws);
+  __syncthreads();
   if (threadIdx.x == 0) {
     M.fbstart[nF] = M.n;
     M.fD_off[nF] = (int64_t)tot[0];
     M.tot[4] = M.tot[0] + tot[1]; M.tot[5] = M.tot[1] + tot[2];
     M.tot[6] = M.tot[2] + tot[3]; M.tot[7] = M.tot[3] + tot[4];
-    M.tot[8] = tot[0]; M.tot[9] = 0; M.tot[10] = 0;
+    M.tot[8] = tot[0]; M.tot[9] = smax; M.tot[10] = 0;
     M.tot[11] = tot[9];
     M.tot[12] = tot[5]; M.tot[13] = tot[6]; M.tot[14] = tot[7]; M.tot[15] = tot[8];
   }
@@ -416,14 +427,18 @@ __device__ int build_union(const MergeArgs &M, int a, int k, bool rows, int *key
 // per merged run a..k (P = e_k - s_a <= max_block), member blocks j with offsets
 // o_j = s_j - s_a:
 //   L_aa (unit lower, identity member diagonal blocks), U_aa = D_j Ũ_j inside the run
-//   D^: X L_aa = D_agg, then U_aa D^ = X        (member-block back/forward steps)
-//   L^: L^ L_aa = L_{>,agg}                       (in place in the output panel)
-//   Ũ^: Ũ^ = L_aa Ũ_{agg,>}                       (in place, members last to first)
+//   Linv:  X L_aa = I                 (member-block steps, last to first)
+//   D^:    U_aa D^ = D_agg Linv        (member-block steps, last to first)
+//   L^ =   L_{>,agg} · Linv            (DMMA GEMM, u x P x P)
+//   Ũ^ =   L_aa · Ũ_{agg,>}            (DMMA GEMM, P x v x P)
+// Global workspace per CTA: [L_aa, U_aa if P > ARITH_PSMEM] Linv (P^2), G (max(u,v) P).
 __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dwork, int64_t dwork_per_cta) {
   extern __shared__ __align__(16) unsigned char msm_raw[];
-  double *sLU = (double *)msm_raw;                                   // 2 * 64^2 doubles
-  int *skeys = (int *)(msm_raw + 2 * ARITH_PSMEM * ARITH_PSMEM * 8);   // ARITH_KEYS
-  int *sflags = skeys + ARITH_KEYS;                                  // ARITH_KEYS
+  double *sLU = (double *)msm_raw;                                            // 2 * 64^2 doubles
+  unsigned char *scratch = msm_raw + 2 * ARITH_PSMEM * ARITH_PSMEM * 8;       // union keys | GEMM staging
+  int *skeys = (int *)scratch;                                                // ARITH_KEYS
+  int *sflags = skeys + ARITH_KEYS;                                           // ARITH_KEYS
+  double *sgemm = (double *)scratch;
   __shared__ int s_tmp[MW + 1];
   __shared__ int s_cnt[130];
   __shared__ int s_mo[130];       // member offsets o_j, j = a..k+1
@@ -444,147 +459,129 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
     }
     const int nm = k - a + 1;
     for (int x = tid; x <= nm; x += MT) s_mo[x] = M.bstart[a + x] - sa;
-    double *Laa, *Uaa;
-    if (P <= ARITH_PSMEM) { Laa = sLU; Uaa = sLU + P * P; }
-    else { Laa = gbase; Uaa = gbase + (size_t)P * P; }
+    double *Laa, *Uaa, *Linv, *G;
+    if (P <= ARITH_PSMEM) { Laa = sLU; Uaa = sLU + P * P; Linv = gbase; }
+    else { Laa = gbase; Uaa = gbase + (size_t)P * P; Linv = Uaa + (size_t)P * P; }
+    G = Linv + (size_t)P * P;
     for (int i = tid; i < P * P; i += MT) {
       const int r = i / P, c = i - r * P;
       Laa[i] = (r == c) ? 1.0 : 0.0;
       Uaa[i] = (r == c) ? 1.0 : 0.0;
-      // X = D_agg (block diagonal), column-major in the output
-      Dout[i] = 0.0;
+      Linv[i] = (r == c) ? 1.0 : 0.0;
     }
     __syncthreads();
-    // L_aa, U_aa and D_agg from the members
+    // L_aa, U_aa from the members
     for (int x = 0; x < nm; ++x) {
       const int j = a + x;
       const int oj = s_mo[x], bj = s_mo[x + 1] - oj;
       const int32_t *rows = M.Lidx + M.Lrow_off[j];
       const double *Lv = M.Lval + M.Lval_off[j];
       const int mj = M.Lm[j];
-      for (int it = tid; it < mj * bj; it += MT) {
+      const int mi = m_lbound(rows, 0, mj, ek);      // rows inside the run are a prefix
+      for (int it = tid; it < mi * bj; it += MT) {
         const int p = it / bj, t = it - p * bj;
-        const int xr = rows[p];
-        if (xr < ek) Laa[(size_t)(xr - sa) * P + oj + t] = Lv[it];
+        Laa[(size_t)(rows[p] - sa) * P + oj + t] = Lv[it];
       }
       const int32_t *cols = M.Uidx + M.Ucol_off[j];
       const double *Uv = M.Uval + M.Uval_off[j];
       const double *Dj = M.D + M.D_off[j];
       const int cj = M.Uc[j];
-      for (int it = tid; it < cj * bj; it += MT) {
+      const int ci = m_lbound(cols, 0, cj, ek);
+      for (int it = tid; it < ci * bj; it += MT) {
         const int q = it / bj, r = it - q * bj;
-        const int y = cols[q];
-        if (y < ek) {
-          double acc = 0.0;
-          for (int t = 0; t < bj; ++t) acc = fma(Dj[r + (size_t)t * bj], Uv[(size_t)q * bj + t], acc);
-          Uaa[(size_t)(oj + r) * P + (y - sa)] = acc;
-        }
-      }
-      for (int it = tid; it < bj * bj; it += MT) {
-        const int r = it % bj, c = it / bj;
-        Dout[(size_t)(oj + c) * P + oj + r] = Dj[it];
+        double acc = 0.0;
+        for (int t = 0; t < bj; ++t) acc = fma(Dj[r + (size_t)t * bj], Uv[(size_t)q * bj + t], acc);
+        Uaa[(size_t)(oj + r) * P + (cols[q] - sa)] = acc;
       }
     }
     __syncthreads();
-    // D^: X L_aa = D_agg, members last to first: X[:, c in m] -= X[:, later] L_aa[later, c]
-    for (int x = nm - 1; x >= 0; --x) {
+    // Linv (row-major): X L_aa = I, members last to first: X[:, c in m] -= X[:, later] L_aa[later, c]
+    for (int x = nm - 2; x >= 0; --x) {
       const int om = s_mo[x], bm = s_mo[x + 1] - om, e = s_mo[x + 1];
       for (int it = tid; it < P * bm; it += MT) {
-        const int i = it % P, c = om + it / P;
+        const int i = it / bm, c = om + it % bm;
+        if (i < e) continue;                 // rows above the later members stay e_i
         double acc = 0.0;
-        for (int t = e; t < P; ++t) acc = fma(Dout[(size_t)t * P + i], Laa[(size_t)t * P + c], acc);
-        Dout[(size_t)c * P + i] -= acc;
+        const double *xr = Linv + (size_t)i * P;
+        for (int t = e; t <= i; ++t) acc = fma(xr[t], Laa[(size_t)t * P + c], acc);
+        Linv[(size_t)i * P + c] = -acc;
       }
       __syncthreads();
     }
-    // U_aa D^ = X, members last to first: D^[r in m, :] -= U_aa[r, later] D^[later, :]
-    for (int x = nm - 1; x >= 0; --x) {
+    // D^ (column-major in Dout): T = D_agg Linv, then U_aa D^ = T, members last to first
+    for (int x = 0; x < nm; ++x) {
+      const int om = s_mo[x], bm = s_mo[x + 1] - om;
+      const double *Dj = M.D + M.D_off[a + x];
+      for (int it = tid; it < P * bm; it += MT) {
+        const int r = it % bm, c = it / bm;
+        double acc = 0.0;
+        for (int t = 0; t < bm; ++t) acc = fma(Dj[r + (size_t)t * bm], Linv[(size_t)(om + t) * P + c], acc);
+        Dout[(size_t)c * P + om + r] = acc;
+      }
+    }
+    __syncthreads();
+    for (int x = nm - 2; x >= 0; --x) {
       const int om = s_mo[x], bm = s_mo[x + 1] - om, e = s_mo[x + 1];
       for (int it = tid; it < P * bm; it += MT) {
         const int r = om + it % bm, c = it / bm;
         double acc = 0.0;
-        for (int t = e; t < P; ++t) acc = fma(Uaa[(size_t)r * P + t], Dout[(size_t)c * P + t], acc);
+        const double *ur = Uaa + (size_t)r * P;
+        const double *dc = Dout + (size_t)c * P;
+        for (int t = e; t < P; ++t) acc = fma(ur[t], dc[t], acc);
         Dout[(size_t)c * P + r] -= acc;
       }
       __syncthreads();
     }
-    // ---- L^ rows
+    // ---- L^ rows: union, gathered L_g (u x P row-major) in G, L^ = G Linv
     const int u = M.fLm[F], v = M.fUc[F];
     {
       int *R = M.Lidx_out + M.fLrow_off[F];
-      const bool sm = true;
-      int cap = ARITH_KEYS;
-      int *kb = skeys, *fb = sflags;
-      int uu = build_union(M, a, k, true, kb, fb, cap, s_cnt, s_tmp, R);
-      if (uu < 0) {
-        (void)sm;
-        uu = build_union(M, a, k, true, gkeys, gkeys + M.work_ints / 2, (int)(M.work_ints / 2), s_cnt, s_tmp, R);
-      }
+      int uu = build_union(M, a, k, true, skeys, sflags, ARITH_KEYS, s_cnt, s_tmp, R);
+      if (uu < 0) uu = build_union(M, a, k, true, gkeys, gkeys + M.work_ints / 2, (int)(M.work_ints / 2), s_cnt, s_tmp, R);
       if (uu != u) { if (tid == 0) atomicExch(M.ovf, uu < 0 ? 1 : 2); return; }
-      double *Lout = M.Lval_out + M.fLval_off[F];
-      for (int i = tid; i < u * P; i += MT) Lout[i] = 0.0;
-      __syncthreads();
-      for (int x = 0; x < nm; ++x) {
-        const int j = a + x;
-        const int oj = s_mo[x], bj = s_mo[x + 1] - oj;
-        const int32_t *rows = M.Lidx + M.Lrow_off[j];
-        const double *Lv = M.Lval + M.Lval_off[j];
-        const int mj = M.Lm[j];
-        for (int it = tid; it < mj * bj; it += MT) {
-          const int p = it / bj, t = it - p * bj;
-          const int xr = rows[p];
-          if (xr >= ek) Lout[(size_t)m_lbound(R, 0, u, xr) * P + oj + t] = Lv[it];
-        }
-      }
-      __syncthreads();
-      for (int x = nm - 1; x >= 0; --x) {
-        const int om = s_mo[x], bm = s_mo[x + 1] - om, e = s_mo[x + 1];
-        if (e < P) {
-          for (int it = tid; it < u * bm; it += MT) {
-            const int i = it / bm, c = om + it % bm;
-            double *row = Lout + (size_t)i * P;
-            double acc = 0.0;
-            for (int t = e; t < P; ++t) acc = fma(row[t], Laa[(size_t)t * P + c], acc);
-            row[c] -= acc;
+      if (u > 0) {
+        for (int i = tid; i < u * P; i += MT) G[i] = 0.0;
+        __syncthreads();
+        for (int x = 0; x < nm; ++x) {
+          const int j = a + x;
+          const int oj = s_mo[x], bj = s_mo[x + 1] - oj;
+          const int32_t *rows = M.Lidx + M.Lrow_off[j];
+          const double *Lv = M.Lval + M.Lval_off[j];
+          const int mj = M.Lm[j];
+          const int mi = m_lbound(rows, 0, mj, ek);
+          for (int it = mi * bj + tid; it < mj * bj; it += MT) {
+            const int p = it / bj, t = it - p * bj;
+            G[(size_t)m_lbound(R, 0, u, rows[p]) * P + oj + t] = Lv[it];
           }
         }
         __syncthreads();
+        cta_dgemm<MT>(u, P, P, 1.0, DMat{G, P, 1}, DMat{Linv, P, 1}, 0.0, M.Lval_out + M.fLval_off[F], P, 1,
+                      sgemm);
       }
     }
-    // ---- Ũ^ columns
+    // ---- Ũ^ columns: union, gathered Ũ_g (P x v column-major) in G, Ũ^ = L_aa G
     {
       int *Cc = M.Uidx_out + M.fUcol_off[F];
       int vv = build_union(M, a, k, false, skeys, sflags, ARITH_KEYS, s_cnt, s_tmp, Cc);
       if (vv < 0) vv = build_union(M, a, k, false, gkeys, gkeys + M.work_ints / 2, (int)(M.work_ints / 2), s_cnt, s_tmp, Cc);
       if (vv != v) { if (tid == 0) atomicExch(M.ovf, vv < 0 ? 1 : 2); return; }
-      double *Uout = M.Uval_out + M.fUval_off[F];
-      for (int i = tid; i < v * P; i += MT) Uout[i] = 0.0;
-      __syncthreads();
-      for (int x = 0; x < nm; ++x) {
-        const int j = a + x;
-        const int oj = s_mo[x], bj = s_mo[x + 1] - oj;
-        const int32_t *cols = M.Uidx + M.Ucol_off[j];
-        const double *Uv = M.Uval + M.Uval_off[j];
-        const int cj = M.Uc[j];
-        for (int it = tid; it < cj * bj; it += MT) {
-          const int q = it / bj, t = it - q * bj;
-          const int y = cols[q];
-          if (y >= ek) Uout[(size_t)m_lbound(Cc, 0, v, y) * P + oj + t] = Uv[it];
-        }
-      }
-      __syncthreads();
-      // rows r of member m: Ũ^[r, y] += L_aa[r, earlier] Ũ_g[earlier, y]
-      for (int x = nm - 1; x >= 1; --x) {
-        const int om = s_mo[x], bm = s_mo[x + 1] - om;
-        for (int it = tid; it < v * bm; it += MT) {
-          const int y = it / bm, r = om + it % bm;
-          double *col = Uout + (size_t)y * P;
-          const double *lr = Laa + (size_t)r * P;
-          double acc = 0.0;
-          for (int t = 0; t < om; ++t) acc = fma(lr[t], col[t], acc);
-          col[r] += acc;
+      if (v > 0) {
+        for (int i = tid; i < v * P; i += MT) G[i] = 0.0;
+        __syncthreads();
+        for (int x = 0; x < nm; ++x) {
+          const int j = a + x;
+          const int oj = s_mo[x], bj = s_mo[x + 1] - oj;
+          const int32_t *cols = M.Uidx + M.Ucol_off[j];
+          const double *Uv = M.Uval + M.Uval_off[j];
+          const int cj = M.Uc[j];
+          const int ci = m_lbound(cols, 0, cj, ek);
+          for (int it = ci * bj + tid; it < cj * bj; it += MT) {
+            const int q = it / bj, t = it - q * bj;
+            G[(size_t)m_lbound(Cc, 0, v, cols[q]) * P + oj + t] = Uv[it];
+          }
         }
         __syncthreads();
+        cta_dgemm<MT>(P, v, P, 1.0, DMat{Laa, P, 1}, DMat{G, 1, P}, 0.0, M.Uval_out + M.fUval_off[F], 1, P, sgemm);
       }
     }
     if (tid == 0) {
@@ -611,10 +608,10 @@ extern "C" int bilu_merge_nchunks(int N) { return N > 1 ? (N - 1 + SCAN_CHUNK - 
 
 extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
                                         cudaStream_t st) {
-  const int smem = 2 * ARITH_PSMEM * ARITH_PSMEM * 8 + 2 * ARITH_KEYS * 4;
+  const int smem = 2 * ARITH_PSMEM * ARITH_PSMEM * 8 + (2 * ARITH_KEYS * 4 > DGEMM_SMEM_DOUBLES * 8 ? 2 * ARITH_KEYS * 4 : DGEMM_SMEM_DOUBLES * 8);
   cudaError_t e = cudaFuncSetAttribute(merge_arith_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  merge_arith_kernel<<<grid, MT, smem, st>>>(M, dwork, dwork_per_cta);
+  merge_arith_kernel<<<grid, MT, smem, st>>>(M, dwork, dwork_per_cta);   // grid = 2 CTAs per SM
   return cudaGetLastError();
 }
 

@@ -42,3 +42,30 @@ extern "C" cudaError_t bilu_launch_permute(double *y, const double *x, const int
 }
 
 }  // namespace bilu
+
+// ------------------------------------------------------------ diagnostics
+// cta_dgemm (DMMA m8n8k4) exercised on its own: `batch` independent products,
+// one CTA each, C_b = alpha A_b B_b + beta C_b (bilu.h: bilu_diag_dgemm).
+#include "dgemm_cta.cuh"
+namespace bilu {
+__global__ void __launch_bounds__(256) diag_dgemm_kernel(int M, int N, int K, double alpha, const double *A,
+                                                         int64_t ars, int64_t acs, const double *B, int64_t brs,
+                                                         int64_t bcs, double beta, double *C, int64_t crs,
+                                                         int64_t ccs, int64_t sa, int64_t sb, int64_t sc) {
+  __shared__ double sm[DGEMM_SMEM_DOUBLES];
+  const int b = blockIdx.x;
+  cta_dgemm<256>(M, N, K, alpha, DMat{A + b * sa, ars, acs}, DMat{B + b * sb, brs, bcs}, beta, C + b * sc, crs,
+                 ccs, sm);
+}
+}  // namespace bilu
+
+extern "C" int bilu_diag_dgemm(int M, int N, int K, double alpha, const double *A, int64_t ars, int64_t acs,
+                               const double *B, int64_t brs, int64_t bcs, double beta, double *C, int64_t crs,
+                               int64_t ccs, int batch, int64_t sa, int64_t sb, int64_t sc, void *stream) {
+  if (M < 0 || N < 0 || K < 0 || batch < 1) return 1;
+  if (M == 0 || N == 0) return 0;
+  if (!A || !B || !C) return 1;
+  bilu::diag_dgemm_kernel<<<batch, 256, 0, (cudaStream_t)stream>>>(M, N, K, alpha, A, ars, acs, B, brs, bcs, beta,
+                                                                   C, crs, ccs, sa, sb, sc);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
