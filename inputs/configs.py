@@ -158,7 +158,89 @@ def config3(seed=1003, N=48, dof=3, leaf=512, top_levels=1):
                     "seed": seed})
 
 
-CONFIGS = {"c1": config1, "c2": config2, "c3": config3}
+# --------------------------------------------------------------------------- c4
+def config4(seed=1004, nblocks=20000, bmin=16, bmax=64, per_row=12, dominance=1.5):
+    """Random block-sparse unsymmetric matrix: nblocks dense diagonal blocks of size
+    U{bmin..bmax}; per block row `per_row` distinct random column blocks != i; every
+    stored block iid N(0,1) (drawn in CSR order); then a_rr = dominance *
+    sum_{c != r} |a_rc| (diagonal block shifted to dominance).  Identity ordering,
+    the generator's blocks as the initial partition, tau = 1e-4."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    bsz = rng.integers(bmin, bmax + 1, size=nblocks).astype(np.int64)
+    bstart = np.concatenate([[0], np.cumsum(bsz)])
+    n = int(bstart[-1])
+    colblk = []
+    for i in range(nblocks):
+        c = rng.choice(nblocks - 1, size=min(per_row, nblocks - 1), replace=False)
+        c = c + (c >= i)
+        colblk.append(np.sort(np.concatenate([[i], c])))
+    # row template of each block row, tiled over its rows
+    rowlen = np.array([int(bsz[cb].sum()) for cb in colblk], dtype=np.int64)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum(np.repeat(rowlen, bsz))
+    nnz = int(indptr[-1])
+    indices = np.empty(nnz, dtype=np.int32)
+    for i in range(nblocks):
+        tmpl = np.concatenate([np.arange(bstart[c], bstart[c + 1], dtype=np.int32) for c in colblk[i]])
+        a, b_ = indptr[bstart[i]], indptr[bstart[i + 1]]
+        indices[a:b_] = np.tile(tmpl, int(bsz[i]))
+    data = rng.standard_normal(nnz)
+    rr = np.repeat(np.arange(n, dtype=np.int64), np.diff(indptr))
+    dmask = rr == indices
+    offsum = np.bincount(rr, weights=np.abs(data) * (~dmask), minlength=n)
+    data[dmask] = dominance * offsum[rr[dmask]]
+    del rr, dmask
+    return Problem("c4", n, indptr, indices, data, np.arange(n, dtype=np.int64), bsz.astype(np.int32), 1e-4,
+                   np.zeros(nblocks, dtype=np.int32),
+                   {"nblocks": nblocks, "bmin": bmin, "bmax": bmax, "per_row": per_row, "seed": seed,
+                    "ordering": "identity"})
+
+
+# --------------------------------------------------------------------------- c5
+def config5(seed=1005, N=128, leaf=512, block=8, top_levels=3, peclet=50.0):
+    """3D 27-pt convection-diffusion on N^3, h = 1/(N+1): node kappa ~ lognormal(0,1)
+    (drawn in node order); off-diagonal -2 k_i k_j / (k_i + k_j) for all 26 neighbours;
+    upwind -h*beta_d on the -e_d face neighbour, beta = Pe*(1, .5, .25); a_ii = sum
+    |a_ij| over the full stencil (out-of-grid neighbours with k_j = k_i, nominal
+    upwind) -> irreducibly diagonally dominant M-matrix.  Geometric ND with
+    `top_levels` levels of top subtrees (8 for the multi-GPU partition), tau = 1e-3."""
+    n = N ** 3
+    h = 1.0 / (N + 1)
+    beta = peclet * np.array([1.0, 0.5, 0.25])
+    rng = np.random.Generator(np.random.PCG64(seed))
+    kappa = rng.lognormal(0.0, 1.0, size=n)
+    offs = _grid_offsets(27)
+    rows, cols, oid = _stencil_pairs(N, N, N, offs)
+    ki, kj = kappa[rows], kappa[cols]
+    vals = -2.0 * ki * kj / (ki + kj)
+    del ki, kj
+    # upwind on the -e_d faces
+    up = np.zeros(len(offs))
+    for d, e in enumerate([(-1, 0, 0), (0, -1, 0), (0, 0, -1)]):
+        up[offs.index(e)] = -h * beta[d]
+    vals += up[oid]
+    diag = np.bincount(rows, weights=np.abs(vals), minlength=n)
+    # out-of-grid neighbours: k_j = k_i -> -k_i (+ upwind), counted into the diagonal
+    present = np.bincount(rows, minlength=n)
+    full = np.zeros(n)
+    for k in range(len(offs)):
+        full += np.abs(-kappa + up[k])
+    present_sum = np.zeros(n)
+    np.add.at(present_sum, rows, np.abs(-kappa[rows] + up[oid]))
+    diag += full - present_sum
+    del present
+    allr = np.concatenate([rows, np.arange(n)])
+    allc = np.concatenate([cols, np.arange(n)])
+    allv = np.concatenate([vals, diag])
+    del rows, cols, vals, oid
+    indptr, indices, data = _csr_from_coo(n, allr, allc, allv)
+    perm, sizes, parts = grid_nd(N, N, N, leaf=leaf, block=block, top_levels=top_levels)
+    return Problem("c5", n, indptr, indices, data, perm, sizes, 1e-3, parts,
+                   {"grid": (N, N, N), "ordering": "geometric ND", "leaf": leaf, "block": block,
+                    "top_levels": top_levels, "peclet": peclet, "seed": seed})
+
+
+CONFIGS = {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5}
 
 
 def make_config(name, **kw) -> Problem:

@@ -25,6 +25,7 @@
 #include <climits>
 
 #include "bilu_internal.h"
+#include "dgemm_cta.cuh"
 
 namespace bilu {
 
@@ -471,7 +472,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
     // ---- bitmap path: dedup by atomicOr in shared memory, sorted for free
     bm = (unsigned *)balloc_top(A, (int64_t)(words + 1) * 4);
     pre = (int *)balloc_top(A, (int64_t)(words + 1) * 4);
-    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
+    if (A.ovf) { if (tid == 0) raise_abort(F, A.bottom_global ? DEV_OVF_HPOOL : DEV_OVF_WORK, K); return false; }
     for (int w = tid; w < words; w += NT) bm[w] = 0u;
     __syncthreads();
     for (int64_t p = ae + tid; p < a1; p += NT) {
@@ -506,7 +507,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
     if (A.bottom_global) {   // a split block: the helpers need the map in global memory
       unsigned *gbm = (unsigned *)balloc(A, (int64_t)(words + 1) * 4);
       int *gpre = (int *)balloc(A, (int64_t)(words + 1) * 4);
-      if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
+      if (A.ovf) { if (tid == 0) raise_abort(F, A.bottom_global ? DEV_OVF_HPOOL : DEV_OVF_WORK, K); return false; }
       for (int w = tid; w < words; w += NT) { gbm[w] = bm[w]; gpre[w] = pre[w]; }
       R.gbm = gbm; R.gpre = gpre;
     }
@@ -532,7 +533,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
     if (tid == 0) S.cnt[2] = 0;
     __syncthreads();
     int *uniq = (int *)balloc_top(A, (int64_t)(occ + 1) * 4);
-    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
+    if (A.ovf) { if (tid == 0) raise_abort(F, A.bottom_global ? DEV_OVF_HPOOL : DEV_OVF_WORK, K); return false; }
     {
       int a = 0;
       for (int o = tid; o < occ; o += NT) {
@@ -559,7 +560,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
   const int nW = base + nU;
   double *W = (double *)balloc(A, (int64_t)nW * b * 8);
   int *lineOf = (int *)balloc(A, (int64_t)(nW + 1) * 4);
-  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
+  if (A.ovf) { if (tid == 0) raise_abort(F, A.bottom_global ? DEV_OVF_HPOOL : DEV_OVF_WORK, K); return false; }
   for (int x = tid; x < base; x += NT) lineOf[x] = s + x;
   if (M.bm) {
     for (int w = tid; w < words; w += NT) {
@@ -640,6 +641,43 @@ __device__ void side_items(const DevFactor &F, int s, int e, const Contrib *C, i
   }
 }
 
+// a-5 for wide blocks: per contributor J (ascending, R13) one dense product on the FP64
+// tensor pipe, "gather ... GEMM ... scatter" (Fig. 2):
+//   SIDE 0: W_L[line(rows of L_J >= s_K), cols of Ũ_J in K] -= L_J(rows >= s_K, :) · Ũ_J(:, cols in K)
+//   SIDE 1: W_U[line(cols of Ũ_J >= e_K), rows of L_J in K] -= Ũ_J(:, cols >= e_K)^T · L_J(rows in K, :)^T
+// Both operands are contiguous slices of the hybrid panels; each output element is
+// scattered once per product, so no atomics are needed.
+template <int SIDE>
+struct EpiScatter {
+  const int32_t *ikey, *jkey;   // matrix index of output row i / column j
+  int s, e, b;
+  LineMap M;
+  double *W;
+  __device__ __forceinline__ void operator()(int i, int j, double v) const {
+    const int key = ikey[i];
+    const int ln = (SIDE == 0 && key < e) ? key - s : M(key);
+    W[(int64_t)ln * b + (jkey[j] - s)] -= v;
+  }
+};
+
+template <int SIDE>
+__device__ void side_gemms(const DevFactor &F, int s, int e, int b, const Contrib *C, int nc, const LineMap &M,
+                           double *W, double *gs) {
+  for (int a = 0; a < nc; ++a) {
+    const Contrib &c = C[a];
+    if (c.n_items == 0 || c.ncol == 0) continue;
+    if (SIDE == 0) {
+      EpiScatter<0> ep{F.Lidx + c.rows, F.Uidx + c.cols, s, e, b, M, W};
+      cta_dgemm_epi<NT>(c.n_items, c.ncol, c.bJ, DMat{F.Lval + c.lval, c.bJ, 1}, DMat{F.Uval + c.uval, 1, c.bJ},
+                        ep, gs);
+    } else {
+      EpiScatter<1> ep{F.Uidx + c.cols, F.Lidx + c.rows, s, e, b, M, W};
+      cta_dgemm_epi<NT>(c.n_items, c.ncol, c.bJ, DMat{F.Uval + c.uval, c.bJ, 1}, DMat{F.Lval + c.lval, 1, c.bJ},
+                        ep, gs);
+    }
+  }
+}
+
 __device__ double side_flops(const Contrib *C, int nc) {
   double f = 0.0;
   for (int a = 0; a < nc; ++a) f += 2.0 * C[a].bJ * (double)C[a].n_items * (double)C[a].ncol;
@@ -688,14 +726,21 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   // split only when CTAs are idle (tickets taken but not yet filled)
   if (tid == 0) {
     const long long idle = (long long)ld_vol64(&F.ctrl[CS * CTRL_QTAIL]) - (long long)ld_vol64(&F.ctrl[CS * CTRL_QHEAD]);
-    S.cnt[3] = (F.heavy_T > 0 && TL + TU >= F.heavy_T && idle >= F.heavy_idle) ? 1 : 0;
+    int wide = b > 16;
+    for (int a = 0; a < nLc && !wide; ++a) wide = CL[a].bJ > 16;
+    for (int a = 0; a < nUc && !wide; ++a) wide = CU[a].bJ > 16;
+    S.cnt[3] = (!wide && F.heavy_T > 0 && TL + TU >= F.heavy_T && idle >= F.heavy_idle) ? 1 : 0;
   }
   __syncthreads();
   const bool heavy = S.cnt[3] != 0;
   if (heavy) {
     const int64_t nAL = aL1 - aLe, nAU = aU1;
     const int64_t lines = (int64_t)b + nAL + TL + 1, cols = nAU - aU0 + TU + 1;
-    const int64_t need = (lines + cols) * (b + 1) + 2 * 8200 + 64 +
+    const int64_t wmax = min(8200, (F.n - e) / 32 + 4);   // bitmap words of one side
+    // upper bound of the pool chunk: W + line maps ((b+1) doubles per line), the scratch of
+    // the pos-map path (1/2 per line), bitmaps + prefix sums of both sides that do not fit
+    // in shared memory and their global copies (4 x (words + pad)), the contributor copies
+    const int64_t need = (lines + cols) * (b + 2) + 4 * (wmax + 8) + 64 +
                          (int64_t)(nLc + nUc) * (int64_t)(sizeof(Contrib) / 8) + 64;
     if (tid == 0) {
       unsigned long long o = atomicAdd(&F.ctrl[CS * CTRL_HPOOL], (unsigned long long)need);
@@ -729,7 +774,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     __syncthreads();
     if (tid == 0) {
       const unsigned long long h = atomicAdd(&F.ctrl[CS * CTRL_HCTX], 1ull);
-      if (h >= (unsigned long long)F.hctx_cap) { raise_abort(F, DEV_OVF_HPOOL, K); S.off[1] = ~0ull; }
+      if (h >= (unsigned long long)F.hctx_cap) { raise_abort(F, DEV_OVF_HCTX, K); S.off[1] = ~0ull; }
       else {
         HeavyCtx &X = F.hctx[h];
         X.K = K; X.nc[0] = nLc; X.nc[1] = nUc; X.T[0] = TL; X.T[1] = TU; X.np[0] = pL; X.np[1] = pU;
@@ -738,7 +783,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
         X.left = pL + pU;
         __threadfence();
         const unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], (unsigned long long)(pL + pU));
-        if (slot + pL + pU > (unsigned long long)F.qcap) raise_abort(F, DEV_OVF_HPOOL, K);
+        if (slot + pL + pU > (unsigned long long)F.qcap) raise_abort(F, DEV_OVF_HCTX, K);
         else
           for (int p = 0; p < pL + pU; ++p) st_vol(&F.queue[slot + p], F.N + (int)h * MAX_PARTS + p);
         S.off[1] = h;
@@ -749,7 +794,15 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   }
 
   // ---------------- a-5, this CTA: every (contributor, item) pair
-  if (heavy) {
+  int maxbJ = 0;
+  for (int a = 0; a < nLc; ++a) maxbJ = max(maxbJ, CL[a].bJ);
+  for (int a = 0; a < nUc; ++a) maxbJ = max(maxbJ, CU[a].bJ);
+  if (b > 16 || maxbJ > 16) {
+    double *gs = (double *)balloc_top(A, (int64_t)DGEMM_SMEM_DOUBLES * 8);
+    OVF_CHECK();
+    side_gemms<0>(F, s, e, b, CL, nLc, RL.M, RL.W, gs);
+    side_gemms<1>(F, s, e, b, CU, nUc, RU.M, RU.W, gs);
+  } else if (heavy) {
     side_items<0, true>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
     side_items<1, true>(F, s, e, CU, nUc, 0, TU, b, RU.M, RU.W);
   } else {
@@ -963,6 +1016,20 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   int *keepR = (int *)balloc(A, (int64_t)(nR + 1) * 4);
   int *keepC = (int *)balloc(A, (int64_t)(nC + 1) * 4);
   OVF_CHECK();
+  // wide blocks: the scaled candidates L_cand = W_L D_K and U_cand^T = Z^T D_K^T on the
+  // FP64 tensor pipe (the trsm-equivalent of PAPER.md:788-790, 210-212)
+  double *Lsc = nullptr, *Usc = nullptr;
+  if (b > 16) {
+    Lsc = (double *)balloc(A, (int64_t)nR * b * 8);
+    Usc = (double *)balloc(A, (int64_t)nC * b * 8);
+    const int sv_stop = A.stop;
+    const int64_t sv_gtop = A.gtop;
+    double *gs = (double *)balloc_top(A, (int64_t)DGEMM_SMEM_DOUBLES * 8);
+    OVF_CHECK();
+    cta_dgemm<NT>(nR, b, b, 1.0, DMat{WL + (int64_t)b * b, b, 1}, DMat{P, 1, b}, 0.0, Lsc, b, 1, gs);
+    cta_dgemm<NT>(nC, b, b, 1.0, DMat{WU, b, 1}, DMat{P, b, 1}, 0.0, Usc, b, 1, gs);
+    A.stop = sv_stop; A.gtop = sv_gtop;   // release the staging scratch
+  }
   for (int i = tid; i < nR; i += NT) {
     double *w = WL + (int64_t)(b + i) * b;
     double mx = 0.0;
@@ -980,11 +1047,8 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
 #pragma unroll
       for (int c = 0; c < 16; ++c) if (c < b) w[c] = l[c];
     } else {
-      for (int c = 0; c < b; ++c) {
-        double acc = 0.0;
-        for (int t = 0; t < b; ++t) acc = fma(w[t], P[t + (int64_t)c * b], acc);
-        mx = fmax(mx, fabs(acc));
-      }
+      const double *l = Lsc + (int64_t)i * b;
+      for (int c = 0; c < b; ++c) mx = fmax(mx, fabs(l[c]));
     }
     const int keep = mx > tau;
     keepR[i] = keep;
@@ -1004,10 +1068,15 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   for (int j = tid; j < nC; j += NT) {
     const double *z = WU + (int64_t)j * b;
     double mx = 0.0;
-    for (int rr = 0; rr < b; ++rr) {
-      double acc = 0.0;
-      for (int t = 0; t < b; ++t) acc = fma(P[rr + (int64_t)t * b], z[t], acc);
-      mx = fmax(mx, fabs(acc));
+    if (b > 16) {
+      const double *u = Usc + (int64_t)j * b;
+      for (int rr = 0; rr < b; ++rr) mx = fmax(mx, fabs(u[rr]));
+    } else {
+      for (int rr = 0; rr < b; ++rr) {
+        double acc = 0.0;
+        for (int t = 0; t < b; ++t) acc = fma(P[rr + (int64_t)t * b], z[t], acc);
+        mx = fmax(mx, fabs(acc));
+      }
     }
     const int keep = mx > tau;
     keepC[j] = keep;
@@ -1101,14 +1170,8 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   for (int x = tid; x < mK; x += NT) F.Lidx[oLi + x] = R[x];
   for (int it = tid; it < mK * b; it += NT) {
     const int x = it / b, c = it - x * b;
-    if (b <= 16) {
-      F.Lval[oLv + it] = WL[(int64_t)kr[ordR[x]] * b + c];
-    } else {
-      const double *w = WL + (int64_t)kr[ordR[x]] * b;
-      double acc = 0.0;
-      for (int t = 0; t < b; ++t) acc = fma(w[t], P[t + (int64_t)c * b], acc);
-      F.Lval[oLv + it] = acc;
-    }
+    if (b <= 16) F.Lval[oLv + it] = WL[(int64_t)kr[ordR[x]] * b + c];
+    else F.Lval[oLv + it] = Lsc[(int64_t)(kr[ordR[x]] - b) * b + c];
   }
   for (int x = tid; x < cK; x += NT) F.Uidx[oUi + x] = Cs[x];
   for (int it = tid; it < cK * b; it += NT) {

@@ -771,6 +771,10 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
       set_err(h, "bilu_factor: pivot block %d is exactly singular", S.breakdown_block);
       return BILU_ERR_BREAKDOWN;
     }
+    if (getenv("BILU_VERBOSE"))
+      fprintf(stderr, "bilu_factor retry %d: code %d block %llu hpool %lld/%lld hctx %llu/%lld work %lld\n", attempt, code,
+              ctrl[CTRL_ERRBLK], (long long)ctrl[CTRL_HPOOL], (long long)h->hpool_cap, ctrl[CTRL_HCTX],
+              (long long)F.hctx_cap, (long long)h->work_per_cta);
     if (attempt >= 12) { set_err(h, "bilu_factor: workspace overflow persists (code %d)", code); return BILU_ERR_OOM; }
     S.n_retries++;
     switch (code) {
@@ -778,9 +782,9 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
       case DEV_OVF_WORK: h->work_per_cta *= 4; break;
       case DEV_OVF_POOL: h->pool_lc *= 2; h->pool_uc *= 2; h->pool_succ *= 2; break;
       case DEV_OVF_HPOOL:
-        if (ctrl[CTRL_HCTX] >= (unsigned long long)F.hctx_cap) F.heavy_T *= 2;   // fewer, larger splits
-        h->hpool_cap = std::max<int64_t>(h->hpool_cap, (int64_t)ctrl[CTRL_HPOOL] + (int64_t)ctrl[CTRL_HPOOL] / 4);
+        h->hpool_cap = std::max<int64_t>(2 * h->hpool_cap, (int64_t)ctrl[CTRL_HPOOL] + (int64_t)ctrl[CTRL_HPOOL] / 4);
         break;
+      case DEV_OVF_HCTX: F.heavy_T *= 2; break;   // fewer split blocks
       default: set_err(h, "bilu_factor: device list overflow (code %d, block %llu)", code, ctrl[CTRL_ERRBLK]); return BILU_ERR_OOM;
     }
   }

@@ -26,7 +26,8 @@ enum : int {
   DEV_OVF_LIST = 3,
   DEV_OVF_WORK = 4,
   DEV_OVF_POOL = 5,
-  DEV_OVF_HPOOL = 6,     // heavy-block pool, context table or task queue
+  DEV_OVF_HPOOL = 6,     // heavy-block pool
+  DEV_OVF_HCTX = 7,      // heavy-block context table or task queue
 };
 
 // control block indices (int64 each)

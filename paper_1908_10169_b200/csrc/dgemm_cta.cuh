@@ -36,9 +36,9 @@ constexpr int DGEMM_SMEM_DOUBLES = 2 * GT * GS;
 
 // smem: DGEMM_SMEM_DOUBLES doubles (20 KB).  All threads of the CTA must call it.
 // Ends with __syncthreads().  C may alias neither A nor B.
-template <int NTH>
-__device__ void cta_dgemm(int M, int N, int K, double alpha, DMat A, DMat B, double beta, double *C, int64_t crs,
-                          int64_t ccs, double *smem) {
+// Epilogue functor: epi(i, j, acc) receives every output element (i < M, j < N) once.
+template <int NTH, class Epi>
+__device__ void cta_dgemm_epi(int M, int N, int K, DMat A, DMat B, Epi epi, double *smem) {
   constexpr int NWARP = NTH / 32;
   constexpr int WN = NWARP >= 4 ? 4 : NWARP;          // warps along n
   constexpr int WM = NWARP / WN;                       // warps along m
@@ -109,14 +109,26 @@ __device__ void cta_dgemm(int M, int N, int K, double alpha, DMat A, DMat B, dou
           for (int h = 0; h < 2; ++h) {
             const int gm = m0 + wm * TM * 8 + i * 8 + g;
             const int gn = n0 + wn * TN * 8 + j * 8 + 2 * q + h;
-            if (gm < M && gn < N) {
-              double *c = C + gm * crs + gn * ccs;
-              *c = beta == 0.0 ? alpha * acc[i][j][h] : fma(alpha, acc[i][j][h], beta * *c);
-            }
+            if (gm < M && gn < N) epi(gm, gn, acc[i][j][h]);
           }
     }
   }
   __syncthreads();
+}
+
+struct EpiAxpby {
+  double alpha, beta; double *C; int64_t crs, ccs;
+  __device__ __forceinline__ void operator()(int i, int j, double v) const {
+    double *c = C + i * crs + j * ccs;
+    *c = beta == 0.0 ? alpha * v : fma(alpha, v, beta * *c);
+  }
+};
+
+// C = alpha A B + beta C
+template <int NTH>
+__device__ void cta_dgemm(int M, int N, int K, double alpha, DMat A, DMat B, double beta, double *C, int64_t crs,
+                          int64_t ccs, double *smem) {
+  cta_dgemm_epi<NTH>(M, N, K, A, B, EpiAxpby{alpha, beta, C, crs, ccs}, smem);
 }
 
 }  // namespace bilu

@@ -218,3 +218,33 @@ def test_small_max_block_merges():
     g, st, gf, of = run_pair(ip, ix, dv, [2] * 200, 1e-3, True, max_block=16)
     assert_parity(gf, of)
     assert np.diff(gf.bstart).max() <= 16
+
+
+def test_c4_reduced_parity_wide_blocks():
+    """BASELINE configs[3] recipe at reduced size: dense blocks of 16-64 (the DMMA
+    Schur-update and scaling paths), random block pattern, tau = 1e-4."""
+    from inputs.configs import config4
+    P = config4(nblocks=80, per_row=4)
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert_parity(gf, of)
+    assert st["n_blocks_final"] == of.nblk
+
+
+def test_c4_reduced_gmres():
+    from inputs.configs import config4
+    P = config4(nblocks=60, per_row=3)
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert_parity(gf, of)
+    it_g, ok_g, it_o, ok_o = _gmres_counts(P, g, of)
+    assert ok_g and ok_o and abs(it_g - it_o) <= 1
+
+
+def test_c5_reduced_parity_and_gmres():
+    """BASELINE configs[4] recipe at reduced size (27-pt, lognormal kappa, Pe 50, ND)."""
+    from inputs.configs import config5
+    P = config5(N=20, top_levels=1)
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert_parity(gf, of)
+    assert st["n_merges"] == of.n_merges
+    it_g, ok_g, it_o, ok_o = _gmres_counts(P, g, of)
+    assert ok_g and ok_o and abs(it_g - it_o) <= 1

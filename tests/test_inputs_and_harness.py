@@ -93,3 +93,39 @@ def test_gmres_restarts():
     x, its, ok, hist = gmres(lambda v: A @ v, np.ones(n), restart=10, tol=1e-8, max_restarts=500)
     assert ok and its > 10
     assert np.linalg.norm(A @ x - 1.0) / np.sqrt(n) <= 1e-8 * 1.01
+
+
+def test_config4_recipe_small():
+    from inputs.configs import config4
+    P = config4(nblocks=50, per_row=5)
+    Q = config4(nblocks=50, per_row=5)
+    assert np.array_equal(P.data, Q.data) and np.array_equal(P.indices, Q.indices)
+    bs = P.block_sizes
+    assert bs.min() >= 16 and bs.max() <= 64 and bs.sum() == P.n
+    # every block row: the diagonal block + 5 distinct off-diagonal blocks, all dense
+    bst = np.concatenate([[0], np.cumsum(bs)])
+    r0 = np.diff(P.indptr)[bst[:-1]]
+    for i in range(50):
+        rows = np.arange(bst[i], bst[i + 1])
+        assert np.all(np.diff(P.indptr)[rows] == r0[i])
+    import scipy.sparse as sp
+    A = sp.csr_matrix((P.data, P.indices, P.indptr), shape=(P.n, P.n))
+    d = np.abs(A.diagonal()); off = np.abs(A).sum(axis=1).A1 - d
+    np.testing.assert_allclose(d / off, 1.5, rtol=1e-12)
+
+
+def test_config5_recipe_small():
+    from inputs.configs import config5
+    N = 12
+    P = config5(N=N, top_levels=1)
+    assert P.nnz == (3 * N - 2) ** 3          # 27-pt stencil incl. self
+    import scipy.sparse as sp
+    A = sp.csr_matrix((P.data, P.indices, P.indptr), shape=(P.n, P.n)).tocoo()
+    off = A.row != A.col
+    assert np.all(A.data[off] < 0)            # Z-matrix
+    d = sp.csr_matrix(A).diagonal()
+    s = np.bincount(A.row[off], weights=-A.data[off], minlength=P.n)
+    assert np.all(d >= s * (1 - 1e-14))       # diagonally dominant (strict on the boundary)
+    assert np.any(d > s * (1 + 1e-6))
+    assert sorted(P.perm.tolist()) == list(range(P.n))
+    assert set(np.unique(P.block_part)) == {-1, 0, 1}
