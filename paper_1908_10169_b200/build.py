@@ -23,11 +23,14 @@ def _newest_source() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
-    lib = LIB_PROF if profile else LIB
+def build(force: bool = False, verbose: bool = False, profile: bool = False, defines=(), out=None) -> str:
+    """Compile and link libbilu.so (or a variant: `defines` extra -D flags, `out` library path)."""
+    lib = out or (LIB_PROF if profile else LIB)
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= _newest_source():
         return lib
     objdir = os.path.join(HERE, "build_prof" if profile else "build")
+    if out:
+        objdir = os.path.join(HERE, "build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for f in CU_SOURCES:
@@ -38,6 +41,8 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
             cmd.insert(1, "-Xptxas=-v")
         if profile:
             cmd.insert(1, "-DBILU_PROFILE")
+        for d in defines:
+            cmd.insert(1, "-D" + d)
         subprocess.check_call(cmd)
         objs.append(o)
     for f in CPP_SOURCES:
@@ -52,4 +57,7 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv,
+                defines=defs, out=os.path.join(HERE, outs[0]) if outs else None))

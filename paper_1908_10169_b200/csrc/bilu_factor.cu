@@ -358,6 +358,84 @@ __device__ int load_contribs(const DevFactor &F, const ChunkList &L, int K, int 
   return nc;
 }
 
+// Both contributor lists of block K in one pass (records -> descriptors), each sorted
+// by J (R13) and prefix-summed over its items (warp 0: Lc, warp 1: Uc).
+// Lc(K): J has Ũ columns in K -> items = rows of L_J >= s_K
+// Uc(K): J has L rows in K    -> items = cols of Ũ_J >= e_K
+__device__ void load_contribs2(const DevFactor &F, int K, Contrib *CL, Contrib *CU, int nLc, int nUc, int *keys,
+                               Shared &S) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nt = nLc + nUc;
+  for (int x = tid; x < nt; x += NT) {
+    const int side = x < nLc ? 0 : 1;
+    const int xi = side ? x - nLc : x;
+    const ChunkList &L = side ? F.uc : F.lc;
+    const int *r = list_rec(L, K, xi);
+    const int J = __ldcg(r);
+    keys[x] = J;
+    Contrib c;
+    c.J = J;
+    const int sJ = F.bstart[J];
+    c.bJ = F.bstart[J + 1] - sJ;
+    const int64_t lro = __ldcg(&F.Lrow_off[J]), lvo = __ldcg(&F.Lval_off[J]);
+    const int64_t uco = __ldcg(&F.Ucol_off[J]), uvo = __ldcg(&F.Uval_off[J]);
+    if (side == 0) {
+      const int c0 = __ldcg(r + 1), c1 = __ldcg(r + 2), lrs = __ldcg(r + 3), lre = __ldcg(r + 4);
+      const int mJ = __ldcg(&F.Lm[J]);
+      c.n_items = mJ - lrs;
+      c.n_cand_skip = lre - lrs;
+      c.ncol = c1 - c0;
+      c.rows = lro + lrs;
+      c.lval = lvo + (int64_t)lrs * c.bJ;
+      c.cols = uco + c0;
+      c.uval = uvo + (int64_t)c0 * c.bJ;
+      CL[nLc + xi] = c;
+    } else {
+      const int r0 = __ldcg(r + 1), r1 = __ldcg(r + 2), cus = __ldcg(r + 3);
+      const int cJ = __ldcg(&F.Uc[J]);
+      c.n_items = cJ - cus;
+      c.n_cand_skip = 0;
+      c.ncol = r1 - r0;
+      c.rows = lro + r0;
+      c.lval = lvo + (int64_t)r0 * c.bJ;
+      c.cols = uco + cus;
+      c.uval = uvo + (int64_t)cus * c.bJ;
+      CU[nUc + xi] = c;
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < nt; x += NT) {       // ascending J within each list (J distinct)
+    const int side = x < nLc ? 0 : 1;
+    const int xi = side ? x - nLc : x, n = side ? nUc : nLc;
+    const int *kk = keys + (side ? nLc : 0);
+    const int k = kk[xi];
+    int rk = 0;
+    for (int y = 0; y < n; ++y) rk += kk[y] < k;
+    Contrib *C = side ? CU : CL;
+    C[rk] = C[n + xi];
+  }
+  __syncthreads();
+  if (wid < 2) {
+    Contrib *C = wid ? CU : CL;
+    const int n = wid ? nUc : nLc;
+    int carry = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const int v = i < n ? C[i].n_items : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < n) C[i].item_off = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) S.cnt[wid] = carry;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ int contrib_of(const Contrib *C, int nc, int t) {
   int lo = 0, hi = nc - 1;
   while (lo < hi) {
@@ -712,10 +790,10 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   const int nLc0 = __ldcg(&F.lc.cnt[K]), nUc0 = __ldcg(&F.uc.cnt[K]);
   Contrib *CL = (Contrib *)balloc(A, (int64_t)2 * nLc0 * sizeof(Contrib));
   Contrib *CU = (Contrib *)balloc(A, (int64_t)2 * nUc0 * sizeof(Contrib));
-  int *tkeys = (int *)balloc(A, (int64_t)(nLc0 > nUc0 ? nLc0 : nUc0) * 4);
+  int *tkeys = (int *)balloc(A, (int64_t)(nLc0 + nUc0 + 1) * 4);
   OVF_CHECK();
-  const int nLc = load_contribs(F, F.lc, K, 0, CL, nullptr, tkeys, S);
-  const int nUc = load_contribs(F, F.uc, K, 1, CU, nullptr, tkeys, S);
+  load_contribs2(F, K, CL, CU, nLc0, nUc0, tkeys, S);
+  const int nLc = nLc0, nUc = nUc0;
   const int TL = S.cnt[0], TU = S.cnt[1];
   const int64_t aL0 = F.AL_ptr[K], aLe = F.AL_ge[K], aL1 = F.AL_ptr[K + 1];
   const int64_t aU0 = F.AU_ptr[K], aU1 = F.AU_ptr[K + 1];
@@ -867,8 +945,22 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
   A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes;
   A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
   A.ovf = false; A.bottom_global = false;
-  finish_block(F, K, S, A, X.R[0].W, X.R[1].W, X.R[0].lineOf, X.R[1].lineOf, X.R[0].nU, X.R[1].nU, true, true,
-               X.flops);
+  // stage the finished buffers in shared memory when they fit in half of it
+  double *WL = X.R[0].W, *WU = X.R[1].W;
+  const int *rowOf = X.R[0].lineOf, *colOf = X.R[1].lineOf;
+  const int nR = X.R[0].nU, nC = X.R[1].nU;
+  const int64_t nwl = (int64_t)(b + nR) * b, nwu = (int64_t)nC * b;
+  if ((nwl + nwu) * 8 + (int64_t)(b + nR + nC + 2) * 4 + 64 <= F.smem_bytes - 24 * 1024) {
+    double *sWL = (double *)balloc(A, nwl * 8), *sWU = (double *)balloc(A, nwu * 8);
+    int *sR = (int *)balloc(A, (int64_t)(b + nR + 1) * 4), *sC = (int *)balloc(A, (int64_t)(nC + 1) * 4);
+    for (int64_t x = tid; x < nwl; x += NT) sWL[x] = __ldcg(WL + x);
+    for (int64_t x = tid; x < nwu; x += NT) sWU[x] = __ldcg(WU + x);
+    for (int x = tid; x < b + nR; x += NT) sR[x] = __ldcg(rowOf + x);
+    for (int x = tid; x < nC; x += NT) sC[x] = __ldcg(colOf + x);
+    __syncthreads();
+    WL = sWL; WU = sWU; rowOf = sR; colOf = sC;
+  }
+  finish_block(F, K, S, A, WL, WU, rowOf, colOf, nR, nC, true, true, X.flops);
 }
 
 // a-6 .. a-1 of block K once W_L (pivot block + candidate rows) and W_U are complete
@@ -1013,6 +1105,7 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   // ---------------- a-7/a-8: scale, drop (R1-R3), compact
   // L rows: l = w D_K, kept iff max|l| > tau; the scaled row overwrites W_L's row
   const double tau = F.tau;
+  SUBP_T0
   int *keepR = (int *)balloc(A, (int64_t)(nR + 1) * 4);
   int *keepC = (int *)balloc(A, (int64_t)(nC + 1) * 4);
   OVF_CHECK();
@@ -1033,16 +1126,33 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   for (int i = tid; i < nR; i += NT) {
     double *w = WL + (int64_t)(b + i) * b;
     double mx = 0.0;
-    if (b <= 16) {
+    if (b <= 8) {
+      double wr[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) wr[t] = t < b ? w[t] : 0.0;     // the row once, into registers
+      double l[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) if (t < b && c < b) acc = fma(wr[t], P[t + c * b], acc);
+        l[c] = acc;
+        mx = fmax(mx, fabs(acc));
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) if (c < b) w[c] = l[c];
+    } else if (b <= 16) {
+      double wr[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) wr[t] = t < b ? w[t] : 0.0;
       double l[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
-        if (c < b) {
-          double acc = 0.0;
-          for (int t = 0; t < b; ++t) acc = fma(w[t], P[t + c * b], acc);
-          l[c] = acc;
-          mx = fmax(mx, fabs(acc));
-        }
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) if (t < b && c < b) acc = fma(wr[t], P[t + c * b], acc);
+        l[c] = acc;
+        mx = fmax(mx, fabs(acc));
       }
 #pragma unroll
       for (int c = 0; c < 16; ++c) if (c < b) w[c] = l[c];
@@ -1071,10 +1181,26 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     if (b > 16) {
       const double *u = Usc + (int64_t)j * b;
       for (int rr = 0; rr < b; ++rr) mx = fmax(mx, fabs(u[rr]));
-    } else {
-      for (int rr = 0; rr < b; ++rr) {
+    } else if (b <= 8) {
+      double zr[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) zr[t] = t < b ? z[t] : 0.0;    // the column once, into registers
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) {
         double acc = 0.0;
-        for (int t = 0; t < b; ++t) acc = fma(P[rr + (int64_t)t * b], z[t], acc);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) if (t < b && rr < b) acc = fma(P[rr + t * b], zr[t], acc);
+        mx = fmax(mx, fabs(acc));
+      }
+    } else {
+      double zr[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) zr[t] = t < b ? z[t] : 0.0;
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) if (t < b && rr < b) acc = fma(P[rr + t * b], zr[t], acc);
         mx = fmax(mx, fabs(acc));
       }
     }
@@ -1093,8 +1219,10 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     }
   }
   __syncthreads();
+  SUBP(11);
   const int mK = cta_scan(keepR, nR, S.tmp);
   const int cK = cta_scan(keepC, nC, S.tmp);
+  SUBP(12);
   if (tid == 0) { keepR[nR] = mK; keepC[nC] = cK; }
   // kept rows / cols (buffer indices), then sorted by matrix index
   int *kr = (int *)balloc(A, (int64_t)(mK + 1) * 4);
@@ -1146,19 +1274,20 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     for (int x = tid; x < cK; x += NT) ordC[lbound(tmpk, 0, cK, kcol[x])] = x;
     __syncthreads();
   }
+  SUBP(13);
   for (int x = tid; x < mK; x += NT) R[x] = krow[ordR[x]];
   for (int x = tid; x < cK; x += NT) Cs[x] = kcol[ordC[x]];
-  if (tid == 0) {
-    // 128-byte aligned slices: no L1 line is ever shared by two blocks' panels
-    const unsigned long long mi = ((unsigned long long)mK + 31) & ~31ull;
-    const unsigned long long mv = ((unsigned long long)mK * b + 15) & ~15ull;
-    const unsigned long long ci = ((unsigned long long)cK + 31) & ~31ull;
-    const unsigned long long cv = ((unsigned long long)cK * b + 15) & ~15ull;
-    S.off[0] = atomicAdd(&F.ctrl[CS * CTRL_CUR_LIDX], mi);
-    S.off[1] = atomicAdd(&F.ctrl[CS * CTRL_CUR_LVAL], mv);
-    S.off[2] = atomicAdd(&F.ctrl[CS * CTRL_CUR_UIDX], ci);
-    S.off[3] = atomicAdd(&F.ctrl[CS * CTRL_CUR_UVAL], cv);
-    atomicAdd(&F.ctrl[CS * CTRL_NDEC], (unsigned long long)(nR + nC));
+  if (tid < 5) {
+    // 128-byte aligned slices: no L1 line is ever shared by two blocks' panels; the four
+    // arena cursors are bumped by four threads at once (one round trip)
+    const unsigned long long amt[5] = {((unsigned long long)mK + 31) & ~31ull,
+                                       ((unsigned long long)mK * b + 15) & ~15ull,
+                                       ((unsigned long long)cK + 31) & ~31ull,
+                                       ((unsigned long long)cK * b + 15) & ~15ull,
+                                       (unsigned long long)(nR + nC)};
+    const int which[5] = {CTRL_CUR_LIDX, CTRL_CUR_LVAL, CTRL_CUR_UIDX, CTRL_CUR_UVAL, CTRL_NDEC};
+    const unsigned long long o = atomicAdd(&F.ctrl[CS * which[tid]], amt[tid]);
+    if (tid < 4) S.off[tid] = o;
   }
   __syncthreads();
   if (S.off[0] + mK > (unsigned long long)F.cap_Lidx || S.off[1] + (unsigned long long)mK * b > (unsigned long long)F.cap_Lval ||
@@ -1166,6 +1295,7 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     if (tid == 0) raise_abort(F, DEV_OVF_ARENA, K);
     return;
   }
+  SUBP(14);
   const int64_t oLi = (int64_t)S.off[0], oLv = (int64_t)S.off[1], oUi = (int64_t)S.off[2], oUv = (int64_t)S.off[3];
   for (int x = tid; x < mK; x += NT) F.Lidx[oLi + x] = R[x];
   for (int it = tid; it < mK * b; it += NT) {
@@ -1184,45 +1314,64 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     F.blk_ncand[2 * K] = nR; F.blk_ncand[2 * K + 1] = nC;
   }
   __syncthreads();
+  SUBP(15);
   PROF(6);
 
   // ---------------- a-2 (producer side): register K with the blocks it feeds,
   // and the chain edges of the readiness rule.
-  int *rrun = keepR;  // reuse
-  int *crun = keepC;
-  for (int i = tid; i < mK; i += NT) rrun[i] = (i == 0 || F.block_of[R[i]] != F.block_of[R[i - 1]]) ? 1 : 0;
-  for (int j = tid; j < cK; j += NT) crun[j] = (j == 0 || F.block_of[Cs[j]] != F.block_of[Cs[j - 1]]) ? 1 : 0;
+  // block of every kept row / column (sorted, so runs are contiguous)
+  int *rb = (int *)balloc(A, (int64_t)(mK + cK + 1) * 4);
+  int *cb = rb + mK;
+  int *run = keepR;   // reuse: run-start flags of rows then columns, scanned together
+  if (nR + 1 < mK + cK + 1) run = (int *)balloc(A, (int64_t)(mK + cK + 1) * 4);
+  OVF_CHECK();
+  for (int i = tid; i < mK; i += NT) rb[i] = F.block_of[R[i]];
+  for (int j = tid; j < cK; j += NT) cb[j] = F.block_of[Cs[j]];
   __syncthreads();
-  const int nRr = cta_scan(rrun, mK, S.tmp);
-  const int nCr = cta_scan(crun, cK, S.tmp);
+  for (int i = tid; i < mK; i += NT) run[i] = (i == 0 || rb[i] != rb[i - 1]) ? 1 : 0;
+  for (int j = tid; j < cK; j += NT) run[mK + j] = (j == 0 || cb[j] != cb[j - 1]) ? 1 : 0;
+  __syncthreads();
+  const int nRun = cta_scan(run, mK + cK, S.tmp);
+  const int nRr = cK > 0 ? run[mK] : nRun, nCr = nRun - nRr;
   int *rstart = (int *)balloc(A, (int64_t)(nRr + 1) * 4);
   int *cstart = (int *)balloc(A, (int64_t)(nCr + 1) * 4);
-  int pN = 1; while (pN < nRr + nCr) pN <<= 1;
-  int *nb = (int *)balloc(A, (int64_t)pN * 4);
-  int *nbf = (int *)balloc(A, (int64_t)pN * 4);
+  int *rblk = (int *)balloc(A, (int64_t)(nRr + 1) * 4);
+  int *cblk = (int *)balloc(A, (int64_t)(nCr + 1) * 4);
+  int *pdr = (int *)balloc(A, (int64_t)(nRr + 1) * 4);
+  int *nb = (int *)balloc(A, (int64_t)(nRr + nCr + 1) * 4);
   OVF_CHECK();
   for (int i = tid; i < mK; i += NT)
-    if (i == 0 || F.block_of[R[i]] != F.block_of[R[i - 1]]) rstart[rrun[i]] = i;
+    if (i == 0 || rb[i] != rb[i - 1]) { rstart[run[i]] = i; rblk[run[i]] = rb[i]; }
   for (int j = tid; j < cK; j += NT)
-    if (j == 0 || F.block_of[Cs[j]] != F.block_of[Cs[j - 1]]) cstart[crun[j]] = j;
+    if (j == 0 || cb[j] != cb[j - 1]) { cstart[run[mK + j] - nRr] = j; cblk[run[mK + j] - nRr] = cb[j]; }
   if (tid == 0) { rstart[nRr] = mK; cstart[nCr] = cK; }
   __syncthreads();
   for (int x = tid; x < nRr; x += NT) {
     const int r0 = rstart[x], r1 = rstart[x + 1];
-    const int T = F.block_of[R[r0]];
+    const int T = rblk[x];
     int rec[REC_INTS] = {K, r0, r1, lbound(Cs, 0, cK, F.bstart[T + 1]), 0, 0, 0, 0};
     list_append(F, F.uc, T, rec);
-    nb[x] = T;
+    const int p = lbound(cblk, 0, nCr, T);
+    pdr[x] = (p < nCr && cblk[p] == T) ? 1 : 0;    // T is also a column block
   }
   for (int x = tid; x < nCr; x += NT) {
     const int c0 = cstart[x], c1 = cstart[x + 1];
-    const int T = F.block_of[Cs[c0]];
+    const int T = cblk[x];
     int rec[REC_INTS] = {K, c0, c1, lbound(R, 0, mK, F.bstart[T]), lbound(R, 0, mK, F.bstart[T + 1]), 0, 0, 0};
     list_append(F, F.lc, T, rec);
-    nb[nRr + x] = T;
   }
   __syncthreads();
-  const int nN = cta_sort_unique(nb, nRr + nCr, nbf, S.tmp);
+  // N(K) = row blocks ∪ column blocks, both sorted: rank of v in the union =
+  // #(rblk < v) + #(cblk < v) - #(common values < v)
+  const int ndup = cta_scan(pdr, nRr, S.tmp);
+  const int nN = nRr + nCr - ndup;
+  for (int x = tid; x < nRr; x += NT) nb[x + lbound(cblk, 0, nCr, rblk[x]) - pdr[x]] = rblk[x];
+  for (int y = tid; y < nCr; y += NT) {
+    const int v = cblk[y], L = lbound(rblk, 0, nRr, v);
+    if (L < nRr && rblk[L] == v) continue;
+    nb[L + y - (L < nRr ? pdr[L] : ndup)] = v;
+  }
+  __syncthreads();
   // chain edges n_i -> n_{i+1}: n_{i+1} additionally waits for n_i
   for (int x = tid; x + 1 < nN; x += NT) {
     atomicAdd(&F.pending[nb[x + 1]], 1);

@@ -439,8 +439,9 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   if (const char *sk = getenv("BILU_SMEM_KB")) F.smem_bytes = std::max(16, std::min(220, atoi(sk))) * 1024;
   int per_sm = 0;
   if (bilu_factor_occupancy(F.smem_bytes, &per_sm) != cudaSuccess || per_sm < 1) per_sm = 1;
+  const int occ = per_sm;
   per_sm = 1;   // one CTA per SM: the rest of the unified L1/shared array caches panels
-  if (const char *cp = getenv("BILU_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(cp)));
+  if (const char *cp = getenv("BILU_CTAS_PER_SM")) per_sm = std::max(1, std::min(occ, atoi(cp)));
   h->grid = opt.n_ctas > 0 ? opt.n_ctas : h->sms * per_sm;
 
   // initial capacities (grown on overflow)
