@@ -255,6 +255,9 @@ struct Shared {
   double pivd;
   int cnt[4];
   unsigned long long off[4];
+  double sflops[2];      // Schur-update flops of each side
+  int maxbJ[2];          // widest contributor of each side
+  int maxkey[2];         // largest candidate key contributed to each side
 };
 
 // per-contributor descriptor kept in shared memory while block K is processed
@@ -268,6 +271,7 @@ struct Contrib {
   int64_t lval;       // matching Lval offset
   int64_t cols;       // L side: Uidx offset of column c0;  U side: of the first col >= e_K
   int64_t uval;       // matching Uval offset
+  int last;           // largest candidate key of this contributor (-1: none)
 };
 
 // ---- open-addressing hash set of row (or column) indices -> dense buffer slot
@@ -389,6 +393,7 @@ __device__ void load_contribs2(const DevFactor &F, int K, Contrib *CL, Contrib *
       c.lval = lvo + (int64_t)lrs * c.bJ;
       c.cols = uco + c0;
       c.uval = uvo + (int64_t)c0 * c.bJ;
+      c.last = c.n_items > c.n_cand_skip ? __ldcg(&F.Lidx[c.rows + c.n_items - 1]) : -1;
       CL[nLc + xi] = c;
     } else {
       const int r0 = __ldcg(r + 1), r1 = __ldcg(r + 2), cus = __ldcg(r + 3);
@@ -400,6 +405,7 @@ __device__ void load_contribs2(const DevFactor &F, int K, Contrib *CL, Contrib *
       c.lval = lvo + (int64_t)r0 * c.bJ;
       c.cols = uco + cus;
       c.uval = uvo + (int64_t)cus * c.bJ;
+      c.last = c.n_items > 0 ? __ldcg(&F.Uidx[c.cols + c.n_items - 1]) : -1;
       CU[nUc + xi] = c;
     }
   }
@@ -418,10 +424,16 @@ __device__ void load_contribs2(const DevFactor &F, int K, Contrib *CL, Contrib *
   if (wid < 2) {
     Contrib *C = wid ? CU : CL;
     const int n = wid ? nUc : nLc;
-    int carry = 0;
+    int carry = 0, mb = 0, mk = -1;
+    double fl = 0.0;
     for (int base = 0; base < n; base += 32) {
       const int i = base + lane;
       const int v = i < n ? C[i].n_items : 0;
+      if (i < n) {
+        fl += 2.0 * C[i].bJ * (double)C[i].n_items * (double)C[i].ncol;
+        mb = max(mb, C[i].bJ);
+        mk = max(mk, C[i].last);
+      }
       int x = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -431,7 +443,13 @@ __device__ void load_contribs2(const DevFactor &F, int K, Contrib *CL, Contrib *
       if (i < n) C[i].item_off = carry + x - v;
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
-    if (lane == 0) S.cnt[wid] = carry;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      fl += __shfl_xor_sync(0xffffffffu, fl, o);
+      mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+      mk = max(mk, __shfl_xor_sync(0xffffffffu, mk, o));
+    }
+    if (lane == 0) { S.cnt[wid] = carry; S.sflops[wid] = fl; S.maxbJ[wid] = mb; S.maxkey[wid] = mk; }
   }
   __syncthreads();
 }
@@ -526,18 +544,9 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
   const int32_t *cidx = SIDE == 0 ? F.Lidx : F.Uidx;     // index list of the item side
   const int nA = (int)(a1 - ae);                           // Ã entries that are candidates
   SUBP_T0
-  // -- range of candidate keys: max over Ã's keys and every contributor's last key
-  if (tid == 0) S.cnt[2] = e - 1;
-  __syncthreads();
-  {
-    int mx = e - 1;
-    for (int64_t p = ae + tid; p < a1; p += NT) mx = max(mx, arc[p] >> 7);
-    for (int a = tid; a < nc; a += NT)
-      if (C[a].n_items > C[a].n_cand_skip) mx = max(mx, cidx[(SIDE == 0 ? C[a].rows : C[a].cols) + C[a].n_items - 1]);
-    atomicMax(&S.cnt[2], mx);
-  }
-  __syncthreads();
-  const int hi = S.cnt[2];
+  // -- range of candidate keys: Ã's block column / row is sorted by key, so its last entry
+  //    is its largest key; the contributors' largest keys come from load_contribs2
+  const int hi = max(max(e - 1, S.maxkey[SIDE]), a1 > ae ? (arc[a1 - 1] >> 7) : e - 1);
   const int words = (hi - e + 1 + 31) >> 5;
   const int base = SIDE == 0 ? b : 0;            // buffer line of the first candidate
   LineMap M;
@@ -769,7 +778,6 @@ __device__ double side_flops(const Contrib *C, int nc) {
 // native global fp64 reductions (a-5) on any idle CTA; the CTA that completes the last
 // part runs a-6..a-1 (finish_block).  Same values as the one-CTA path up to the
 // summation order (R13).
-constexpr int ITEMS_PER_PART = 1024;
 constexpr int MAX_PARTS = 32;          // per block (both sides)
 
 __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
@@ -797,16 +805,15 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   const int TL = S.cnt[0], TU = S.cnt[1];
   const int64_t aL0 = F.AL_ptr[K], aLe = F.AL_ge[K], aL1 = F.AL_ptr[K + 1];
   const int64_t aU0 = F.AU_ptr[K], aU1 = F.AU_ptr[K + 1];
-  const double flops = side_flops(CL, nLc) + side_flops(CU, nUc);
+  const double flops = S.sflops[0] + S.sflops[1];
+  const int maxbJ = max(S.maxbJ[0], S.maxbJ[1]);
   PROF(1);
 
   // ---------------- split decision: heavy blocks take their buffers from the global pool
   // split only when CTAs are idle (tickets taken but not yet filled)
   if (tid == 0) {
     const long long idle = (long long)ld_vol64(&F.ctrl[CS * CTRL_QTAIL]) - (long long)ld_vol64(&F.ctrl[CS * CTRL_QHEAD]);
-    int wide = b > 16;
-    for (int a = 0; a < nLc && !wide; ++a) wide = CL[a].bJ > 16;
-    for (int a = 0; a < nUc && !wide; ++a) wide = CU[a].bJ > 16;
+    const int wide = b > 16 || maxbJ > 16;
     S.cnt[3] = (!wide && F.heavy_T > 0 && TL + TU >= F.heavy_T && idle >= F.heavy_idle) ? 1 : 0;
   }
   __syncthreads();
@@ -847,8 +854,8 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     OVF_CHECK();
     for (int x = tid; x < nLc; x += NT) gCL[x] = CL[x];
     for (int x = tid; x < nUc; x += NT) gCU[x] = CU[x];
-    const int pL = min(MAX_PARTS / 2, (TL + ITEMS_PER_PART - 1) / ITEMS_PER_PART);
-    const int pU = min(MAX_PARTS / 2, (TU + ITEMS_PER_PART - 1) / ITEMS_PER_PART);
+    const int pL = min(MAX_PARTS / 2, (TL + F.part_items - 1) / F.part_items);
+    const int pU = min(MAX_PARTS / 2, (TU + F.part_items - 1) / F.part_items);
     __syncthreads();
     if (tid == 0) {
       const unsigned long long h = atomicAdd(&F.ctrl[CS * CTRL_HCTX], 1ull);
@@ -872,9 +879,6 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   }
 
   // ---------------- a-5, this CTA: every (contributor, item) pair
-  int maxbJ = 0;
-  for (int a = 0; a < nLc; ++a) maxbJ = max(maxbJ, CL[a].bJ);
-  for (int a = 0; a < nUc; ++a) maxbJ = max(maxbJ, CU[a].bJ);
   if (b > 16 || maxbJ > 16) {
     double *gs = (double *)balloc_top(A, (int64_t)DGEMM_SMEM_DOUBLES * 8);
     OVF_CHECK();
@@ -1347,18 +1351,9 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   if (tid == 0) { rstart[nRr] = mK; cstart[nCr] = cK; }
   __syncthreads();
   for (int x = tid; x < nRr; x += NT) {
-    const int r0 = rstart[x], r1 = rstart[x + 1];
     const int T = rblk[x];
-    int rec[REC_INTS] = {K, r0, r1, lbound(Cs, 0, cK, F.bstart[T + 1]), 0, 0, 0, 0};
-    list_append(F, F.uc, T, rec);
     const int p = lbound(cblk, 0, nCr, T);
     pdr[x] = (p < nCr && cblk[p] == T) ? 1 : 0;    // T is also a column block
-  }
-  for (int x = tid; x < nCr; x += NT) {
-    const int c0 = cstart[x], c1 = cstart[x + 1];
-    const int T = cblk[x];
-    int rec[REC_INTS] = {K, c0, c1, lbound(R, 0, mK, F.bstart[T]), lbound(R, 0, mK, F.bstart[T + 1]), 0, 0, 0};
-    list_append(F, F.lc, T, rec);
   }
   __syncthreads();
   // N(K) = row blocks ∪ column blocks, both sorted: rank of v in the union =
@@ -1372,11 +1367,24 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     nb[L + y - (L < nRr ? pdr[L] : ndup)] = v;
   }
   __syncthreads();
-  // chain edges n_i -> n_{i+1}: n_{i+1} additionally waits for n_i
-  for (int x = tid; x + 1 < nN; x += NT) {
-    atomicAdd(&F.pending[nb[x + 1]], 1);
-    int rec1 = nb[x + 1];
-    list_append(F, F.succ, nb[x], &rec1);
+  // one parallel pass: register K in Uc(T) / Lc(T) of every run, and the chain edges
+  // n_i -> n_{i+1} (n_{i+1} additionally waits for n_i)
+  for (int x = tid; x < nRr + nCr + max(nN - 1, 0); x += NT) {
+    if (x < nRr) {
+      const int r0 = rstart[x], r1 = rstart[x + 1], T = rblk[x];
+      int rec[REC_INTS] = {K, r0, r1, lbound(Cs, 0, cK, F.bstart[T + 1]), 0, 0, 0, 0};
+      list_append(F, F.uc, T, rec);
+    } else if (x < nRr + nCr) {
+      const int y = x - nRr;
+      const int c0 = cstart[y], c1 = cstart[y + 1], T = cblk[y];
+      int rec[REC_INTS] = {K, c0, c1, lbound(R, 0, mK, F.bstart[T]), lbound(R, 0, mK, F.bstart[T + 1]), 0, 0, 0};
+      list_append(F, F.lc, T, rec);
+    } else {
+      const int z = x - nRr - nCr;
+      atomicAdd(&F.pending[nb[z + 1]], 1);
+      int rec1 = nb[z + 1];
+      list_append(F, F.succ, nb[z], &rec1);
+    }
   }
   if (tid == 0) { F.blk_flops[K] = flops; atomicAdd((double *)&F.ctrl[CS * CTRL_FLOPS], flops); }
   __threadfence();

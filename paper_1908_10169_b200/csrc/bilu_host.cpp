@@ -414,9 +414,11 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     h->owned.push_back(hc);
     F.hctx = (HeavyCtx *)hc;
   }
-  F.heavy_T = 2048;
+  F.heavy_T = 1024;
   if (const char *ht = getenv("BILU_HEAVY_T")) F.heavy_T = atoi(ht);
   F.heavy_idle = 8;
+  F.part_items = 512;
+  if (const char *pi = getenv("BILU_PART_ITEMS")) F.part_items = std::max(64, atoi(pi));
   if (const char *hi = getenv("BILU_HEAVY_IDLE")) F.heavy_idle = atoi(hi);
   ALLOC(F.ctrl, CTRL_COUNT * CS);
   ALLOC(F.Lrow_off, n_blocks); ALLOC(F.Lm, n_blocks); ALLOC(F.Lval_off, n_blocks);

@@ -102,6 +102,7 @@ struct DevFactor {
   double *hpool; int64_t hpool_cap;     // doubles
   int heavy_T;                          // item count from which a block is split (0 = never)
   int heavy_idle;                       // ... if at least this many CTAs are idle
+  int part_items;                       // items per update-part task
   int smem_bytes;
   double tau, near_rel;
   int exp;                              // experiment switches (diagnostics only)
