@@ -559,7 +559,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
     // ---- bitmap path: dedup by atomicOr in shared memory, sorted for free
     bm = (unsigned *)balloc_top(A, (int64_t)(words + 1) * 4);
     pre = (int *)balloc_top(A, (int64_t)(words + 1) * 4);
-    if (A.ovf) { if (tid == 0) raise_abort(F, A.bottom_global ? DEV_OVF_HPOOL : DEV_OVF_WORK, K); return false; }
+    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
     for (int w = tid; w < words; w += NT) bm[w] = 0u;
     __syncthreads();
     for (int64_t p = ae + tid; p < a1; p += NT) {
@@ -591,13 +591,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
     __syncthreads();
     nU = cta_scan(pre, words, S.tmp);
     M.bm = bm; M.pre = pre;
-    if (A.bottom_global) {   // a split block: the helpers need the map in global memory
-      unsigned *gbm = (unsigned *)balloc(A, (int64_t)(words + 1) * 4);
-      int *gpre = (int *)balloc(A, (int64_t)(words + 1) * 4);
-      if (A.ovf) { if (tid == 0) raise_abort(F, A.bottom_global ? DEV_OVF_HPOOL : DEV_OVF_WORK, K); return false; }
-      for (int w = tid; w < words; w += NT) { gbm[w] = bm[w]; gpre[w] = pre[w]; }
-      R.gbm = gbm; R.gpre = gpre;
-    }
+
   } else {
     // ---- pos-map path: every occurrence writes its id, the surviving writer appends
     const int occ = nA + T;
@@ -620,7 +614,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
     if (tid == 0) S.cnt[2] = 0;
     __syncthreads();
     int *uniq = (int *)balloc_top(A, (int64_t)(occ + 1) * 4);
-    if (A.ovf) { if (tid == 0) raise_abort(F, A.bottom_global ? DEV_OVF_HPOOL : DEV_OVF_WORK, K); return false; }
+    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
     {
       int a = 0;
       for (int o = tid; o < occ; o += NT) {
@@ -645,9 +639,31 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
   }
   SUBP(8 * SIDE + 0);
   const int nW = base + nU;
-  double *W = (double *)balloc(A, (int64_t)nW * b * 8);
-  int *lineOf = (int *)balloc(A, (int64_t)(nW + 1) * 4);
-  if (A.ovf) { if (tid == 0) raise_abort(F, A.bottom_global ? DEV_OVF_HPOOL : DEV_OVF_WORK, K); return false; }
+  double *W;
+  int *lineOf;
+  if (A.bottom_global) {
+    // a split block: W, the line map and a copy of the bitmap map live in the global pool
+    // (read by the helpers), allocated exactly now that the candidate count is known
+    const int64_t wd = (int64_t)nW * b, ld = ((int64_t)nW + 2) / 2 + 1;
+    const int64_t md = M.bm ? (int64_t)words + 2 : 0;     // bitmap + prefix (2 x words ints)
+    if (tid == 0) S.off[3] = atomicAdd(&F.ctrl[CS * CTRL_HPOOL], (unsigned long long)(wd + ld + md));
+    __syncthreads();
+    const unsigned long long o = S.off[3];
+    __syncthreads();
+    if (o + wd + ld + md > (unsigned long long)F.hpool_cap) { if (tid == 0) raise_abort(F, DEV_OVF_HPOOL, K); return false; }
+    W = F.hpool + o;
+    lineOf = (int *)(W + wd);
+    if (M.bm) {
+      unsigned *gbm = (unsigned *)(W + wd + ld);
+      int *gpre = (int *)(gbm + words + 1);
+      for (int w = tid; w < words; w += NT) { gbm[w] = bm[w]; gpre[w] = pre[w]; }
+      R.gbm = gbm; R.gpre = gpre;
+    }
+  } else {
+    W = (double *)balloc(A, (int64_t)nW * b * 8);
+    lineOf = (int *)balloc(A, (int64_t)(nW + 1) * 4);
+    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return false; }
+  }
   for (int x = tid; x < base; x += NT) lineOf[x] = s + x;
   if (M.bm) {
     for (int w = tid; w < words; w += NT) {
@@ -818,24 +834,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   }
   __syncthreads();
   const bool heavy = S.cnt[3] != 0;
-  if (heavy) {
-    const int64_t nAL = aL1 - aLe, nAU = aU1;
-    const int64_t lines = (int64_t)b + nAL + TL + 1, cols = nAU - aU0 + TU + 1;
-    const int64_t wmax = min(8200, (F.n - e) / 32 + 4);   // bitmap words of one side
-    // upper bound of the pool chunk: W + line maps ((b+1) doubles per line), the scratch of
-    // the pos-map path (1/2 per line), bitmaps + prefix sums of both sides that do not fit
-    // in shared memory and their global copies (4 x (words + pad)), the contributor copies
-    const int64_t need = (lines + cols) * (b + 2) + 4 * (wmax + 8) + 64 +
-                         (int64_t)(nLc + nUc) * (int64_t)(sizeof(Contrib) / 8) + 64;
-    if (tid == 0) {
-      unsigned long long o = atomicAdd(&F.ctrl[CS * CTRL_HPOOL], (unsigned long long)need);
-      S.off[0] = o;
-    }
-    __syncthreads();
-    if (S.off[0] + need > (unsigned long long)F.hpool_cap) { if (tid == 0) raise_abort(F, DEV_OVF_HPOOL, K); return; }
-    A.gbase = F.hpool + S.off[0]; A.gused = 0; A.gcap = need; A.gtop = need;
-    A.bottom_global = true;   // W and line maps in the pool (read by the helpers); scratch stays in shared memory
-  }
+  if (heavy) A.bottom_global = true;   // W and line maps in the global pool (read by the helpers)
 
   // ---------------- a-3 / a-4 for both sides
   SideState RL, RU;
@@ -849,9 +848,12 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
 #ifdef BILU_PROFILE
     if (tid == 0 && g_blkprof) { g_blkprof[32 * (size_t)K + 19] = gtimer(); g_blkprof[32 * (size_t)K + 20] = ~0ull; }
 #endif
-    Contrib *gCL = (Contrib *)balloc(A, (int64_t)nLc * sizeof(Contrib));
-    Contrib *gCU = (Contrib *)balloc(A, (int64_t)nUc * sizeof(Contrib));
-    OVF_CHECK();
+    const int64_t cd = ((int64_t)(nLc + nUc) * (int64_t)sizeof(Contrib) + 7) / 8 + 2;
+    if (tid == 0) S.off[3] = atomicAdd(&F.ctrl[CS * CTRL_HPOOL], (unsigned long long)cd);
+    __syncthreads();
+    if (S.off[3] + cd > (unsigned long long)F.hpool_cap) { if (tid == 0) raise_abort(F, DEV_OVF_HPOOL, K); return; }
+    Contrib *gCL = (Contrib *)(F.hpool + S.off[3]);
+    Contrib *gCU = gCL + nLc;
     for (int x = tid; x < nLc; x += NT) gCL[x] = CL[x];
     for (int x = tid; x < nUc; x += NT) gCU[x] = CU[x];
     const int pL = min(MAX_PARTS / 2, (TL + F.part_items - 1) / F.part_items);

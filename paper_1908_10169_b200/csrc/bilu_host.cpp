@@ -450,7 +450,12 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   h->cap_val = opt.arena_hint > 0 ? opt.arena_hint : std::max<int64_t>(16 * nnz, (int64_t)n * max_b * 4);
   h->cap_idx = h->cap_val;
   h->work_per_cta = 256 * 1024;
-  h->hpool_cap = std::max<int64_t>(1 << 22, 8 * nnz);
+  {
+    // split-block pool: W buffers of the blocks processed as parallel tasks (grows on demand)
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    h->hpool_cap = std::min<int64_t>(std::max<int64_t>(1 << 22, 40 * nnz), (int64_t)(fr / 8 / 8));
+  }
   h->pool_lc = h->pool_uc = std::max(2 * n_blocks, 1024);
   h->pool_succ = std::max(2 * n_blocks, 1024);
 
