@@ -265,6 +265,27 @@ def random_dd(n, density=0.1, seed=0, dominance=1.5, sym_pattern=False):
     return A
 
 
+def wide_range_matrix(n=300_000, nfar=40, seed=7):
+    """Tridiagonal, plus `nfar` symmetric couplings between the first and the last 4000
+    unknowns, uniform(-1,1) entries, row-dominant diagonal: candidate key ranges wider
+    than 2^18 (the pos-map path of the factor kernel) at a cost the oracle finishes fast."""
+    rng = np.random.default_rng(seed)
+    i = np.arange(n)
+    a = rng.integers(0, 4000, nfar)
+    b = rng.integers(n - 4000, n, nfar)
+    r = np.concatenate([i, i[1:], i[:-1], a, b])
+    c = np.concatenate([i, i[:-1], i[1:], b, a])
+    key = np.unique(r.astype(np.int64) * n + c)
+    r, c = key // n, key % n
+    v = rng.uniform(-1, 1, len(r))
+    ip, ix, dv = _csr_from_coo(n, r, c, v)
+    rr = np.repeat(np.arange(n), np.diff(ip))
+    d = rr == ix
+    off = np.bincount(rr, weights=np.abs(dv) * (~d), minlength=n)
+    dv[d] = 1.5 * off[rr[d]] + 1.0
+    return ip, ix, dv
+
+
 def dense_to_csr(A):
     n = A.shape[0]
     rows, cols = np.nonzero(A)

@@ -829,8 +829,8 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   // split only when CTAs are idle (tickets taken but not yet filled)
   if (tid == 0) {
     const long long idle = (long long)ld_vol64(&F.ctrl[CS * CTRL_QTAIL]) - (long long)ld_vol64(&F.ctrl[CS * CTRL_QHEAD]);
-    const int wide = b > 16 || maxbJ > 16;
-    S.cnt[3] = (!wide && F.heavy_T > 0 && TL + TU >= F.heavy_T && idle >= F.heavy_idle) ? 1 : 0;
+    const int wide_ = b > 16 || maxbJ > 16;
+    S.cnt[3] = (!wide_ && F.heavy_T > 0 && TL + TU >= F.heavy_T && idle >= F.heavy_idle) ? 1 : 0;
   }
   __syncthreads();
   const bool heavy = S.cnt[3] != 0;
@@ -838,8 +838,25 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
 
   // ---------------- a-3 / a-4 for both sides
   SideState RL, RU;
+  const bool wide = b > 16 || maxbJ > 16;
+  double *gs = nullptr;
+  if (wide) {
+    gs = (double *)balloc_top(A, (int64_t)DGEMM_SMEM_DOUBLES * 8);
+    OVF_CHECK();
+  }
   if (!side_prepare<0>(F, K, s, e, b, CL, nLc, TL, aL0, aLe, aL1, A, S, RL)) return;
   PROF(2);
+  // the pos-map candidate path (key ranges wider than the shared bitmap) keeps its line map
+  // in a per-CTA global array that the other side's preparation reuses: apply this side's
+  // updates first
+  bool l_done = false;
+  if (!RL.sorted) {
+    if (wide) side_gemms<0>(F, s, e, b, CL, nLc, RL.M, RL.W, gs);
+    else if (heavy) side_items<0, true>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
+    else side_items<0, false>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
+    __syncthreads();
+    l_done = true;
+  }
   if (!side_prepare<1>(F, K, s, e, b, CU, nUc, TU, aU0, aU0, aU1, A, S, RU)) return;
   PROF(3);
 
@@ -881,16 +898,14 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   }
 
   // ---------------- a-5, this CTA: every (contributor, item) pair
-  if (b > 16 || maxbJ > 16) {
-    double *gs = (double *)balloc_top(A, (int64_t)DGEMM_SMEM_DOUBLES * 8);
-    OVF_CHECK();
-    side_gemms<0>(F, s, e, b, CL, nLc, RL.M, RL.W, gs);
+  if (wide) {
+    if (!l_done) side_gemms<0>(F, s, e, b, CL, nLc, RL.M, RL.W, gs);
     side_gemms<1>(F, s, e, b, CU, nUc, RU.M, RU.W, gs);
   } else if (heavy) {
-    side_items<0, true>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
+    if (!l_done) side_items<0, true>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
     side_items<1, true>(F, s, e, CU, nUc, 0, TU, b, RU.M, RU.W);
   } else {
-    side_items<0, false>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
+    if (!l_done) side_items<0, false>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
     side_items<1, false>(F, s, e, CU, nUc, 0, TU, b, RU.M, RU.W);
   }
   __syncthreads();

@@ -248,3 +248,37 @@ def test_c5_reduced_parity_and_gmres():
     assert st["n_merges"] == of.n_merges
     it_g, ok_g, it_o, ok_o = _gmres_counts(P, g, of)
     assert ok_g and ok_o and abs(it_g - it_o) <= 1
+
+
+@pytest.mark.parametrize("agg", [False, True])
+def test_edge_wide_key_range_posmap(agg):
+    """Candidate key ranges wider than 2^18 unknowns (the per-CTA pos-map path of a-3
+    instead of the shared-memory bitmap): n = 300,000 with couplings between the
+    first and the last 4000 unknowns."""
+    from inputs.configs import wide_range_matrix
+    ip, ix, dv = wide_range_matrix()
+    bs = np.full(300_000 // 8, 8)
+    g, st, gf, of = run_pair(ip, ix, dv, bs, 1e-3, agg)
+    assert_parity(gf, of)
+
+
+def test_c3_full_parity():
+    """BASELINE configs[2] at full size (48^3 nodes x 3 dof, n = 331,776, 25.8M nnz)."""
+    P = config3()
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert st["n_blocks_init"] == 110592
+    assert_parity(gf, of)
+    assert st["n_merges"] == of.n_merges
+
+
+def test_c5_full_parity_and_gmres():
+    """BASELINE configs[4] at full size (27-pt 128^3, n = 2,097,152, 55.7M nnz; the
+    oracle takes a few minutes single-threaded)."""
+    from inputs.configs import config5
+    P = config5()
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert P.nnz == 55742968
+    assert_parity(gf, of)
+    assert st["n_merges"] == of.n_merges
+    it_g, ok_g, it_o, ok_o = _gmres_counts(P, g, of)
+    assert ok_g and ok_o and abs(it_g - it_o) <= 1
