@@ -447,8 +447,19 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   h->grid = opt.n_ctas > 0 ? opt.n_ctas : h->sms * per_sm;
 
   // initial capacities (grown on overflow)
-  h->cap_val = opt.arena_hint > 0 ? opt.arena_hint : std::max<int64_t>(16 * nnz, (int64_t)n * max_b * 4);
-  h->cap_idx = h->cap_val;
+  {
+    // factor arenas (grow on overflow): values ~ max(4 nnz, 400 n) doubles each for L and Ũ
+    // (3D ND stencils keep ~300-400 values per row at tau = 1e-3, block-sparse inputs ~nnz/2),
+    // indices one per kept row / column, capped at half of the free device memory
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const double avg_b = (double)n / std::max<int32_t>(n_blocks, 1);
+    int64_t cv = opt.arena_hint > 0 ? opt.arena_hint : std::max<int64_t>(4 * nnz, 400 * (int64_t)n);
+    const int64_t budget = (int64_t)(0.5 * (double)fr / (16.0 + 8.0 / avg_b));
+    if (opt.arena_hint <= 0) cv = std::max<int64_t>(std::min(cv, budget), (int64_t)n * max_b);
+    h->cap_val = cv;
+    h->cap_idx = (int64_t)((double)cv / avg_b) + 2 * (int64_t)n + 1024;
+  }
   h->work_per_cta = 256 * 1024;
   {
     // split-block pool: W buffers of the blocks processed as parallel tasks (grows on demand)
