@@ -160,6 +160,49 @@ typedef struct {
 bilu_status bilu_export(bilu_ctx *h, bilu_factor_view *v);
 void bilu_factor_view_free(bilu_factor_view *v);
 
+/* ---- multi-GPU factorization over nested-dissection subtrees ----
+ * One context per rank (one process per GPU), every rank with the same global matrix,
+ * ordering and partition.  Sequence, on every rank:
+ *   bilu_dist_setup(ctx, owner, rank)          once, before the first factorization
+ *   bilu_factor_local(ctx, tau, &st)           phase A: this rank's subtree blocks
+ *   bilu_interface_pack(ctx, NULL, 0, &bytes)  size of this rank's packed interface panels
+ *   bilu_interface_pack(ctx, buf, bytes, &bytes)  ... packed into the caller's device buffer
+ *   -- the caller exchanges the packed buffers (all-gather of variable-size device
+ *      buffers, e.g. NCCL broadcasts from every rank) --
+ *   bilu_interface_unpack(ctx, buf_r, bytes_r) for every other rank r
+ *   bilu_factor_separators(ctx, &st)           phase B: the separator blocks (replicated)
+ * Inside an ND subtree every contributor of a block is a block of the same subtree, so
+ * phase A needs no communication; the separator blocks' Schur updates need the kept L rows
+ * and Ũ columns of the subtree blocks that lie in separator rows / columns ("interface"
+ * panels), which is what the ranks exchange.  Aggregation (Sec. 3.5)
+ * does not cross the ownership boundaries (R18).  The final factors are
+ * distributed: each rank holds its own subtree blocks and all separator blocks; bilu_export
+ * reports the other ranks' blocks as empty (L, Ũ with no rows / columns) and bilu_apply
+ * returns BILU_ERR_STATE.
+ *
+ * bilu_dist_setup -- owner: HOST int32[n_blocks]: rank owning each initial block (its ND
+ *   subtree), or -1 for separator blocks (factored by every rank).  Returns BILU_ERR_ARG if
+ *   blocks of different ranks are coupled in Ã or a subtree block follows a separator block
+ *   it is coupled to (not a nested-dissection partition), BILU_ERR_STATE after a
+ *   factorization.
+ * bilu_factor_local -- phase A (same arithmetic as bilu_factor on this rank's blocks).
+ * bilu_interface_pack -- dst: DEVICE buffer of `capacity` bytes owned by the caller (16-byte
+ *   aligned); *bytes receives the packed size.  With dst == NULL or capacity < the size it
+ *   only reports the size.  Format: int64 header {magic, count, bytes, rank}, `count` table
+ *   entries {J, b, m, c, byte offsets of the row list, L panel, column list, Ũ panel}, then
+ *   the payload.
+ * bilu_interface_unpack -- buf: DEVICE pointer (same device) to another rank's packed
+ *   buffer of `bytes` bytes, borrowed for the call.  BILU_ERR_ARG for a malformed buffer,
+ *   one of this rank, or blocks that are not remote subtree blocks.
+ * bilu_factor_separators -- phase B and the aggregation post-pass; st covers both phases
+ *   (flops, device time; the caller times the exchange).
+ */
+bilu_status bilu_dist_setup(bilu_ctx *h, const int32_t *owner, int32_t rank);
+bilu_status bilu_factor_local(bilu_ctx *h, double tau, bilu_factor_stats *st);
+bilu_status bilu_interface_pack(bilu_ctx *h, void *dst, int64_t capacity, int64_t *bytes);
+bilu_status bilu_interface_unpack(bilu_ctx *h, const void *buf, int64_t bytes);
+bilu_status bilu_factor_separators(bilu_ctx *h, bilu_factor_stats *st);
+
 /* Destroys the context and frees all device memory.  NULL-safe. */
 void bilu_destroy(bilu_ctx *h);
 

@@ -50,6 +50,9 @@ def grid_nd(nx, ny, nz, leaf=512, block=8, top_levels=0):
             part = counter[0]
             counter[0] += 1
         if cnt <= leaf or max(dims) < 3:
+            if top_levels > 0 and part < 0:      # a leaf above the top levels is a subtree of its own
+                part = counter[0]
+                counter[0] += 1
             nodes = _lex_nodes(x0, x1, y0, y1, z0, z1, nx, ny)
             perm_parts.append(nodes)
             bs = _cut(len(nodes), block)

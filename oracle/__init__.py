@@ -70,6 +70,12 @@ def _load():
             ctypes.c_int32, ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
             ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(_Factor),
         ]
+        lib.orc_bilu_factor_seg.restype = ctypes.c_int
+        lib.orc_bilu_factor_seg.argtypes = [
+            ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_int32, ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.POINTER(_Factor),
+        ]
         lib.orc_bilu_apply.restype = ctypes.c_int
         lib.orc_bilu_apply.argtypes = [ctypes.POINTER(_Factor), ctypes.c_void_p, ctypes.c_void_p]
         lib.orc_aggregate_test.restype = ctypes.c_int
@@ -135,8 +141,9 @@ def _np(ptr, count, dtype):
 
 
 def factor(indptr, indices, data, block_sizes, tau, aggregate=True, max_block=128,
-           overrides=None, near_rel=1e-8) -> OracleFactor:
-    """Run the oracle on an already-permuted CSR matrix (Ã)."""
+           overrides=None, near_rel=1e-8, seg=None) -> OracleFactor:
+    """Run the oracle on an already-permuted CSR matrix (Ã).  seg: optional aggregation
+    segment per initial block (merges only inside a segment, R18)."""
     lib = _load()
     indptr = np.ascontiguousarray(indptr, dtype=np.int64)
     indices = np.ascontiguousarray(indices, dtype=np.int32)
@@ -152,10 +159,19 @@ def factor(indptr, indices, data, block_sizes, tau, aggregate=True, max_block=12
         ov = ctypes.cast(arr, ctypes.c_void_p)
         nov = len(overrides)
     f = _Factor()
-    rc = lib.orc_bilu_factor(
-        n, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data,
-        len(bsz), bsz.ctypes.data, float(tau), int(bool(aggregate)), int(max_block),
-        ov, nov, float(near_rel), ctypes.byref(f))
+    if seg is None:
+        rc = lib.orc_bilu_factor(
+            n, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data,
+            len(bsz), bsz.ctypes.data, float(tau), int(bool(aggregate)), int(max_block),
+            ov, nov, float(near_rel), ctypes.byref(f))
+    else:
+        sg = np.ascontiguousarray(seg, dtype=np.int32)
+        if len(sg) != len(bsz):
+            raise OracleError("seg must have one entry per initial block")
+        rc = lib.orc_bilu_factor_seg(
+            n, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data,
+            len(bsz), bsz.ctypes.data, float(tau), int(bool(aggregate)), int(max_block),
+            ov, nov, float(near_rel), sg.ctypes.data, ctypes.byref(f))
     if rc != 0:
         bb = f.breakdown_block
         lib.orc_free(ctypes.byref(f))

@@ -179,11 +179,14 @@ static int decide(decider *d, int32_t blk, int32_t side, int32_t idx, double mx)
 }
 
 /* ---------------- the factorization ---------------- */
-int orc_bilu_factor(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
-                    const double *val, int32_t nblk, const int32_t *bsizes,
-                    double tau, int32_t aggregate, int32_t max_block,
-                    const orc_override *ovr, int64_t n_ovr, double near_rel,
-                    orc_factor *f) {
+/* seg (may be NULL): aggregation segment of every initial block; block K is merged into
+ * the aggregate ending at K-1 only if seg[K] == seg[K-1] (the distributed factorization
+ * keeps aggregation inside each rank's blocks, reading R18). */
+static int factor_impl(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                       const double *val, int32_t nblk, const int32_t *bsizes,
+                       double tau, int32_t aggregate, int32_t max_block,
+                       const orc_override *ovr, int64_t n_ovr, double near_rel,
+                       const int32_t *seg, orc_factor *f) {
   int32_t i, K;
   int64_t e64;
   memset(f, 0, sizeof(*f));
@@ -436,7 +439,7 @@ int orc_bilu_factor(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
     }
 
     /* -- progressive aggregation of the previous (aggregated) block and K (Sec. 3.5) -- */
-    if (aggregate && K > 0 && !B[K - 1].is_void) {
+    if (aggregate && K > 0 && !B[K - 1].is_void && (!seg || seg[K] == seg[K - 1])) {
       oblk *Pb = &B[K - 1];
       const int32_t pp = Pb->b, qq = b;
       /* rows of L_{k-1} inside block k (r) and below it (s); same for U */
@@ -653,4 +656,22 @@ void orc_free(orc_factor *f) {
   free(f->bstart); free(f->Lp); free(f->Li); free(f->Lvp); free(f->Lv);
   free(f->Up); free(f->Ui); free(f->Uvp); free(f->Uv); free(f->Dp); free(f->Dv);
   memset(f, 0, sizeof(*f));
+}
+
+int orc_bilu_factor(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                    const double *val, int32_t nblk, const int32_t *bsizes,
+                    double tau, int32_t aggregate, int32_t max_block,
+                    const orc_override *ovr, int64_t n_ovr, double near_rel,
+                    orc_factor *f) {
+  return factor_impl(n, row_ptr, col_idx, val, nblk, bsizes, tau, aggregate, max_block, ovr, n_ovr,
+                     near_rel, NULL, f);
+}
+
+int orc_bilu_factor_seg(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                        const double *val, int32_t nblk, const int32_t *bsizes,
+                        double tau, int32_t aggregate, int32_t max_block,
+                        const orc_override *ovr, int64_t n_ovr, double near_rel,
+                        const int32_t *seg, orc_factor *f) {
+  return factor_impl(n, row_ptr, col_idx, val, nblk, bsizes, tau, aggregate, max_block, ovr, n_ovr,
+                     near_rel, seg, f);
 }

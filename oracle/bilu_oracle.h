@@ -59,6 +59,14 @@ int orc_bilu_factor(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
                     const orc_override *ovr, int64_t n_ovr, double near_rel,
                     orc_factor *f);
 
+/* As orc_bilu_factor, with aggregation segments: seg[K] (initial block K) -- block K is
+ * merged into the aggregate ending at K-1 only if seg[K] == seg[K-1] (R18). */
+int orc_bilu_factor_seg(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                        const double *val, int32_t nblk, const int32_t *bsizes,
+                        double tau, int32_t aggregate, int32_t max_block,
+                        const orc_override *ovr, int64_t n_ovr, double near_rel,
+                        const int32_t *seg, orc_factor *f);
+
 /* y = (L P U)^{-1} x in the permuted ordering (forward/backward substitution
  * with D multiplies).  x, y host arrays of length n. */
 int orc_bilu_apply(const orc_factor *f, const double *x, double *y);

@@ -20,7 +20,9 @@ STATUS = {0: "BILU_OK", 1: "BILU_ERR_ARG", 2: "BILU_ERR_BREAKDOWN", 3: "BILU_ERR
 # every symbol include/bilu.h declares
 ABI_SYMBOLS = ["bilu_options_default", "bilu_analyze", "bilu_set_values", "bilu_factor",
                "bilu_apply", "bilu_export", "bilu_factor_view_free", "bilu_destroy",
-               "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm"]
+               "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm",
+               "bilu_dist_setup", "bilu_factor_local", "bilu_interface_pack", "bilu_interface_unpack",
+               "bilu_factor_separators"]
 
 
 class BiluError(RuntimeError):
@@ -106,6 +108,16 @@ def load_library():
     lib.bilu_diag_dgemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, D, P, I64, I64, P, I64, I64, D, P,
                                     I64, I64, ctypes.c_int, I64, I64, I64, P]
     lib.bilu_diag_dgemm.restype = ctypes.c_int
+    lib.bilu_dist_setup.argtypes = [P, P, ctypes.c_int32]
+    lib.bilu_dist_setup.restype = ctypes.c_int
+    lib.bilu_factor_local.argtypes = [P, ctypes.c_double, ctypes.POINTER(FactorStats)]
+    lib.bilu_factor_local.restype = ctypes.c_int
+    lib.bilu_interface_pack.argtypes = [P, P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+    lib.bilu_interface_pack.restype = ctypes.c_int
+    lib.bilu_interface_unpack.argtypes = [P, P, ctypes.c_int64]
+    lib.bilu_interface_unpack.restype = ctypes.c_int
+    lib.bilu_factor_separators.argtypes = [P, ctypes.POINTER(FactorStats)]
+    lib.bilu_factor_separators.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -196,6 +208,39 @@ class BILU:
     def factor(self, tau) -> dict:
         st = FactorStats()
         rc = self.lib.bilu_factor(self.h, float(tau), ctypes.byref(st))
+        self._check(rc, st.breakdown_block)
+        self.stats = st.as_dict()
+        return self.stats
+
+    # ---- multi-GPU phases (include/bilu.h "multi-GPU factorization")
+    def dist_setup(self, owner, rank: int):
+        ow = np.ascontiguousarray(owner, dtype=np.int32)
+        self._check(self.lib.bilu_dist_setup(self.h, ow.ctypes.data, int(rank)))
+
+    def factor_local(self, tau) -> dict:
+        st = FactorStats()
+        rc = self.lib.bilu_factor_local(self.h, float(tau), ctypes.byref(st))
+        self._check(rc, st.breakdown_block)
+        return st.as_dict()
+
+    def interface_pack(self, device=None):
+        """This rank's packed interface panels as a CUDA uint8 tensor (torch owns the memory)."""
+        import torch
+        nb = ctypes.c_int64()
+        self._check(self.lib.bilu_interface_pack(self.h, None, 0, ctypes.byref(nb)))
+        buf = torch.empty(max(int(nb.value), 16), dtype=torch.uint8,
+                          device=device if device is not None else "cuda:%d" % self.opt.device)
+        self._check(self.lib.bilu_interface_pack(self.h, ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                                 ctypes.byref(nb)))
+        return buf[:int(nb.value)]
+
+    def interface_unpack(self, buf):
+        """Append another rank's packed interface panels (CUDA uint8 tensor on this device)."""
+        self._check(self.lib.bilu_interface_unpack(self.h, ctypes.c_void_p(buf.data_ptr()), int(buf.numel())))
+
+    def factor_separators(self) -> dict:
+        st = FactorStats()
+        rc = self.lib.bilu_factor_separators(self.h, ctypes.byref(st))
         self._check(rc, st.breakdown_block)
         self.stats = st.as_dict()
         return self.stats

@@ -1413,7 +1413,7 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   const int nS = __ldcg(&F.succ.cnt[K]);
   for (int x = tid; x < (a1 - a0) + nS; x += NT) {
     int T = x < (a1 - a0) ? F.adj[a0 + x] : __ldcg(list_rec(F.succ, K, x - (a1 - a0)));
-    if (atomicSub(&F.pending[T], 1) == 1) {
+    if (atomicSub(&F.pending[T], 1) == 1 && (F.owned == nullptr || F.owned[T])) {
       unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
       __threadfence();
       st_vol(&F.queue[slot], T);
@@ -1445,7 +1445,7 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
           K = ld_vol(&F.queue[idx]);
           if (K >= 0) break;
           if ((++polls & 15u) == 0 &&
-              (aborted(F) || ld_vol64(&F.ctrl[CS * CTRL_DONE]) >= (unsigned long long)F.N)) { K = -1; break; }
+              (aborted(F) || ld_vol64(&F.ctrl[CS * CTRL_DONE]) >= (unsigned long long)F.n_target)) { K = -1; break; }
           __nanosleep(ns);
           if (ns < 256) ns <<= 1;
         }
@@ -1467,6 +1467,170 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
     else run_part(F, K, S, smem);
     __syncthreads();
   }
+}
+
+// ------------------------------------------------------------ distributed phases
+// Multi-GPU factorization over the subtrees of a nested-dissection ordering (SURVEY.md
+// 8(e)): phase A factors each rank's own subtree blocks (no communication: inside an ND
+// subtree every contributor is a block of the same subtree); the ranks then exchange the
+// panels of their "interface" blocks -- subtree blocks with kept L rows or Ũ columns in
+// separator blocks, i.e. the operands of the separator Schur updates -- and phase B
+// factors the separator blocks (replicated on every rank).  Before phase B the separator
+// blocks' contributor lists, successor lists and pending counts are rebuilt from the
+// interface blocks of all ranks (register_kernel) and the static separator adjacency.
+
+// separator targets: empty contributor / successor lists, pending = static separator count
+__global__ void sep_reset_kernel(DevFactor F, const int32_t *sep_list, int nsep, const int32_t *static_sep) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nsep; x += gridDim.x * blockDim.x) {
+    const int K = sep_list[x];
+    F.lc.cnt[K] = 0; F.uc.cnt[K] = 0; F.succ.cnt[K] = 0;
+    for (int d = 0; d < DIR_SLOTS; ++d) {
+      F.lc.dir[(size_t)K * DIR_SLOTS + d] = -1;
+      F.uc.dir[(size_t)K * DIR_SLOTS + d] = -1;
+      F.succ.dir[(size_t)K * DIR_SLOTS + d] = -1;
+    }
+    F.pending[K] = static_sep[x];
+  }
+}
+
+// register interface block J with the separator blocks it feeds (records of Lc/Uc, the
+// same as finish_block's a-2) and the chain edges between consecutive separator blocks
+// of N(J) (the readiness rule; the subtree blocks of N(J) are finished)
+constexpr int REG_CAP = 4096;
+__global__ void __launch_bounds__(NT) register_kernel(DevFactor F, const int32_t *blocks, int nb, const uint8_t *sep) {
+  __shared__ int nbk[REG_CAP];
+  __shared__ int flags[REG_CAP];
+  __shared__ Shared S;
+  const int tid = threadIdx.x;
+  for (int x = blockIdx.x; x < nb; x += gridDim.x) {
+    const int J = blocks[x];
+    const int32_t *R = F.Lidx + F.Lrow_off[J];
+    const int mK = F.Lm[J];
+    const int32_t *Cs = F.Uidx + F.Ucol_off[J];
+    const int cK = F.Uc[J];
+    if (tid == 0) S.cnt[0] = 0;
+    __syncthreads();
+    for (int p = tid; p < mK; p += NT) {
+      const int T = F.block_of[R[p]];
+      if (!sep[T] || (p > 0 && F.block_of[R[p - 1]] == T)) continue;
+      int r1 = p + 1;
+      while (r1 < mK && F.block_of[R[r1]] == T) ++r1;
+      int rec[REC_INTS] = {J, p, r1, lbound(Cs, 0, cK, F.bstart[T + 1]), 0, 0, 0, 0};
+      list_append(F, F.uc, T, rec);
+      const int slot = atomicAdd(&S.cnt[0], 1);
+      if (slot < REG_CAP) nbk[slot] = T;
+    }
+    for (int p = tid; p < cK; p += NT) {
+      const int T = F.block_of[Cs[p]];
+      if (!sep[T] || (p > 0 && F.block_of[Cs[p - 1]] == T)) continue;
+      int c1 = p + 1;
+      while (c1 < cK && F.block_of[Cs[c1]] == T) ++c1;
+      int rec[REC_INTS] = {J, p, c1, lbound(R, 0, mK, F.bstart[T]), lbound(R, 0, mK, F.bstart[T + 1]), 0, 0, 0};
+      list_append(F, F.lc, T, rec);
+      const int slot = atomicAdd(&S.cnt[0], 1);
+      if (slot < REG_CAP) nbk[slot] = T;
+    }
+    __syncthreads();
+    const int cnt = S.cnt[0];
+    if (cnt > REG_CAP) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, J); return; }
+    const int nN = cta_sort_unique(nbk, cnt, flags, S.tmp);
+    for (int z = tid; z + 1 < nN; z += NT) {
+      atomicAdd(&F.pending[nbk[z + 1]], 1);
+      int rec1 = nbk[z + 1];
+      list_append(F, F.succ, nbk[z], &rec1);
+    }
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+__global__ void sep_ready_kernel(DevFactor F, const int32_t *sep_list, int nsep) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nsep; x += gridDim.x * blockDim.x) {
+    const int K = sep_list[x];
+    if (F.pending[K] == 0) {
+      const unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
+      F.queue[slot] = K;
+    }
+  }
+}
+
+// own block J is an interface block iff its last kept row or column lies in a separator
+// (rows / columns are sorted and the separators follow the subtree in the ND order)
+__global__ void interface_flag_kernel(DevFactor F, const int32_t *own_list, int nown, const uint8_t *sep,
+                                      uint8_t *flag) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nown; x += gridDim.x * blockDim.x) {
+    const int J = own_list[x];
+    const int m = F.Lm[J], c = F.Uc[J];
+    bool f = false;
+    if (m > 0) f = f || sep[F.block_of[F.Lidx[F.Lrow_off[J] + m - 1]]];
+    if (c > 0) f = f || sep[F.block_of[F.Uidx[F.Ucol_off[J] + c - 1]]];
+    flag[x] = f ? 1 : 0;
+  }
+}
+
+__global__ void pack_kernel(DevFactor F, const PackEntry *tab, int count, unsigned char *buf) {
+  for (int x = blockIdx.x; x < count; x += gridDim.x) {
+    const PackEntry e = tab[x];
+    const int J = (int)e.J;
+    int32_t *li = (int32_t *)(buf + e.offLi);
+    int32_t *ui = (int32_t *)(buf + e.offUi);
+    double *lv = (double *)(buf + e.offLv);
+    double *uv = (double *)(buf + e.offUv);
+    const int64_t lro = F.Lrow_off[J], lvo = F.Lval_off[J], uco = F.Ucol_off[J], uvo = F.Uval_off[J];
+    for (int64_t i = threadIdx.x; i < e.Lm; i += blockDim.x) li[i] = F.Lidx[lro + i];
+    for (int64_t i = threadIdx.x; i < e.Uc; i += blockDim.x) ui[i] = F.Uidx[uco + i];
+    for (int64_t i = threadIdx.x; i < e.Lm * e.b; i += blockDim.x) lv[i] = F.Lval[lvo + i];
+    for (int64_t i = threadIdx.x; i < e.Uc * e.b; i += blockDim.x) uv[i] = F.Uval[uvo + i];
+  }
+}
+
+// remote interface blocks into this rank's arenas at base[4 x] = (Li, Lv, Ui, Uv) offsets
+__global__ void unpack_kernel(DevFactor F, const unsigned char *buf, const PackEntry *tab, int count,
+                              const int64_t *base) {
+  for (int x = blockIdx.x; x < count; x += gridDim.x) {
+    const PackEntry e = tab[x];
+    const int J = (int)e.J;
+    const int32_t *li = (const int32_t *)(buf + e.offLi);
+    const int32_t *ui = (const int32_t *)(buf + e.offUi);
+    const double *lv = (const double *)(buf + e.offLv);
+    const double *uv = (const double *)(buf + e.offUv);
+    const int64_t bLi = base[4 * x], bLv = base[4 * x + 1], bUi = base[4 * x + 2], bUv = base[4 * x + 3];
+    for (int64_t i = threadIdx.x; i < e.Lm; i += blockDim.x) F.Lidx[bLi + i] = li[i];
+    for (int64_t i = threadIdx.x; i < e.Uc; i += blockDim.x) F.Uidx[bUi + i] = ui[i];
+    for (int64_t i = threadIdx.x; i < e.Lm * e.b; i += blockDim.x) F.Lval[bLv + i] = lv[i];
+    for (int64_t i = threadIdx.x; i < e.Uc * e.b; i += blockDim.x) F.Uval[bUv + i] = uv[i];
+    if (threadIdx.x == 0) {
+      F.Lrow_off[J] = bLi; F.Lm[J] = (int32_t)e.Lm; F.Lval_off[J] = bLv;
+      F.Ucol_off[J] = bUi; F.Uc[J] = (int32_t)e.Uc; F.Uval_off[J] = bUv;
+    }
+  }
+}
+
+extern "C" cudaError_t bilu_launch_sep_prepare(const DevFactor &F, const int32_t *sep_list, int nsep,
+                                               const int32_t *static_sep, const int32_t *ifc, int nifc,
+                                               const uint8_t *sep, cudaStream_t st) {
+  if (nsep > 0) sep_reset_kernel<<<(nsep + 255) / 256, 256, 0, st>>>(F, sep_list, nsep, static_sep);
+  if (nifc > 0) register_kernel<<<nifc < 1184 ? nifc : 1184, NT, 0, st>>>(F, ifc, nifc, sep);
+  if (nsep > 0) sep_ready_kernel<<<(nsep + 255) / 256, 256, 0, st>>>(F, sep_list, nsep);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t bilu_launch_interface_flags(const DevFactor &F, const int32_t *own_list, int nown,
+                                                   const uint8_t *sep, uint8_t *flag, cudaStream_t st) {
+  if (nown > 0) interface_flag_kernel<<<(nown + 255) / 256, 256, 0, st>>>(F, own_list, nown, sep, flag);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t bilu_launch_pack(const DevFactor &F, const PackEntry *tab, int count, unsigned char *buf,
+                                        cudaStream_t st) {
+  if (count > 0) pack_kernel<<<count < 2048 ? count : 2048, 256, 0, st>>>(F, tab, count, buf);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t bilu_launch_unpack(const DevFactor &F, const unsigned char *buf, const PackEntry *tab,
+                                          int count, const int64_t *base, cudaStream_t st) {
+  if (count > 0) unpack_kernel<<<count < 2048 ? count : 2048, 256, 0, st>>>(F, buf, tab, count, base);
+  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------- launchers

@@ -36,6 +36,15 @@ extern "C" cudaError_t bilu_launch_permute(double *y, const double *x, const int
 extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_t st);
 extern "C" int bilu_merge_plan_launches();
 extern "C" int bilu_heavyctx_size();
+extern "C" cudaError_t bilu_launch_sep_prepare(const DevFactor &F, const int32_t *sep_list, int nsep,
+                                               const int32_t *static_sep, const int32_t *ifc, int nifc,
+                                               const uint8_t *sep, cudaStream_t st);
+extern "C" cudaError_t bilu_launch_interface_flags(const DevFactor &F, const int32_t *own_list, int nown,
+                                                   const uint8_t *sep, uint8_t *flag, cudaStream_t st);
+extern "C" cudaError_t bilu_launch_pack(const DevFactor &F, const PackEntry *tab, int count, unsigned char *buf,
+                                        cudaStream_t st);
+extern "C" cudaError_t bilu_launch_unpack(const DevFactor &F, const unsigned char *buf, const PackEntry *tab,
+                                          int count, const int64_t *base, cudaStream_t st);
 extern "C" int bilu_max_parts();
 extern "C" int bilu_merge_nchunks(int N);
 extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
@@ -76,6 +85,21 @@ struct bilu_ctx {
   int max_b = 0;
   // host copies
   std::vector<int32_t> bstart, ready0;
+  std::vector<int32_t> adj_ptr_h, adj_h, pending0_h;   // block graph (successors > K), static counts
+  // distributed factorization (bilu_dist_setup)
+  bool dist = false, dist_local_done = false;
+  int32_t rank = 0;
+  std::vector<int32_t> owner, seg, own_list, sep_list, static_sep, own_ifc, remote_ifc;
+  int32_t *d_own_list = nullptr, *d_sep_list = nullptr, *d_static_sep = nullptr, *d_seg = nullptr;
+  int32_t *d_ifc = nullptr; int64_t ifc_cap = 0;
+  uint8_t *d_own_mask = nullptr, *d_sep_mask = nullptr, *d_flag = nullptr;
+  std::vector<PackEntry> pack_tab; int64_t pack_bytes = 0; bool pack_valid = false;
+  int64_t *d_base = nullptr; int64_t base_cap = 0;
+  unsigned long long cur[4] = {0, 0, 0, 0};      // arena cursors after phase A + unpacks
+  unsigned long long qhead0 = 0, ctrl_init[CTRL_COUNT * CS];
+  int32_t *d_own_ready = nullptr; int32_t n_own_ready = 0;
+  double flops_local = 0.0, t_local_ms = 0.0;
+  int64_t ndec_local = 0, nnear_local = 0;
   std::vector<int64_t> D_off;
   std::vector<int64_t> map_csr;            // Ã entry -> original CSR entry
   std::vector<int32_t> perm;
@@ -360,6 +384,7 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   for (int32_t K = 0; K < n_blocks; ++K) adj_ptr[K + 1] += adj_ptr[K];
   for (size_t x = 0; x < edges.size(); ++x) adj[x] = (int32_t)(uint32_t)edges[x];  // sorted by (a, b)
   for (int32_t K = 0; K < n_blocks; ++K) if (pending0[K] == 0) h->ready0.push_back(K);
+  h->adj_ptr_h = adj_ptr; h->adj_h = adj; h->pending0_h = pending0;
   h->nready0 = (int32_t)h->ready0.size();
   h->nready0_ull = (unsigned long long)h->nready0;
   h->D_off.assign(n_blocks + 1, 0);
@@ -492,6 +517,7 @@ extern "C" bilu_status bilu_set_values(bilu_ctx *h, const double *val, int32_t o
 }
 
 // ------------------------------------------------------------ capacities
+static bilu_status ensure_aux(bilu_ctx *h);
 static bilu_status ensure_capacity(bilu_ctx *h) {
   DevFactor &F = h->F;
   if (F.cap_Lval != h->cap_val) {
@@ -506,6 +532,12 @@ static bilu_status ensure_capacity(bilu_ctx *h) {
     CUDA_TRY(h, dalloc(h, &F.Uidx, h->cap_idx));
     F.cap_Lidx = F.cap_Uidx = h->cap_idx;
   }
+  return ensure_aux(h);
+}
+
+// workspaces that hold no factor data (safe to reallocate between phases)
+static bilu_status ensure_aux(bilu_ctx *h) {
+  DevFactor &F = h->F;
   if (!F.posmap) CUDA_TRY(h, dalloc(h, &F.posmap, (size_t)h->grid * h->n));
   if (F.hpool_cap != h->hpool_cap) {
     dfree(h, F.hpool);
@@ -535,16 +567,17 @@ static bilu_status ensure_capacity(bilu_ctx *h) {
   return BILU_OK;
 }
 
-static bilu_status reset_schedule(bilu_ctx *h) {
+static bilu_status reset_schedule(bilu_ctx *h, const int32_t *d_ready, int32_t nready) {
   DevFactor &F = h->F;
   cudaStream_t st = h->stream;
   const size_t N = h->N;
+  h->qhead0 = (unsigned long long)nready;
   CUDA_TRY(h, cudaMemcpyAsync(F.pending, h->d_pending0, N * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(F.queue, 0xFF, F.qcap * sizeof(int32_t), st));
-  if (h->nready0)
-    CUDA_TRY(h, cudaMemcpyAsync(F.queue, h->d_ready0, h->nready0 * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  if (nready)
+    CUDA_TRY(h, cudaMemcpyAsync(F.queue, d_ready, nready * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(F.ctrl, 0, CTRL_COUNT * CS * sizeof(unsigned long long), st));
-  CUDA_TRY(h, cudaMemcpyAsync(F.ctrl + CS * CTRL_QHEAD, &h->nready0_ull, sizeof(unsigned long long),
+  CUDA_TRY(h, cudaMemcpyAsync(F.ctrl + CS * CTRL_QHEAD, &h->qhead0, sizeof(unsigned long long),
                               cudaMemcpyHostToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(F.lc.cnt, 0, N * sizeof(int), st));
   CUDA_TRY(h, cudaMemsetAsync(F.uc.cnt, 0, N * sizeof(int), st));
@@ -611,7 +644,9 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
           int W = 0;
           if (k > 0) {
             const int sk = bs[k], q = bs[k + 1] - sk;
-            while (k - 1 - W >= 0 && (sk - bs[k - 1 - W]) + q <= h->opt.max_block && W < 127) ++W;
+            while (k - 1 - W >= 0 && (sk - bs[k - 1 - W]) + q <= h->opt.max_block && W < 127 &&
+                   (h->seg.empty() || h->seg[k - 1 - W] == h->seg[k]))
+              ++W;
           }
           wofs[k] = acc;
           acc += W + 1;
@@ -633,6 +668,7 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       h->merge_alloc = true;
     }
     M.n = h->n; M.N = N; M.max_block = h->opt.max_block;
+    M.seg = h->dist ? h->d_seg : nullptr;
     M.bstart = h->d_bstart;
     M.Lrow_off = F.Lrow_off; M.Lm = F.Lm; M.Lval_off = F.Lval_off;
     M.Ucol_off = F.Ucol_off; M.Uc = F.Uc; M.Uval_off = F.Uval_off;
@@ -725,27 +761,28 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
 }
 
 // ------------------------------------------------------------ factor
-extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *st_out) {
-  if (!h) { set_err(nullptr, "bilu_factor: null context"); return BILU_ERR_ARG; }
-  if (!(tau >= 0.0)) { set_err(h, "bilu_factor: tau must be >= 0"); return BILU_ERR_ARG; }
-  cudaSetDevice(h->opt.device);
+enum Phase { PH_ALL = 0, PH_LOCAL = 1, PH_SEP = 2 };
+
+static bilu_status prepare_separators(bilu_ctx *h);
+
+// One launch of the persistent factor kernel over the blocks of `ph` (all blocks, this
+// rank's subtree blocks, or the separator blocks), with the regrow-and-retry loop for the
+// device workspaces.  e0/e1 bracket the successful attempt.
+static bilu_status run_phase(bilu_ctx *h, Phase ph, bilu_factor_stats &S, unsigned long long *ctrl, cudaEvent_t e0,
+                             cudaEvent_t e1, int &launches) {
   DevFactor &F = h->F;
-  F.tau = tau;
-  F.near_rel = h->opt.near_rel;
-  F.exp = getenv("BILU_EXP") ? atoi(getenv("BILU_EXP")) : 0;
-  bilu_factor_stats S{};
-  S.breakdown_block = -1;
-  S.n_blocks_init = h->N;
-  cudaEvent_t e0, e1, e2;
-  CUDA_TRY(h, cudaEventCreate(&e0)); CUDA_TRY(h, cudaEventCreate(&e1)); CUDA_TRY(h, cudaEventCreate(&e2));
-  h->factored = false;
-  int launches = 0;
-  unsigned long long ctrl[CTRL_COUNT];
   for (int attempt = 0;; ++attempt) {
-    bilu_status bs = ensure_capacity(h);
+    bilu_status bs = ph == PH_SEP ? ensure_aux(h) : ensure_capacity(h);
     if (bs != BILU_OK) return bs;
     CUDA_TRY(h, cudaEventRecord(e0, h->stream));
-    bs = reset_schedule(h);
+    if (ph == PH_ALL) { F.owned = nullptr; F.n_target = h->N; bs = reset_schedule(h, h->d_ready0, h->nready0); }
+    else if (ph == PH_LOCAL) {
+      F.owned = h->d_own_mask; F.n_target = (int64_t)h->own_list.size();
+      bs = reset_schedule(h, h->d_own_ready, h->n_own_ready);
+    } else {
+      F.owned = h->d_sep_mask; F.n_target = h->N;
+      bs = prepare_separators(h);
+    }
     if (bs != BILU_OK) return bs;
     const char *dbg_env = getenv("BILU_DEBUG_TIMEOUT");
     if (dbg_env && !F.dbg) {
@@ -757,7 +794,7 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
       h->dbg_host = (volatile int *)hp;
     }
     CUDA_TRY(h, bilu_launch_factor(F, h->grid, h->stream));
-    launches = 1;
+    launches += 1;
     if (dbg_env) {
       const double limit = atof(dbg_env);
       const double t_start = (double)clock() / CLOCKS_PER_SEC;
@@ -778,26 +815,36 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
     for (int i = 0; i < CTRL_COUNT; ++i) ctrl[i] = h->ctrl_full[CS * i];
     const int code = (int)ctrl[CTRL_ABORT];
     if (code == DEV_OK) {
-      if (ctrl[CTRL_DONE] != (unsigned long long)h->N) {
-        set_err(h, "bilu_factor: schedule finished %llu of %d blocks", ctrl[CTRL_DONE], h->N);
+      if (ctrl[CTRL_DONE] != (unsigned long long)F.n_target) {
+        set_err(h, "bilu_factor: schedule finished %llu of %lld blocks", ctrl[CTRL_DONE], (long long)F.n_target);
         return BILU_ERR_STATE;
       }
-      break;
+      return BILU_OK;
     }
     if (code == DEV_BREAKDOWN) {
       S.breakdown_block = (int32_t)ctrl[CTRL_ERRBLK];
-      if (st_out) *st_out = S;
       set_err(h, "bilu_factor: pivot block %d is exactly singular", S.breakdown_block);
       return BILU_ERR_BREAKDOWN;
     }
     if (getenv("BILU_VERBOSE"))
-      fprintf(stderr, "bilu_factor retry %d: code %d block %llu hpool %lld/%lld hctx %llu/%lld work %lld\n", attempt, code,
-              ctrl[CTRL_ERRBLK], (long long)ctrl[CTRL_HPOOL], (long long)h->hpool_cap, ctrl[CTRL_HCTX],
-              (long long)F.hctx_cap, (long long)h->work_per_cta);
+      fprintf(stderr, "bilu_factor retry %d (phase %d): code %d block %llu hpool %lld/%lld hctx %llu/%lld work %lld\n",
+              attempt, (int)ph, code, ctrl[CTRL_ERRBLK], (long long)ctrl[CTRL_HPOOL], (long long)h->hpool_cap,
+              ctrl[CTRL_HCTX], (long long)F.hctx_cap, (long long)h->work_per_cta);
     if (attempt >= 12) { set_err(h, "bilu_factor: workspace overflow persists (code %d)", code); return BILU_ERR_OOM; }
     S.n_retries++;
     switch (code) {
-      case DEV_OVF_ARENA: h->cap_val *= 2; h->cap_idx *= 2; break;
+      case DEV_OVF_ARENA:
+        if (ph == PH_SEP) {   // keep the factors of phase A and of the received interface blocks
+          bilu_status gs;
+          if ((gs = grow_keep(h, F.Lidx, F.cap_Lidx, 2 * F.cap_Lidx, (int64_t)h->cur[0])) != BILU_OK) return gs;
+          if ((gs = grow_keep(h, F.Lval, F.cap_Lval, 2 * F.cap_Lval, (int64_t)h->cur[1])) != BILU_OK) return gs;
+          if ((gs = grow_keep(h, F.Uidx, F.cap_Uidx, 2 * F.cap_Uidx, (int64_t)h->cur[2])) != BILU_OK) return gs;
+          if ((gs = grow_keep(h, F.Uval, F.cap_Uval, 2 * F.cap_Uval, (int64_t)h->cur[3])) != BILU_OK) return gs;
+          h->cap_val = std::max(F.cap_Lval, F.cap_Uval); h->cap_idx = std::max(F.cap_Lidx, F.cap_Uidx);
+        } else {
+          h->cap_val *= 2; h->cap_idx *= 2;
+        }
+        break;
       case DEV_OVF_WORK: h->work_per_cta *= 4; break;
       case DEV_OVF_POOL: h->pool_lc *= 2; h->pool_uc *= 2; h->pool_succ *= 2; break;
       case DEV_OVF_HPOOL:
@@ -807,10 +854,21 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
       default: set_err(h, "bilu_factor: device list overflow (code %d, block %llu)", code, ctrl[CTRL_ERRBLK]); return BILU_ERR_OOM;
     }
   }
+}
+
+static void factor_setup(bilu_ctx *h, double tau) {
+  DevFactor &F = h->F;
+  F.tau = tau;
+  F.near_rel = h->opt.near_rel;
+  F.exp = getenv("BILU_EXP") ? atoi(getenv("BILU_EXP")) : 0;
+}
+
+// finalize (aggregation post-pass) + statistics shared by bilu_factor and the separator phase
+static bilu_status finish_factor(bilu_ctx *h, bilu_factor_stats &S, unsigned long long *ctrl, cudaEvent_t e0,
+                                 cudaEvent_t e1, cudaEvent_t e2, int launches, bilu_factor_stats *st_out) {
   h->launches += launches;
-  S.n_decisions = (int64_t)ctrl[CTRL_NDEC];
-  S.n_near = (int64_t)ctrl[CTRL_NEAR];
-  // ---- progressive aggregation post-pass + final factor descriptors
+  S.n_decisions += (int64_t)ctrl[CTRL_NDEC];
+  S.n_near += (int64_t)ctrl[CTRL_NEAR];
   int mlaunch = 0;
   bilu_status ms = finalize(h, ctrl, S, mlaunch);
   if (ms != BILU_OK) return ms;
@@ -821,12 +879,288 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
   float ms1 = 0.f, ms2 = 0.f;
   cudaEventElapsedTime(&ms1, e0, e1);
   cudaEventElapsedTime(&ms2, e1, e2);
-  S.t_factor_ms = ms1 + ms2;
+  S.t_factor_ms += ms1 + ms2;
   S.t_merge_ms = ms2;
-  S.n_kernel_launches = launches;
-  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
+  S.n_kernel_launches += launches;
   h->factored = true;
   h->last = S;
+  if (st_out) *st_out = S;
+  return BILU_OK;
+}
+
+struct Events {
+  cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+  ~Events() { for (auto x : e) if (x) cudaEventDestroy(x); }
+};
+
+extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *st_out) {
+  if (!h) { set_err(nullptr, "bilu_factor: null context"); return BILU_ERR_ARG; }
+  if (!(tau >= 0.0)) { set_err(h, "bilu_factor: tau must be >= 0"); return BILU_ERR_ARG; }
+  if (h->dist) { set_err(h, "bilu_factor: distributed context; use bilu_factor_local / bilu_factor_separators"); return BILU_ERR_STATE; }
+  cudaSetDevice(h->opt.device);
+  factor_setup(h, tau);
+  bilu_factor_stats S{};
+  S.breakdown_block = -1;
+  S.n_blocks_init = h->N;
+  Events ev;
+  for (auto &x : ev.e) CUDA_TRY(h, cudaEventCreate(&x));
+  h->factored = false;
+  int launches = 0;
+  unsigned long long ctrl[CTRL_COUNT];
+  bilu_status bs = run_phase(h, PH_ALL, S, ctrl, ev.e[0], ev.e[1], launches);
+  if (bs != BILU_OK) { if (st_out) *st_out = S; return bs; }
+  return finish_factor(h, S, ctrl, ev.e[0], ev.e[1], ev.e[2], launches, st_out);
+}
+
+// ------------------------------------------------------------ distributed
+extern "C" bilu_status bilu_dist_setup(bilu_ctx *h, const int32_t *owner, int32_t rank) {
+  if (!h || !owner || rank < 0) { set_err(h, "bilu_dist_setup: null argument or negative rank"); return BILU_ERR_ARG; }
+  if (h->merge_alloc || h->factored) {
+    set_err(h, "bilu_dist_setup: must be called before the first factorization");
+    return BILU_ERR_STATE;
+  }
+  const int N = h->N;
+  h->owner.assign(owner, owner + N);
+  h->rank = rank;
+  h->own_list.clear(); h->sep_list.clear();
+  for (int K = 0; K < N; ++K) {
+    if (owner[K] < -1) { set_err(h, "bilu_dist_setup: owner[%d] = %d < -1", K, owner[K]); return BILU_ERR_ARG; }
+    if (owner[K] == rank) h->own_list.push_back(K);
+    else if (owner[K] == -1) h->sep_list.push_back(K);
+  }
+  // the partition must separate: no coupling between blocks of different ranks, and no
+  // subtree block after a separator block it is coupled to (it could not finish in phase A)
+  h->static_sep.assign(h->sep_list.size(), 0);
+  std::vector<int32_t> sep_pos(N, -1);
+  for (size_t x = 0; x < h->sep_list.size(); ++x) sep_pos[h->sep_list[x]] = (int32_t)x;
+  for (int a = 0; a < N; ++a)
+    for (int32_t q = h->adj_ptr_h[a]; q < h->adj_ptr_h[a + 1]; ++q) {
+      const int b = h->adj_h[q];   // a < b, coupled
+      if (owner[a] >= 0 && owner[b] >= 0 && owner[a] != owner[b]) {
+        set_err(h, "bilu_dist_setup: blocks %d (rank %d) and %d (rank %d) are coupled", a, owner[a], b, owner[b]);
+        return BILU_ERR_ARG;
+      }
+      if (owner[a] == -1 && owner[b] >= 0) {
+        set_err(h, "bilu_dist_setup: subtree block %d follows separator block %d it is coupled to", b, a);
+        return BILU_ERR_ARG;
+      }
+      if (owner[a] == -1 && owner[b] == -1) h->static_sep[sep_pos[b]]++;
+    }
+  std::vector<int32_t> ready, segv(N);
+  std::vector<uint8_t> own_mask(N, 0), sep_mask(N, 0);
+  for (int K : h->own_list) { own_mask[K] = 1; if (h->pending0_h[K] == 0) ready.push_back(K); }
+  for (int K : h->sep_list) sep_mask[K] = 1;
+  for (int K = 0; K < N; ++K) segv[K] = (owner[K] == rank || owner[K] == -1) ? owner[K] : -(K + 2);
+  h->seg = segv;
+  h->n_own_ready = (int32_t)ready.size();
+  const size_t nown = h->own_list.size(), nsep = h->sep_list.size();
+  CUDA_TRY(h, dalloc(h, &h->d_own_mask, (size_t)N)); CUDA_TRY(h, dalloc(h, &h->d_sep_mask, (size_t)N));
+  CUDA_TRY(h, dalloc(h, &h->d_own_list, std::max<size_t>(nown, 1))); CUDA_TRY(h, dalloc(h, &h->d_sep_list, std::max<size_t>(nsep, 1)));
+  CUDA_TRY(h, dalloc(h, &h->d_static_sep, std::max<size_t>(nsep, 1)));
+  CUDA_TRY(h, dalloc(h, &h->d_seg, (size_t)N));
+  CUDA_TRY(h, dalloc(h, &h->d_own_ready, std::max<size_t>(ready.size(), 1)));
+  CUDA_TRY(h, dalloc(h, &h->d_flag, std::max<size_t>(nown, 1)));
+  CUDA_TRY(h, cudaMemcpy(h->d_own_mask, own_mask.data(), N, cudaMemcpyHostToDevice));
+  CUDA_TRY(h, cudaMemcpy(h->d_sep_mask, sep_mask.data(), N, cudaMemcpyHostToDevice));
+  if (nown) CUDA_TRY(h, cudaMemcpy(h->d_own_list, h->own_list.data(), nown * 4, cudaMemcpyHostToDevice));
+  if (nsep) CUDA_TRY(h, cudaMemcpy(h->d_sep_list, h->sep_list.data(), nsep * 4, cudaMemcpyHostToDevice));
+  if (nsep) CUDA_TRY(h, cudaMemcpy(h->d_static_sep, h->static_sep.data(), nsep * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(h, cudaMemcpy(h->d_seg, segv.data(), (size_t)N * 4, cudaMemcpyHostToDevice));
+  if (!ready.empty()) CUDA_TRY(h, cudaMemcpy(h->d_own_ready, ready.data(), ready.size() * 4, cudaMemcpyHostToDevice));
+  h->dist = true;
+  h->dist_local_done = false;
+  return BILU_OK;
+}
+
+extern "C" bilu_status bilu_factor_local(bilu_ctx *h, double tau, bilu_factor_stats *st_out) {
+  if (!h) { set_err(nullptr, "bilu_factor_local: null context"); return BILU_ERR_ARG; }
+  if (!h->dist) { set_err(h, "bilu_factor_local: call bilu_dist_setup first"); return BILU_ERR_STATE; }
+  if (!(tau >= 0.0)) { set_err(h, "bilu_factor_local: tau must be >= 0"); return BILU_ERR_ARG; }
+  cudaSetDevice(h->opt.device);
+  factor_setup(h, tau);
+  DevFactor &F = h->F;
+  bilu_factor_stats S{};
+  S.breakdown_block = -1;
+  S.n_blocks_init = h->N;
+  Events ev;
+  for (auto &x : ev.e) CUDA_TRY(h, cudaEventCreate(&x));
+  h->factored = false;
+  h->dist_local_done = false;
+  h->remote_ifc.clear();
+  h->own_ifc.clear();
+  // descriptors of every block empty: blocks of other ranks stay absent
+  {
+    bilu_status bs = ensure_capacity(h);
+    if (bs != BILU_OK) return bs;
+    const size_t N = h->N;
+    CUDA_TRY(h, cudaMemsetAsync(F.Lm, 0, N * 4, h->stream)); CUDA_TRY(h, cudaMemsetAsync(F.Uc, 0, N * 4, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(F.Lrow_off, 0, N * 8, h->stream)); CUDA_TRY(h, cudaMemsetAsync(F.Lval_off, 0, N * 8, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(F.Ucol_off, 0, N * 8, h->stream)); CUDA_TRY(h, cudaMemsetAsync(F.Uval_off, 0, N * 8, h->stream));
+  }
+  int launches = 0;
+  unsigned long long ctrl[CTRL_COUNT];
+  bilu_status bs = run_phase(h, PH_LOCAL, S, ctrl, ev.e[0], ev.e[1], launches);
+  if (bs != BILU_OK) { if (st_out) *st_out = S; return bs; }
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev.e[0], ev.e[1]);
+  for (int i = 0; i < 4; ++i) h->cur[i] = ctrl[CTRL_CUR_LIDX + i];
+  memcpy(&h->flops_local, &ctrl[CTRL_FLOPS], sizeof(double));
+  h->t_local_ms = ms;
+  h->ndec_local = (int64_t)ctrl[CTRL_NDEC];
+  h->nnear_local = (int64_t)ctrl[CTRL_NEAR];
+  h->launches += launches;
+  h->dist_local_done = true;
+  h->pack_valid = false;
+  S.flops = h->flops_local;
+  S.t_factor_ms = ms;
+  S.n_decisions = h->ndec_local;
+  S.n_near = h->nnear_local;
+  S.n_kernel_launches = launches;
+  if (st_out) *st_out = S;
+  return BILU_OK;
+}
+
+static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+extern "C" bilu_status bilu_interface_pack(bilu_ctx *h, void *dst, int64_t capacity, int64_t *nbytes) {
+  if (!h || !nbytes) { set_err(h, "bilu_interface_pack: null argument"); return BILU_ERR_ARG; }
+  if (!h->dist_local_done) { set_err(h, "bilu_interface_pack: bilu_factor_local has not run"); return BILU_ERR_STATE; }
+  cudaSetDevice(h->opt.device);
+  DevFactor &F = h->F;
+  if (!h->pack_valid) {
+    const int nown = (int)h->own_list.size();
+    std::vector<uint8_t> flag(std::max(nown, 1));
+    std::vector<int32_t> Lm(h->N), Uc(h->N);
+    CUDA_TRY(h, bilu_launch_interface_flags(F, h->d_own_list, nown, h->d_sep_mask, h->d_flag, h->stream));
+    if (nown) CUDA_TRY(h, cudaMemcpyAsync(flag.data(), h->d_flag, nown, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(Lm.data(), F.Lm, h->N * 4, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(Uc.data(), F.Uc, h->N * 4, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    h->launches += 1;
+    h->own_ifc.clear();
+    for (int x = 0; x < nown; ++x) if (flag[x]) h->own_ifc.push_back(h->own_list[x]);
+    const int cnt = (int)h->own_ifc.size();
+    h->pack_tab.assign(cnt, PackEntry{});
+    int64_t off = align_up((PACK_HEADER * 8) + (int64_t)cnt * (int64_t)sizeof(PackEntry), 16);
+    for (int x = 0; x < cnt; ++x) {
+      const int J = h->own_ifc[x];
+      PackEntry &e = h->pack_tab[x];
+      e.J = J; e.b = h->bstart[J + 1] - h->bstart[J]; e.Lm = Lm[J]; e.Uc = Uc[J];
+      e.offLi = off; off = align_up(off + e.Lm * 4, 16);
+      e.offUi = off; off = align_up(off + e.Uc * 4, 16);
+      e.offLv = off; off = align_up(off + e.Lm * e.b * 8, 16);
+      e.offUv = off; off = align_up(off + e.Uc * e.b * 8, 16);
+    }
+    h->pack_bytes = off;
+    h->pack_valid = true;
+  }
+  *nbytes = h->pack_bytes;
+  if (!dst || capacity < h->pack_bytes) return BILU_OK;   // size query
+  const int cnt = (int)h->pack_tab.size();
+  unsigned char *buf = (unsigned char *)dst;
+  const int64_t hdr[PACK_HEADER] = {PACK_MAGIC, cnt, h->pack_bytes, h->rank};
+  CUDA_TRY(h, cudaMemcpyAsync(buf, hdr, sizeof(hdr), cudaMemcpyHostToDevice, h->stream));
+  if (cnt) CUDA_TRY(h, cudaMemcpyAsync(buf + PACK_HEADER * 8, h->pack_tab.data(), cnt * sizeof(PackEntry), cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, bilu_launch_pack(F, (const PackEntry *)(buf + PACK_HEADER * 8), cnt, buf, h->stream));
+  h->launches += cnt > 0;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return BILU_OK;
+}
+
+extern "C" bilu_status bilu_interface_unpack(bilu_ctx *h, const void *dbuf, int64_t nbytes) {
+  if (!h || !dbuf || nbytes < PACK_HEADER * 8) { set_err(h, "bilu_interface_unpack: bad argument"); return BILU_ERR_ARG; }
+  if (!h->dist_local_done) { set_err(h, "bilu_interface_unpack: bilu_factor_local has not run"); return BILU_ERR_STATE; }
+  cudaSetDevice(h->opt.device);
+  DevFactor &F = h->F;
+  int64_t hdr[PACK_HEADER];
+  CUDA_TRY(h, cudaMemcpy(hdr, dbuf, sizeof(hdr), cudaMemcpyDeviceToHost));
+  if (hdr[0] != PACK_MAGIC || hdr[2] != nbytes || hdr[1] < 0) { set_err(h, "bilu_interface_unpack: not a packed interface buffer"); return BILU_ERR_ARG; }
+  if (hdr[3] == h->rank) { set_err(h, "bilu_interface_unpack: buffer of this rank"); return BILU_ERR_ARG; }
+  const int cnt = (int)hdr[1];
+  std::vector<PackEntry> tab(cnt);
+  if (cnt) CUDA_TRY(h, cudaMemcpy(tab.data(), (const unsigned char *)dbuf + PACK_HEADER * 8, cnt * sizeof(PackEntry), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> base(4 * (size_t)std::max(cnt, 1));
+  unsigned long long c[4] = {h->cur[0], h->cur[1], h->cur[2], h->cur[3]};
+  for (int x = 0; x < cnt; ++x) {
+    const PackEntry &e = tab[x];
+    if (e.J < 0 || e.J >= h->N || h->owner[e.J] == h->rank || h->owner[e.J] < 0) {
+      set_err(h, "bilu_interface_unpack: block %lld is not a remote subtree block", (long long)e.J);
+      return BILU_ERR_ARG;
+    }
+    base[4 * x] = (int64_t)c[0]; c[0] += ((unsigned long long)e.Lm + 31) & ~31ull;
+    base[4 * x + 1] = (int64_t)c[1]; c[1] += ((unsigned long long)(e.Lm * e.b) + 15) & ~15ull;
+    base[4 * x + 2] = (int64_t)c[2]; c[2] += ((unsigned long long)e.Uc + 31) & ~31ull;
+    base[4 * x + 3] = (int64_t)c[3]; c[3] += ((unsigned long long)(e.Uc * e.b) + 15) & ~15ull;
+  }
+  bilu_status gs;
+  if ((gs = grow_keep(h, F.Lidx, F.cap_Lidx, (int64_t)c[0], (int64_t)h->cur[0])) != BILU_OK) return gs;
+  if ((gs = grow_keep(h, F.Lval, F.cap_Lval, (int64_t)c[1], (int64_t)h->cur[1])) != BILU_OK) return gs;
+  if ((gs = grow_keep(h, F.Uidx, F.cap_Uidx, (int64_t)c[2], (int64_t)h->cur[2])) != BILU_OK) return gs;
+  if ((gs = grow_keep(h, F.Uval, F.cap_Uval, (int64_t)c[3], (int64_t)h->cur[3])) != BILU_OK) return gs;
+  h->cap_val = std::max(F.cap_Lval, F.cap_Uval); h->cap_idx = std::max(F.cap_Lidx, F.cap_Uidx);
+  if ((int64_t)base.size() > h->base_cap) {
+    dfree(h, h->d_base);
+    CUDA_TRY(h, dalloc(h, &h->d_base, base.size()));
+    h->base_cap = (int64_t)base.size();
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(h->d_base, base.data(), base.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, bilu_launch_unpack(F, (const unsigned char *)dbuf, (const PackEntry *)((const unsigned char *)dbuf + PACK_HEADER * 8),
+                                 cnt, h->d_base, h->stream));
+  h->launches += cnt > 0;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  for (int i = 0; i < 4; ++i) h->cur[i] = c[i];
+  for (int x = 0; x < cnt; ++x) h->remote_ifc.push_back((int32_t)tab[x].J);
+  return BILU_OK;
+}
+
+// phase-B schedule: control block with the arena cursors of phase A + unpacks, empty queue,
+// separator lists / pending rebuilt from every interface block
+static bilu_status prepare_separators(bilu_ctx *h) {
+  DevFactor &F = h->F;
+  cudaStream_t st = h->stream;
+  const int nsep = (int)h->sep_list.size();
+  memset(h->ctrl_init, 0, sizeof(h->ctrl_init));
+  for (int i = 0; i < 4; ++i) h->ctrl_init[CS * (CTRL_CUR_LIDX + i)] = h->cur[i];
+  h->ctrl_init[CS * CTRL_DONE] = (unsigned long long)(h->N - nsep);
+  CUDA_TRY(h, cudaMemcpyAsync(F.ctrl, h->ctrl_init, sizeof(h->ctrl_init), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h, cudaMemsetAsync(F.queue, 0xFF, F.qcap * sizeof(int32_t), st));
+  std::vector<int32_t> ifc(h->own_ifc);
+  ifc.insert(ifc.end(), h->remote_ifc.begin(), h->remote_ifc.end());
+  if ((int64_t)ifc.size() > h->ifc_cap) {
+    dfree(h, h->d_ifc);
+    CUDA_TRY(h, dalloc(h, &h->d_ifc, std::max<size_t>(ifc.size(), 1)));
+    h->ifc_cap = (int64_t)ifc.size();
+  }
+  if (!ifc.empty()) CUDA_TRY(h, cudaMemcpyAsync(h->d_ifc, ifc.data(), ifc.size() * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h, bilu_launch_sep_prepare(F, h->d_sep_list, nsep, h->d_static_sep, h->d_ifc, (int)ifc.size(), h->d_sep_mask, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  h->launches += 3;
+  return BILU_OK;
+}
+
+extern "C" bilu_status bilu_factor_separators(bilu_ctx *h, bilu_factor_stats *st_out) {
+  if (!h) { set_err(nullptr, "bilu_factor_separators: null context"); return BILU_ERR_ARG; }
+  if (!h->dist_local_done) { set_err(h, "bilu_factor_separators: bilu_factor_local has not run"); return BILU_ERR_STATE; }
+  cudaSetDevice(h->opt.device);
+  bilu_factor_stats S{};
+  S.breakdown_block = -1;
+  S.n_blocks_init = h->N;
+  Events ev;
+  for (auto &x : ev.e) CUDA_TRY(h, cudaEventCreate(&x));
+  int launches = 0;
+  unsigned long long ctrl[CTRL_COUNT];
+  bilu_status bs = run_phase(h, PH_SEP, S, ctrl, ev.e[0], ev.e[1], launches);
+  if (bs != BILU_OK) { if (st_out) *st_out = S; return bs; }
+  S.n_decisions = h->ndec_local;
+  S.n_near = h->nnear_local;
+  S.t_factor_ms = h->t_local_ms;
+  bs = finish_factor(h, S, ctrl, ev.e[0], ev.e[1], ev.e[2], launches, nullptr);
+  if (bs != BILU_OK) return bs;
+  S = h->last;
+  S.flops += h->flops_local;
+  h->last = S;
+  h->dist_local_done = false;
   if (st_out) *st_out = S;
   return BILU_OK;
 }
@@ -1016,6 +1350,7 @@ static bilu_status build_apply(bilu_ctx *h) {
 }
 
 extern "C" bilu_status bilu_apply(bilu_ctx *h, const double *x, double *y, void *stream) {
+  if (h && h->dist) { set_err(h, "bilu_apply: distributed factors are spread over the ranks (not supported)"); return BILU_ERR_STATE; }
   if (!h || !x || !y) { set_err(h, "bilu_apply: null argument"); return BILU_ERR_ARG; }
   if (x == y) { set_err(h, "bilu_apply: x and y may not alias"); return BILU_ERR_ARG; }
   if (!h->factored) { set_err(h, "bilu_apply: no factorization"); return BILU_ERR_STATE; }

@@ -97,6 +97,10 @@ struct DevFactor {
   double *work; int64_t work_per_cta;   // doubles per CTA
   int *posmap;                          // [grid * n] index -> occurrence / buffer line
   volatile int *dbg;                    // mapped host memory for the deadlock watchdog (or NULL)
+  // distributed factorization (bilu_dist_setup): blocks this launch may enqueue and the
+  // finished-block count at which it stops
+  const uint8_t *owned;                 // [N] or NULL (every block)
+  int64_t n_target;
   // split heavy blocks
   HeavyCtx *hctx; int64_t hctx_cap;
   double *hpool; int64_t hpool_cap;     // doubles
@@ -124,6 +128,7 @@ struct MergeArgs {
   int32_t *flag;          // [N] run-start flags
   int32_t *first;         // [N+1] first original block of each final block
   int32_t *nF;            // [1]
+  const int32_t *seg;     // [N] aggregation segments (merges only inside one segment) or NULL
   int32_t *fbstart;       // [N+1]
   int32_t *fLm, *fUc;     // [N]
   int64_t *fLrow_off, *fLval_off, *fUcol_off, *fUval_off, *fD_off;  // [N] / [N+1]
@@ -152,5 +157,13 @@ struct ApplyArgs {
   unsigned long long *ctrl;       // [4]: qhead, qtail
   double *w, *y;                  // permuted work vectors
 };
+
+// packed interface blocks exchanged between ranks (bilu_interface_pack/unpack)
+struct PackEntry {
+  int64_t J, b, Lm, Uc;
+  int64_t offLi, offLv, offUi, offUv;   // byte offsets into the packed buffer
+};
+constexpr int64_t PACK_MAGIC = 0x42494c5550414b31LL;   // "BILUPAK1"
+constexpr int64_t PACK_HEADER = 4;                     // int64 words: magic, count, bytes, rank
 
 }  // namespace bilu

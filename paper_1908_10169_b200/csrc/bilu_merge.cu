@@ -102,11 +102,14 @@ __device__ __forceinline__ bool agg_test(long long p, long long q, long long r, 
   return (5 * nu <= 6 * mu) || (nu <= mu + 2 * (p + q));
 }
 
-// window of block k: the largest W with s_k - s_{k-W} + q <= max_block (W <= 127)
-__device__ __forceinline__ int merge_window(const int32_t *bstart, int k, int max_block) {
+// window of block k: the largest W with s_k - s_{k-W} + q <= max_block (W <= 127), and
+// (distributed factorization) blocks k-W..k in one aggregation segment (R18)
+__device__ __forceinline__ int merge_window(const int32_t *bstart, const int32_t *seg, int k, int max_block) {
   const int s_k = bstart[k], q = bstart[k + 1] - s_k;
   int W = 0;
-  while (k - 1 - W >= 0 && (s_k - bstart[k - 1 - W]) + q <= max_block && W < 127) ++W;
+  while (k - 1 - W >= 0 && (s_k - bstart[k - 1 - W]) + q <= max_block && W < 127 &&
+         (seg == nullptr || seg[k - 1 - W] == seg[k]))
+    ++W;
   return W;
 }
 
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(TEST_T) merge_test_kernel(MergeArgs M) {
   const int tid = threadIdx.x;
   for (int k = blockIdx.x; k < M.N; k += gridDim.x) {
     if (tid < 4) s_mask[tid] = 0u;
-    const int W = k > 0 ? merge_window(M.bstart, k, M.max_block) : 0;
+    const int W = k > 0 ? merge_window(M.bstart, M.seg, k, M.max_block) : 0;
     __syncthreads();
     if (W > 0) {
       test_side(M, k, W, true, stage, s_len, s_off, s_ptr, SR, s_tmp);

@@ -59,3 +59,35 @@ def dense_LPU(f, n):
         if len(cols):
             U[np.arange(s, e)[:, None], np.asarray(cols)[None, :]] = D @ Ut
     return L, P, U
+
+
+def compare_present_blocks(g, o, present_start, tol=1e-10):
+    """compare_factors restricted to the final blocks of `o` that start at an index in
+    `present_start` (the blocks a rank of the distributed factorization holds); each must
+    exist in `g` with the same extent."""
+    problems = []
+    gstart = {int(s): K for K, s in enumerate(np.asarray(g.bstart)[:-1])}
+    worst = 0.0
+    checked = 0
+    for K in range(o.nblk):
+        s0 = int(o.bstart[K])
+        if s0 not in present_start:
+            continue
+        if s0 not in gstart or int(g.bstart[gstart[s0] + 1]) != int(o.bstart[K + 1]):
+            problems.append("block at %d: extent differs" % s0)
+            continue
+        s, e, gr, gL, gc, gU, gD = g.block(gstart[s0])
+        _, _, orr, oL, oc, oU, oD = o.block(K)
+        checked += 1
+        if not np.array_equal(gr, orr) or not np.array_equal(gc, oc):
+            problems.append("block at %d: pattern differs" % s0)
+            continue
+        for a, b_ in ((gL, oL), (gU.T, oU.T)):
+            if a.size:
+                den = np.maximum(np.abs(b_).max(axis=1), 1e-300)
+                worst = max(worst, (np.abs(a - b_).max(axis=1) / den).max())
+        if gD.size:
+            worst = max(worst, np.abs(gD - oD).max() / max(np.abs(oD).max(), 1e-300))
+    if worst > tol:
+        problems.append("max normwise relative difference %.3e > %.1e" % (worst, tol))
+    return {"problems": problems, "max_rel": worst, "checked": checked}
