@@ -6,9 +6,11 @@
 A step is one bilu_factor (the whole hot path: scatter, Schur updates, pivot
 inverses, scaling/dropping, progressive aggregation) of the configs[1] matrix
 (3D 7-pt convection-diffusion 64^3, ND ordering, tau = 1e-3), inputs resident in
-HBM.  value = factorizations per second over all ranks (N>1: independent
-replicas, weak scaling); ms_per_step = device time of one factorization (CUDA
-events on the library's stream, max over ranks).  `e2e` repeats the step through
+HBM.  At N > 1 the same factorization is split over the ranks (strong scaling):
+phase A factors each rank's top-level ND subtrees, the interface panels are
+all-gathered over NCCL, phase B factors the separators.  value = factorizations
+per second; ms_per_step = device time of one factorization (CUDA events, max over
+ranks).  `e2e` repeats the step through
 the C-ABI with the matrix values copied from pinned HOST memory every step.
 Rank 0 prints one JSON line.
 """
@@ -40,8 +42,15 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def make_problem(name):
+def make_problem(name, world=1):
+    """The bench workload; at world > 1 the same matrix and ordering with the top log2(world)
+    ND levels labelled as subtrees (the ordering does not depend on the labels)."""
     from inputs.configs import make_config
+    if world > 1:
+        lv = int(round(np.log2(world)))
+        if 2 ** lv != world:
+            raise SystemExit("bench.py: --gpus must be a power of two for the subtree partition")
+        return make_config(name, top_levels=lv)
     return make_config(name)
 
 
@@ -94,11 +103,16 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
 
 
-def dist_init(n_gpus):
+def dist_init(n_gpus, force=False):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or force:
+        if force and "MASTER_ADDR" not in os.environ:
+            os.environ["MASTER_ADDR"] = "127.0.0.1"
+            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         import torch.distributed as dist
         dist.init_process_group("nccl" if n_gpus > 0 else "gloo")
     return rank, world, local
@@ -117,6 +131,16 @@ def allreduce_max(x, world):
     import torch.distributed as dist
     t = torch.tensor([x], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x, world):
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
 
@@ -172,9 +196,11 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the distributed (subtree) path even at N=1 (checks its mechanics on one GPU)")
     args = ap.parse_args()
 
-    rank, world, local = dist_init(args.gpus)
+    rank, world, local = dist_init(args.gpus, force=args.dist)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -187,12 +213,29 @@ def main():
         build()
     barrier(world)
 
-    P = make_problem(args.config)
+    use_dist = world > 1 or args.dist
+    P = make_problem(args.config, max(world, 2) if use_dist else 1)
     g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm, device=local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2 (126 MB)
+    xfer = [0, 0]
+    local_flops = [0.0]
+    if use_dist:
+        # multi-GPU: phase A on this rank's ND subtrees, interface exchange (NCCL), phase B
+        from paper_1908_10169_b200.dist import factor_distributed, partition_owner
+        owner = partition_owner(P.block_part, world)
+        g.dist_setup(owner, rank)
+
+        def step():
+            st_, sent, recv = factor_distributed(g, P.tau)
+            xfer[0], xfer[1] = sent, recv
+            local_flops[0] = g.local_stats["flops"]
+            return st_
+    else:
+        def step():
+            return g.factor(P.tau)
 
     for _ in range(args.warmup):
-        st = g.factor(P.tau)
+        st = step()
     torch.cuda.synchronize()
 
     # ---------------- device-timed steps (inputs resident in HBM)
@@ -208,19 +251,21 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        st = g.factor(P.tau)
+        st = step()
         e1.record()
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
-        kern_ms.append(st["t_factor_ms"] - st["t_merge_ms"])
+        kern_ms.append(st["t_factor_ms"] - st["t_merge_ms"])   # factor kernel(s) (phases A + B at N > 1)
         launches += int(st["n_kernel_launches"])
         flops = st["flops"]
     torch.cuda.synchronize()
     barrier(world)
     clocks = clk.stop()
+    if use_dist:   # the factorization's flops: every rank's subtrees + the separators once
+        flops = allreduce_sum(local_flops[0], world) + (flops - local_flops[0])
     t_step = allreduce_max(float(np.sum(step_ms)), world) / args.steps
     t_kern = allreduce_max(float(np.mean(kern_ms)), world)
-    value = world / (t_step * 1e-3)
+    value = (world if world == 1 else 1) / (t_step * 1e-3)   # N > 1: one factorization per step
 
     # ---------------- e2e through the C-ABI with host buffers
     e2e = None
@@ -233,10 +278,10 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.steps):
             g.lib.bilu_set_values(g.h, ctypes.c_void_p(host_ptr), 0)
-            g.factor(P.tau)                          # ends with its device->host status read
+            step()                                   # ends with its device->host status read
         torch.cuda.synchronize()
         t_e2e = allreduce_max((time.perf_counter() - t0) / args.steps, world)
-        e2e = {"value": world / t_e2e, "unit": "factorizations/s",
+        e2e = {"value": (world if world == 1 else 1) / t_e2e, "unit": "factorizations/s",
                "h2d_bytes_per_step": int(P.nnz * 8),
                "d2h_bytes_per_step": int(16 * 8 + (16 * 8 + 4 + 8 + 4 if g.opt.aggregate else 0)),
                "ms_per_step": t_e2e * 1e3}
@@ -247,15 +292,19 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "factorizations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.config + " (BASELINE.json configs[1]): 3D 7-pt conv-diff 64^3, "
                                    "geometric ND, tau=1e-3, initial blocks <=8, aggregation on, max_block 128",
                        "n": P.n, "nnz": P.nnz, "tau": P.tau, "blocks_init": int(len(P.block_sizes)),
                        "blocks_final": int(st["n_blocks_final"]), "merges": int(st["n_merges"]),
-                       "parallelism": "replicas x%d" % world if world > 1 else "single GPU",
+                       "parallelism": ("ND subtrees over %d GPUs (%d top levels), interface panels "
+                                       "all-gathered over NCCL, separators replicated" % (world, int(np.log2(world))))
+                                      if use_dist else "single GPU",
+                       "exchange_bytes_per_rank": {"sent": xfer[0], "received": xfer[1]} if use_dist else None,
                        "l2": "flushed between timed steps (256 MB write)"},
-            "gflops": world * flops / (t_step * 1e-3) / 1e9,
+            "gflops": flops / (t_step * 1e-3) / 1e9,
             "flops_per_factorization": flops,
             "fp64_peak_fraction": (flops / (t_step * 1e-3) / 1e12) / FP64_PEAK_TFLOPS,
             "nnz_factors": int(st["nnz_L"] + st["nnz_U"] + st["nnz_D"]),
@@ -275,7 +324,7 @@ def main():
             out["cpu_baseline"] = cpu_baseline(P)
         print(json.dumps(out), flush=True)
     g.close()
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
         dist.destroy_process_group()
 

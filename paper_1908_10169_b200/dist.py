@@ -62,7 +62,7 @@ def factor_distributed(g, tau, group=None, timer=None):
     Returns (stats, bytes sent, bytes received)."""
     import torch.distributed as dist
     me = dist.get_rank(group)
-    g.factor_local(tau)
+    g.local_stats = g.factor_local(tau)
     if timer:
         timer("local")
     mine = g.interface_pack()
