@@ -42,6 +42,18 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def load_traffic(config):
+    """DRAM bytes per factor_kernel launch from the committed ncu --set full capture (or None)."""
+    p = os.path.join(ROOT, "profiles", "r01_factor_traffic.json")
+    try:
+        d = json.load(open(p))
+        if not d["workload"].startswith(config):
+            return None
+        return float(d["dram_bytes_read"] + d["dram_bytes_write"])
+    except Exception:
+        return None
+
+
 def make_problem(name, world=1):
     """The bench workload; at world > 1 the same matrix and ordering with the top log2(world)
     ND levels labelled as subtrees (the ordering does not depend on the labels)."""
@@ -310,7 +322,9 @@ def main():
             "nnz_factors": int(st["nnz_L"] + st["nnz_U"] + st["nnz_D"]),
             "roofline": {"bound": "tensor", "kernel": "factor_kernel (persistent, all of a-1..a-8)",
                          "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": None,
+                         "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": load_traffic(args.config),
+                         "traffic_source": "profiles/r01_factor_traffic.json (ncu --set full, DRAM read+write bytes "
+                                           "per factor_kernel launch)",
                          "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_fp64_peak.md)",
                          "kernel_ms": t_kern,
                          "hbm": {"achieved_gbs": st["bytes_min"] / (t_kern * 1e-3) / 1e9,
