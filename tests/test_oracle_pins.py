@@ -310,3 +310,33 @@ def test_decision_override_replays():
     ip, ix, dv = dense_to_csr(A)
     g = oracle.factor(ip, ix, dv, [1, 1], 0.01, aggregate=False, overrides=[(0, 0, 1, 1)])
     assert list(g.Li) == [1]
+
+
+def test_aggregation_segments_reading_r18():
+    """seg (R18): one segment == no segments; all-distinct segments == no
+    aggregation; piecewise segments: merged blocks never straddle a segment boundary and
+    the operator L P U equals the unmerged one."""
+    from inputs.configs import config5
+    P = config5(N=10, top_levels=1)
+    ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
+    bs = P.block_sizes
+    nb = len(bs)
+    a = oracle.factor(ip, ix, dv, bs, P.tau)
+    b = oracle.factor(ip, ix, dv, bs, P.tau, seg=np.zeros(nb, np.int32))
+    assert np.array_equal(a.bstart, b.bstart) and np.array_equal(a.Lv, b.Lv)
+    c = oracle.factor(ip, ix, dv, bs, P.tau, seg=np.arange(nb, dtype=np.int32))
+    d = oracle.factor(ip, ix, dv, bs, P.tau, aggregate=False)
+    assert c.n_merges == 0 and np.array_equal(c.bstart, d.bstart)
+    seg = np.where(P.block_part >= 0, P.block_part, -1).astype(np.int32)
+    e = oracle.factor(ip, ix, dv, bs, P.tau, seg=seg)
+    assert 0 < e.n_merges < a.n_merges + 1
+    bst = np.concatenate([[0], np.cumsum(bs)])
+    seg_of_row = np.repeat(seg, bs)
+    for K in range(e.nblk):
+        s0, s1 = int(e.bstart[K]), int(e.bstart[K + 1])
+        assert len(np.unique(seg_of_row[s0:s1])) == 1
+    from tests.parity import dense_LPU
+    L1, P1, U1 = dense_LPU(e, P.n)
+    L0, P0, U0 = dense_LPU(d, P.n)
+    M1, M0 = L1 @ P1 @ U1, L0 @ P0 @ U0
+    assert np.abs(M1 - M0).max() <= 1e-12 * np.abs(M0).max()
