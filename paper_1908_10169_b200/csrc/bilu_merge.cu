@@ -28,8 +28,7 @@ namespace bilu {
 
 constexpr int MT = 256;
 constexpr int MW = MT / 32;
-constexpr int TEST_T = 128;            // threads of merge_test_kernel
-constexpr int TEST_STAGE = 6144;       // list elements staged in shared memory per side
+constexpr int TEST_T = 256;            // threads of merge_test_kernel
 constexpr int SCAN_CHUNK = 256;        // blocks per chunk of the parallel scan
 constexpr int ARITH_KEYS = 4096;       // union keys sorted in shared memory
 constexpr int ARITH_PSMEM = 64;        // runs with P <= this keep L_aa, U_aa in shared memory
@@ -124,8 +123,16 @@ struct TestSide {
   int r[128], s[128], u[128];   // cumulative, index d (0 unused)
 };
 
-__device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *stage, int *s_len, int *s_off,
-                          const int **s_ptr, TestSide &R, int *s_tmp) {
+// Per distinct key x of the window's lists: dmin(x) = smallest d >= 1 with x in l_d and
+// whether x is in l_0, from an open-addressing hash table in shared memory (O(total list
+// length) per block); windows with more entries than the table holds use binary searches
+// in the (global) lists instead.
+constexpr int TEST_HT = 8192;      // hash slots (power of two)
+
+__device__ __forceinline__ unsigned t_hash(int key, unsigned mask) { return ((unsigned)key * 0x9E3779B1u) >> 5 & mask; }
+
+__device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *hkeys, int *hdmin, uint8_t *hflag,
+                          int *s_len, int *s_off, const int **s_ptr, TestSide &R) {
   const int tid = threadIdx.x;
   const int s_k = M.bstart[k], e_k = M.bstart[k + 1];
   const int32_t *idx = rows ? M.Lidx : M.Uidx;
@@ -149,30 +156,50 @@ __device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *stag
   }
   __syncthreads();
   const int total = s_off[W + 1];
-  const bool staged = total <= TEST_STAGE;
-  if (staged) {
-    for (int d = 0; d <= W; ++d) {
-      const int *src = s_ptr[d];
-      int *dst = stage + s_off[d];
-      for (int i = tid; i < s_len[d]; i += TEST_T) dst[i] = src[i];
+  if (2 * total <= TEST_HT) {
+    unsigned hs = 64;
+    while (hs < 2u * (unsigned)total) hs <<= 1;
+    const unsigned mask = hs - 1;
+    for (unsigned h = tid; h < hs; h += TEST_T) { hkeys[h] = -1; hdmin[h] = 255; hflag[h] = 0; }
+    __syncthreads();
+    for (int x = tid; x < total; x += TEST_T) {
+      int lo = 0, hi = W;
+      while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= x) lo = mid; else hi = mid - 1; }
+      const int d = lo;
+      const int key = s_ptr[d][x - s_off[d]];
+      unsigned h = t_hash(key, mask);
+      while (true) {
+        const int old = atomicCAS(&hkeys[h], -1, key);
+        if (old == -1 || old == key) break;
+        h = (h + 1) & mask;
+      }
+      if (d == 0) hflag[h] = 1;
+      else atomicMin(&hdmin[h], d);
     }
     __syncthreads();
-    for (int d = tid; d <= W; d += TEST_T) s_ptr[d] = stage + s_off[d];
-    __syncthreads();
-  }
-  for (int x = s_len[0] + tid; x < total; x += TEST_T) {
-    // list of element x: last d with s_off[d] <= x
-    int lo = 1, hi = W;
-    while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= x) lo = mid; else hi = mid - 1; }
-    const int d = lo;
-    const int key = s_ptr[d][x - s_off[d]];
-    bool first = true;
-    for (int d2 = 1; d2 < d && first; ++d2) first = !m_contains(s_ptr[d2], s_len[d2], key);
-    if (!first) continue;
-    if (key < e_k) atomicAdd(&R.r[d], 1);
-    else {
-      atomicAdd(&R.s[d], 1);
-      if (!m_contains(s_ptr[0], s_len[0], key)) atomicAdd(&R.u[d], 1);
+    for (unsigned h = tid; h < hs; h += TEST_T) {
+      const int key = hkeys[h], d = hdmin[h];
+      if (key < 0 || d > W) continue;
+      if (key < e_k) atomicAdd(&R.r[d], 1);
+      else {
+        atomicAdd(&R.s[d], 1);
+        if (!hflag[h]) atomicAdd(&R.u[d], 1);
+      }
+    }
+  } else {
+    for (int x = s_len[0] + tid; x < total; x += TEST_T) {
+      int lo = 1, hi = W;
+      while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= x) lo = mid; else hi = mid - 1; }
+      const int d = lo;
+      const int key = s_ptr[d][x - s_off[d]];
+      bool first = true;
+      for (int d2 = 1; d2 < d && first; ++d2) first = !m_contains(s_ptr[d2], s_len[d2], key);
+      if (!first) continue;
+      if (key < e_k) atomicAdd(&R.r[d], 1);
+      else {
+        atomicAdd(&R.s[d], 1);
+        if (!m_contains(s_ptr[0], s_len[0], key)) atomicAdd(&R.u[d], 1);
+      }
     }
   }
   __syncthreads();
@@ -181,24 +208,25 @@ __device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *stag
     for (int d = 1; d <= W; ++d) { r += R.r[d]; s += R.s[d]; u += R.u[d]; R.r[d] = r; R.s[d] = s; R.u[d] = u; }
   }
   __syncthreads();
-  (void)s_tmp;
 }
 
 __global__ void __launch_bounds__(TEST_T) merge_test_kernel(MergeArgs M) {
-  __shared__ int stage[TEST_STAGE];
+  extern __shared__ __align__(16) unsigned char tsm[];
+  int *hkeys = (int *)tsm;
+  int *hdmin = hkeys + TEST_HT;
+  uint8_t *hflag = (uint8_t *)(hdmin + TEST_HT);
   __shared__ int s_len[129], s_off[130];
   __shared__ const int *s_ptr[129];
   __shared__ TestSide SR, SC;
   __shared__ uint32_t s_mask[4];
-  __shared__ int s_tmp[8];
   const int tid = threadIdx.x;
   for (int k = blockIdx.x; k < M.N; k += gridDim.x) {
     if (tid < 4) s_mask[tid] = 0u;
     const int W = k > 0 ? merge_window(M.bstart, M.seg, k, M.max_block) : 0;
     __syncthreads();
     if (W > 0) {
-      test_side(M, k, W, true, stage, s_len, s_off, s_ptr, SR, s_tmp);
-      test_side(M, k, W, false, stage, s_len, s_off, s_ptr, SC, s_tmp);
+      test_side(M, k, W, true, hkeys, hdmin, hflag, s_len, s_off, s_ptr, SR);
+      test_side(M, k, W, false, hkeys, hdmin, hflag, s_len, s_off, s_ptr, SC);
       const int s_k = M.bstart[k], q = M.bstart[k + 1] - s_k;
       int32_t *uv = M.UV + 2 * M.wofs[k];
       for (int d = 1 + tid; d <= W; d += TEST_T) {
@@ -599,7 +627,10 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
 // ----------------------------------------------------------------- launchers
 extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_t st) {
   const int nchunks = M.N > 1 ? (M.N - 1 + SCAN_CHUNK - 1) / SCAN_CHUNK : 0;
-  merge_test_kernel<<<grid * 8, TEST_T, 0, st>>>(M);
+  const int tsmem = TEST_HT * 9;
+  cudaError_t e = cudaFuncSetAttribute(merge_test_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
+  if (e != cudaSuccess) return e;
+  merge_test_kernel<<<grid * 3, TEST_T, tsmem, st>>>(M);
   if (nchunks > 0) merge_chunkmap_kernel<<<nchunks, 128, 0, st>>>(M);
   merge_scan_kernel<<<1, 1024, 0, st>>>(M, nchunks);
   merge_offsets_kernel<<<1, 1024, 0, st>>>(M);
