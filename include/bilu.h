@@ -224,6 +224,12 @@ int64_t bilu_kernel_launches(const bilu_ctx *h);
 int bilu_diag_dgemm(int M, int N, int K, double alpha, const double *A, int64_t ars, int64_t acs,
                     const double *B, int64_t brs, int64_t bcs, double beta, double *C, int64_t crs,
                     int64_t ccs, int batch, int64_t sa, int64_t sb, int64_t sc, void *stream);
+/* bilu_diag_tsgemm -- the tall-skinny variant (B staged in shared memory, warps streaming
+ * 8-row tiles of A; used for the per-contributor Schur updates and the panel scaling of
+ * blocks wider than 16), same arguments; requires K <= 128 and N <= 128 (else 1). */
+int bilu_diag_tsgemm(int M, int N, int K, double alpha, const double *A, int64_t ars, int64_t acs,
+                     const double *B, int64_t brs, int64_t bcs, double beta, double *C, int64_t crs,
+                     int64_t ccs, int batch, int64_t sa, int64_t sb, int64_t sc, void *stream);
 
 #ifdef __cplusplus
 }

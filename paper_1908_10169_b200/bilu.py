@@ -20,7 +20,7 @@ STATUS = {0: "BILU_OK", 1: "BILU_ERR_ARG", 2: "BILU_ERR_BREAKDOWN", 3: "BILU_ERR
 # every symbol include/bilu.h declares
 ABI_SYMBOLS = ["bilu_options_default", "bilu_analyze", "bilu_set_values", "bilu_factor",
                "bilu_apply", "bilu_export", "bilu_factor_view_free", "bilu_destroy",
-               "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm",
+               "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm", "bilu_diag_tsgemm",
                "bilu_dist_setup", "bilu_factor_local", "bilu_interface_pack", "bilu_interface_unpack",
                "bilu_factor_separators"]
 
@@ -108,6 +108,8 @@ def load_library():
     lib.bilu_diag_dgemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, D, P, I64, I64, P, I64, I64, D, P,
                                     I64, I64, ctypes.c_int, I64, I64, I64, P]
     lib.bilu_diag_dgemm.restype = ctypes.c_int
+    lib.bilu_diag_tsgemm.argtypes = lib.bilu_diag_dgemm.argtypes
+    lib.bilu_diag_tsgemm.restype = ctypes.c_int
     lib.bilu_dist_setup.argtypes = [P, P, ctypes.c_int32]
     lib.bilu_dist_setup.restype = ctypes.c_int
     lib.bilu_factor_local.argtypes = [P, ctypes.c_double, ctypes.POINTER(FactorStats)]
@@ -299,14 +301,15 @@ class BILU:
             pass
 
 
-def diag_dgemm(A, B, C, alpha=1.0, beta=0.0, stream=0):
+def diag_dgemm(A, B, C, alpha=1.0, beta=0.0, stream=0, tall_skinny=False):
     """C[b] = alpha A[b] B[b] + beta C[b] with the library's DMMA CTA GEMM (one CTA per
     batch entry).  A, B, C: CUDA float64 tensors of shape (batch, M, K), (batch, K, N),
     (batch, M, N), any strides.  Diagnostics only (tests, microbenchmarks)."""
     lib = load_library()
     bt, M, K = A.shape
     N = B.shape[2]
-    rc = lib.bilu_diag_dgemm(M, N, K, alpha, A.data_ptr(), A.stride(1), A.stride(2), B.data_ptr(), B.stride(1),
+    fn = lib.bilu_diag_tsgemm if tall_skinny else lib.bilu_diag_dgemm
+    rc = fn(M, N, K, alpha, A.data_ptr(), A.stride(1), A.stride(2), B.data_ptr(), B.stride(1),
                              B.stride(2), beta, C.data_ptr(), C.stride(1), C.stride(2), bt, A.stride(0),
                              B.stride(0), C.stride(0), ctypes.c_void_p(stream))
     if rc != 0:

@@ -515,6 +515,8 @@ struct SideState {
   const unsigned *gbm; const int *gpre;   // global copies of the bitmap map (split blocks)
 };
 
+constexpr int MAX_PARTS = 32;          // per block (both sides)
+
 // a split heavy block (see process_block)
 struct HeavyCtx {
   int K, nc[2], T[2], np[2];
@@ -522,6 +524,9 @@ struct HeavyCtx {
   const Contrib *C[2];
   SideState R[2];
   double flops;
+  int wide;                 // parts run per-contributor DMMA products over contributor ranges
+  const int *iline[2];      // wide: destination line of every item of each side
+  int cb[2][MAX_PARTS / 2 + 1];   // wide: contributor range of every part
 };
 
 // One side of block K (SIDE 0: block column of L incl. the pivot block; SIDE 1:
@@ -763,21 +768,59 @@ struct EpiScatter {
   }
 };
 
+// B of one contributor's product (SIDE 0: Ũ_J(:, cols in K), b_J x ncol; SIDE 1:
+// L_J(rows in K, :)^T, b_J x ncol) staged in shared memory, then the tall-skinny product
+// over the contributor's items.  bs: scratch of >= 128 x TsB<128>::LDB doubles.
+template <int SIDE, int NMAX>
+__device__ void contrib_tsgemm(const DevFactor &F, int s, int e, int b, const Contrib &c, const LineMap &M, double *W,
+                               double *bs) {
+  if (SIDE == 0) {
+    tsgemm_stage_b<NT, NMAX>(c.bJ, c.ncol, DMat{F.Uval + c.uval, 1, c.bJ}, bs);
+    EpiScatter<0> ep{F.Lidx + c.rows, F.Uidx + c.cols, s, e, b, M, W};
+    cta_tsgemm<NT, NMAX>(c.n_items, c.ncol, c.bJ, DMat{F.Lval + c.lval, c.bJ, 1}, bs, ep);
+  } else {
+    tsgemm_stage_b<NT, NMAX>(c.bJ, c.ncol, DMat{F.Lval + c.lval, 1, c.bJ}, bs);
+    EpiScatter<1> ep{F.Uidx + c.cols, F.Lidx + c.rows, s, e, b, M, W};
+    cta_tsgemm<NT, NMAX>(c.n_items, c.ncol, c.bJ, DMat{F.Uval + c.uval, c.bJ, 1}, bs, ep);
+  }
+  __syncthreads();   // bs is restaged by the next contributor
+}
+
+// split wide blocks: the item's line comes from the owner's per-item table; reductions
+// into the global W of the block (several parts update it concurrently)
+struct EpiScatterRed {
+  const int *iline;        // line of output row i (this contributor's items)
+  const int32_t *jkey;     // matrix index of output column j
+  int s, b;
+  double *W;
+  __device__ __forceinline__ void operator()(int i, int j, double v) const {
+    red_add_f64(&W[(int64_t)iline[i] * b + (jkey[j] - s)], -v);
+  }
+};
+
+template <int SIDE, int NMAX>
+__device__ void contrib_tsgemm_red(const DevFactor &F, int s, int b, const Contrib &c, const int *iline, double *W,
+                                   double *bs) {
+  if (SIDE == 0) {
+    tsgemm_stage_b<NT, NMAX>(c.bJ, c.ncol, DMat{F.Uval + c.uval, 1, c.bJ}, bs);
+    cta_tsgemm<NT, NMAX>(c.n_items, c.ncol, c.bJ, DMat{F.Lval + c.lval, c.bJ, 1}, bs,
+                         EpiScatterRed{iline + c.item_off, F.Uidx + c.cols, s, b, W});
+  } else {
+    tsgemm_stage_b<NT, NMAX>(c.bJ, c.ncol, DMat{F.Lval + c.lval, 1, c.bJ}, bs);
+    cta_tsgemm<NT, NMAX>(c.n_items, c.ncol, c.bJ, DMat{F.Uval + c.uval, c.bJ, 1}, bs,
+                         EpiScatterRed{iline + c.item_off, F.Lidx + c.rows, s, b, W});
+  }
+  __syncthreads();
+}
+
 template <int SIDE>
 __device__ void side_gemms(const DevFactor &F, int s, int e, int b, const Contrib *C, int nc, const LineMap &M,
                            double *W, double *gs) {
   for (int a = 0; a < nc; ++a) {
     const Contrib &c = C[a];
     if (c.n_items == 0 || c.ncol == 0) continue;
-    if (SIDE == 0) {
-      EpiScatter<0> ep{F.Lidx + c.rows, F.Uidx + c.cols, s, e, b, M, W};
-      cta_dgemm_epi<NT>(c.n_items, c.ncol, c.bJ, DMat{F.Lval + c.lval, c.bJ, 1}, DMat{F.Uval + c.uval, 1, c.bJ},
-                        ep, gs);
-    } else {
-      EpiScatter<1> ep{F.Uidx + c.cols, F.Lidx + c.rows, s, e, b, M, W};
-      cta_dgemm_epi<NT>(c.n_items, c.ncol, c.bJ, DMat{F.Uval + c.uval, c.bJ, 1}, DMat{F.Lval + c.lval, 1, c.bJ},
-                        ep, gs);
-    }
+    if (c.ncol <= 64) contrib_tsgemm<SIDE, 64>(F, s, e, b, c, M, W, gs);
+    else contrib_tsgemm<SIDE, 128>(F, s, e, b, c, M, W, gs);
   }
 }
 
@@ -794,10 +837,34 @@ __device__ double side_flops(const Contrib *C, int nc) {
 // native global fp64 reductions (a-5) on any idle CTA; the CTA that completes the last
 // part runs a-6..a-1 (finish_block).  Same values as the one-CTA path up to the
 // summation order (R13).
-constexpr int MAX_PARTS = 32;          // per block (both sides)
 
 __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
                              const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops);
+
+// the destination line of every item of one side, into the global pool (split wide blocks)
+template <int SIDE>
+__device__ bool item_lines(const DevFactor &F, int K, int s, int e, const Contrib *C, int nc, int T, const LineMap &M,
+                           Shared &S, int **out) {
+  const int tid = threadIdx.x;
+  const int32_t *cidx = SIDE == 0 ? F.Lidx : F.Uidx;
+  const int64_t d = ((int64_t)T + 1) / 2 + 1;
+  if (tid == 0) S.off[3] = atomicAdd(&F.ctrl[CS * CTRL_HPOOL], (unsigned long long)d);
+  __syncthreads();
+  const unsigned long long o = S.off[3];
+  __syncthreads();
+  if (o + d > (unsigned long long)F.hpool_cap) { if (tid == 0) raise_abort(F, DEV_OVF_HPOOL, K); return false; }
+  int *il = (int *)(F.hpool + o);
+  int a = contrib_of(C, nc, tid < T ? tid : 0);
+  for (int t = tid; t < T; t += NT) {
+    while (a + 1 < nc && C[a + 1].item_off <= t) ++a;
+    const int i = t - C[a].item_off;
+    const int key = cidx[(SIDE == 0 ? C[a].rows : C[a].cols) + i];
+    il[t] = (SIDE == 0 && key < e) ? key - s : M(key);
+  }
+  __syncthreads();
+  *out = il;
+  return true;
+}
 
 __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned char *smem, uint64_t *mbar,
                               unsigned &mphase) {
@@ -830,7 +897,8 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   if (tid == 0) {
     const long long idle = (long long)ld_vol64(&F.ctrl[CS * CTRL_QTAIL]) - (long long)ld_vol64(&F.ctrl[CS * CTRL_QHEAD]);
     const int wide_ = b > 16 || maxbJ > 16;
-    S.cnt[3] = (!wide_ && F.heavy_T > 0 && TL + TU >= F.heavy_T && idle >= F.heavy_idle) ? 1 : 0;
+    S.cnt[3] = (F.heavy_T > 0 && idle >= F.heavy_idle &&
+                (wide_ ? (S.sflops[0] + S.sflops[1] >= F.wide_flops) : (TL + TU >= F.heavy_T))) ? 1 : 0;
   }
   __syncthreads();
   const bool heavy = S.cnt[3] != 0;
@@ -840,17 +908,21 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   SideState RL, RU;
   const bool wide = b > 16 || maxbJ > 16;
   double *gs = nullptr;
-  if (wide) {
-    gs = (double *)balloc_top(A, (int64_t)DGEMM_SMEM_DOUBLES * 8);
+  if (wide) {   // staging of the contributors' B operands (b_J <= 128 rows of TsB<128>::LDB)
+    gs = (double *)balloc_top(A, (int64_t)max(maxbJ, 1) * TsB<128>::LDB * 8);
     OVF_CHECK();
   }
   if (!side_prepare<0>(F, K, s, e, b, CL, nLc, TL, aL0, aLe, aL1, A, S, RL)) return;
   PROF(2);
+  int *ilineL = nullptr, *ilineU = nullptr;
+  if (heavy && wide) {   // the line of every item, so that the helpers need no line map
+    if (!item_lines<0>(F, K, s, e, CL, nLc, TL, RL.M, S, &ilineL)) return;
+  }
   // the pos-map candidate path (key ranges wider than the shared bitmap) keeps its line map
   // in a per-CTA global array that the other side's preparation reuses: apply this side's
   // updates first
   bool l_done = false;
-  if (!RL.sorted) {
+  if (!RL.sorted && !(heavy && wide)) {
     if (wide) side_gemms<0>(F, s, e, b, CL, nLc, RL.M, RL.W, gs);
     else if (heavy) side_items<0, true>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
     else side_items<0, false>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
@@ -859,8 +931,11 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   }
   if (!side_prepare<1>(F, K, s, e, b, CU, nUc, TU, aU0, aU0, aU1, A, S, RU)) return;
   PROF(3);
+  if (heavy && wide) {
+    if (!item_lines<1>(F, K, s, e, CU, nUc, TU, RU.M, S, &ilineU)) return;
+  }
 
-  if (heavy && RL.sorted && RU.sorted) {
+  if (heavy && (wide || (RL.sorted && RU.sorted))) {
     // publish the context and the part tasks; this CTA is free afterwards
 #ifdef BILU_PROFILE
     if (tid == 0 && g_blkprof) { g_blkprof[32 * (size_t)K + 19] = gtimer(); g_blkprof[32 * (size_t)K + 20] = ~0ull; }
@@ -873,8 +948,13 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     Contrib *gCU = gCL + nLc;
     for (int x = tid; x < nLc; x += NT) gCL[x] = CL[x];
     for (int x = tid; x < nUc; x += NT) gCU[x] = CU[x];
-    const int pL = min(MAX_PARTS / 2, (TL + F.part_items - 1) / F.part_items);
-    const int pU = min(MAX_PARTS / 2, (TU + F.part_items - 1) / F.part_items);
+    int pL = min(MAX_PARTS / 2, (TL + F.part_items - 1) / F.part_items);
+    int pU = min(MAX_PARTS / 2, (TU + F.part_items - 1) / F.part_items);
+    if (wide) {   // parts = flop-balanced contributor ranges
+      pL = (int)min((double)min(MAX_PARTS / 2, nLc), ceil(S.sflops[0] / F.wide_part_flops));
+      pU = (int)min((double)min(MAX_PARTS / 2, nUc), ceil(S.sflops[1] / F.wide_part_flops));
+      pL = max(pL, nLc > 0 ? 1 : 0); pU = max(pU, nUc > 0 ? 1 : 0);
+    }
     __syncthreads();
     if (tid == 0) {
       const unsigned long long h = atomicAdd(&F.ctrl[CS * CTRL_HCTX], 1ull);
@@ -884,6 +964,27 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
         X.K = K; X.nc[0] = nLc; X.nc[1] = nUc; X.T[0] = TL; X.T[1] = TU; X.np[0] = pL; X.np[1] = pU;
         X.C[0] = gCL; X.C[1] = gCU; X.R[0] = RL; X.R[1] = RU; X.flops = flops;
         X.R[0].M.bm = RL.gbm; X.R[0].M.pre = RL.gpre; X.R[1].M.bm = RU.gbm; X.R[1].M.pre = RU.gpre;
+        X.wide = wide ? 1 : 0;
+        X.iline[0] = ilineL; X.iline[1] = ilineU;
+        if (wide) {
+          for (int sd = 0; sd < 2; ++sd) {
+            const Contrib *Cs = sd ? CU : CL;
+            const int nc = sd ? nUc : nLc, np = sd ? pU : pL;
+            const double tot = S.sflops[sd];
+            int a = 0;
+            double acc = 0.0;
+            X.cb[sd][0] = 0;
+            for (int p = 1; p < np; ++p) {
+              const double goal = tot * p / np;
+              while (a < nc && acc + 0.5 * 2.0 * Cs[a].bJ * (double)Cs[a].n_items * Cs[a].ncol < goal) {
+                acc += 2.0 * Cs[a].bJ * (double)Cs[a].n_items * Cs[a].ncol;
+                ++a;
+              }
+              X.cb[sd][p] = a;
+            }
+            X.cb[sd][np] = nc;
+          }
+        }
         X.left = pL + pU;
         __threadfence();
         const unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], (unsigned long long)(pL + pU));
@@ -933,10 +1034,41 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
   const int per = (T + np - 1) / np;
   const int t0 = min(T, pp * per), t1 = min(T, t0 + per);
   const SideState &R = X.R[side];
-  // the contributor descriptors of this side, staged in shared memory
-  Contrib *C = (Contrib *)smem;
   const int nc = X.nc[side];
-  const bool cs = (int64_t)nc * (int64_t)sizeof(Contrib) <= (int64_t)F.smem_bytes;
+  Contrib *C = (Contrib *)smem;
+  bool cs = false;
+  if (X.wide) {
+    // contributors [cb[pp], cb[pp+1]) of this side: one DMMA product each, reductions into W
+    const int a0 = X.cb[side][pp], a1 = X.cb[side][pp + 1];
+    int mb = 0;
+    for (int a = a0; a < a1; ++a) mb = max(mb, X.C[side][a].bJ);
+    // B staging: shared memory when it fits, else this CTA's global workspace
+    double *bs = (int64_t)mb * TsB<128>::LDB * 8 <= (int64_t)F.smem_bytes ? (double *)smem
+                                                                          : F.work + (size_t)blockIdx.x * F.work_per_cta;
+#ifdef BILU_PROFILE
+    if (tid == 0 && g_blkprof) {
+      atomicMin(&g_blkprof[32 * (size_t)K + 20], gtimer());
+      atomicAdd(&g_blkprof[32 * (size_t)K + 22], 1ull);
+    }
+#endif
+    for (int a = a0; a < a1; ++a) {
+      const Contrib c = X.C[side][a];
+      if (c.n_items == 0 || c.ncol == 0) continue;
+      if (side == 0) {
+        if (c.ncol <= 64) contrib_tsgemm_red<0, 64>(F, s, b, c, X.iline[0], R.W, bs);
+        else contrib_tsgemm_red<0, 128>(F, s, b, c, X.iline[0], R.W, bs);
+      } else {
+        if (c.ncol <= 64) contrib_tsgemm_red<1, 64>(F, s, b, c, X.iline[1], R.W, bs);
+        else contrib_tsgemm_red<1, 128>(F, s, b, c, X.iline[1], R.W, bs);
+      }
+    }
+#ifdef BILU_PROFILE
+    __syncthreads();
+    if (tid == 0 && g_blkprof) atomicMax(&g_blkprof[32 * (size_t)K + 21], gtimer());
+#endif
+  } else {
+  // the contributor descriptors of this side, staged in shared memory
+  cs = (int64_t)nc * (int64_t)sizeof(Contrib) <= (int64_t)F.smem_bytes;
   if (cs) for (int x = tid; x < nc; x += NT) C[x] = X.C[side][x];
   __syncthreads();
 #ifdef BILU_PROFILE
@@ -956,6 +1088,7 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
     atomicAdd(&g_blkprof[32 * (size_t)K + 23], (unsigned long long)(clock64() - _pc0));   // part cycles
   }
 #endif
+  }
   __threadfence();
   __syncthreads();
   if (tid == 0) S.piv = atomicSub(&X.left, 1);
@@ -981,7 +1114,7 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
     __syncthreads();
     WL = sWL; WU = sWU; rowOf = sR; colOf = sC;
   }
-  finish_block(F, K, S, A, WL, WU, rowOf, colOf, nR, nC, true, true, X.flops);
+  finish_block(F, K, S, A, WL, WU, rowOf, colOf, nR, nC, X.R[0].sorted, X.R[1].sorted, X.flops);
 }
 
 // a-6 .. a-1 of block K once W_L (pivot block + candidate rows) and W_U are complete
@@ -991,10 +1124,17 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
   PROF_T0C
 #define OVF_CHECK() do { if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; } } while (0)
+  // wide blocks: shared staging of D_K for the scaling products, reserved first so that it
+  // stays in shared memory
+  double *gsc = nullptr;
+  if (b > 16) {
+    gsc = (double *)balloc_top(A, (int64_t)b * (b <= 64 ? TsB<64>::LDB : TsB<128>::LDB) * 8);
+    OVF_CHECK();
+  }
   // ---------------- a-6: D_K = P_K^{-1}, Gauss-Jordan with partial pivoting (column-major P)
-  double *P = (double *)balloc(A, (int64_t)b * b * 8);
+  double *P = (double *)balloc(A, (int64_t)b * b * 8 * (b > 8 ? 2 : 1));
   int *ipiv = (int *)balloc(A, (int64_t)b * 4);
-  double *fcol = (double *)balloc(A, (int64_t)b * 8);
+  double *fcol = (double *)balloc(A, (int64_t)b * 8 * 3);
   OVF_CHECK();
   for (int i = tid; i < b * b; i += NT) {
     int rr = i % b, cc = i / b;
@@ -1064,53 +1204,70 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     __syncthreads();
     singular = S.piv != 0;
   } else {
+    // all warps; column j owned by warp j % NW (lanes over rows); the pivot column of step k
+    // is read from a double buffer written by its owner at the end of step k-1, so one CTA
+    // barrier per step suffices (P_K column-major in shared memory)
+    double *cbuf = fcol;                         // 2 x b doubles
+    if (wid == 0) for (int i = lane; i < b; i += 32) cbuf[i] = P[i];
+    __syncthreads();
+    bool sing = false;
     for (int k = 0; k < b; ++k) {
-      if (wid == 0) {
-        double best = -1.0; int bi = k;
-        for (int i = k + lane; i < b; i += 32) {
-          double v = fabs(P[i + (int64_t)k * b]);
-          if (v > best) { best = v; bi = i; }
-        }
+      const double *cb = cbuf + (k & 1) * b;
+      double best = -1.0; int bi = k;
+      for (int i = k + lane; i < b; i += 32) {
+        const double v = fabs(cb[i]);
+        if (v > best) { best = v; bi = i; }
+      }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          double ob = __shfl_down_sync(0xffffffffu, best, o);
-          int oi = __shfl_down_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, o);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      best = __shfl_sync(0xffffffffu, best, 0);
+      bi = __shfl_sync(0xffffffffu, bi, 0);
+      if (best == 0.0) { sing = true; break; }     // identical decision in every warp
+      if (tid == 0) ipiv[k] = bi;
+      const double d = 1.0 / cb[bi];
+      double *nb_ = cbuf + ((k + 1) & 1) * b;
+      for (int j = wid; j < b; j += NW) {
+        double *pc = P + (int64_t)j * b;
+        if (bi != k && lane == 0) { const double t = pc[k]; pc[k] = pc[bi]; pc[bi] = t; }
+        __syncwarp();
+        const double pr = (j == k) ? d : pc[k] * d;
+        for (int i = lane; i < b; i += 32) {
+          if (i == k) continue;
+          const double f = (i == bi) ? cb[k] : cb[i];          // column k after the row swap
+          pc[i] = ((j == k) ? 0.0 : pc[i]) - f * pr;
         }
-        if (lane == 0) { S.piv = bi; S.pivd = best; ipiv[k] = bi; }
+        __syncwarp();
+        if (lane == 0) pc[k] = pr;
+        __syncwarp();
+        if (j == k + 1) for (int i = lane; i < b; i += 32) nb_[i] = pc[i];
       }
       __syncthreads();
-      if (S.pivd == 0.0) { singular = true; break; }
-      const int pv = S.piv;
-      if (pv != k)
-        for (int j = tid; j < b; j += NT) {
-          double t = P[k + (int64_t)j * b]; P[k + (int64_t)j * b] = P[pv + (int64_t)j * b]; P[pv + (int64_t)j * b] = t;
+    }
+    if (!sing) {
+      // undo the row interchanges as column interchanges, in reverse order: composite map
+      if (tid == 0) {
+        for (int j = 0; j < b; ++j) fcol[2 * b + j] = j;
+        for (int k = b - 1; k >= 0; --k) {
+          const int pv = ipiv[k];
+          if (pv != k) { const double t = fcol[2 * b + k]; fcol[2 * b + k] = fcol[2 * b + pv]; fcol[2 * b + pv] = t; }
         }
+      }
       __syncthreads();
-      const double d = 1.0 / P[k + (int64_t)k * b];
-      for (int i = tid; i < b; i += NT) fcol[i] = P[i + (int64_t)k * b];
-      __syncthreads();
+      double *Q = P + (int64_t)b * b;              // permuted copy, then back
       for (int it = tid; it < b * b; it += NT) {
         const int i = it % b, j = it / b;
-        const double pr = (j == k) ? d : P[k + (int64_t)j * b] * d;
-        if (i == k) continue;
-        const double base = (j == k) ? 0.0 : P[i + (int64_t)j * b];
-        P[i + (int64_t)j * b] = base - fcol[i] * pr;
+        Q[it] = P[i + (int64_t)(int)fcol[2 * b + j] * b];
       }
       __syncthreads();
-      for (int j = tid; j < b; j += NT) P[k + (int64_t)j * b] = (j == k) ? d : P[k + (int64_t)j * b] * d;
-      __syncthreads();
+      for (int it = tid; it < b * b; it += NT) P[it] = Q[it];
     }
-    if (!singular) {
-      for (int k = b - 1; k >= 0; --k) {
-        const int pv = ipiv[k];
-        if (pv != k)
-          for (int i = tid; i < b; i += NT) {
-            double t = P[i + (int64_t)k * b]; P[i + (int64_t)k * b] = P[i + (int64_t)pv * b]; P[i + (int64_t)pv * b] = t;
-          }
-        __syncthreads();
-      }
-    }
+    if (tid == 0) S.piv = sing ? 1 : 0;
+    __syncthreads();
+    singular = S.piv != 0;
   }
   if (singular) {
     if (tid == 0) raise_abort(F, DEV_BREAKDOWN, K);
@@ -1132,17 +1289,27 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   OVF_CHECK();
   // wide blocks: the scaled candidates L_cand = W_L D_K and U_cand^T = Z^T D_K^T on the
   // FP64 tensor pipe (the trsm-equivalent of PAPER.md:788-790, 210-212)
-  double *Lsc = nullptr, *Usc = nullptr;
+  double *Lsc = nullptr, *Usc = nullptr, *Lmx = nullptr, *Umx = nullptr;
   if (b > 16) {
+    Lmx = (double *)balloc(A, (int64_t)nR * 8);
+    Umx = (double *)balloc(A, (int64_t)nC * 8);
     Lsc = (double *)balloc(A, (int64_t)nR * b * 8);
     Usc = (double *)balloc(A, (int64_t)nC * b * 8);
-    const int sv_stop = A.stop;
-    const int64_t sv_gtop = A.gtop;
-    double *gs = (double *)balloc_top(A, (int64_t)DGEMM_SMEM_DOUBLES * 8);
-    OVF_CHECK();
-    cta_dgemm<NT>(nR, b, b, 1.0, DMat{WL + (int64_t)b * b, b, 1}, DMat{P, 1, b}, 0.0, Lsc, b, 1, gs);
-    cta_dgemm<NT>(nC, b, b, 1.0, DMat{WU, b, 1}, DMat{P, b, 1}, 0.0, Usc, b, 1, gs);
-    A.stop = sv_stop; A.gtop = sv_gtop;   // release the staging scratch
+    double *gs = gsc;
+    if (b <= 64) {
+      tsgemm_stage_b<NT, 64>(b, b, DMat{P, 1, b}, gs);
+      cta_tsgemm<NT, 64>(nR, b, b, DMat{WL + (int64_t)b * b, b, 1}, gs, EpiAxpby{1.0, 0.0, Lsc, b, 1}, Lmx);
+      __syncthreads();
+      tsgemm_stage_b<NT, 64>(b, b, DMat{P, b, 1}, gs);
+      cta_tsgemm<NT, 64>(nC, b, b, DMat{WU, b, 1}, gs, EpiAxpby{1.0, 0.0, Usc, b, 1}, Umx);
+    } else {
+      tsgemm_stage_b<NT, 128>(b, b, DMat{P, 1, b}, gs);
+      cta_tsgemm<NT, 128>(nR, b, b, DMat{WL + (int64_t)b * b, b, 1}, gs, EpiAxpby{1.0, 0.0, Lsc, b, 1}, Lmx);
+      __syncthreads();
+      tsgemm_stage_b<NT, 128>(b, b, DMat{P, b, 1}, gs);
+      cta_tsgemm<NT, 128>(nC, b, b, DMat{WU, b, 1}, gs, EpiAxpby{1.0, 0.0, Usc, b, 1}, Umx);
+    }
+    __syncthreads();
   }
   for (int i = tid; i < nR; i += NT) {
     double *w = WL + (int64_t)(b + i) * b;
@@ -1178,8 +1345,7 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
 #pragma unroll
       for (int c = 0; c < 16; ++c) if (c < b) w[c] = l[c];
     } else {
-      const double *l = Lsc + (int64_t)i * b;
-      for (int c = 0; c < b; ++c) mx = fmax(mx, fabs(l[c]));
+      mx = Lmx[i];
     }
     const int keep = mx > tau;
     keepR[i] = keep;
@@ -1200,8 +1366,7 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     const double *z = WU + (int64_t)j * b;
     double mx = 0.0;
     if (b > 16) {
-      const double *u = Usc + (int64_t)j * b;
-      for (int rr = 0; rr < b; ++rr) mx = fmax(mx, fabs(u[rr]));
+      mx = Umx[j];
     } else if (b <= 8) {
       double zr[8];
 #pragma unroll

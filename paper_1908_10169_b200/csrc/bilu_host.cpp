@@ -428,7 +428,7 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   F.adj_ptr = h->d_adj_ptr; F.adj = h->d_adj;
   ALLOC(F.pending, n_blocks);
   // heavy-block splitting: contexts, part tasks in the queue
-  F.hctx_cap = std::max<int64_t>(256, n_blocks / 4);
+  F.hctx_cap = std::max<int64_t>(256, n_blocks);          // a block is split at most once
   F.qcap = (int64_t)n_blocks + F.hctx_cap * bilu_max_parts();
   ALLOC(F.queue, F.qcap);
   {
@@ -443,6 +443,10 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   if (const char *ht = getenv("BILU_HEAVY_T")) F.heavy_T = atoi(ht);
   F.heavy_idle = 8;
   F.part_items = 512;
+  F.wide_flops = 4e6;
+  F.wide_part_flops = 2e6;
+  if (const char *wf = getenv("BILU_WIDE_FLOPS")) F.wide_flops = atof(wf);
+  if (const char *wp = getenv("BILU_WIDE_PART_FLOPS")) F.wide_part_flops = atof(wp);
   if (const char *pi = getenv("BILU_PART_ITEMS")) F.part_items = std::max(64, atoi(pi));
   if (const char *hi = getenv("BILU_HEAVY_IDLE")) F.heavy_idle = atoi(hi);
   ALLOC(F.ctrl, CTRL_COUNT * CS);
@@ -850,7 +854,7 @@ static bilu_status run_phase(bilu_ctx *h, Phase ph, bilu_factor_stats &S, unsign
       case DEV_OVF_HPOOL:
         h->hpool_cap = std::max<int64_t>(2 * h->hpool_cap, (int64_t)ctrl[CTRL_HPOOL] + (int64_t)ctrl[CTRL_HPOOL] / 4);
         break;
-      case DEV_OVF_HCTX: F.heavy_T *= 2; break;   // fewer split blocks
+      case DEV_OVF_HCTX: F.heavy_T *= 2; F.wide_flops *= 2; break;   // fewer split blocks
       default: set_err(h, "bilu_factor: device list overflow (code %d, block %llu)", code, ctrl[CTRL_ERRBLK]); return BILU_ERR_OOM;
     }
   }

@@ -107,6 +107,8 @@ struct DevFactor {
   int heavy_T;                          // item count from which a block is split (0 = never)
   int heavy_idle;                       // ... if at least this many CTAs are idle
   int part_items;                       // items per update-part task
+  double wide_flops;                    // blocks wider than 16 are split from this many update flops
+  double wide_part_flops;               // ... into parts of about this many flops
   int smem_bytes;
   double tau, near_rel;
   int exp;                              // experiment switches (diagnostics only)

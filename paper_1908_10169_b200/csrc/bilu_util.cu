@@ -57,7 +57,38 @@ __global__ void __launch_bounds__(256) diag_dgemm_kernel(int M, int N, int K, do
   cta_dgemm<256>(M, N, K, alpha, DMat{A + b * sa, ars, acs}, DMat{B + b * sb, brs, bcs}, beta, C + b * sc, crs,
                  ccs, sm);
 }
+template <int NMAX>
+__global__ void __launch_bounds__(256) diag_tsgemm_kernel(int M, int N, int K, double alpha, const double *A,
+                                                          int64_t ars, int64_t acs, const double *B, int64_t brs,
+                                                          int64_t bcs, double beta, double *C, int64_t crs,
+                                                          int64_t ccs, int64_t sa, int64_t sb, int64_t sc) {
+  extern __shared__ double bsm[];
+  const int b = blockIdx.x;
+  tsgemm_stage_b<256, NMAX>(K, N, DMat{B + b * sb, brs, bcs}, bsm);
+  cta_tsgemm<256, NMAX>(M, N, K, DMat{A + b * sa, ars, acs}, bsm, EpiAxpby{alpha, beta, C + b * sc, crs, ccs});
+}
 }  // namespace bilu
+
+// tall-skinny variant (K, N <= 128): mode 1 of bilu_diag_dgemm
+extern "C" int bilu_diag_tsgemm(int M, int N, int K, double alpha, const double *A, int64_t ars, int64_t acs,
+                                const double *B, int64_t brs, int64_t bcs, double beta, double *C, int64_t crs,
+                                int64_t ccs, int batch, int64_t sa, int64_t sb, int64_t sc, void *stream) {
+  if (M < 0 || N < 0 || K < 0 || batch < 1 || N > 128 || K > 128) return 1;
+  if (M == 0 || N == 0) return 0;
+  if (!A || !B || !C) return 1;
+  if (N <= 64) {
+    const int smem = K * bilu::TsB<64>::LDB * 8;
+    cudaFuncSetAttribute(bilu::diag_tsgemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bilu::diag_tsgemm_kernel<64><<<batch, 256, smem, (cudaStream_t)stream>>>(M, N, K, alpha, A, ars, acs, B, brs,
+                                                                              bcs, beta, C, crs, ccs, sa, sb, sc);
+  } else {
+    const int smem = K * bilu::TsB<128>::LDB * 8;
+    cudaFuncSetAttribute(bilu::diag_tsgemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bilu::diag_tsgemm_kernel<128><<<batch, 256, smem, (cudaStream_t)stream>>>(M, N, K, alpha, A, ars, acs, B, brs,
+                                                                               bcs, beta, C, crs, ccs, sa, sb, sc);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
 
 extern "C" int bilu_diag_dgemm(int M, int N, int K, double alpha, const double *A, int64_t ars, int64_t acs,
                                const double *B, int64_t brs, int64_t bcs, double beta, double *C, int64_t crs,

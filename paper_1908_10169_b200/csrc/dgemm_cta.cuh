@@ -116,6 +116,82 @@ __device__ void cta_dgemm_epi(int M, int N, int K, DMat A, DMat B, Epi epi, doub
   __syncthreads();
 }
 
+// Tall-skinny product C[M x N] = A[M x K] * B[K x N] with K, N <= NMAX: B is staged once
+// in shared memory (Bs, K rows of ldb = NMAX + 4 doubles, zero-padded to NMAX columns) and
+// every warp streams its own 8-row tiles of A from global memory (one m8n8k4 A fragment
+// per k-step: lane (g, q) loads A[row g][k + q]), so many independent tiles are in flight
+// -- the shape of the Schur-update products (m rows of L_J x b_J) and of the panel
+// scaling W·D_K.  Callers stage B with tsgemm_stage_b; epi(i, j, acc) gets each element.
+template <int NMAX>
+struct TsB {
+  static constexpr int LDB = NMAX + 4;
+};
+
+// Bs[k * LDB + n] = B(k, n) for k < K, n < N, 0 for N <= n < NMAX.  CTA-wide; ends with a barrier.
+template <int NTH, int NMAX>
+__device__ void tsgemm_stage_b(int K, int N, DMat B, double *Bs) {
+  constexpr int LDB = TsB<NMAX>::LDB;
+  for (int e = threadIdx.x; e < K * NMAX; e += NTH) {
+    const int k = e / NMAX, n = e - k * NMAX;
+    Bs[k * LDB + n] = n < N ? B.p[k * B.rs + n * B.cs] : 0.0;
+  }
+  __syncthreads();
+}
+
+// rmax (optional): rmax[i] = max_j |C(i, j)| (every tile spans all N columns, so a 4-lane
+// shuffle reduction gives complete row maxima)
+template <int NTH, int NMAX, class Epi>
+__device__ void cta_tsgemm(int M, int N, int K, DMat A, const double *Bs, Epi epi, double *rmax = nullptr) {
+  constexpr int NWARP = NTH / 32, NF = NMAX / 8, LDB = TsB<NMAX>::LDB;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int nf = (N + 7) >> 3;
+  for (int m0 = wid * 8; m0 < M; m0 += NWARP * 8) {
+    const int row = m0 + g;
+    const bool rv = row < M;
+    const double *ar = A.p + (int64_t)(rv ? row : 0) * A.rs;
+    double acc[NF][2];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
+    // A fragments of 8 k-steps loaded together (independent loads in flight), then used
+    for (int kc = 0; kc < K; kc += 32) {
+      double a8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int kk = kc + 4 * u + q;
+        a8[u] = (rv && kk < K) ? ar[(int64_t)kk * A.cs] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int kk = kc + 4 * u + q;
+        if (kc + 4 * u >= K) break;                 // warp-uniform
+        const bool kv = kk < K;
+        const double *br = Bs + (kv ? kk : 0) * LDB + g;
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+          if (f < nf) dmma_8x8x4(acc[f][0], acc[f][1], a8[u], kv ? br[f * 8] : 0.0);
+      }
+    }
+    double mx = 0.0;
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+      if (f < nf)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = f * 8 + 2 * q + h;
+          if (rv && col < N) {
+            epi(row, col, acc[f][h]);
+            mx = fmax(mx, fabs(acc[f][h]));
+          }
+        }
+    if (rmax) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      if (rv && q == 0) rmax[row] = mx;
+    }
+  }
+}
+
 struct EpiAxpby {
   double alpha, beta; double *C; int64_t crs, ccs;
   __device__ __forceinline__ void operator()(int i, int j, double v) const {
