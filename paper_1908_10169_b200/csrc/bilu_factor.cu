@@ -897,11 +897,14 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   if (tid == 0) {
     const long long idle = (long long)ld_vol64(&F.ctrl[CS * CTRL_QTAIL]) - (long long)ld_vol64(&F.ctrl[CS * CTRL_QHEAD]);
     const int wide_ = b > 16 || maxbJ > 16;
-    S.cnt[3] = (F.heavy_T > 0 && idle >= F.heavy_idle &&
-                (wide_ ? (S.sflops[0] + S.sflops[1] >= F.wide_flops) : (TL + TU >= F.heavy_T))) ? 1 : 0;
+    const bool big = F.heavy_T > 0 && (wide_ ? (S.sflops[0] + S.sflops[1] >= F.wide_flops) : (TL + TU >= F.heavy_T));
+    // big blocks keep W in global memory (native fp64 reductions); they are split into
+    // parts only when CTAs are idle, else this CTA applies every part itself
+    S.cnt[3] = big ? ((idle >= F.heavy_idle ? 2 : 0) | (!(F.exp & 2) || idle >= F.heavy_idle ? 1 : 0)) : 0;
   }
   __syncthreads();
-  const bool heavy = S.cnt[3] != 0;
+  const bool heavy = (S.cnt[3] & 1) != 0;
+  const bool publish = (S.cnt[3] & 2) != 0;
   if (heavy) A.bottom_global = true;   // W and line maps in the global pool (read by the helpers)
 
   // ---------------- a-3 / a-4 for both sides
@@ -915,14 +918,14 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   if (!side_prepare<0>(F, K, s, e, b, CL, nLc, TL, aL0, aLe, aL1, A, S, RL)) return;
   PROF(2);
   int *ilineL = nullptr, *ilineU = nullptr;
-  if (heavy && wide) {   // the line of every item, so that the helpers need no line map
+  if (publish && wide) {   // the line of every item, so that the helpers need no line map
     if (!item_lines<0>(F, K, s, e, CL, nLc, TL, RL.M, S, &ilineL)) return;
   }
   // the pos-map candidate path (key ranges wider than the shared bitmap) keeps its line map
   // in a per-CTA global array that the other side's preparation reuses: apply this side's
   // updates first
   bool l_done = false;
-  if (!RL.sorted && !(heavy && wide)) {
+  if (!RL.sorted && !(publish && wide)) {
     if (wide) side_gemms<0>(F, s, e, b, CL, nLc, RL.M, RL.W, gs);
     else if (heavy) side_items<0, true>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
     else side_items<0, false>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
@@ -931,11 +934,11 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   }
   if (!side_prepare<1>(F, K, s, e, b, CU, nUc, TU, aU0, aU0, aU1, A, S, RU)) return;
   PROF(3);
-  if (heavy && wide) {
+  if (publish && wide) {
     if (!item_lines<1>(F, K, s, e, CU, nUc, TU, RU.M, S, &ilineU)) return;
   }
 
-  if (heavy && (wide || (RL.sorted && RU.sorted))) {
+  if (publish && (wide || (RL.sorted && RU.sorted))) {
     // publish the context and the part tasks; this CTA is free afterwards
 #ifdef BILU_PROFILE
     if (tid == 0 && g_blkprof) { g_blkprof[32 * (size_t)K + 19] = gtimer(); g_blkprof[32 * (size_t)K + 20] = ~0ull; }
