@@ -515,7 +515,9 @@ struct SideState {
   const unsigned *gbm; const int *gpre;   // global copies of the bitmap map (split blocks)
 };
 
-constexpr int MAX_PARTS = 32;          // per block (both sides)
+constexpr int MAX_PARTS = 32;          // update parts per block (both sides)
+constexpr int MAX_SPARTS = 32;         // scaling parts per block (wide split blocks)
+constexpr int TASK_STRIDE = MAX_PARTS + MAX_SPARTS;   // task = N + ctx * TASK_STRIDE + part
 
 // a split heavy block (see process_block)
 struct HeavyCtx {
@@ -527,6 +529,10 @@ struct HeavyCtx {
   int wide;                 // parts run per-contributor DMMA products over contributor ranges
   const int *iline[2];      // wide: destination line of every item of each side
   int cb[2][MAX_PARTS / 2 + 1];   // wide: contributor range of every part
+  // wide: scaling split (finish_block mode 1 -> scale parts -> mode 2)
+  double *Lsc, *Usc, *Lmx, *Umx;
+  int ns, left2;
+  int sortedR, sortedC;
 };
 
 // One side of block K (SIDE 0: block column of L incl. the pivot block; SIDE 1:
@@ -839,7 +845,8 @@ __device__ double side_flops(const Contrib *C, int nc) {
 // summation order (R13).
 
 __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
-                             const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops);
+                             const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops,
+                             HeavyCtx *X = nullptr, int mode = 0);
 
 // the destination line of every item of one side, into the global pool (split wide blocks)
 template <int SIDE>
@@ -958,6 +965,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
       pU = (int)min((double)min(MAX_PARTS / 2, nUc), ceil(S.sflops[1] / F.wide_part_flops));
       pL = max(pL, nLc > 0 ? 1 : 0); pU = max(pU, nUc > 0 ? 1 : 0);
     }
+    __threadfence();   // W, the line maps and the contributor copies written by every thread
     __syncthreads();
     if (tid == 0) {
       const unsigned long long h = atomicAdd(&F.ctrl[CS * CTRL_HCTX], 1ull);
@@ -993,7 +1001,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
         const unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], (unsigned long long)(pL + pU));
         if (slot + pL + pU > (unsigned long long)F.qcap) raise_abort(F, DEV_OVF_HCTX, K);
         else
-          for (int p = 0; p < pL + pU; ++p) st_vol(&F.queue[slot + p], F.N + (int)h * MAX_PARTS + p);
+          for (int p = 0; p < pL + pU; ++p) st_vol(&F.queue[slot + p], F.N + (int)h * TASK_STRIDE + p);
         S.off[1] = h;
       }
     }
@@ -1024,11 +1032,66 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
 #undef OVF_CHECK
 }
 
+// one scaling part of a wide split block: rows [r0, r1) of the candidates, L rows scaled by
+// D_K from the right, U columns from the left (the trsm-equivalent of PAPER.md:210-212),
+// with row maxima for the drop test; the CTA completing the last part finishes the block
+__device__ void run_scale_part(const DevFactor &F, HeavyCtx &X, int p, Shared &S, unsigned char *smem) {
+  const int tid = threadIdx.x;
+  const int K = X.K;
+  const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
+  const int nR = X.R[0].nU, nC = X.R[1].nU, tot = nR + nC;
+  const int per = (tot + X.ns - 1) / X.ns;
+  const int r0 = min(tot, p * per), r1 = min(tot, r0 + per);
+  const double *D = F.D + F.D_off[K];
+  double *bs = (double *)smem;
+  const double *WL = X.R[0].W, *WU = X.R[1].W;
+  // L rows [r0, min(r1, nR)): Lsc = W_L[b + i, :] D_K
+  if (r0 < nR) {
+    const int a = r0, z = min(r1, nR);
+    if (b <= 64) {
+      tsgemm_stage_b<NT, 64>(b, b, DMat{D, 1, b}, bs);
+      cta_tsgemm<NT, 64>(z - a, b, b, DMat{WL + (int64_t)(b + a) * b, b, 1}, bs,
+                         EpiAxpby{1.0, 0.0, X.Lsc + (int64_t)a * b, b, 1}, X.Lmx + a);
+    } else {
+      tsgemm_stage_b<NT, 128>(b, b, DMat{D, 1, b}, bs);
+      cta_tsgemm<NT, 128>(z - a, b, b, DMat{WL + (int64_t)(b + a) * b, b, 1}, bs,
+                          EpiAxpby{1.0, 0.0, X.Lsc + (int64_t)a * b, b, 1}, X.Lmx + a);
+    }
+    __syncthreads();
+  }
+  if (r1 > nR) {
+    const int a = max(r0, nR) - nR, z = r1 - nR;
+    if (b <= 64) {
+      tsgemm_stage_b<NT, 64>(b, b, DMat{D, b, 1}, bs);
+      cta_tsgemm<NT, 64>(z - a, b, b, DMat{WU + (int64_t)a * b, b, 1}, bs,
+                         EpiAxpby{1.0, 0.0, X.Usc + (int64_t)a * b, b, 1}, X.Umx + a);
+    } else {
+      tsgemm_stage_b<NT, 128>(b, b, DMat{D, b, 1}, bs);
+      cta_tsgemm<NT, 128>(z - a, b, b, DMat{WU + (int64_t)a * b, b, 1}, bs,
+                          EpiAxpby{1.0, 0.0, X.Usc + (int64_t)a * b, b, 1}, X.Umx + a);
+    }
+    __syncthreads();
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) S.piv = atomicSub(&X.left2, 1);
+  __syncthreads();
+  if (S.piv != 1) return;
+  __threadfence();
+  Bump A;
+  A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes;
+  A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
+  A.ovf = false; A.bottom_global = false;
+  finish_block(F, K, S, A, X.R[0].W, X.R[1].W, X.R[0].lineOf, X.R[1].lineOf, nR, nC, X.sortedR != 0,
+               X.sortedC != 0, X.flops, &X, 2);
+}
+
 // one part task: items of one side of a split heavy block; the CTA that completes the
 // last part finishes the block
 __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char *smem) {
   const int tid = threadIdx.x;
-  const int h = (task - F.N) / MAX_PARTS, p = (task - F.N) % MAX_PARTS;
+  const int h = (task - F.N) / TASK_STRIDE, p = (task - F.N) % TASK_STRIDE;
+  if (p >= MAX_PARTS) { run_scale_part(F, F.hctx[h], p - MAX_PARTS, S, smem); return; }
   HeavyCtx &X = F.hctx[h];
   const int K = X.K;
   const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
@@ -1117,12 +1180,14 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
     __syncthreads();
     WL = sWL; WU = sWU; rowOf = sR; colOf = sC;
   }
-  finish_block(F, K, S, A, WL, WU, rowOf, colOf, nR, nC, X.R[0].sorted, X.R[1].sorted, X.flops);
+  const int fmode = (X.wide && b > 16 && nR + nC >= F.scale_split) ? 1 : 0;
+  finish_block(F, K, S, A, WL, WU, rowOf, colOf, nR, nC, X.R[0].sorted, X.R[1].sorted, X.flops, &X, fmode);
 }
 
 // a-6 .. a-1 of block K once W_L (pivot block + candidate rows) and W_U are complete
 __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
-                             const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops) {
+                             const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops,
+                             HeavyCtx *X, int mode) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
   PROF_T0C
@@ -1134,8 +1199,13 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     gsc = (double *)balloc_top(A, (int64_t)b * (b <= 64 ? TsB<64>::LDB : TsB<128>::LDB) * 8);
     OVF_CHECK();
   }
+  // mode 0: a-6 .. a-1 here.  mode 1 (wide split block): a-6, then the scaling of the
+  // candidate rows / columns is published as parts.  mode 2: the parts are done, a-8 .. a-1.
+  double *P = nullptr;
+  if (mode == 2) goto scaled;
+  {
   // ---------------- a-6: D_K = P_K^{-1}, Gauss-Jordan with partial pivoting (column-major P)
-  double *P = (double *)balloc(A, (int64_t)b * b * 8 * (b > 8 ? 2 : 1));
+  P = (double *)balloc(A, (int64_t)b * b * 8 * (b > 8 ? 2 : 1));
   int *ipiv = (int *)balloc(A, (int64_t)b * 4);
   double *fcol = (double *)balloc(A, (int64_t)b * 8 * 3);
   OVF_CHECK();
@@ -1282,6 +1352,35 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   }
   flops += 2.0 * b * b * (double)b + 2.0 * b * b * (double)(nR + nC);
   PROF(5);
+  if (mode == 1) {
+    // scale parts: rows [r0, r1) of the nR L candidates followed by the nC U candidates;
+    // D_K is read back from F.D by every part (every thread's D writes fenced first)
+    __threadfence();
+    __syncthreads();
+    const int64_t d = (int64_t)(nR + nC) * (b + 1) + 4;
+    if (tid == 0) S.off[3] = atomicAdd(&F.ctrl[CS * CTRL_HPOOL], (unsigned long long)d);
+    __syncthreads();
+    if (S.off[3] + d > (unsigned long long)F.hpool_cap) { if (tid == 0) raise_abort(F, DEV_OVF_HPOOL, K); return; }
+    if (tid == 0) {
+      double *base = F.hpool + S.off[3];
+      X->Lsc = base; X->Usc = base + (int64_t)nR * b;
+      X->Lmx = base + (int64_t)(nR + nC) * b; X->Umx = X->Lmx + nR;
+      X->ns = min(MAX_SPARTS, max(1, (nR + nC + F.scale_rows - 1) / F.scale_rows));
+      X->left2 = X->ns;
+      X->flops = flops;
+      X->sortedR = sortedR; X->sortedC = sortedC;
+      __threadfence();
+      const unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], (unsigned long long)X->ns);
+      const int h = (int)(X - F.hctx);
+      if (slot + X->ns > (unsigned long long)F.qcap) raise_abort(F, DEV_OVF_HCTX, K);
+      else
+        for (int p2 = 0; p2 < X->ns; ++p2) st_vol(&F.queue[slot + p2], F.N + h * TASK_STRIDE + MAX_PARTS + p2);
+    }
+    __syncthreads();
+    return;
+  }
+  }
+scaled:
 
   // ---------------- a-7/a-8: scale, drop (R1-R3), compact
   // L rows: l = w D_K, kept iff max|l| > tau; the scaled row overwrites W_L's row
@@ -1293,7 +1392,9 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   // wide blocks: the scaled candidates L_cand = W_L D_K and U_cand^T = Z^T D_K^T on the
   // FP64 tensor pipe (the trsm-equivalent of PAPER.md:788-790, 210-212)
   double *Lsc = nullptr, *Usc = nullptr, *Lmx = nullptr, *Umx = nullptr;
-  if (b > 16) {
+  if (mode == 2) {
+    Lsc = X->Lsc; Usc = X->Usc; Lmx = X->Lmx; Umx = X->Umx;
+  } else if (b > 16) {
     Lmx = (double *)balloc(A, (int64_t)nR * 8);
     Umx = (double *)balloc(A, (int64_t)nC * 8);
     Lsc = (double *)balloc(A, (int64_t)nR * b * 8);
@@ -1817,7 +1918,7 @@ extern "C" cudaError_t bilu_launch_factor(const DevFactor &F, int grid, cudaStre
 }
 
 extern "C" int bilu_heavyctx_size() { return (int)sizeof(HeavyCtx); }
-extern "C" int bilu_max_parts() { return MAX_PARTS; }
+extern "C" int bilu_max_parts() { return TASK_STRIDE; }
 
 extern "C" cudaError_t bilu_factor_occupancy(int smem_bytes, int *blocks_per_sm) {
   cudaError_t err = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);

@@ -444,6 +444,10 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   F.heavy_idle = 8;
   F.part_items = 512;
   F.wide_flops = 4e6;
+  F.scale_split = 1024;
+  F.scale_rows = 384;
+  if (const char *ss = getenv("BILU_SCALE_SPLIT")) F.scale_split = atoi(ss);
+  if (const char *sr = getenv("BILU_SCALE_ROWS")) F.scale_rows = std::max(32, atoi(sr));
   F.wide_part_flops = 2e6;
   if (const char *wf = getenv("BILU_WIDE_FLOPS")) F.wide_flops = atof(wf);
   if (const char *wp = getenv("BILU_WIDE_PART_FLOPS")) F.wide_part_flops = atof(wp);

@@ -109,6 +109,8 @@ struct DevFactor {
   int part_items;                       // items per update-part task
   double wide_flops;                    // blocks wider than 16 are split from this many update flops
   double wide_part_flops;               // ... into parts of about this many flops
+  int scale_split;                      // wide split blocks: candidates from which the scaling is split
+  int scale_rows;                       // ... into parts of this many rows
   int smem_bytes;
   double tau, near_rel;
   int exp;                              // experiment switches (diagnostics only)
