@@ -689,7 +689,8 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
   } else {
     for (int x = tid; x < nU; x += NT) lineOf[base + x] = pre[x];
   }
-  for (int x = tid; x < nW * b; x += NT) W[x] = 0.0;
+  if (!A.bottom_global)                  // the global pool is zero at every launch
+    for (int x = tid; x < nW * b; x += NT) W[x] = 0.0;
   __syncthreads();
   // -- a-4: scatter Ã
   for (int64_t p = a0 + tid; p < a1; p += NT) {

@@ -120,7 +120,7 @@ struct bilu_ctx {
   // dynamic
   DevFactor F{};
   int grid = 0;
-  int64_t cap_val = 0, cap_idx = 0, work_per_cta = 0, hpool_cap = 0;
+  int64_t cap_val = 0, cap_idx = 0, work_per_cta = 0, hpool_cap = 0, hpool_dirty = 0;
   int pool_lc = 0, pool_uc = 0, pool_succ = 0;
   int64_t near_cap = 1 << 20;
   // results
@@ -551,6 +551,9 @@ static bilu_status ensure_aux(bilu_ctx *h) {
     dfree(h, F.hpool);
     CUDA_TRY(h, dalloc(h, &F.hpool, (size_t)h->hpool_cap));
     F.hpool_cap = h->hpool_cap;
+    // invariant: the pool is zero when a launch starts (split blocks' W need no zero fill)
+    CUDA_TRY(h, cudaMemsetAsync(F.hpool, 0, (size_t)h->hpool_cap * 8, h->stream));
+    h->hpool_dirty = 0;
   }
   if (F.work_per_cta != h->work_per_cta) {
     dfree(h, F.work);
@@ -801,6 +804,10 @@ static bilu_status run_phase(bilu_ctx *h, Phase ph, bilu_factor_stats &S, unsign
       F.dbg = (volatile int *)dp;
       h->dbg_host = (volatile int *)hp;
     }
+    if (h->hpool_dirty > 0) {   // re-zero what the previous launch used
+      CUDA_TRY(h, cudaMemsetAsync(F.hpool, 0, (size_t)std::min(h->hpool_dirty, F.hpool_cap) * 8, h->stream));
+      h->hpool_dirty = 0;
+    }
     CUDA_TRY(h, bilu_launch_factor(F, h->grid, h->stream));
     launches += 1;
     if (dbg_env) {
@@ -821,6 +828,7 @@ static bilu_status run_phase(bilu_ctx *h, Phase ph, bilu_factor_stats &S, unsign
     CUDA_TRY(h, cudaMemcpyAsync(h->ctrl_full, F.ctrl, sizeof(h->ctrl_full), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     for (int i = 0; i < CTRL_COUNT; ++i) ctrl[i] = h->ctrl_full[CS * i];
+    h->hpool_dirty = std::min<int64_t>((int64_t)ctrl[CTRL_HPOOL], F.hpool_cap);
     const int code = (int)ctrl[CTRL_ABORT];
     if (code == DEV_OK) {
       if (ctrl[CTRL_DONE] != (unsigned long long)F.n_target) {
