@@ -705,6 +705,134 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
   return true;
 }
 
+// a-3 / a-4 of both sides in lockstep (bitmap path on both sides): one pass per step over
+// the two sides' Ã entries and items, one prefix scan over the two bitmaps, so the two
+// sides' memory latencies overlap and the barriers are shared.  Same result as
+// side_prepare<0> followed by side_prepare<1>.  Returns false (nothing done) when either
+// side's key range needs the pos-map path.
+__device__ int prep_words(const Shared &S, int side, int e, const int32_t *arc, int64_t ae, int64_t a1) {
+  const int hi = max(max(e - 1, S.maxkey[side]), a1 > ae ? (arc[a1 - 1] >> 7) : e - 1);
+  return (hi - e + 1 + 31) >> 5;
+}
+
+__device__ bool prepare_both(const DevFactor &F, int K, int s, int e, int b, const Contrib *CL, int nLc, int TL,
+                             const Contrib *CU, int nUc, int TU, int64_t aL0, int64_t aLe, int64_t aL1, int64_t aU0,
+                             int64_t aU1, Bump &A, Shared &S, SideState &RL, SideState &RU, bool &ok) {
+  const int tid = threadIdx.x;
+  ok = true;
+  const int wL = prep_words(S, 0, e, F.AL_rc, aLe, aL1), wU = prep_words(S, 1, e, F.AU_rc, aU0, aU1);
+  if (wL > 8192 || wU > 8192) return false;
+  const int nAL = (int)(aL1 - aLe), nAU = (int)(aU1 - aU0);
+  unsigned *bm = (unsigned *)balloc_top(A, (int64_t)(wL + wU + 2) * 4);
+  int *pre = (int *)balloc_top(A, (int64_t)(wL + wU + 2) * 4);
+  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); ok = false; return true; }
+  unsigned *bmL = bm, *bmU = bm + wL;
+  for (int w = tid; w < wL + wU; w += NT) bm[w] = 0u;
+  __syncthreads();
+  // Ã entries of both sides, then the items of both sides
+  for (int x = tid; x < nAL + nAU; x += NT) {
+    if (x < nAL) { const int r = (F.AL_rc[aLe + x] >> 7) - e; atomicOr(&bmL[r >> 5], 1u << (r & 31)); }
+    else { const int r = (F.AU_rc[aU0 + (x - nAL)] >> 7) - e; atomicOr(&bmU[r >> 5], 1u << (r & 31)); }
+  }
+  {
+    int aL = 0, aU = 0;
+    for (int t0 = tid; t0 < TL + TU; t0 += 4 * NT) {
+      int r4[4], sd[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u * NT;
+        r4[u] = -1; sd[u] = 0;
+        if (t < TL) {
+          while (aL + 1 < nLc && CL[aL + 1].item_off <= t) ++aL;
+          const int i = t - CL[aL].item_off;
+          if (i >= CL[aL].n_cand_skip) r4[u] = F.Lidx[CL[aL].rows + i] - e;   // pivot rows excluded
+        } else if (t < TL + TU) {
+          const int tu = t - TL;
+          while (aU + 1 < nUc && CU[aU + 1].item_off <= tu) ++aU;
+          r4[u] = F.Uidx[CU[aU].cols + (tu - CU[aU].item_off)] - e;
+          sd[u] = 1;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r4[u] >= 0) atomicOr(&(sd[u] ? bmU : bmL)[r4[u] >> 5], 1u << (r4[u] & 31));
+    }
+  }
+  __syncthreads();
+  for (int w = tid; w < wL + wU; w += NT) pre[w] = __popc(bm[w]);
+  __syncthreads();
+  const int tot = cta_scan(pre, wL + wU, S.tmp);
+  const int nUL = wU > 0 ? pre[wL] : tot, nUU = tot - nUL;
+  // line maps: L lines start at b (pivot rows first); U prefix sums are offset by nUL
+  LineMap ML, MU;
+  ML.e = e; ML.base = b; ML.bm = bmL; ML.pre = pre; ML.words = wL; ML.pos = nullptr;
+  MU.e = e; MU.base = -nUL; MU.bm = bmU; MU.pre = pre + wL; MU.words = wU; MU.pos = nullptr;
+  const int nWL = b + nUL, nWU = nUU;
+  double *WL, *WU;
+  int *lineL, *lineU;
+  if (A.bottom_global) {
+    const int64_t wdL = (int64_t)nWL * b, ldL = ((int64_t)nWL + 2) / 2 + 1, mdL = (int64_t)wL + 2;
+    const int64_t wdU = (int64_t)nWU * b, ldU = ((int64_t)nWU + 2) / 2 + 1, mdU = (int64_t)wU + 2;
+    const int64_t d = wdL + ldL + mdL + wdU + ldU + mdU;
+    if (tid == 0) S.off[3] = atomicAdd(&F.ctrl[CS * CTRL_HPOOL], (unsigned long long)d);
+    __syncthreads();
+    const unsigned long long o = S.off[3];
+    __syncthreads();
+    if (o + d > (unsigned long long)F.hpool_cap) { if (tid == 0) raise_abort(F, DEV_OVF_HPOOL, K); ok = false; return true; }
+    WL = F.hpool + o;
+    lineL = (int *)(WL + wdL);
+    unsigned *gbmL = (unsigned *)(WL + wdL + ldL);
+    WU = WL + wdL + ldL + mdL;
+    lineU = (int *)(WU + wdU);
+    unsigned *gbmU = (unsigned *)(WU + wdU + ldU);
+    int *gpreL = (int *)(gbmL + wL + 1), *gpreU = (int *)(gbmU + wU + 1);
+    for (int w = tid; w < wL; w += NT) { gbmL[w] = bmL[w]; gpreL[w] = pre[w]; }
+    for (int w = tid; w < wU; w += NT) { gbmU[w] = bmU[w]; gpreU[w] = pre[wL + w]; }
+    RL.gbm = gbmL; RL.gpre = gpreL; RU.gbm = gbmU; RU.gpre = gpreU;   // global copies (same bases)
+  } else {
+    WL = (double *)balloc(A, (int64_t)nWL * b * 8);
+    lineL = (int *)balloc(A, (int64_t)(nWL + 1) * 4);
+    WU = (double *)balloc(A, (int64_t)nWU * b * 8);
+    lineU = (int *)balloc(A, (int64_t)(nWU + 1) * 4);
+    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); ok = false; return true; }
+  }
+  for (int x = tid; x < b; x += NT) lineL[x] = s + x;
+  for (int w = tid; w < wL + wU; w += NT) {
+    const bool u = w >= wL;
+    unsigned m = bm[w];
+    int at = u ? pre[w] - nUL : b + pre[w];
+    int *lo = u ? lineU : lineL;
+    const int wb = u ? w - wL : w;
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      lo[at++] = e + (wb << 5) + bit;
+      m &= m - 1;
+    }
+  }
+  if (!A.bottom_global) {
+    for (int x = tid; x < nWL * b; x += NT) WL[x] = 0.0;
+    for (int x = tid; x < nWU * b; x += NT) WU[x] = 0.0;
+  }
+  __syncthreads();
+  // a-4: scatter Ã's block column (incl. the pivot block) and block row
+  const int nL0 = (int)(aL1 - aL0);
+  for (int x = tid; x < nL0 + nAU; x += NT) {
+    if (x < nL0) {
+      const int rc = F.AL_rc[aL0 + x], key = rc >> 7;
+      const int w = key < e ? key - s : ML(key);
+      WL[(int64_t)w * b + (rc & 127)] = F.AL_val[aL0 + x];
+    } else {
+      const int64_t p = aU0 + (x - nL0);
+      const int rc = F.AU_rc[p], key = rc >> 7;
+      WU[(int64_t)MU(key) * b + (rc & 127)] = F.AU_val[p];
+    }
+  }
+  __syncthreads();
+  RL.W = WL; RL.lineOf = lineL; RL.nU = nUL; RL.M = ML; RL.sorted = true;
+  RU.W = WU; RU.lineOf = lineU; RU.nU = nUU; RU.M = MU; RU.sorted = true;
+  return true;
+}
+
 // a-5 for the items [t0, t1) of one side: W -= L_J Ũ_J, "gather ... GEMM ... scatter"
 // (Fig. 2): one thread per item (a row of L_J >= s_K, resp. a column of
 // Ũ_J >= e_K); contributions are added atomically (shared-memory W) or with native
@@ -923,7 +1051,11 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     gs = (double *)balloc_top(A, (int64_t)max(maxbJ, 1) * TsB<128>::LDB * 8);
     OVF_CHECK();
   }
-  if (!side_prepare<0>(F, K, s, e, b, CL, nLc, TL, aL0, aLe, aL1, A, S, RL)) return;
+  bool both_ok = true;
+  const bool both = !(F.exp & 4) &&
+                    prepare_both(F, K, s, e, b, CL, nLc, TL, CU, nUc, TU, aL0, aLe, aL1, aU0, aU1, A, S, RL, RU, both_ok);
+  if (!both_ok) return;
+  if (!both && !side_prepare<0>(F, K, s, e, b, CL, nLc, TL, aL0, aLe, aL1, A, S, RL)) return;
   PROF(2);
   int *ilineL = nullptr, *ilineU = nullptr;
   if (publish && wide) {   // the line of every item, so that the helpers need no line map
@@ -933,14 +1065,14 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   // in a per-CTA global array that the other side's preparation reuses: apply this side's
   // updates first
   bool l_done = false;
-  if (!RL.sorted && !(publish && wide)) {
+  if (!both && !RL.sorted && !(publish && wide)) {
     if (wide) side_gemms<0>(F, s, e, b, CL, nLc, RL.M, RL.W, gs);
     else if (heavy) side_items<0, true>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
     else side_items<0, false>(F, s, e, CL, nLc, 0, TL, b, RL.M, RL.W);
     __syncthreads();
     l_done = true;
   }
-  if (!side_prepare<1>(F, K, s, e, b, CU, nUc, TU, aU0, aU0, aU1, A, S, RU)) return;
+  if (!both && !side_prepare<1>(F, K, s, e, b, CU, nUc, TU, aU0, aU0, aU1, A, S, RU)) return;
   PROF(3);
   if (publish && wide) {
     if (!item_lines<1>(F, K, s, e, CU, nUc, TU, RU.M, S, &ilineU)) return;
