@@ -414,8 +414,12 @@ __global__ void __launch_bounds__(1024) merge_offsets_kernel(MergeArgs M) {
 }
 
 // ---------------------------------------------------------------- M4: arithmetic
-// Sorted union of the members' kept indices >= e_k, written to out[0..u).
-// Returns the number of distinct keys (must equal the test's union size).
+// Sorted union of the members' kept indices >= e_k, written to out[0..u): the members'
+// suffixes are concatenated (each sorted); an element is "first" if no earlier member's
+// suffix contains it; its rank in the union is the number of first elements smaller than it,
+// summed over the suffixes via a prefix scan of the first-flags and binary searches.
+// Returns the number of distinct keys (must equal the test's union size), -1 if the
+// buffers are too small.
 __device__ int build_union(const MergeArgs &M, int a, int k, bool rows, int *keys, int *flags, int cap,
                            int *s_cnt, int *s_tmp, int *out) {
   const int tid = threadIdx.x;
@@ -431,9 +435,9 @@ __device__ int build_union(const MergeArgs &M, int a, int k, bool rows, int *key
     s_cnt[x] = m - m_lbound(L, 0, m, e_k);
   }
   __syncthreads();
-  const int total = m_scan<MT>(s_cnt, nm, s_tmp);
-  int pw = 1; while (pw < total) pw <<= 1;
-  if (pw > cap) return -1;
+  const int total = m_scan<MT>(s_cnt, nm, s_tmp);     // s_cnt[x] = start of member x's suffix
+  if (total + 1 > cap) return -1;
+  if (tid == 0) s_cnt[nm] = total;
   for (int x = 0; x < nm; ++x) {
     const int j = a + x;
     const int32_t *L = idx + off[j];
@@ -441,15 +445,34 @@ __device__ int build_union(const MergeArgs &M, int a, int k, bool rows, int *key
     const int c = (x + 1 < nm ? s_cnt[x + 1] : total) - s_cnt[x];
     for (int i = tid; i < c; i += MT) keys[s_cnt[x] + i] = L[m - c + i];
   }
-  for (int i = total + tid; i < pw; i += MT) keys[i] = INT_MAX;
   __syncthreads();
-  if (pw > 1) m_bitonic(keys, pw);
-  for (int i = tid; i < total; i += MT) flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+  // member of element t: the last x with s_cnt[x] <= t
+  for (int t = tid; t < total; t += MT) {
+    int lo = 0, hi = nm - 1;
+    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_cnt[mid] <= t) lo = mid; else hi = mid - 1; }
+    const int key = keys[t];
+    bool first = true;
+    for (int x2 = 0; x2 < lo && first; ++x2) {
+      const int b0 = s_cnt[x2], b1 = s_cnt[x2 + 1];
+      const int p = m_lbound(keys, b0, b1, key);
+      first = !(p < b1 && keys[p] == key);
+    }
+    flags[t] = first ? 1 : 0;
+  }
   __syncthreads();
-  const int u = m_scan<MT>(flags, total, s_tmp);
-  for (int i = tid; i < total; i += MT) {
-    const int nxt = i + 1 < total ? flags[i + 1] : u;
-    if (nxt > flags[i]) out[flags[i]] = keys[i];
+  const int u = m_scan<MT>(flags, total, s_tmp);      // exclusive prefix of the first-flags
+  if (tid == 0) flags[total] = u;
+  __syncthreads();
+  for (int t = tid; t < total; t += MT) {
+    const int f = (t + 1 <= total ? flags[t + 1] : u) - flags[t];
+    if (!f) continue;
+    const int key = keys[t];
+    int rank = 0;
+    for (int x2 = 0; x2 < nm; ++x2) {
+      const int b0 = s_cnt[x2], b1 = s_cnt[x2 + 1];
+      rank += flags[m_lbound(keys, b0, b1, key)] - flags[b0];
+    }
+    out[rank] = key;
   }
   __syncthreads();
   return u;
