@@ -648,7 +648,7 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       CUDA_TRY(h, dalloc(h, &M.tot, 16)); CUDA_TRY(h, dalloc(h, &M.flops, 1)); CUDA_TRY(h, dalloc(h, &M.ovf, 1));
       // test windows: W_k = largest W <= 127 with s_k - s_{k-W} + q_k <= max_block
       {
-        std::vector<int64_t> wofs(N);
+        std::vector<int64_t> wofs(N + 1);
         int64_t acc = 0;
         const std::vector<int32_t> &bs = h->bstart;
         for (int k = 0; k < N; ++k) {
@@ -662,9 +662,10 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
           wofs[k] = acc;
           acc += W + 1;
         }
+        wofs[N] = acc;     // W_k = wofs[k+1] - wofs[k] - 1
         int64_t *d_wofs = nullptr;
-        CUDA_TRY(h, dalloc(h, &d_wofs, (size_t)N));
-        CUDA_TRY(h, cudaMemcpy(d_wofs, wofs.data(), N * sizeof(int64_t), cudaMemcpyHostToDevice));
+        CUDA_TRY(h, dalloc(h, &d_wofs, (size_t)N + 1));
+        CUDA_TRY(h, cudaMemcpy(d_wofs, wofs.data(), (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
         M.wofs = d_wofs;
         CUDA_TRY(h, dalloc(h, &M.UV, 2 * (size_t)std::max<int64_t>(acc, 1)));
         const int nch = bilu_merge_nchunks(N);

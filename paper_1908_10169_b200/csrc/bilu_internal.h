@@ -125,7 +125,7 @@ struct MergeArgs {
   const double *Lval; const double *Uval; const double *D; const int64_t *D_off;
   // outputs / workspace
   uint32_t *T;            // [4N] test bitmasks, bit d-1 <=> merge(a = k-d, k)
-  const int64_t *wofs;    // [N] offsets of the per-block windows (W_k + 1 entries each)
+  const int64_t *wofs;    // [N+1] offsets of the per-block windows (W_k + 1 entries each)
   int32_t *UV;            // [2 * sum(W_k + 1)] union sizes u(d), v(d) of the test
   uint8_t *chunkmap;      // [nchunks * 128] scan state maps
   uint8_t *chunkstart;    // [nchunks]

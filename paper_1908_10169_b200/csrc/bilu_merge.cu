@@ -148,11 +148,22 @@ __device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *hkey
   }
   for (int d = tid; d < 128; d += TEST_T) { R.r[d] = 0; R.s[d] = 0; R.u[d] = 0; }
   __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    for (int d = 0; d <= W; ++d) { s_off[d] = acc; acc += s_len[d]; }
-    s_off[W + 1] = acc;
-    R.t = s_len[0];
+  if (tid < 32) {   // exclusive prefix of the W+1 list lengths, one warp
+    const int lane = tid;
+    int carry = 0;
+    for (int base = 0; base <= W; base += 32) {
+      const int d = base + lane;
+      const int v = d <= W ? s_len[d] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (d <= W) s_off[d] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) { s_off[W + 1] = carry; R.t = s_len[0]; }
   }
   __syncthreads();
   const int total = s_off[W + 1];
@@ -222,7 +233,7 @@ __global__ void __launch_bounds__(TEST_T) merge_test_kernel(MergeArgs M) {
   const int tid = threadIdx.x;
   for (int k = blockIdx.x; k < M.N; k += gridDim.x) {
     if (tid < 4) s_mask[tid] = 0u;
-    const int W = k > 0 ? merge_window(M.bstart, M.seg, k, M.max_block) : 0;
+    const int W = (int)(M.wofs[k + 1] - M.wofs[k]) - 1;     // the host's window (same rule)
     __syncthreads();
     if (W > 0) {
       test_side(M, k, W, true, hkeys, hdmin, hflag, s_len, s_off, s_ptr, SR);
@@ -421,7 +432,7 @@ __global__ void __launch_bounds__(1024) merge_offsets_kernel(MergeArgs M) {
 // Returns the number of distinct keys (must equal the test's union size), -1 if the
 // buffers are too small.
 __device__ int build_union(const MergeArgs &M, int a, int k, bool rows, int *keys, int *flags, int cap,
-                           int *s_cnt, int *s_tmp, int *out) {
+                           int *s_cnt, int *s_tmp, int *out, int *sout) {
   const int tid = threadIdx.x;
   const int e_k = M.bstart[k + 1];
   const int32_t *idx = rows ? M.Lidx : M.Uidx;
@@ -475,6 +486,10 @@ __device__ int build_union(const MergeArgs &M, int a, int k, bool rows, int *key
     out[rank] = key;
   }
   __syncthreads();
+  if (sout && u <= ARITH_KEYS) {   // shared copy for the lookups (the key buffer is dead now)
+    for (int x = tid; x < u; x += MT) sout[x] = out[x];
+    __syncthreads();
+  }
   return u;
 }
 
@@ -492,6 +507,7 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
   unsigned char *scratch = msm_raw + 2 * ARITH_PSMEM * ARITH_PSMEM * 8;       // union keys | GEMM staging
   int *skeys = (int *)scratch;                                                // ARITH_KEYS
   int *sflags = skeys + ARITH_KEYS;                                           // ARITH_KEYS
+  int *sunion = skeys;                                                        // the union, for lookups
   double *sgemm = (double *)scratch;
   __shared__ int s_tmp[MW + 1];
   __shared__ int s_cnt[130];
@@ -590,8 +606,9 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
     const int u = M.fLm[F], v = M.fUc[F];
     {
       int *R = M.Lidx_out + M.fLrow_off[F];
-      int uu = build_union(M, a, k, true, skeys, sflags, ARITH_KEYS, s_cnt, s_tmp, R);
-      if (uu < 0) uu = build_union(M, a, k, true, gkeys, gkeys + M.work_ints / 2, (int)(M.work_ints / 2), s_cnt, s_tmp, R);
+      int uu = build_union(M, a, k, true, skeys, sflags, ARITH_KEYS, s_cnt, s_tmp, R, sunion);
+      if (uu < 0) uu = build_union(M, a, k, true, gkeys, gkeys + M.work_ints / 2, (int)(M.work_ints / 2), s_cnt, s_tmp, R, sunion);
+      const int *Rl = uu <= ARITH_KEYS ? sunion : R;     // lookups in shared memory when it fits
       if (uu != u) { if (tid == 0) atomicExch(M.ovf, uu < 0 ? 1 : 2); return; }
       if (u > 0) {
         for (int i = tid; i < u * P; i += MT) G[i] = 0.0;
@@ -605,7 +622,7 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
           const int mi = m_lbound(rows, 0, mj, ek);
           for (int it = mi * bj + tid; it < mj * bj; it += MT) {
             const int p = it / bj, t = it - p * bj;
-            G[(size_t)m_lbound(R, 0, u, rows[p]) * P + oj + t] = Lv[it];
+            G[(size_t)m_lbound(Rl, 0, u, rows[p]) * P + oj + t] = Lv[it];
           }
         }
         __syncthreads();
@@ -616,8 +633,9 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
     // ---- Ũ^ columns: union, gathered Ũ_g (P x v column-major) in G, Ũ^ = L_aa G
     {
       int *Cc = M.Uidx_out + M.fUcol_off[F];
-      int vv = build_union(M, a, k, false, skeys, sflags, ARITH_KEYS, s_cnt, s_tmp, Cc);
-      if (vv < 0) vv = build_union(M, a, k, false, gkeys, gkeys + M.work_ints / 2, (int)(M.work_ints / 2), s_cnt, s_tmp, Cc);
+      int vv = build_union(M, a, k, false, skeys, sflags, ARITH_KEYS, s_cnt, s_tmp, Cc, sunion);
+      if (vv < 0) vv = build_union(M, a, k, false, gkeys, gkeys + M.work_ints / 2, (int)(M.work_ints / 2), s_cnt, s_tmp, Cc, sunion);
+      const int *Cl = vv <= ARITH_KEYS ? sunion : Cc;
       if (vv != v) { if (tid == 0) atomicExch(M.ovf, vv < 0 ? 1 : 2); return; }
       if (v > 0) {
         for (int i = tid; i < v * P; i += MT) G[i] = 0.0;
@@ -631,7 +649,7 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
           const int ci = m_lbound(cols, 0, cj, ek);
           for (int it = ci * bj + tid; it < cj * bj; it += MT) {
             const int q = it / bj, t = it - q * bj;
-            G[(size_t)m_lbound(Cc, 0, v, cols[q]) * P + oj + t] = Uv[it];
+            G[(size_t)m_lbound(Cl, 0, v, cols[q]) * P + oj + t] = Uv[it];
           }
         }
         __syncthreads();

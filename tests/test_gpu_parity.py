@@ -282,3 +282,13 @@ def test_c5_full_parity_and_gmres():
     assert st["n_merges"] == of.n_merges
     it_g, ok_g, it_o, ok_o = _gmres_counts(P, g, of)
     assert ok_g and ok_o and abs(it_g - it_o) <= 1
+
+
+def test_c4_2000_blocks_parity():
+    """BASELINE configs[3] recipe with 2,000 of its 20,000 blocks (n ~ 80k, nnz ~ 43M): the
+    split wide-block path (contributor-range GEMM parts, scaling parts) at scale."""
+    from inputs.configs import config4
+    P = config4(nblocks=2000)
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert_parity(gf, of)
+    assert st["n_blocks_final"] == of.nblk
