@@ -215,6 +215,7 @@ struct Bump {
   double *gbase; int64_t gused, gtop, gcap;        // global spill region, same scheme (doubles)
   bool ovf;
   bool bottom_global;                              // persistent allocations in global memory only
+  bool pool;                                       // ... from the shared heavy-block pool (split blocks)
 };
 __device__ __forceinline__ void *balloc(Bump &A, int64_t bytes) {
   bytes = (bytes + 15) & ~int64_t(15);
@@ -652,7 +653,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
   const int nW = base + nU;
   double *W;
   int *lineOf;
-  if (A.bottom_global) {
+  if (A.pool) {
     // a split block: W, the line map and a copy of the bitmap map live in the global pool
     // (read by the helpers), allocated exactly now that the candidate count is known
     const int64_t wd = (int64_t)nW * b, ld = ((int64_t)nW + 2) / 2 + 1;
@@ -689,7 +690,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
   } else {
     for (int x = tid; x < nU; x += NT) lineOf[base + x] = pre[x];
   }
-  if (!A.bottom_global)                  // the global pool is zero at every launch
+  if (!A.pool)                           // the global pool is zero at every launch
     for (int x = tid; x < nW * b; x += NT) W[x] = 0.0;
   __syncthreads();
   // -- a-4: scatter Ã
@@ -770,7 +771,7 @@ __device__ bool prepare_both(const DevFactor &F, int K, int s, int e, int b, con
   const int nWL = b + nUL, nWU = nUU;
   double *WL, *WU;
   int *lineL, *lineU;
-  if (A.bottom_global) {
+  if (A.pool) {
     const int64_t wdL = (int64_t)nWL * b, ldL = ((int64_t)nWL + 2) / 2 + 1, mdL = (int64_t)wL + 2;
     const int64_t wdU = (int64_t)nWU * b, ldU = ((int64_t)nWU + 2) / 2 + 1, mdU = (int64_t)wU + 2;
     const int64_t d = wdL + ldL + mdL + wdU + ldU + mdU;
@@ -809,7 +810,7 @@ __device__ bool prepare_both(const DevFactor &F, int K, int s, int e, int b, con
       m &= m - 1;
     }
   }
-  if (!A.bottom_global) {
+  if (!A.pool) {
     for (int x = tid; x < nWL * b; x += NT) WL[x] = 0.0;
     for (int x = tid; x < nWU * b; x += NT) WU[x] = 0.0;
   }
@@ -1009,7 +1010,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   Bump A;
   A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes;
   A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
-  A.ovf = false; A.bottom_global = false;
+  A.ovf = false; A.bottom_global = false; A.pool = false;
   PROF_T0
 #define OVF_CHECK() do { if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; } } while (0)
 
@@ -1041,7 +1042,9 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   __syncthreads();
   const bool heavy = (S.cnt[3] & 1) != 0;
   const bool publish = (S.cnt[3] & 2) != 0;
-  if (heavy) A.bottom_global = true;   // W and line maps in the global pool (read by the helpers)
+  // big blocks: W and the line maps in global memory -- the shared pool if the block is
+  // split into parts (read by the helpers), else this CTA's reusable workspace
+  if (heavy) { A.bottom_global = true; A.pool = publish; }
 
   // ---------------- a-3 / a-4 for both sides
   SideState RL, RU;
@@ -1155,9 +1158,14 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
   }
   __syncthreads();
   PROF(4);
-  if (heavy) {   // scratch of the finish phase from this CTA's own shared memory / workspace
+  if (heavy) {   // finish scratch: shared memory from the start, the workspace after W (if W is there)
     A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes; A.bottom_global = false;
-    A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
+    if (A.pool) {
+      A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
+    } else {
+      A.gtop = A.gcap;
+    }
+    A.pool = false;
   } else {
     A.stop = A.scap; A.gtop = A.gcap;   // release the bitmaps / scratch
   }
@@ -1214,7 +1222,7 @@ __device__ void run_scale_part(const DevFactor &F, HeavyCtx &X, int p, Shared &S
   Bump A;
   A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes;
   A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
-  A.ovf = false; A.bottom_global = false;
+  A.ovf = false; A.bottom_global = false; A.pool = false;
   finish_block(F, K, S, A, X.R[0].W, X.R[1].W, X.R[0].lineOf, X.R[1].lineOf, nR, nC, X.sortedR != 0,
                X.sortedC != 0, X.flops, &X, 2);
 }
@@ -1297,7 +1305,7 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
   Bump A;
   A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes;
   A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
-  A.ovf = false; A.bottom_global = false;
+  A.ovf = false; A.bottom_global = false; A.pool = false;
   // stage the finished buffers in shared memory when they fit in half of it
   double *WL = X.R[0].W, *WU = X.R[1].W;
   const int *rowOf = X.R[0].lineOf, *colOf = X.R[1].lineOf;

@@ -498,7 +498,7 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     // split-block pool: W buffers of the blocks processed as parallel tasks (grows on demand)
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    h->hpool_cap = std::min<int64_t>(std::max<int64_t>(1 << 22, 40 * nnz), (int64_t)(fr / 8 / 8));
+    h->hpool_cap = std::min<int64_t>(std::max<int64_t>(1 << 22, 64 * nnz), (int64_t)(fr / 8 / 8));
   }
   h->pool_lc = h->pool_uc = std::max(2 * n_blocks, 1024);
   h->pool_succ = std::max(2 * n_blocks, 1024);

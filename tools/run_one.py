@@ -13,4 +13,4 @@ else:
 g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm)
 for _ in range(reps):
     st = g.factor(P.tau)
-print(name, "ms", st["t_factor_ms"], "flops", st["flops"])
+print(name, "ms", st["t_factor_ms"], "flops", st["flops"], "launches", g.kernel_launches(), "retries(last)", st["n_retries"])
