@@ -64,12 +64,22 @@ typedef struct {
   double  near_rel;      /* decisions with |max/tau - 1| <= near_rel are logged  */
   int64_t arena_hint;    /* initial factor arena, doubles (0 = auto); grows on overflow */
   void   *stream;        /* cudaStream_t to run on (NULL = the legacy default stream) */
-  int32_t rank, world;   /* multi-GPU: this rank / ranks (world = 1 only, round 1) */
-  void   *nccl_comm;     /* ncclComm_t or NULL                                   */
+  int32_t rank, world;   /* reserved (multi-GPU runs through bilu_dist_setup; world = 1) */
+  void   *nccl_comm;     /* reserved                                             */
+  /* Sec. 3.6 perturbation of singular / ill-conditioned pivot blocks (PAPER.md:1505-1538,
+   * DESIGN.md R19): off by default (an exactly singular pivot block is then a breakdown).
+   * When on, a pivot block with a zero column / row, an exactly zero pivot or a 1-norm
+   * condition number |P|_1 |P^{-1}|_1 > cond_max is perturbed with the absolute / relative
+   * tolerances perturb_tau (x max|a_ij|) and perturb_rho. */
+  int32_t perturb;       /* 0 = off (default), 1 = on                            */
+  double  perturb_tau;   /* default 1e-2 (the paper's practice)                   */
+  double  perturb_rho;   /* default 1e-1                                          */
+  double  cond_max;      /* default 1e12                                          */
 } bilu_options;
 
 /* Fills *opt with the defaults (device 0, max_block 128, aggregate 1, near_rel
- * 1e-8, auto sizes, default stream, world 1). */
+ * 1e-8, auto sizes, default stream, world 1, perturbation off with tau 1e-2, rho 1e-1,
+ * cond_max 1e12). */
 void bilu_options_default(bilu_options *opt);
 
 typedef struct {
@@ -85,6 +95,7 @@ typedef struct {
   int64_t n_decisions;           /* drop/keep decisions taken                     */
   int64_t n_near;                /* of which |max/tau - 1| <= near_rel            */
   double  min_margin;            /* min |max/tau - 1| over all decisions (tau>0)  */
+  int64_t n_perturbed;           /* pivot blocks modified by the Sec. 3.6 perturbation */
 } bilu_factor_stats;
 
 /*

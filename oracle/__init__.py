@@ -48,8 +48,13 @@ class _Factor(ctypes.Structure):
         ("flops", ctypes.c_double), ("t_factor_s", ctypes.c_double),
         ("n_merges", ctypes.c_int32), ("breakdown_block", ctypes.c_int32),
         ("n_decisions", ctypes.c_int64), ("n_near", ctypes.c_int64),
-        ("min_margin", ctypes.c_double),
+        ("min_margin", ctypes.c_double), ("n_perturbed", ctypes.c_int64),
     ]
+
+
+class _Perturb(ctypes.Structure):
+    _fields_ = [("perturb", ctypes.c_int32), ("tau", ctypes.c_double), ("rho", ctypes.c_double),
+                ("cond_max", ctypes.c_double)]
 
 
 class _Override(ctypes.Structure):
@@ -75,6 +80,13 @@ def _load():
             ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.c_int32, ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
             ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.POINTER(_Factor),
+        ]
+        lib.orc_bilu_factor_pt.restype = ctypes.c_int
+        lib.orc_bilu_factor_pt.argtypes = [
+            ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_int32, ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.POINTER(_Perturb),
+            ctypes.POINTER(_Factor),
         ]
         lib.orc_bilu_apply.restype = ctypes.c_int
         lib.orc_bilu_apply.argtypes = [ctypes.POINTER(_Factor), ctypes.c_void_p, ctypes.c_void_p]
@@ -117,6 +129,7 @@ class OracleFactor:
     n_decisions: int = 0
     n_near: int = 0
     min_margin: float = float("inf")
+    n_perturbed: int = 0
     _keep: object = field(default=None, repr=False)
 
     @property
@@ -141,9 +154,10 @@ def _np(ptr, count, dtype):
 
 
 def factor(indptr, indices, data, block_sizes, tau, aggregate=True, max_block=128,
-           overrides=None, near_rel=1e-8, seg=None) -> OracleFactor:
+           overrides=None, near_rel=1e-8, seg=None, perturb=None) -> OracleFactor:
     """Run the oracle on an already-permuted CSR matrix (Ã).  seg: optional aggregation
-    segment per initial block (merges only inside a segment, R18)."""
+    segment per initial block (merges only inside a segment, R18).  perturb:
+    None (off) or (tau_p, rho, cond_max) for the Sec. 3.6 perturbation (R19)."""
     lib = _load()
     indptr = np.ascontiguousarray(indptr, dtype=np.int64)
     indices = np.ascontiguousarray(indices, dtype=np.int32)
@@ -159,7 +173,14 @@ def factor(indptr, indices, data, block_sizes, tau, aggregate=True, max_block=12
         ov = ctypes.cast(arr, ctypes.c_void_p)
         nov = len(overrides)
     f = _Factor()
-    if seg is None:
+    if perturb is not None:
+        pt = _Perturb(1, float(perturb[0]), float(perturb[1]), float(perturb[2]))
+        sg = None if seg is None else np.ascontiguousarray(seg, dtype=np.int32)
+        rc = lib.orc_bilu_factor_pt(
+            n, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data,
+            len(bsz), bsz.ctypes.data, float(tau), int(bool(aggregate)), int(max_block),
+            ov, nov, float(near_rel), None if sg is None else sg.ctypes.data, ctypes.byref(pt), ctypes.byref(f))
+    elif seg is None:
         rc = lib.orc_bilu_factor(
             n, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data,
             len(bsz), bsz.ctypes.data, float(tau), int(bool(aggregate)), int(max_block),
@@ -190,7 +211,7 @@ def factor(indptr, indices, data, block_sizes, tau, aggregate=True, max_block=12
         Uvp=Uvp, Uv=_np(f.Uv, int(Uvp[-1]), np.float64), Dp=Dp,
         Dv=_np(f.Dv, int(Dp[-1]), np.float64), flops=f.flops, t_factor_s=f.t_factor_s,
         n_merges=f.n_merges, n_decisions=f.n_decisions, n_near=f.n_near,
-        min_margin=f.min_margin)
+        min_margin=f.min_margin, n_perturbed=f.n_perturbed)
     lib.orc_free(ctypes.byref(f))
     return out
 

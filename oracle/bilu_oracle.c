@@ -101,6 +101,91 @@ static int gauss_jordan_inverse(int b, double *a, double *inv) {
   return 0;
 }
 
+/* ---------------- diagonal-block perturbation (Sec. 3.6) ----------------
+ * alpha = max |a_ij| of the matrix; tau_p, rho the absolute / relative tolerances (the paper
+ * uses 1e-2 and 1e-1).  Column j of the pivot block with entries d and
+ * delta_j = max|d|: the largest entry d_kj (the diagonal d_jj instead whenever
+ * 2|d_jj| >= |d_kj|) becomes d_kj (1 + rho beta_j) + sign(d_kj) tau_p alpha
+ * (PAPER.md:1524), beta_j := delta_j (beta_j is undefined in the paper, R19,
+ * as in SPEC), sign(0) := +1; "after that we proceed analogously with respect to the rows"
+ * (PAPER.md:1526-1527).  Trigger (R19): a zero column / row ("if d = 0") perturbs that
+ * column / row; a singular block (zero pivot in the Gauss-Jordan elimination) or an
+ * ill-conditioned one (kappa_1 = |P|_1 |P^{-1}|_1 > cond_max) perturbs every column, then
+ * every row; if that is still singular / ill-conditioned, sign(p_ii) tau_p alpha is added to
+ * every diagonal entry; if that fails too, the block is reported as a breakdown. */
+static double sgn1(double x) { return x < 0.0 ? -1.0 : 1.0; }
+
+static void perturb_col(int b, double *P, int j, double alpha, double tau_p, double rho) {
+  int i, k = 0;
+  double dmax = -1.0;
+  for (i = 0; i < b; ++i) {
+    double v = fabs(P[i + (size_t)j * b]);
+    if (v > dmax) { dmax = v; k = i; }
+  }
+  if (2.0 * fabs(P[j + (size_t)j * b]) >= fabs(P[k + (size_t)j * b])) k = j;
+  double *d = &P[k + (size_t)j * b];
+  *d = *d * (1.0 + rho * dmax) + sgn1(*d) * tau_p * alpha;
+}
+
+static void perturb_row(int b, double *P, int i, double alpha, double tau_p, double rho) {
+  int j, k = 0;
+  double dmax = -1.0;
+  for (j = 0; j < b; ++j) {
+    double v = fabs(P[i + (size_t)j * b]);
+    if (v > dmax) { dmax = v; k = j; }
+  }
+  if (2.0 * fabs(P[i + (size_t)i * b]) >= fabs(P[i + (size_t)k * b])) k = i;
+  double *d = &P[i + (size_t)k * b];
+  *d = *d * (1.0 + rho * dmax) + sgn1(*d) * tau_p * alpha;
+}
+
+static double norm1(int b, const double *M) {
+  double best = 0.0;
+  for (int j = 0; j < b; ++j) {
+    double s = 0.0;
+    for (int i = 0; i < b; ++i) s += fabs(M[i + (size_t)j * b]);
+    if (s > best) best = s;
+  }
+  return best;
+}
+
+/* inverse of P (column-major, b x b; P is modified: it ends as the perturbed block), with the
+ * perturbation of Sec. 3.6 when enabled.  Returns 0 (D = inverse), 1 (breakdown).
+ * *perturbed is set to 1 if the block was modified. */
+static int pivot_inverse(int b, double *P, double *D, double *A, int perturb, double alpha, double tau_p,
+                         double rho, double cond_max, int *perturbed) {
+  int i, j, zero_any = 0;
+  *perturbed = 0;
+  if (!perturb) {
+    memcpy(A, P, sizeof(double) * (size_t)b * b);
+    return gauss_jordan_inverse(b, A, D);
+  }
+  for (j = 0; j < b; ++j) {
+    double m = 0.0;
+    for (i = 0; i < b; ++i) m = fmax(m, fabs(P[i + (size_t)j * b]));
+    if (m == 0.0) { perturb_col(b, P, j, alpha, tau_p, rho); zero_any = 1; }
+  }
+  for (i = 0; i < b; ++i) {
+    double m = 0.0;
+    for (j = 0; j < b; ++j) m = fmax(m, fabs(P[i + (size_t)j * b]));
+    if (m == 0.0) { perturb_row(b, P, i, alpha, tau_p, rho); zero_any = 1; }
+  }
+  for (int stage = 0; stage < 3; ++stage) {
+    if (stage == 1) {
+      for (j = 0; j < b; ++j) perturb_col(b, P, j, alpha, tau_p, rho);
+      for (i = 0; i < b; ++i) perturb_row(b, P, i, alpha, tau_p, rho);
+    } else if (stage == 2) {
+      for (i = 0; i < b; ++i) P[i + (size_t)i * b] += sgn1(P[i + (size_t)i * b]) * tau_p * alpha;
+    }
+    memcpy(A, P, sizeof(double) * (size_t)b * b);
+    if (!gauss_jordan_inverse(b, A, D) && norm1(b, P) * norm1(b, D) <= cond_max) {
+      *perturbed = zero_any || stage > 0;
+      return 0;
+    }
+  }
+  return 1;
+}
+
 /* ---------------- helpers ---------------- */
 static int cmp_i32(const void *a, const void *b) {
   int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
@@ -186,7 +271,7 @@ static int factor_impl(int32_t n, const int64_t *row_ptr, const int32_t *col_idx
                        const double *val, int32_t nblk, const int32_t *bsizes,
                        double tau, int32_t aggregate, int32_t max_block,
                        const orc_override *ovr, int64_t n_ovr, double near_rel,
-                       const int32_t *seg, orc_factor *f) {
+                       const int32_t *seg, const orc_perturb *pt, orc_factor *f) {
   int32_t i, K;
   int64_t e64;
   memset(f, 0, sizeof(*f));
@@ -254,6 +339,9 @@ static int factor_impl(int32_t n, const int64_t *row_ptr, const int32_t *col_idx
   double *wl = NULL, *wu = NULL;   /* (slots) x b each */
   size_t wl_cap = 0, wu_cap = 0;
   double *P = (double *)xmalloc(sizeof(double) * (size_t)max_block * max_block);
+  double *Pw = (double *)xmalloc(sizeof(double) * (size_t)max_block * max_block);
+  double alpha = 0.0;                      /* max |a_ij| (Sec. 3.6) */
+  for (e64 = 0; e64 < row_ptr[n]; ++e64) alpha = fmax(alpha, fabs(val[e64]));
   double *tmp = (double *)xmalloc(sizeof(double) * (size_t)max_block * 2);
   int32_t *keep_idx = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)n);
   int status = 0;
@@ -359,7 +447,14 @@ static int factor_impl(int32_t n, const int64_t *row_ptr, const int32_t *col_idx
     Kb->D = (double *)xmalloc(sizeof(double) * (size_t)b * b);
     for (int32_t r = 0; r < b; ++r)
       for (int32_t c = 0; c < b; ++c) P[r + (size_t)c * b] = wl[(size_t)r * b + c];
-    if (gauss_jordan_inverse(b, P, Kb->D)) { status = 2; f->breakdown_block = K; break; }
+    {
+      int pert = 0;
+      if (pivot_inverse(b, P, Kb->D, Pw, pt && pt->perturb, alpha, pt ? pt->tau : 0.0, pt ? pt->rho : 0.0,
+                        pt ? pt->cond_max : 0.0, &pert)) {
+        status = 2; f->breakdown_block = K; break;
+      }
+      f->n_perturbed += pert;
+    }
     flops += 2.0 * b * b * (double)b + 2.0 * b * b * (double)((nr - b) + nc);
 
     /* -- L rows: l_i = w_i D_K, keep iff max|l_i| > tau -- */
@@ -607,7 +702,7 @@ static int factor_impl(int32_t n, const int64_t *row_ptr, const int32_t *col_idx
     free(B[K].Li); free(B[K].Lv); free(B[K].Ui); free(B[K].Uv); free(B[K].D);
   }
   free(B); free(Lhead); free(Uhead); free(rslot); free(cslot); free(rrows); free(ccols);
-  free(Lc); free(Uc); free(wl); free(wu); free(P); free(tmp); free(keep_idx);
+  free(Lc); free(Uc); free(wl); free(wu); free(P); free(Pw); free(tmp); free(keep_idx);
   free(cp); free(cr); free(cv); free(block_of); free(bs); free(ov);
   return status;
 }
@@ -664,7 +759,16 @@ int orc_bilu_factor(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
                     const orc_override *ovr, int64_t n_ovr, double near_rel,
                     orc_factor *f) {
   return factor_impl(n, row_ptr, col_idx, val, nblk, bsizes, tau, aggregate, max_block, ovr, n_ovr,
-                     near_rel, NULL, f);
+                     near_rel, NULL, NULL, f);
+}
+
+int orc_bilu_factor_pt(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                       const double *val, int32_t nblk, const int32_t *bsizes,
+                       double tau, int32_t aggregate, int32_t max_block,
+                       const orc_override *ovr, int64_t n_ovr, double near_rel,
+                       const int32_t *seg, const orc_perturb *pt, orc_factor *f) {
+  return factor_impl(n, row_ptr, col_idx, val, nblk, bsizes, tau, aggregate, max_block, ovr, n_ovr,
+                     near_rel, seg, pt, f);
 }
 
 int orc_bilu_factor_seg(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
@@ -673,5 +777,5 @@ int orc_bilu_factor_seg(int32_t n, const int64_t *row_ptr, const int32_t *col_id
                         const orc_override *ovr, int64_t n_ovr, double near_rel,
                         const int32_t *seg, orc_factor *f) {
   return factor_impl(n, row_ptr, col_idx, val, nblk, bsizes, tau, aggregate, max_block, ovr, n_ovr,
-                     near_rel, seg, f);
+                     near_rel, seg, NULL, f);
 }

@@ -45,7 +45,11 @@ typedef struct {
   int64_t n_decisions;      /* drop/keep decisions taken                    */
   int64_t n_near;           /* decisions with margin <= near_rel            */
   double  min_margin;       /* min |max/tau - 1| over all decisions         */
+  int64_t n_perturbed;      /* pivot blocks modified by the Sec. 3.6 perturbation */
 } orc_factor;
+
+/* Sec. 3.6 perturbation parameters (R19); perturb = 0 disables it. */
+typedef struct { int32_t perturb; double tau, rho, cond_max; } orc_perturb;
 
 /* One forced decision (decision replay, SURVEY.md 8(c) reading 15).
  * side 0 = L row `idx` of original block `blk`, side 1 = U col `idx`. */
@@ -66,6 +70,13 @@ int orc_bilu_factor_seg(int32_t n, const int64_t *row_ptr, const int32_t *col_id
                         double tau, int32_t aggregate, int32_t max_block,
                         const orc_override *ovr, int64_t n_ovr, double near_rel,
                         const int32_t *seg, orc_factor *f);
+
+/* As orc_bilu_factor_seg, with the diagonal-block perturbation of Sec. 3.6 (pt may be NULL). */
+int orc_bilu_factor_pt(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                       const double *val, int32_t nblk, const int32_t *bsizes,
+                       double tau, int32_t aggregate, int32_t max_block,
+                       const orc_override *ovr, int64_t n_ovr, double near_rel,
+                       const int32_t *seg, const orc_perturb *pt, orc_factor *f);
 
 /* y = (L P U)^{-1} x in the permuted ordering (forward/backward substitution
  * with D multiplies).  x, y host arrays of length n. */

@@ -1325,36 +1325,11 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
   finish_block(F, K, S, A, WL, WU, rowOf, colOf, nR, nC, X.R[0].sorted, X.R[1].sorted, X.flops, &X, fmode);
 }
 
-// a-6 .. a-1 of block K once W_L (pivot block + candidate rows) and W_U are complete
-__device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
-                             const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops,
-                             HeavyCtx *X, int mode) {
+// D_K = P_K^{-1} in place (P column-major b x b in shared memory; b > 8 needs 2 b^2 doubles
+// of P and 3 b of fcol), Gauss-Jordan with partial pivoting inside the block
+// (ties -> lowest row, R6).  CTA-wide; returns true if a pivot is exactly 0.
+__device__ bool gj_invert(double *P, int b, int *ipiv, double *fcol, Shared &S) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
-  PROF_T0C
-#define OVF_CHECK() do { if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; } } while (0)
-  // wide blocks: shared staging of D_K for the scaling products, reserved first so that it
-  // stays in shared memory
-  double *gsc = nullptr;
-  if (b > 16) {
-    gsc = (double *)balloc_top(A, (int64_t)b * (b <= 64 ? TsB<64>::LDB : TsB<128>::LDB) * 8);
-    OVF_CHECK();
-  }
-  // mode 0: a-6 .. a-1 here.  mode 1 (wide split block): a-6, then the scaling of the
-  // candidate rows / columns is published as parts.  mode 2: the parts are done, a-8 .. a-1.
-  double *P = nullptr;
-  if (mode == 2) goto scaled;
-  {
-  // ---------------- a-6: D_K = P_K^{-1}, Gauss-Jordan with partial pivoting (column-major P)
-  P = (double *)balloc(A, (int64_t)b * b * 8 * (b > 8 ? 2 : 1));
-  int *ipiv = (int *)balloc(A, (int64_t)b * 4);
-  double *fcol = (double *)balloc(A, (int64_t)b * 8 * 3);
-  OVF_CHECK();
-  for (int i = tid; i < b * b; i += NT) {
-    int rr = i % b, cc = i / b;
-    P[i] = WL[(int64_t)rr * b + cc];
-  }
-  __syncthreads();
   bool singular = false;
   if (b <= 8) {
     // one warp, lane j holds column j of P_K in registers; pivot search by the lane
@@ -1482,6 +1457,123 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
     if (tid == 0) S.piv = sing ? 1 : 0;
     __syncthreads();
     singular = S.piv != 0;
+  }
+  return singular;
+}
+
+// Sec. 3.6 perturbation passes on the pivot block Pp (column-major, shared memory), lanes of
+// warp 0 over columns / rows (R19): the largest entry of column j (the diagonal if
+// 2|d_jj| >= |d_kj|) becomes d (1 + rho delta_j) + sign(d) tau_p alpha.  which: 0 = only zero
+// columns then zero rows (returns whether any), 1 = every column then every row, 2 = sign-aware
+// tau_p alpha on the diagonal.
+__device__ bool perturb_pass(double *Pp, int b, int which, double alpha, double tp, double rho, Shared &S) {
+  const int tid = threadIdx.x;
+  if (tid == 0) S.cnt[3] = 0;
+  __syncthreads();
+  if (tid < 32) {
+    if (which == 2) {
+      for (int i = tid; i < b; i += 32) {
+        double &d = Pp[i + (int64_t)i * b];
+        d += (d < 0.0 ? -1.0 : 1.0) * tp * alpha;
+      }
+    } else {
+      for (int j = tid; j < b; j += 32) {           // columns
+        double dm = -1.0; int k = 0;
+        for (int i = 0; i < b; ++i) { const double v = fabs(Pp[i + (int64_t)j * b]); if (v > dm) { dm = v; k = i; } }
+        if (which == 0 && dm != 0.0) continue;
+        if (2.0 * fabs(Pp[j + (int64_t)j * b]) >= fabs(Pp[k + (int64_t)j * b])) k = j;
+        double &d = Pp[k + (int64_t)j * b];
+        d = d * (1.0 + rho * dm) + (d < 0.0 ? -1.0 : 1.0) * tp * alpha;
+        S.cnt[3] = 1;
+      }
+      __syncwarp();
+      for (int i = tid; i < b; i += 32) {           // rows
+        double dm = -1.0; int k = 0;
+        for (int j = 0; j < b; ++j) { const double v = fabs(Pp[i + (int64_t)j * b]); if (v > dm) { dm = v; k = j; } }
+        if (which == 0 && dm != 0.0) continue;
+        if (2.0 * fabs(Pp[i + (int64_t)i * b]) >= fabs(Pp[i + (int64_t)k * b])) k = i;
+        double &d = Pp[i + (int64_t)k * b];
+        d = d * (1.0 + rho * dm) + (d < 0.0 ? -1.0 : 1.0) * tp * alpha;
+        S.cnt[3] = 1;
+      }
+    }
+  }
+  __syncthreads();
+  return S.cnt[3] != 0;
+}
+
+// |M|_1 (max column sum), warp 0, broadcast through shared memory
+__device__ double norm1_cta(const double *M, int b, Shared &S) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    double best = 0.0;
+    for (int j = tid; j < b; j += 32) {
+      double sum = 0.0;
+      for (int i = 0; i < b; ++i) sum += fabs(M[i + (int64_t)j * b]);
+      best = fmax(best, sum);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (tid == 0) S.pivd = best;
+  }
+  __syncthreads();
+  const double r = S.pivd;
+  __syncthreads();
+  return r;
+}
+
+// a-6 .. a-1 of block K once W_L (pivot block + candidate rows) and W_U are complete
+__device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
+                             const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops,
+                             HeavyCtx *X, int mode) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
+  PROF_T0C
+#define OVF_CHECK() do { if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; } } while (0)
+  // wide blocks: shared staging of D_K for the scaling products, reserved first so that it
+  // stays in shared memory
+  double *gsc = nullptr;
+  if (b > 16) {
+    gsc = (double *)balloc_top(A, (int64_t)b * (b <= 64 ? TsB<64>::LDB : TsB<128>::LDB) * 8);
+    OVF_CHECK();
+  }
+  // mode 0: a-6 .. a-1 here.  mode 1 (wide split block): a-6, then the scaling of the
+  // candidate rows / columns is published as parts.  mode 2: the parts are done, a-8 .. a-1.
+  double *P = nullptr;
+  if (mode == 2) goto scaled;
+  {
+  // ---------------- a-6: D_K = P_K^{-1}, Gauss-Jordan with partial pivoting (column-major P)
+  P = (double *)balloc(A, (int64_t)b * b * 8 * (b > 8 ? 2 : 1));
+  int *ipiv = (int *)balloc(A, (int64_t)b * 4);
+  double *fcol = (double *)balloc(A, (int64_t)b * 8 * 3);
+  OVF_CHECK();
+  for (int i = tid; i < b * b; i += NT) {
+    int rr = i % b, cc = i / b;
+    P[i] = WL[(int64_t)rr * b + cc];
+  }
+  __syncthreads();
+  bool singular;
+  if (!F.perturb) {
+    singular = gj_invert(P, b, ipiv, fcol, S);
+  } else {
+    // Sec. 3.6 (R19): zero columns / rows first; a singular or
+    // ill-conditioned block (kappa_1 > cond_max) then gets every column and row perturbed,
+    // then a diagonal shift; otherwise a breakdown
+    double *Pp = (double *)balloc(A, (int64_t)b * b * 8);
+    OVF_CHECK();
+    for (int i = tid; i < b * b; i += NT) Pp[i] = P[i];
+    __syncthreads();
+    const double alpha = *F.alpha;
+    bool changed = perturb_pass(Pp, b, 0, alpha, F.ptau, F.prho, S);
+    singular = true;
+    for (int stage = 0; stage < 3 && singular; ++stage) {
+      if (stage > 0) { perturb_pass(Pp, b, stage, alpha, F.ptau, F.prho, S); changed = true; }
+      for (int i = tid; i < b * b; i += NT) P[i] = Pp[i];
+      __syncthreads();
+      singular = gj_invert(P, b, ipiv, fcol, S);
+      if (!singular) singular = norm1_cta(Pp, b, S) * norm1_cta(P, b, S) > F.cond_max;
+    }
+    if (!singular && changed && tid == 0) atomicAdd(&F.ctrl[CS * CTRL_NPERT], 1ull);
   }
   if (singular) {
     if (tid == 0) raise_abort(F, DEV_BREAKDOWN, K);

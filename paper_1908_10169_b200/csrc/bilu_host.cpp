@@ -36,6 +36,7 @@ extern "C" cudaError_t bilu_launch_permute(double *y, const double *x, const int
 extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_t st);
 extern "C" int bilu_merge_plan_launches();
 extern "C" int bilu_heavyctx_size();
+extern "C" cudaError_t bilu_launch_maxabs(double *out, const double *x, int64_t n, cudaStream_t st);
 extern "C" cudaError_t bilu_launch_sep_prepare(const DevFactor &F, const int32_t *sep_list, int nsep,
                                                const int32_t *static_sep, const int32_t *ifc, int nifc,
                                                const uint8_t *sep, cudaStream_t st);
@@ -99,6 +100,8 @@ struct bilu_ctx {
   unsigned long long qhead0 = 0, ctrl_init[CTRL_COUNT * CS];
   int32_t *d_own_ready = nullptr; int32_t n_own_ready = 0;
   double flops_local = 0.0, t_local_ms = 0.0;
+  double *d_alpha = nullptr;
+  int64_t npert_local = 0;
   int64_t ndec_local = 0, nnear_local = 0;
   std::vector<int64_t> D_off;
   std::vector<int64_t> map_csr;            // Ã entry -> original CSR entry
@@ -193,6 +196,10 @@ extern "C" void bilu_options_default(bilu_options *opt) {
   opt->rank = 0;
   opt->world = 1;
   opt->nccl_comm = nullptr;
+  opt->perturb = 0;
+  opt->perturb_tau = 1e-2;
+  opt->perturb_rho = 1e-1;
+  opt->cond_max = 1e12;
 }
 
 extern "C" const char *bilu_status_string(bilu_status s) {
@@ -439,6 +446,18 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     h->owned.push_back(hc);
     F.hctx = (HeavyCtx *)hc;
   }
+  F.perturb = opt.perturb ? 1 : 0;
+  F.ptau = opt.perturb_tau; F.prho = opt.perturb_rho; F.cond_max = opt.cond_max;
+  {
+    double *da = nullptr;
+    if (cudaMalloc(&da, sizeof(double)) != cudaSuccess) {
+      set_err(nullptr, "bilu_analyze: out of device memory"); bilu_destroy(h); return BILU_ERR_OOM;
+    }
+    h->owned.push_back(da);
+    cudaMemset(da, 0, sizeof(double));
+    F.alpha = da;
+    h->d_alpha = da;
+  }
   F.heavy_T = 1024;
   if (const char *ht = getenv("BILU_HEAVY_T")) F.heavy_T = atoi(ht);
   F.heavy_idle = 8;
@@ -517,6 +536,8 @@ extern "C" bilu_status bilu_set_values(bilu_ctx *h, const double *val, int32_t o
   cudaSetDevice(h->opt.device);
   CUDA_TRY(h, cudaMemcpyAsync(h->d_val_orig, val, h->nnz * sizeof(double),
                               on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, bilu_launch_maxabs(h->d_alpha, h->d_val_orig, h->nnz, h->stream));   // alpha of Sec. 3.6
+  h->launches += 1;
   if (h->nAL) CUDA_TRY(h, bilu_launch_gather(h->d_AL_val, h->d_val_orig, h->d_AL_map, h->nAL, h->stream));
   if (h->nAU) CUDA_TRY(h, bilu_launch_gather(h->d_AU_val, h->d_val_orig, h->d_AU_map, h->nAU, h->stream));
   h->launches += 2;
@@ -886,6 +907,7 @@ static bilu_status finish_factor(bilu_ctx *h, bilu_factor_stats &S, unsigned lon
   h->launches += launches;
   S.n_decisions += (int64_t)ctrl[CTRL_NDEC];
   S.n_near += (int64_t)ctrl[CTRL_NEAR];
+  S.n_perturbed += (int64_t)ctrl[CTRL_NPERT];
   int mlaunch = 0;
   bilu_status ms = finalize(h, ctrl, S, mlaunch);
   if (ms != BILU_OK) return ms;
@@ -1026,6 +1048,7 @@ extern "C" bilu_status bilu_factor_local(bilu_ctx *h, double tau, bilu_factor_st
   h->t_local_ms = ms;
   h->ndec_local = (int64_t)ctrl[CTRL_NDEC];
   h->nnear_local = (int64_t)ctrl[CTRL_NEAR];
+  h->npert_local = (int64_t)ctrl[CTRL_NPERT];
   h->launches += launches;
   h->dist_local_done = true;
   h->pack_valid = false;
@@ -1171,6 +1194,7 @@ extern "C" bilu_status bilu_factor_separators(bilu_ctx *h, bilu_factor_stats *st
   if (bs != BILU_OK) { if (st_out) *st_out = S; return bs; }
   S.n_decisions = h->ndec_local;
   S.n_near = h->nnear_local;
+  S.n_perturbed = h->npert_local;
   S.t_factor_ms = h->t_local_ms;
   bs = finish_factor(h, S, ctrl, ev.e[0], ev.e[1], ev.e[2], launches, nullptr);
   if (bs != BILU_OK) return bs;

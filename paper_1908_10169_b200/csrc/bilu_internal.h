@@ -49,6 +49,7 @@ enum : int {
   CTRL_FLOPS,
   CTRL_HPOOL,      // doubles used in the heavy-block pool
   CTRL_HCTX,       // heavy contexts used
+  CTRL_NPERT,      // pivot blocks perturbed (Sec. 3.6)
   CTRL_COUNT = 24
 };
 constexpr int CS = 16;   // ctrl stride: every control word on its own 128-byte line
@@ -113,6 +114,9 @@ struct DevFactor {
   int scale_rows;                       // ... into parts of this many rows
   int smem_bytes;
   double tau, near_rel;
+  // Sec. 3.6 perturbation of singular / ill-conditioned pivot blocks (R19)
+  int perturb; double ptau, prho, cond_max;
+  const double *alpha;                  // device scalar: max |a_ij|
   int exp;                              // experiment switches (diagnostics only)
 };
 

@@ -22,6 +22,16 @@ __global__ void permute_kernel(double *__restrict__ y, const double *__restrict_
   }
 }
 
+// max |x_i| (non-negative doubles order like their bit patterns): alpha of Sec. 3.6
+__global__ void maxabs_kernel(unsigned long long *out, const double *__restrict__ x, int64_t n) {
+  double m = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) m = fmax(m, fabs(x[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
 static int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -32,6 +42,13 @@ static int grid_for(int64_t n) {
 extern "C" cudaError_t bilu_launch_gather(double *dst, const double *src, const int64_t *map,
                                           int64_t n, cudaStream_t st) {
   gather_kernel<<<grid_for(n), 256, 0, st>>>(dst, src, map, n);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t bilu_launch_maxabs(double *out, const double *x, int64_t n, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  if (n > 0) maxabs_kernel<<<grid_for(n), 256, 0, st>>>((unsigned long long *)out, x, n);
   return cudaGetLastError();
 }
 

@@ -292,3 +292,64 @@ def test_c4_2000_blocks_parity():
     g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
     assert_parity(gf, of)
     assert st["n_blocks_final"] == of.nblk
+
+
+# ---------------- Sec. 3.6 perturbation (R19) ----------------
+PT = (1e-2, 1e-1, 1e12)
+
+
+def run_pair_pt(ip, ix, dv, bs, tau, agg=True):
+    from paper_1908_10169_b200 import BILU
+    g = BILU(ip, ix, dv, bs, aggregate=int(agg), perturb=1, perturb_tau=PT[0], perturb_rho=PT[1],
+             cond_max=PT[2])
+    st = g.factor(tau)
+    gf = g.export()
+    of = oracle.factor(ip, ix, dv, bs, tau, aggregate=agg, perturb=PT, overrides=overrides_from_near(gf.near))
+    return g, st, gf, of
+
+
+def test_perturbation_zero_column_block():
+    A = np.array([[2.0, 0.0, 0.5], [1.0, 0.0, 0.0], [0.0, 0.0, 4.0]])
+    ip, ix, dv = dense_to_csr(A)
+    g, st, gf, of = run_pair_pt(ip, ix, dv, [2, 1], 0.0, agg=False)
+    assert st["n_perturbed"] == 1 == of.n_perturbed
+    assert_parity(gf, of)
+
+
+def _singular_blocks_matrix(n, nsing, seed, bsz=2):
+    rng = np.random.default_rng(seed)
+    A = random_dd(n, 0.08, seed, dominance=1.6)
+    starts = rng.choice(np.arange(1, n // bsz - 1), nsing, replace=False) * bsz
+    for s0 in starts:
+        A[s0:s0 + bsz, :] = 0.0
+        A[:, s0:s0 + bsz] = 0.0
+        A[s0:s0 + bsz, s0:s0 + bsz] = rng.uniform(0.5, 1.5) * np.ones((bsz, bsz))   # rank 1, decoupled
+    return A
+
+
+@pytest.mark.parametrize("agg", [False, True])
+def test_perturbation_singular_blocks_match_oracle(agg):
+    A = _singular_blocks_matrix(160, 6, 21)
+    ip, ix, dv = dense_to_csr(A)
+    bs = [2] * 80
+    g, st, gf, of = run_pair_pt(ip, ix, dv, bs, 1e-3, agg)
+    assert st["n_perturbed"] == of.n_perturbed >= 6
+    assert_parity(gf, of)
+
+
+def test_perturbation_wide_singular_block():
+    """A rank-deficient 24 x 24 pivot block (multi-warp Gauss-Jordan path)."""
+    A = _singular_blocks_matrix(240, 2, 23, bsz=24)
+    ip, ix, dv = dense_to_csr(A)
+    bs = [24] * 10
+    g, st, gf, of = run_pair_pt(ip, ix, dv, bs, 1e-3, False)
+    assert st["n_perturbed"] == of.n_perturbed >= 2
+    assert_parity(gf, of)
+
+
+def test_perturbation_inactive_on_c2_reduced():
+    P = config2(N=16, leaf=64)
+    pip, pix, pdv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
+    g, st, gf, of = run_pair_pt(pip, pix, pdv, P.block_sizes, P.tau, True)
+    assert st["n_perturbed"] == 0 == of.n_perturbed
+    assert_parity(gf, of)

@@ -340,3 +340,64 @@ def test_aggregation_segments_reading_r18():
     L0, P0, U0 = dense_LPU(d, P.n)
     M1, M0 = L1 @ P1 @ U1, L0 @ P0 @ U0
     assert np.abs(M1 - M0).max() <= 1e-12 * np.abs(M0).max()
+
+
+# ---------------- Sec. 3.6 diagonal-block perturbation (R19) ----------------
+PT = (1e-2, 1e-1, 1e12)          # tau_p, rho, cond_max (SPEC default)
+
+
+def test_perturbation_inactive_on_well_conditioned_blocks():
+    """Strictly dominant input: no pivot block is singular or ill-conditioned, so the
+    factors with the perturbation enabled are those without it."""
+    A = random_dd(120, 0.1, 11, dominance=1.5)
+    ip, ix, dv = dense_to_csr(A)
+    bs = [4] * 30
+    a = oracle.factor(ip, ix, dv, bs, 1e-2)
+    b = oracle.factor(ip, ix, dv, bs, 1e-2, perturb=PT)
+    assert b.n_perturbed == 0
+    assert np.array_equal(a.Lv, b.Lv) and np.array_equal(a.Dv, b.Dv) and np.array_equal(a.Uv, b.Uv)
+
+
+def test_perturbation_zero_column_closed_form():
+    """Pivot block [[2, 0], [1, 0]] (zero column, "if d = 0"): its largest entry is
+    the diagonal zero, which becomes 0 (1 + rho 0) + sign(0) tau_p alpha = tau_p alpha;
+    rows are then nonzero.  D = [[2, 0], [1, t]]^{-1} = [[1/2, 0], [-1/(2t), 1/t]]."""
+    A = np.array([[2.0, 0.0, 0.5], [1.0, 0.0, 0.0], [0.0, 0.0, 4.0]])
+    ip, ix, dv = dense_to_csr(A)
+    with pytest.raises(oracle.OracleError):
+        oracle.factor(ip, ix, dv, [2, 1], 0.0, aggregate=False)
+    f = oracle.factor(ip, ix, dv, [2, 1], 0.0, aggregate=False, perturb=PT)
+    t = PT[0] * 4.0                                   # alpha = max |a_ij| = 4
+    D0 = f.block(0)[6]
+    np.testing.assert_allclose(D0, [[0.5, 0.0], [-1.0 / (2 * t), 1.0 / t]], rtol=1e-14)
+    assert f.n_perturbed == 1
+
+
+def test_perturbation_singular_block_bounded_modification():
+    """A singular pivot block ([[1, 1], [1, 1]] inside a dominant matrix) is perturbed and the
+    factorization completes; with tau = 0 (no dropping) L P U - Ã is zero except on the
+    perturbed diagonal block, where each entry moved by at most rho |p| delta + tau_p alpha
+    per perturbation pass (SPEC: a bounded modification)."""
+    rng = np.random.default_rng(5)
+    n = 12
+    A = np.zeros((n, n))
+    A[np.arange(n), np.arange(n)] = 6.0
+    A[np.arange(n - 1), np.arange(1, n)] = rng.uniform(-1, 1, n - 1)
+    A[np.arange(1, n), np.arange(n - 1)] = rng.uniform(-1, 1, n - 1)
+    A[4:6, 4:6] = [[1.0, 1.0], [1.0, 1.0]]            # singular diagonal block of block 2
+    A[4, 3] = A[5, 6] = A[3, 4] = A[6, 5] = 0.0         # decouple -> its Schur block stays singular
+    ip, ix, dv = dense_to_csr(A)
+    bs = [2] * 6
+    with pytest.raises(oracle.OracleError):
+        oracle.factor(ip, ix, dv, bs, 0.0, aggregate=False)
+    f = oracle.factor(ip, ix, dv, bs, 0.0, aggregate=False, perturb=PT)
+    assert f.n_perturbed == 1
+    from tests.parity import dense_LPU
+    L, P, U = dense_LPU(f, n)
+    E = L @ P @ U - A
+    mask = np.zeros((n, n), bool); mask[4:6, 4:6] = True
+    assert np.abs(E[~mask]).max() <= 1e-13 * np.abs(A).max()
+    alpha, (tp, rho, _) = np.abs(A).max(), PT
+    pmax = np.abs(L @ P @ U)[4:6, 4:6].max()
+    assert np.abs(E[mask]).max() > 0
+    assert np.abs(E[mask]).max() <= 3 * (rho * pmax * pmax + tp * alpha)
