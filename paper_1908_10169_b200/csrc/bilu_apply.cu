@@ -5,9 +5,10 @@
 // method": with P_K = D_K^{-1} and U = D Ũ,
 //   forward   w_F = x_F - sum_J L_J[rows in F, :] w_J          (unit block-lower L)
 //   backward  y_F = D_F (w_F - Ũ_F y[cols(Ũ_F)])              (U = D Ũ unit upper)
-// Both sweeps are persistent dataflow kernels over the final blocks (a block
-// starts when every block it reads is finished), pulling in a fixed order so
-// that the result is deterministic.
+// Both sweeps are persistent dataflow kernels over the final blocks, one warp per block
+// (16 independent warps per CTA): the forward sweep pushes L_J w_J into its targets with
+// native fp64 reductions (summation order unspecified: rounding only), the backward sweep
+// pulls from the blocks in its Ũ columns.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -15,90 +16,101 @@
 
 namespace bilu {
 
-constexpr int AT = 128;
+constexpr int AT = 512;             // 16 warps per CTA, each an independent worker
+constexpr int AW = AT / 32;
 
 __device__ __forceinline__ int a_ld_vol(const int *p) { return *(const volatile int *)p; }
-
-__device__ __forceinline__ int a_pop(const ApplyArgs &A, int *s_blk) {
-  if (threadIdx.x == 0) {
-    int F = -1;
-    unsigned long long idx = atomicAdd(&A.ctrl[1], 1ull);
-    if (idx < (unsigned long long)A.nF) {
-      while ((F = a_ld_vol(&A.queue[idx])) < 0) __nanosleep(32);
-    }
-    *s_blk = F;
-  }
-  __syncthreads();
-  int F = *s_blk;
-  __syncthreads();
-  return F;
+__device__ __forceinline__ void a_red_add(double *p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-__device__ __forceinline__ void a_release(const ApplyArgs &A, const int32_t *ptr, const int32_t *succ, int F) {
+// one warp pops the next ready block (lane 0), broadcast to the warp; -1 when all done
+__device__ __forceinline__ int a_pop_warp(const ApplyArgs &A) {
+  int F = -1;
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long idx = atomicAdd(&A.ctrl[1], 1ull);
+    if (idx < (unsigned long long)A.nF) {
+      while ((F = a_ld_vol(&A.queue[idx])) < 0) __nanosleep(20);
+    }
+  }
+  return __shfl_sync(0xffffffffu, F, 0);
+}
+
+__device__ __forceinline__ void a_release_warp(const ApplyArgs &A, const int32_t *ptr, const int32_t *succ, int F) {
   __threadfence();
-  __syncthreads();
-  for (int x = ptr[F] + threadIdx.x; x < ptr[F + 1]; x += AT) {
-    int T = succ[x];
+  __syncwarp();
+  for (int x = ptr[F] + (threadIdx.x & 31); x < ptr[F + 1]; x += 32) {
+    const int T = succ[x];
     if (atomicSub(&A.cnt[T], 1) == 1) {
-      unsigned long long slot = atomicAdd(&A.ctrl[0], 1ull);
+      const unsigned long long slot = atomicAdd(&A.ctrl[0], 1ull);
       __threadfence();
       *(volatile int *)&A.queue[slot] = T;
     }
   }
 }
 
+// forward sweep, push form: when block J is final (every block with L rows in J has pushed),
+// w[rows of L_J] -= L_J w_J with native fp64 reductions, then J's targets are released
 __global__ void __launch_bounds__(AT) apply_fwd_kernel(ApplyArgs A) {
-  __shared__ int s_blk;
-  __shared__ double s_w[128];
+  __shared__ double s_w[AW][128];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *wj = s_w[wid];
   while (true) {
-    const int F = a_pop(A, &s_blk);
-    if (F < 0) break;
+    const int J = a_pop_warp(A);
+    if (J < 0) break;
     __threadfence();
-    const int s = A.fbstart[F], b = A.fbstart[F + 1] - s;
-    for (int i = threadIdx.x; i < b; i += AT) s_w[i] = __ldcg(A.w + s + i);
-    __syncthreads();
-    for (int x = A.fl_ptr[F]; x < A.fl_ptr[F + 1]; ++x) {
-      const int J = A.fl_rec[3 * x], r0 = A.fl_rec[3 * x + 1], r1 = A.fl_rec[3 * x + 2];
-      const int sJ = A.fbstart[J], bJ = A.fbstart[J + 1] - sJ;
-      const int32_t *rows = A.Lidx + A.Lrow_off[J];
-      const double *Lv = A.Lval + A.Lval_off[J];
-      for (int p = r0 + threadIdx.x; p < r1; p += AT) {
-        const double *l = Lv + (int64_t)p * bJ;
-        double acc = 0.0;
-        for (int t = 0; t < bJ; ++t) acc = fma(l[t], __ldcg(A.w + sJ + t), acc);
-        s_w[rows[p] - s] -= acc;
-      }
-      __syncthreads();
+    const int sJ = A.fbstart[J], bJ = A.fbstart[J + 1] - sJ;
+    for (int t = lane; t < bJ; t += 32) wj[t] = __ldcg(A.w + sJ + t);
+    __syncwarp();
+    const int m = A.Lm[J];
+    const int32_t *rows = A.Lidx + A.Lrow_off[J];
+    const double *Lv = A.Lval + A.Lval_off[J];
+    for (int p = lane; p < m; p += 32) {
+      const double *l = Lv + (int64_t)p * bJ;
+      double acc0 = 0.0, acc1 = 0.0;
+      int t = 0;
+      for (; t + 1 < bJ; t += 2) { acc0 = fma(l[t], wj[t], acc0); acc1 = fma(l[t + 1], wj[t + 1], acc1); }
+      if (t < bJ) acc0 = fma(l[t], wj[t], acc0);
+      a_red_add(A.w + rows[p], -(acc0 + acc1));
     }
-    for (int i = threadIdx.x; i < b; i += AT) A.w[s + i] = s_w[i];
-    a_release(A, A.fs_ptr, A.fs, F);
+    a_release_warp(A, A.fs_ptr, A.fs, J);
   }
 }
 
+// backward sweep, pull form: y_F = D_F (w_F - Ũ_F y[cols(Ũ_F)]) once every block in F's Ũ
+// columns is final.  Lanes over the rows of F (groups of lanes split the columns when b < 32)
 __global__ void __launch_bounds__(AT) apply_bwd_kernel(ApplyArgs A) {
-  __shared__ int s_blk;
-  __shared__ double s_z[128];
+  __shared__ double s_z[AW][128];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *z = s_z[wid];
   while (true) {
-    const int F = a_pop(A, &s_blk);
+    const int F = a_pop_warp(A);
     if (F < 0) break;
     __threadfence();
     const int s = A.fbstart[F], b = A.fbstart[F + 1] - s;
     const int c = A.Uc[F];
     const int32_t *cols = A.Uidx + A.Ucol_off[F];
     const double *Uv = A.Uval + A.Uval_off[F];
-    for (int r = threadIdx.x; r < b; r += AT) {
-      double acc = A.w[s + r];
-      for (int q = 0; q < c; ++q) acc = fma(-Uv[(int64_t)q * b + r], __ldcg(A.y + cols[q]), acc);
-      s_z[r] = acc;
-    }
-    __syncthreads();
-    const double *D = A.D + A.D_off[F];
-    for (int r = threadIdx.x; r < b; r += AT) {
+    int R = 1;
+    while (R < b && R < 32) R <<= 1;                 // lanes per row group
+    const int G = 32 / R, gi = lane / R, rl = lane % R;
+    for (int r0 = 0; r0 < b; r0 += R) {
+      const int r = r0 + rl;
       double acc = 0.0;
-      for (int t = 0; t < b; ++t) acc = fma(D[r + (int64_t)t * b], s_z[t], acc);
+      if (r < b)
+        for (int q = gi; q < c; q += G) acc = fma(Uv[(int64_t)q * b + r], __ldcg(A.y + cols[q]), acc);
+      for (int o = R; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (gi == 0 && r < b) z[r] = __ldcg(A.w + s + r) - acc;
+    }
+    __syncwarp();
+    const double *D = A.D + A.D_off[F];
+    for (int r = lane; r < b; r += 32) {
+      double acc = 0.0;
+      for (int t = 0; t < b; ++t) acc = fma(D[r + (int64_t)t * b], z[t], acc);
       A.y[s + r] = acc;
     }
-    a_release(A, A.bs_ptr, A.bs, F);
+    __syncwarp();
+    a_release_warp(A, A.bs_ptr, A.bs, F);
   }
 }
 

@@ -1400,7 +1400,7 @@ extern "C" bilu_status bilu_apply(bilu_ctx *h, const double *x, double *y, void 
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
   ApplyArgs &A = h->AA;
   const int nF = h->fin.nF;
-  const int grid = std::max(1, std::min(nF, h->sms * 8));
+  const int grid = std::max(1, std::min((nF + 15) / 16, h->sms * 2));   // 16 warp-workers per CTA
   CUDA_TRY(h, bilu_launch_permute(h->d_w, x, h->d_perm, h->n, 0, st));
   for (int pass = 0; pass < 2; ++pass) {
     const int32_t *cnt0 = pass ? h->d_cnt_b0 : h->d_cnt_f0;
