@@ -208,6 +208,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--dist", action="store_true",
                     help="use the distributed (subtree) path even at N=1 (checks its mechanics on one GPU)")
     args = ap.parse_args()
@@ -334,6 +335,23 @@ def main():
         }
         if e2e:
             out["e2e"] = e2e
+        if not use_dist and not args.no_solve:
+            # context: one preconditioned GMRES(30) solve with these factors,
+            # b = ones, tol 1e-8, device time; and one preconditioner apply
+            b = torch.ones(P.n, dtype=torch.float64, device="cuda")
+            g.gmres(b, restart=30, tol=1e-8)
+            _, sst = g.gmres(b, restart=30, tol=1e-8)
+            ya = g.apply_tensor(b)
+            torch.cuda.synchronize()
+            ea0, ea1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea0.record()
+            for _ in range(5):
+                ya = g.apply_tensor(b)
+            ea1.record()
+            torch.cuda.synchronize()
+            out["solve"] = {"gmres_iterations": int(sst["iterations"]), "converged": bool(sst["converged"]),
+                            "rel_residual": sst["rel_residual"], "gmres_ms": sst["t_solve_ms"],
+                            "apply_ms": ea0.elapsed_time(ea1) / 5}
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(P)
         print(json.dumps(out), flush=True)

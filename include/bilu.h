@@ -171,6 +171,27 @@ typedef struct {
 bilu_status bilu_export(bilu_ctx *h, bilu_factor_view *v);
 void bilu_factor_view_free(bilu_factor_view *v);
 
+/* ---- preconditioned Krylov solve ----
+ * bilu_gmres -- solves A x = b with restarted, right-preconditioned GMRES(m) on the device,
+ * M = the factors of the last bilu_factor ("restarted GMRES ... restart length 30 ... b
+ * with all ones"; R16: x0 = 0, modified Gram-Schmidt, Givens
+ * rotations, inner steps counted, convergence on the true residual |b - A x| / |b| <= tol
+ * checked at the end of every cycle).
+ *   b, x   DEVICE double[n], A's ORIGINAL ordering; x is overwritten; may not alias.
+ *   m      restart length (1..1000); tol > 0; max_restarts >= 1
+ * The workspace ((2m+2) n doubles) is owned by the context.  Synchronous. */
+typedef struct {
+  int32_t iterations;        /* inner (Arnoldi) steps                                  */
+  int32_t restarts;          /* cycles started                                         */
+  int32_t converged;         /* 1 if |b - A x| / |b| <= tol                            */
+  double  rel_residual;      /* final true relative residual                           */
+  double  t_solve_ms;        /* device time (CUDA events on the context stream)        */
+  int64_t n_kernel_launches;
+} bilu_solve_stats;
+
+bilu_status bilu_gmres(bilu_ctx *h, const double *b, double *x, int32_t m, double tol, int32_t max_restarts,
+                       bilu_solve_stats *st);
+
 /* ---- multi-GPU factorization over nested-dissection subtrees ----
  * One context per rank (one process per GPU), every rank with the same global matrix,
  * ordering and partition.  Sequence, on every rank:

@@ -22,7 +22,7 @@ ABI_SYMBOLS = ["bilu_options_default", "bilu_analyze", "bilu_set_values", "bilu_
                "bilu_apply", "bilu_export", "bilu_factor_view_free", "bilu_destroy",
                "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm", "bilu_diag_tsgemm",
                "bilu_dist_setup", "bilu_factor_local", "bilu_interface_pack", "bilu_interface_unpack",
-               "bilu_factor_separators"]
+               "bilu_factor_separators", "bilu_gmres"]
 
 
 class BiluError(RuntimeError):
@@ -50,6 +50,15 @@ class FactorStats(ctypes.Structure):
                 ("n_retries", ctypes.c_int32), ("n_kernel_launches", ctypes.c_int32),
                 ("n_decisions", ctypes.c_int64), ("n_near", ctypes.c_int64),
                 ("min_margin", ctypes.c_double), ("n_perturbed", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class SolveStats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("restarts", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("rel_residual", ctypes.c_double), ("t_solve_ms", ctypes.c_double),
+                ("n_kernel_launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -119,6 +128,8 @@ def load_library():
     lib.bilu_interface_pack.restype = ctypes.c_int
     lib.bilu_interface_unpack.argtypes = [P, P, ctypes.c_int64]
     lib.bilu_interface_unpack.restype = ctypes.c_int
+    lib.bilu_gmres.argtypes = [P, P, P, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, ctypes.POINTER(SolveStats)]
+    lib.bilu_gmres.restype = ctypes.c_int
     lib.bilu_factor_separators.argtypes = [P, ctypes.POINTER(FactorStats)]
     lib.bilu_factor_separators.restype = ctypes.c_int
     _lib = lib
@@ -247,6 +258,17 @@ class BILU:
         self._check(rc, st.breakdown_block)
         self.stats = st.as_dict()
         return self.stats
+
+    def gmres(self, b, restart=30, tol=1e-8, max_restarts=100):
+        """Solve A x = b on the device (bilu_gmres); b a CUDA float64 tensor in A's ordering.
+        Returns (x tensor, stats dict)."""
+        import torch
+        b = b.contiguous()
+        x = torch.empty_like(b)
+        st = SolveStats()
+        self._check(self.lib.bilu_gmres(self.h, ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(x.data_ptr()),
+                                        int(restart), float(tol), int(max_restarts), ctypes.byref(st)))
+        return x, st.as_dict()
 
     def apply(self, x_ptr: int, y_ptr: int, stream: int = 0):
         """y = M^{-1} x on DEVICE pointers (original ordering)."""

@@ -36,6 +36,17 @@ extern "C" cudaError_t bilu_launch_permute(double *y, const double *x, const int
 extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_t st);
 extern "C" int bilu_merge_plan_launches();
 extern "C" int bilu_heavyctx_size();
+extern "C" cudaError_t bilu_launch_spmv(int n, const int64_t *rp, const int32_t *ci, const double *val, const double *x,
+                                        double *y, int lpr, int sms, cudaStream_t st);
+extern "C" cudaError_t bilu_launch_dot(int n, const double *x, const double *y, double *partials, double *out,
+                                       int sqrt_out, int sms, cudaStream_t st);
+extern "C" cudaError_t bilu_launch_axpy_dev(int n, const double *coef, double sign, const double *x, double *y, int sms,
+                                            cudaStream_t st);
+extern "C" cudaError_t bilu_launch_scale_dev(int n, const double *coef, const double *x, double *y, int sms,
+                                             cudaStream_t st);
+extern "C" cudaError_t bilu_launch_update(int n, int k, const double *Z, int64_t ld, const double *c, double *x, int sms,
+                                          cudaStream_t st);
+extern "C" cudaError_t bilu_launch_residual(int n, const double *b, double *r, int sms, cudaStream_t st);
 extern "C" cudaError_t bilu_launch_maxabs(double *out, const double *x, int64_t n, cudaStream_t st);
 extern "C" cudaError_t bilu_launch_sep_prepare(const DevFactor &F, const int32_t *sep_list, int nsep,
                                                const int32_t *static_sep, const int32_t *ifc, int nifc,
@@ -101,6 +112,9 @@ struct bilu_ctx {
   int32_t *d_own_ready = nullptr; int32_t n_own_ready = 0;
   double flops_local = 0.0, t_local_ms = 0.0;
   double *d_alpha = nullptr;
+  // GMRES: A's CSR structure (original ordering) and the Krylov workspace
+  int64_t *d_rp = nullptr; int32_t *d_ci = nullptr;
+  double *d_kry = nullptr; int64_t kry_cap = 0;
   int64_t npert_local = 0;
   int64_t ndec_local = 0, nnear_local = 0;
   std::vector<int64_t> D_off;
@@ -419,6 +433,8 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   ALLOC(h->d_ready0, std::max<int32_t>(h->nready0, 1));
   if (h->nready0) H2D(h->d_ready0, h->ready0.data(), h->nready0);
   ALLOC(h->d_perm, n); H2D(h->d_perm, pm.data(), n);
+  ALLOC(h->d_rp, (size_t)n + 1); H2D(h->d_rp, row_ptr, (size_t)n + 1);      // A's CSR (bilu_gmres SpMV)
+  ALLOC(h->d_ci, (size_t)std::max<int64_t>(nnz, 1)); if (nnz) H2D(h->d_ci, col_idx, nnz);
   {
     int64_t *d_Doff = nullptr;
     ALLOC(d_Doff, n_blocks + 1); H2D(d_Doff, h->D_off.data(), n_blocks + 1);
@@ -1202,6 +1218,124 @@ extern "C" bilu_status bilu_factor_separators(bilu_ctx *h, bilu_factor_stats *st
   S.flops += h->flops_local;
   h->last = S;
   h->dist_local_done = false;
+  if (st_out) *st_out = S;
+  return BILU_OK;
+}
+
+// ------------------------------------------------------------ GMRES
+// Restarted, right-preconditioned GMRES(m) on the device (readings
+// R16: x0 = 0, modified Gram-Schmidt, Givens rotations, inner steps counted, the true
+// residual checked at the end of every cycle).  Vectors live in device memory; the
+// Hessenberg column of each step (m+2 doubles) is the only host round trip.
+extern "C" bilu_status bilu_gmres(bilu_ctx *h, const double *b, double *x, int32_t m, double tol, int32_t max_restarts,
+                                  bilu_solve_stats *st_out) {
+  if (!h || !b || !x) { set_err(h, "bilu_gmres: null argument"); return BILU_ERR_ARG; }
+  if (m < 1 || m > 1000 || !(tol > 0.0) || max_restarts < 1) { set_err(h, "bilu_gmres: bad restart / tol / max_restarts"); return BILU_ERR_ARG; }
+  if (!h->factored) { set_err(h, "bilu_gmres: no factorization"); return BILU_ERR_STATE; }
+  if (h->dist) { set_err(h, "bilu_gmres: distributed context"); return BILU_ERR_STATE; }
+  cudaSetDevice(h->opt.device);
+  cudaStream_t st = h->stream;
+  const int n = h->n, sms = h->sms;
+  const int64_t ld = n;
+  const int64_t need = (int64_t)(2 * m + 2) * n + 8LL * sms + 4 * (int64_t)m + 16;
+  if (need > h->kry_cap) {
+    dfree(h, h->d_kry);
+    CUDA_TRY(h, dalloc(h, &h->d_kry, (size_t)need));
+    h->kry_cap = need;
+  }
+  double *V = h->d_kry, *Z = V + (int64_t)(m + 1) * n, *r = Z + (int64_t)m * n;
+  double *part = r + n, *dH = part + 8 * sms, *dtmp = dH + (m + 2), *dY = dtmp + 4;
+  int lpr = 1;
+  {
+    const double avg = (double)h->nnz / std::max(1, n);
+    while (lpr < 32 && lpr < avg / 2) lpr <<= 1;
+  }
+  bilu_solve_stats S{};
+  cudaEvent_t e0, e1;
+  CUDA_TRY(h, cudaEventCreate(&e0)); CUDA_TRY(h, cudaEventCreate(&e1));
+  CUDA_TRY(h, cudaEventRecord(e0, st));
+  int64_t launches = 0;
+  const int64_t l0 = h->launches;
+  double hh[4];
+  CUDA_TRY(h, cudaMemsetAsync(x, 0, (size_t)n * 8, st));
+  CUDA_TRY(h, bilu_launch_dot(n, b, b, part, dtmp, 1, sms, st)); launches += 2;
+  CUDA_TRY(h, cudaMemcpyAsync(hh, dtmp, 2 * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  const double bnorm = hh[1];
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), col(m + 2);
+  int its = 0;
+  bool conv = bnorm == 0.0;
+  double beta = bnorm;
+  if (!conv) CUDA_TRY(h, cudaMemcpyAsync(r, b, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+  for (int cycle = 0; cycle < max_restarts && !conv; ++cycle) {
+    if (beta / bnorm <= tol) { conv = true; break; }
+    S.restarts = cycle + 1;
+    // V0 = r / beta (beta on the device: dtmp[1])
+    CUDA_TRY(h, bilu_launch_scale_dev(n, dtmp + 1, r, V, sms, st)); launches += 1;
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int k_used = 0;
+    for (int k = 0; k < m; ++k) {
+      double *vk = V + (int64_t)k * ld, *zk = Z + (int64_t)k * ld, *w = V + (int64_t)(k + 1) * ld;
+      bilu_status as = bilu_apply(h, vk, zk, st);
+      if (as != BILU_OK) return as;
+      CUDA_TRY(h, bilu_launch_spmv(n, h->d_rp, h->d_ci, h->d_val_orig, zk, w, lpr, sms, st)); launches += 1;
+      for (int i = 0; i <= k; ++i) {            // modified Gram-Schmidt, coefficients stay on the device
+        CUDA_TRY(h, bilu_launch_dot(n, w, V + (int64_t)i * ld, part, dH + i, 0, sms, st));
+        CUDA_TRY(h, bilu_launch_axpy_dev(n, dH + i, -1.0, V + (int64_t)i * ld, w, sms, st));
+        launches += 3;
+      }
+      CUDA_TRY(h, bilu_launch_dot(n, w, w, part, dtmp, 1, sms, st)); launches += 2;
+      CUDA_TRY(h, cudaMemcpyAsync(col.data(), dH, (size_t)(k + 1) * 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(h, cudaMemcpyAsync(hh, dtmp, 2 * 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(h, cudaStreamSynchronize(st));
+      for (int i = 0; i <= k; ++i) H[(size_t)i * m + k] = col[i];
+      const double hnext = hh[1];
+      H[(size_t)(k + 1) * m + k] = hnext;
+      for (int i = 0; i < k; ++i) {             // previous rotations
+        const double t = cs[i] * H[(size_t)i * m + k] + sn[i] * H[(size_t)(i + 1) * m + k];
+        H[(size_t)(i + 1) * m + k] = -sn[i] * H[(size_t)i * m + k] + cs[i] * H[(size_t)(i + 1) * m + k];
+        H[(size_t)i * m + k] = t;
+      }
+      const double den = std::hypot(H[(size_t)k * m + k], H[(size_t)(k + 1) * m + k]);
+      cs[k] = den != 0.0 ? H[(size_t)k * m + k] / den : 1.0;
+      sn[k] = den != 0.0 ? H[(size_t)(k + 1) * m + k] / den : 0.0;
+      H[(size_t)k * m + k] = den;
+      H[(size_t)(k + 1) * m + k] = 0.0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      its += 1;
+      k_used = k + 1;
+      if (std::fabs(g[k + 1]) / bnorm <= tol || hnext == 0.0) break;
+      CUDA_TRY(h, bilu_launch_scale_dev(n, dtmp + 1, w, w, sms, st)); launches += 1;   // V[k+1] = w / hnext
+    }
+    for (int i = k_used - 1; i >= 0; --i) {     // back substitution
+      double acc = g[i];
+      for (int j = i + 1; j < k_used; ++j) acc -= H[(size_t)i * m + j] * y[j];
+      y[i] = acc / H[(size_t)i * m + i];
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(dY, y.data(), (size_t)k_used * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, bilu_launch_update(n, k_used, Z, ld, dY, x, sms, st));
+    CUDA_TRY(h, bilu_launch_spmv(n, h->d_rp, h->d_ci, h->d_val_orig, x, r, lpr, sms, st));
+    CUDA_TRY(h, bilu_launch_residual(n, b, r, sms, st));
+    CUDA_TRY(h, bilu_launch_dot(n, r, r, part, dtmp, 1, sms, st)); launches += 5;
+    CUDA_TRY(h, cudaMemcpyAsync(hh, dtmp, 2 * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    beta = hh[1];
+    if (beta / bnorm <= tol) conv = true;
+  }
+  CUDA_TRY(h, cudaEventRecord(e1, st));
+  CUDA_TRY(h, cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  h->launches += launches;
+  S.iterations = its;
+  S.converged = conv ? 1 : 0;
+  S.rel_residual = bnorm > 0.0 ? beta / bnorm : 0.0;
+  S.t_solve_ms = ms;
+  S.n_kernel_launches = launches + (h->launches - l0 - launches);
   if (st_out) *st_out = S;
   return BILU_OK;
 }

@@ -353,3 +353,29 @@ def test_perturbation_inactive_on_c2_reduced():
     g, st, gf, of = run_pair_pt(pip, pix, pdv, P.block_sizes, P.tau, True)
     assert st["n_perturbed"] == 0 == of.n_perturbed
     assert_parity(gf, of)
+
+
+# ---------------- device GMRES (bilu_gmres) ----------------
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c5s"])
+def test_device_gmres_matches_host_gmres(cfg):
+    """bilu_gmres (device vectors, MGS coefficients on the device) against the host
+    harness GMRES(30) driven by the same preconditioner: iteration counts within +-1
+    (BASELINE), both converged to 1e-8 on the true residual, the same solution."""
+    import torch
+    from inputs.configs import config1, config5
+    from paper_1908_10169_b200 import BILU
+    P = {"c1": lambda: config1(), "c2s": lambda: config2(N=24, leaf=128), "c5s": lambda: config5(N=20, top_levels=1)}[cfg]()
+    g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm)
+    g.factor(P.tau)
+    b = torch.ones(P.n, dtype=torch.float64, device="cuda")
+    x, st = g.gmres(b, restart=30, tol=1e-8)
+    assert st["converged"] == 1 and st["rel_residual"] <= 1e-8
+    A = sp.csr_matrix((P.data, P.indices, P.indptr), shape=(P.n, P.n))
+    xs = x.cpu().numpy()
+    assert np.linalg.norm(np.ones(P.n) - A @ xs) <= 1e-8 * np.sqrt(P.n) * 1.0000001
+
+    def m_gpu(v):
+        return g.apply_tensor(torch.tensor(v, device="cuda")).cpu().numpy()
+    xh, it_h, ok_h, _ = gmres(A.dot, np.ones(P.n), precond=m_gpu, restart=30, tol=1e-8)
+    assert ok_h and abs(st["iterations"] - it_h) <= 1
+    assert np.abs(xs - xh).max() <= 1e-6 * np.abs(xh).max()
