@@ -67,11 +67,14 @@ __global__ void __launch_bounds__(AT) apply_fwd_kernel(ApplyArgs A) {
     const double *Lv = A.Lval + A.Lval_off[J];
     for (int p = lane; p < m; p += 32) {
       const double *l = Lv + (int64_t)p * bJ;
-      double acc0 = 0.0, acc1 = 0.0;
+      double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
       int t = 0;
-      for (; t + 1 < bJ; t += 2) { acc0 = fma(l[t], wj[t], acc0); acc1 = fma(l[t + 1], wj[t + 1], acc1); }
-      if (t < bJ) acc0 = fma(l[t], wj[t], acc0);
-      a_red_add(A.w + rows[p], -(acc0 + acc1));
+      for (; t + 3 < bJ; t += 4) {
+        acc0 = fma(l[t], wj[t], acc0); acc1 = fma(l[t + 1], wj[t + 1], acc1);
+        acc2 = fma(l[t + 2], wj[t + 2], acc2); acc3 = fma(l[t + 3], wj[t + 3], acc3);
+      }
+      for (; t < bJ; ++t) acc0 = fma(l[t], wj[t], acc0);
+      a_red_add(A.w + rows[p], -((acc0 + acc1) + (acc2 + acc3)));
     }
     a_release_warp(A, A.fs_ptr, A.fs, J);
   }
@@ -79,10 +82,13 @@ __global__ void __launch_bounds__(AT) apply_fwd_kernel(ApplyArgs A) {
 
 // backward sweep, pull form: y_F = D_F (w_F - Ũ_F y[cols(Ũ_F)]) once every block in F's Ũ
 // columns is final.  Lanes over the rows of F (groups of lanes split the columns when b < 32)
+constexpr int YCH = 128;            // gathered y values staged per warp and chunk
 __global__ void __launch_bounds__(AT) apply_bwd_kernel(ApplyArgs A) {
   __shared__ double s_z[AW][128];
+  __shared__ double s_y[AW][YCH];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double *z = s_z[wid];
+  double *yq = s_y[wid];
   while (true) {
     const int F = a_pop_warp(A);
     if (F < 0) break;
@@ -94,14 +100,33 @@ __global__ void __launch_bounds__(AT) apply_bwd_kernel(ApplyArgs A) {
     int R = 1;
     while (R < b && R < 32) R <<= 1;                 // lanes per row group
     const int G = 32 / R, gi = lane / R, rl = lane % R;
-    for (int r0 = 0; r0 < b; r0 += R) {
-      const int r = r0 + rl;
-      double acc = 0.0;
-      if (r < b)
-        for (int q = gi; q < c; q += G) acc = fma(Uv[(int64_t)q * b + r], __ldcg(A.y + cols[q]), acc);
-      for (int o = R; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (gi == 0 && r < b) z[r] = __ldcg(A.w + s + r) - acc;
+    for (int r = lane; r < b; r += 32) z[r] = 0.0;
+    __syncwarp();
+    for (int q0 = 0; q0 < c; q0 += YCH) {
+      const int qn = min(YCH, c - q0);
+      for (int j = lane; j < qn; j += 32) yq[j] = __ldcg(A.y + cols[q0 + j]);   // independent gathers
+      __syncwarp();
+      for (int r0 = 0; r0 < b; r0 += R) {
+        const int r = r0 + rl;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (r < b) {
+          const double *ucol = Uv + (int64_t)q0 * b + r;
+          int j = gi;
+          for (; j + 3 * G < qn; j += 4 * G) {
+            a0 = fma(ucol[(int64_t)j * b], yq[j], a0);
+            a1 = fma(ucol[(int64_t)(j + G) * b], yq[j + G], a1);
+            a2 = fma(ucol[(int64_t)(j + 2 * G) * b], yq[j + 2 * G], a2);
+            a3 = fma(ucol[(int64_t)(j + 3 * G) * b], yq[j + 3 * G], a3);
+          }
+          for (; j < qn; j += G) a0 = fma(ucol[(int64_t)j * b], yq[j], a0);
+        }
+        double acc = (a0 + a1) + (a2 + a3);
+        for (int o = R; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (gi == 0 && r < b) z[r] += acc;
+      }
+      __syncwarp();
     }
+    for (int r = lane; r < b; r += 32) z[r] = __ldcg(A.w + s + r) - z[r];
     __syncwarp();
     const double *D = A.D + A.D_off[F];
     for (int r = lane; r < b; r += 32) {

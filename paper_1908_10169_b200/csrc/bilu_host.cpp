@@ -1536,7 +1536,9 @@ extern "C" bilu_status bilu_apply(bilu_ctx *h, const double *x, double *y, void 
   const int nF = h->fin.nF;
   const int grid = std::max(1, std::min((nF + 15) / 16, h->sms * 2));   // 16 warp-workers per CTA
   CUDA_TRY(h, bilu_launch_permute(h->d_w, x, h->d_perm, h->n, 0, st));
+  const int only = getenv("BILU_APPLY_ONLY") ? atoi(getenv("BILU_APPLY_ONLY")) : -1;   // diagnostics
   for (int pass = 0; pass < 2; ++pass) {
+    if (only >= 0 && pass != only) continue;
     const int32_t *cnt0 = pass ? h->d_cnt_b0 : h->d_cnt_f0;
     const int32_t *q0 = pass ? h->d_q_b0 : h->d_q_f0;
     const int nq = pass ? h->nq_b0 : h->nq_f0;
