@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
   __shared__ int s_tmp[MW + 1];
   __shared__ int s_cnt[130];
   __shared__ int s_mo[130];       // member offsets o_j, j = a..k+1
+  __shared__ int s_mi[130], s_ci[130];   // per member: kept rows / cols inside the run (a prefix)
   const int tid = threadIdx.x;
   const int nF = *M.nF;
   double *gbase = dwork + (size_t)blockIdx.x * dwork_per_cta;
@@ -529,6 +530,11 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
     }
     const int nm = k - a + 1;
     for (int x = tid; x <= nm; x += MT) s_mo[x] = M.bstart[a + x] - sa;
+    for (int x = tid; x < nm; x += MT) {   // one binary search per member list, shared by all threads
+      const int j = a + x;
+      s_mi[x] = m_lbound(M.Lidx + M.Lrow_off[j], 0, M.Lm[j], ek);
+      s_ci[x] = m_lbound(M.Uidx + M.Ucol_off[j], 0, M.Uc[j], ek);
+    }
     double *Laa, *Uaa, *Linv, *G;
     if (P <= ARITH_PSMEM) { Laa = sLU; Uaa = sLU + P * P; Linv = gbase; }
     else { Laa = gbase; Uaa = gbase + (size_t)P * P; Linv = Uaa + (size_t)P * P; }
@@ -547,7 +553,7 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
       const int32_t *rows = M.Lidx + M.Lrow_off[j];
       const double *Lv = M.Lval + M.Lval_off[j];
       const int mj = M.Lm[j];
-      const int mi = m_lbound(rows, 0, mj, ek);      // rows inside the run are a prefix
+      const int mi = s_mi[x];      // rows inside the run are a prefix
       for (int it = tid; it < mi * bj; it += MT) {
         const int p = it / bj, t = it - p * bj;
         Laa[(size_t)(rows[p] - sa) * P + oj + t] = Lv[it];
@@ -556,7 +562,7 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
       const double *Uv = M.Uval + M.Uval_off[j];
       const double *Dj = M.D + M.D_off[j];
       const int cj = M.Uc[j];
-      const int ci = m_lbound(cols, 0, cj, ek);
+      const int ci = s_ci[x];
       for (int it = tid; it < ci * bj; it += MT) {
         const int q = it / bj, r = it - q * bj;
         double acc = 0.0;
@@ -578,7 +584,9 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
       }
       __syncthreads();
     }
-    // D^ (column-major in Dout): T = D_agg Linv, then U_aa D^ = T, members last to first
+    // D^ (column-major): T = D_agg Linv, then U_aa D^ = T, members last to first; computed in
+    // the shared scratch (idle in this phase) when it fits, then stored to Dout
+    double *Dw = (P <= ARITH_PSMEM) ? (double *)scratch : Dout;
     for (int x = 0; x < nm; ++x) {
       const int om = s_mo[x], bm = s_mo[x + 1] - om;
       const double *Dj = M.D + M.D_off[a + x];
@@ -586,7 +594,7 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
         const int r = it % bm, c = it / bm;
         double acc = 0.0;
         for (int t = 0; t < bm; ++t) acc = fma(Dj[r + (size_t)t * bm], Linv[(size_t)(om + t) * P + c], acc);
-        Dout[(size_t)c * P + om + r] = acc;
+        Dw[(size_t)c * P + om + r] = acc;
       }
     }
     __syncthreads();
@@ -596,10 +604,14 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
         const int r = om + it % bm, c = it / bm;
         double acc = 0.0;
         const double *ur = Uaa + (size_t)r * P;
-        const double *dc = Dout + (size_t)c * P;
+        const double *dc = Dw + (size_t)c * P;
         for (int t = e; t < P; ++t) acc = fma(ur[t], dc[t], acc);
-        Dout[(size_t)c * P + r] -= acc;
+        Dw[(size_t)c * P + r] -= acc;
       }
+      __syncthreads();
+    }
+    if (Dw != Dout) {
+      for (int i = tid; i < P * P; i += MT) Dout[i] = Dw[i];
       __syncthreads();
     }
     // ---- L^ rows: union, gathered L_g (u x P row-major) in G, L^ = G Linv
@@ -619,7 +631,7 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
           const int32_t *rows = M.Lidx + M.Lrow_off[j];
           const double *Lv = M.Lval + M.Lval_off[j];
           const int mj = M.Lm[j];
-          const int mi = m_lbound(rows, 0, mj, ek);
+          const int mi = s_mi[x];
           for (int it = mi * bj + tid; it < mj * bj; it += MT) {
             const int p = it / bj, t = it - p * bj;
             G[(size_t)m_lbound(Rl, 0, u, rows[p]) * P + oj + t] = Lv[it];
@@ -646,7 +658,7 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
           const int32_t *cols = M.Uidx + M.Ucol_off[j];
           const double *Uv = M.Uval + M.Uval_off[j];
           const int cj = M.Uc[j];
-          const int ci = m_lbound(cols, 0, cj, ek);
+          const int ci = s_ci[x];
           for (int it = ci * bj + tid; it < cj * bj; it += MT) {
             const int q = it / bj, t = it - q * bj;
             G[(size_t)m_lbound(Cl, 0, v, cols[q]) * P + oj + t] = Uv[it];
