@@ -85,13 +85,6 @@ __device__ __forceinline__ int lbound(const int *a, int lo, int hi, int key) {
   }
   return lo;
 }
-__device__ __forceinline__ int lbound_cg(const int *a, int lo, int hi, int key) {
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (__ldcg(a + mid) < key) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
 
 // exclusive scan of a[0..n) in place (any memory), returns the total. CTA-wide.
 // Each warp owns a contiguous chunk and walks it in coalesced 32-element tiles
@@ -275,24 +268,6 @@ struct Contrib {
   int last;           // largest candidate key of this contributor (-1: none)
 };
 
-// ---- open-addressing hash set of row (or column) indices -> dense buffer slot
-__device__ __forceinline__ unsigned hslot(int key, unsigned mask) {
-  return ((unsigned)key * 0x9E3779B1u) >> 7 & mask;
-}
-__device__ __forceinline__ void hinsert(int *keys, unsigned mask, int key) {
-  unsigned h = hslot(key, mask);
-  while (true) {
-    int old = atomicCAS(&keys[h], -1, key);
-    if (old == -1 || old == key) return;
-    h = (h + 1) & mask;
-  }
-}
-__device__ __forceinline__ int hlookup(const int *keys, const int *vals, unsigned mask, int key) {
-  unsigned h = hslot(key, mask);
-  while (keys[h] != key) h = (h + 1) & mask;
-  return vals[h];
-}
-
 // rank sort of distinct keys: out[rank(x)] = x (n small; thread per element)
 __device__ void cta_rank_sort(const int *keys, int n, int *out) {
   for (int x = threadIdx.x; x < n; x += NT) {
@@ -302,65 +277,6 @@ __device__ void cta_rank_sort(const int *keys, int n, int *out) {
     out[r] = x;
   }
   __syncthreads();
-}
-
-// Load the contributor list of one side into shared descriptors, sorted by J.
-// side 0 (Lc: J has Ũ columns in K): items = rows of L_J >= s_K
-// side 1 (Uc: J has L rows in K):    items = cols of Ũ_J >= e_K
-__device__ int load_contribs(const DevFactor &F, const ChunkList &L, int K, int side, Contrib *C, int *ord,
-                             int *tmp_keys, Shared &S) {
-  const int tid = threadIdx.x;
-  const int nc = __ldcg(&L.cnt[K]);
-  for (int x = tid; x < nc; x += NT) {
-    const int *r = list_rec(L, K, x);
-    const int J = __ldcg(r);
-    tmp_keys[x] = J;
-    Contrib c;
-    c.J = J;
-    const int sJ = F.bstart[J];
-    c.bJ = F.bstart[J + 1] - sJ;
-    const int64_t lro = __ldcg(&F.Lrow_off[J]), lvo = __ldcg(&F.Lval_off[J]);
-    const int64_t uco = __ldcg(&F.Ucol_off[J]), uvo = __ldcg(&F.Uval_off[J]);
-    if (side == 0) {
-      const int c0 = __ldcg(r + 1), c1 = __ldcg(r + 2), lrs = __ldcg(r + 3), lre = __ldcg(r + 4);
-      const int mJ = __ldcg(&F.Lm[J]);
-      c.n_items = mJ - lrs;
-      c.n_cand_skip = lre - lrs;
-      c.ncol = c1 - c0;
-      c.rows = lro + lrs;
-      c.lval = lvo + (int64_t)lrs * c.bJ;
-      c.cols = uco + c0;
-      c.uval = uvo + (int64_t)c0 * c.bJ;
-    } else {
-      const int r0 = __ldcg(r + 1), r1 = __ldcg(r + 2), cus = __ldcg(r + 3);
-      const int cJ = __ldcg(&F.Uc[J]);
-      c.n_items = cJ - cus;
-      c.n_cand_skip = 0;
-      c.ncol = r1 - r0;
-      c.rows = lro + r0;
-      c.lval = lvo + (int64_t)r0 * c.bJ;
-      c.cols = uco + cus;
-      c.uval = uvo + (int64_t)cus * c.bJ;
-    }
-    C[nc + x] = c;  // staging copy (second half), permuted below
-  }
-  __syncthreads();
-  // ascending J (R13): rank sort (J distinct within one list)
-  for (int x = tid; x < nc; x += NT) {
-    const int k = tmp_keys[x];
-    int rk = 0;
-    for (int y = 0; y < nc; ++y) rk += tmp_keys[y] < k;
-    C[rk] = C[nc + x];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    for (int x = 0; x < nc; ++x) { C[x].item_off = acc; acc += C[x].n_items; }
-    S.cnt[side] = acc;
-  }
-  __syncthreads();
-  (void)ord;
-  return nc;
 }
 
 // Both contributor lists of block K in one pass (records -> descriptors), each sorted
@@ -464,30 +380,6 @@ __device__ __forceinline__ int contrib_of(const Contrib *C, int nc, int t) {
   return lo;
 }
 
-
-// ------------------------------------------------ bulk async copies (TMA engine)
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ bool is_smem(const void *p) { return __isShared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
 
 // key -> buffer line of the candidate set of one side.  Two representations:
 //  * bitmap (range of keys [e, e + 32*words) small enough for shared memory): bit per
@@ -960,11 +852,6 @@ __device__ void side_gemms(const DevFactor &F, int s, int e, int b, const Contri
   }
 }
 
-__device__ double side_flops(const Contrib *C, int nc) {
-  double f = 0.0;
-  for (int a = 0; a < nc; ++a) f += 2.0 * C[a].bJ * (double)C[a].n_items * (double)C[a].ncol;
-  return f;
-}
 
 // ---------------------------------------------------------- split heavy blocks
 // A block whose Schur-update item count is large is processed as several tasks of the
@@ -1003,8 +890,7 @@ __device__ bool item_lines(const DevFactor &F, int K, int s, int e, const Contri
   return true;
 }
 
-__device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned char *smem, uint64_t *mbar,
-                              unsigned &mphase) {
+__device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned char *smem) {
   const int tid = threadIdx.x;
   const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
   Bump A;
@@ -1526,7 +1412,7 @@ __device__ double norm1_cta(const double *M, int b, Shared &S) {
 __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
                              const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops,
                              HeavyCtx *X, int mode) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x;
   const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
   PROF_T0C
 #define OVF_CHECK() do { if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; } } while (0)
@@ -1930,9 +1816,6 @@ scaled:
 __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Shared S;
-  __shared__ __align__(8) uint64_t s_mbar;
-  unsigned mphase = 0;
-  if (threadIdx.x == 0) mbar_init(&s_mbar, 1);
   __syncthreads();
   while (true) {
     if (threadIdx.x == 0) {
@@ -1963,9 +1846,7 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
     if (K < 0) break;
     DBGK(K);
     __threadfence();
-    // order the bulk (async-proxy) reads of other blocks' panels after the acquire
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    if (K < F.N) process_block(F, K, S, smem, &s_mbar, mphase);
+    if (K < F.N) process_block(F, K, S, smem);
     else run_part(F, K, S, smem);
     __syncthreads();
   }

@@ -101,16 +101,6 @@ __device__ __forceinline__ bool agg_test(long long p, long long q, long long r, 
   return (5 * nu <= 6 * mu) || (nu <= mu + 2 * (p + q));
 }
 
-// window of block k: the largest W with s_k - s_{k-W} + q <= max_block (W <= 127), and
-// (distributed factorization) blocks k-W..k in one aggregation segment (R18)
-__device__ __forceinline__ int merge_window(const int32_t *bstart, const int32_t *seg, int k, int max_block) {
-  const int s_k = bstart[k], q = bstart[k + 1] - s_k;
-  int W = 0;
-  while (k - 1 - W >= 0 && (s_k - bstart[k - 1 - W]) + q <= max_block && W < 127 &&
-         (seg == nullptr || seg[k - 1 - W] == seg[k]))
-    ++W;
-  return W;
-}
 
 // ---------------------------------------------------------------- M1: test
 // One side (rows of L or columns of Ũ) of block k: the lists l_d = kept indices
@@ -552,7 +542,6 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
       const int oj = s_mo[x], bj = s_mo[x + 1] - oj;
       const int32_t *rows = M.Lidx + M.Lrow_off[j];
       const double *Lv = M.Lval + M.Lval_off[j];
-      const int mj = M.Lm[j];
       const int mi = s_mi[x];      // rows inside the run are a prefix
       for (int it = tid; it < mi * bj; it += MT) {
         const int p = it / bj, t = it - p * bj;
@@ -561,7 +550,6 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
       const int32_t *cols = M.Uidx + M.Ucol_off[j];
       const double *Uv = M.Uval + M.Uval_off[j];
       const double *Dj = M.D + M.D_off[j];
-      const int cj = M.Uc[j];
       const int ci = s_ci[x];
       for (int it = tid; it < ci * bj; it += MT) {
         const int q = it / bj, r = it - q * bj;
