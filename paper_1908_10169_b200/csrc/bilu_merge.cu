@@ -565,10 +565,15 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
       for (int it = tid; it < P * bm; it += MT) {
         const int i = it / bm, c = om + it % bm;
         if (i < e) continue;                 // rows above the later members stay e_i
-        double acc = 0.0;
         const double *xr = Linv + (size_t)i * P;
-        for (int t = e; t <= i; ++t) acc = fma(xr[t], Laa[(size_t)t * P + c], acc);
-        Linv[(size_t)i * P + c] = -acc;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int t = e;
+        for (; t + 3 <= i; t += 4) {
+          a0 = fma(xr[t], Laa[(size_t)t * P + c], a0); a1 = fma(xr[t + 1], Laa[(size_t)(t + 1) * P + c], a1);
+          a2 = fma(xr[t + 2], Laa[(size_t)(t + 2) * P + c], a2); a3 = fma(xr[t + 3], Laa[(size_t)(t + 3) * P + c], a3);
+        }
+        for (; t <= i; ++t) a0 = fma(xr[t], Laa[(size_t)t * P + c], a0);
+        Linv[(size_t)i * P + c] = -((a0 + a1) + (a2 + a3));
       }
       __syncthreads();
     }
@@ -590,11 +595,16 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
       const int om = s_mo[x], bm = s_mo[x + 1] - om, e = s_mo[x + 1];
       for (int it = tid; it < P * bm; it += MT) {
         const int r = om + it % bm, c = it / bm;
-        double acc = 0.0;
         const double *ur = Uaa + (size_t)r * P;
         const double *dc = Dw + (size_t)c * P;
-        for (int t = e; t < P; ++t) acc = fma(ur[t], dc[t], acc);
-        Dw[(size_t)c * P + r] -= acc;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int t = e;
+        for (; t + 3 < P; t += 4) {
+          a0 = fma(ur[t], dc[t], a0); a1 = fma(ur[t + 1], dc[t + 1], a1);
+          a2 = fma(ur[t + 2], dc[t + 2], a2); a3 = fma(ur[t + 3], dc[t + 3], a3);
+        }
+        for (; t < P; ++t) a0 = fma(ur[t], dc[t], a0);
+        Dw[(size_t)c * P + r] -= (a0 + a1) + (a2 + a3);
       }
       __syncthreads();
     }
