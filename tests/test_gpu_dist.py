@@ -96,3 +96,18 @@ def test_distributed_context_refuses_plain_calls():
         g.factor(P.tau)
     with pytest.raises(BiluError):
         g.interface_pack()            # before phase A
+
+
+def test_simulated_ranks_c2_full_size_four_ranks():
+    """BASELINE configs[1] at full size split over 4 simulated ranks (the bench's N=4 split)."""
+    P = config2(top_levels=2)
+    owner, ctxs, stats, bufs = run_simulated(P, 4)
+    exports = [g.export() for g in ctxs]
+    near = {tuple(int(x) for x in row) for f in exports for row in np.asarray(f.near)}
+    ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
+    of = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
+    bst = np.concatenate([[0], np.cumsum(P.block_sizes)])
+    for r, f in enumerate(exports):
+        present = {int(bst[K]) for K in range(len(owner)) if owner[K] in (r, -1)}
+        res = compare_present_blocks(f, of, present)
+        assert not res["problems"], (r, res["problems"][:3])
