@@ -88,6 +88,12 @@ def _load():
             ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.POINTER(_Perturb),
             ctypes.POINTER(_Factor),
         ]
+        lib.orc_ilu1_blocks.restype = ctypes.c_int32
+        lib.orc_ilu1_blocks.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_double, ctypes.c_int32, ctypes.c_void_p]
+        lib.orc_ilu1_set.restype = ctypes.c_int32
+        lib.orc_ilu1_set.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
         lib.orc_bilu_apply.restype = ctypes.c_int
         lib.orc_bilu_apply.argtypes = [ctypes.POINTER(_Factor), ctypes.c_void_p, ctypes.c_void_p]
         lib.orc_aggregate_test.restype = ctypes.c_int
@@ -270,3 +276,33 @@ def permute_csr(indptr, indices, data, perm):
     A = sp.csr_matrix(A)
     A.sort_indices()
     return A.indptr.astype(np.int64), A.indices.astype(np.int32), A.data.astype(np.float64)
+
+
+def ilu1_blocks(indptr, indices, data, tau, max_size=8) -> np.ndarray:
+    """ILU(1,tau) initial block sizes of Sec. 3.4 (R20) of an already-permuted CSR matrix."""
+    lib = _load()
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    indices = np.ascontiguousarray(indices, dtype=np.int32)
+    data = np.ascontiguousarray(data, dtype=np.float64)
+    n = len(indptr) - 1
+    out = np.zeros(n, dtype=np.int32)
+    nb = lib.orc_ilu1_blocks(n, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, float(tau),
+                             int(max_size), out.ctypes.data)
+    if nb < 0:
+        raise OracleError("bad argument")
+    return out[:nb].copy()
+
+
+def ilu1_set(indptr, indices, data, tau, k, lower=True) -> np.ndarray:
+    """Estimated pattern I~_k (lower) or J~_k of Sec. 3.4, ascending."""
+    lib = _load()
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    indices = np.ascontiguousarray(indices, dtype=np.int32)
+    data = np.ascontiguousarray(data, dtype=np.float64)
+    n = len(indptr) - 1
+    out = np.zeros(n, dtype=np.int32)
+    m = lib.orc_ilu1_set(n, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, float(tau), int(k),
+                         1 if lower else 0, out.ctypes.data)
+    if m < 0:
+        raise OracleError("bad argument")
+    return out[:m].copy()

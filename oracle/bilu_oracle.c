@@ -779,3 +779,168 @@ int orc_bilu_factor_seg(int32_t n, const int64_t *row_ptr, const int32_t *col_id
   return factor_impl(n, row_ptr, col_idx, val, nblk, bsizes, tau, aggregate, max_block, ovr, n_ovr,
                      near_rel, seg, NULL, f);
 }
+
+/* ---------------- ILU(1,tau) initial block estimate (Sec. 3.4) ----------------
+ * For step k the estimated pattern of column k of L is
+ *   I~_k = { i > k : a_ik != 0, |a_ik| >= tau |a_kk| }                                  (I^)
+ *        u { i > k : exists j < k, a_jk != 0, a_ij != 0, |a_ij a_jk| >= tau |a_jj a_kk| }  (ILU(1) fill)
+ * and of row k of U, symmetrically,
+ *   J~_k = { j > k : a_kj != 0, |a_kj| >= tau |a_kk| }
+ *        u { j > k : exists i < k, a_ki != 0, a_ij != 0, |a_ki a_ij| >= tau |a_ii a_kk| }.
+ * Blocks grow greedily from k0: with l columns in the block, r / s the
+ * sizes of the unions of I~_t / J~_t (t in the block) outside the block, f_l = (r + s + l) l;
+ * the scalar count of the block is c' = sum_t (|I~_t| + |J~_t| + 1) (R20: "f_l - c"
+ * is the scalar nnz, c the wasted zeros); column k0+l joins iff
+ *   3 f_{l+1} <= 4 c'  or  f_{l+1} <= c' + 4 (l+1)   (exact integers for 4/3)
+ * and l+1 <= max_size.  Returns the number of blocks, sizes in out (n entries capacity). */
+static int cmp_int(const void *a, const void *b) { int x = *(const int *)a, y = *(const int *)b; return (x > y) - (x < y); }
+
+static int32_t est_set(int32_t n, const int64_t *rp, const int32_t *ci, const double *val, const int64_t *cp,
+                       const int32_t *cr, const int64_t *cmap, const double *diag, int32_t k, double tau, int lower,
+                       int32_t *buf) {
+  /* lower: column k of L via the CSC (rows i > k); else row k of U via the CSR (cols j > k) */
+  int32_t m = 0;
+  const double akk = diag[k];
+  if (lower) {
+    for (int64_t p = cp[k]; p < cp[k + 1]; ++p) {
+      const int32_t i = cr[p];
+      if (i > k && fabs(val[cmap[p]]) >= tau * fabs(akk)) buf[m++] = i;
+    }
+    for (int64_t p = cp[k]; p < cp[k + 1]; ++p) {          /* j < k with a_jk != 0 */
+      const int32_t j = cr[p];
+      if (j >= k) continue;
+      const double ajk = val[cmap[p]];
+      for (int64_t q = cp[j]; q < cp[j + 1]; ++q) {         /* i > k with a_ij != 0 */
+        const int32_t i = cr[q];
+        if (i > k && fabs(val[cmap[q]] * ajk) >= tau * fabs(diag[j] * akk)) buf[m++] = i;
+      }
+    }
+  } else {
+    for (int64_t p = rp[k]; p < rp[k + 1]; ++p) {
+      const int32_t j = ci[p];
+      if (j > k && fabs(val[p]) >= tau * fabs(akk)) buf[m++] = j;
+    }
+    for (int64_t p = rp[k]; p < rp[k + 1]; ++p) {          /* i < k with a_ki != 0 */
+      const int32_t i = ci[p];
+      if (i >= k) continue;
+      const double aki = val[p];
+      for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {         /* j > k with a_ij != 0 */
+        const int32_t j = ci[q];
+        if (j > k && fabs(aki * val[q]) >= tau * fabs(diag[i] * akk)) buf[m++] = j;
+      }
+    }
+  }
+  qsort(buf, (size_t)m, sizeof(int32_t), cmp_int);
+  int32_t u = 0;
+  for (int32_t x = 0; x < m; ++x) if (x == 0 || buf[x] != buf[x - 1]) buf[u++] = buf[x];
+  return u;
+}
+
+/* CSC of the matrix (rows ascending within a column) with a map to the CSR entries, and the diagonal */
+static void est_csc(int32_t n, const int64_t *rp, const int32_t *ci, const double *val, int64_t **cp_o,
+                    int32_t **cr_o, int64_t **cmap_o, double **diag_o) {
+  const int64_t nnz = rp[n];
+  int64_t *cp = (int64_t *)xcalloc((size_t)n + 1, sizeof(int64_t));
+  int32_t *cr = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)(nnz > 0 ? nnz : 1));
+  int64_t *cmap = (int64_t *)xmalloc(sizeof(int64_t) * (size_t)(nnz > 0 ? nnz : 1));
+  double *diag = (double *)xcalloc((size_t)n, sizeof(double));
+  for (int64_t p = 0; p < nnz; ++p) cp[ci[p] + 1]++;
+  for (int32_t j = 0; j < n; ++j) cp[j + 1] += cp[j];
+  int64_t *fill = (int64_t *)xmalloc(sizeof(int64_t) * (size_t)n);
+  for (int32_t j = 0; j < n; ++j) fill[j] = cp[j];
+  for (int32_t i = 0; i < n; ++i)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t q = fill[ci[p]]++;
+      cr[q] = i; cmap[q] = p;
+      if (ci[p] == i) diag[i] = val[p];
+    }
+  free(fill);
+  *cp_o = cp; *cr_o = cr; *cmap_o = cmap; *diag_o = diag;
+}
+
+static int64_t est_bound(const int64_t *rp, const int32_t *ci, const int64_t *cp, const int32_t *cr, int32_t k,
+                         int lower) {
+  int64_t bound = 0;
+  if (lower) { bound = cp[k + 1] - cp[k]; for (int64_t p = cp[k]; p < cp[k + 1]; ++p) if (cr[p] < k) bound += cp[cr[p] + 1] - cp[cr[p]]; }
+  else { bound = rp[k + 1] - rp[k]; for (int64_t p = rp[k]; p < rp[k + 1]; ++p) if (ci[p] < k) bound += rp[ci[p] + 1] - rp[ci[p]]; }
+  return bound;
+}
+
+/* One estimated set (test/diagnostic export): lower = 1 -> I~_k, 0 -> J~_k, ascending in out
+ * (capacity n).  Returns its size, -1 on a bad argument. */
+int32_t orc_ilu1_set(int32_t n, const int64_t *rp, const int32_t *ci, const double *val, double tau, int32_t k,
+                     int32_t lower, int32_t *out) {
+  if (n < 1 || !rp || !ci || !val || !out || k < 0 || k >= n || !(tau >= 0.0)) return -1;
+  int64_t *cp, *cmap; int32_t *cr; double *diag;
+  est_csc(n, rp, ci, val, &cp, &cr, &cmap, &diag);
+  const int64_t bound = est_bound(rp, ci, cp, cr, k, lower);
+  int32_t *buf = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)(bound > 0 ? bound : 1));
+  const int32_t m = est_set(n, rp, ci, val, cp, cr, cmap, diag, k, tau, lower, buf);
+  memcpy(out, buf, sizeof(int32_t) * (size_t)m);
+  free(buf); free(cp); free(cr); free(cmap); free(diag);
+  return m;
+}
+
+int32_t orc_ilu1_blocks(int32_t n, const int64_t *rp, const int32_t *ci, const double *val, double tau,
+                        int32_t max_size, int32_t *out) {
+  if (n < 1 || !rp || !ci || !val || !out || max_size < 1 || !(tau >= 0.0)) return -1;
+  const int64_t nnz = rp[n];
+  int64_t *cp, *cmap; int32_t *cr; double *diag;
+  est_csc(n, rp, ci, val, &cp, &cr, &cmap, &diag);
+  /* per step: sorted estimated sets */
+  int64_t *Ip = (int64_t *)xcalloc((size_t)n + 1, sizeof(int64_t)), *Jp = (int64_t *)xcalloc((size_t)n + 1, sizeof(int64_t));
+  int64_t capI = nnz + n, capJ = nnz + n, usedI = 0, usedJ = 0;
+  int32_t *Is = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)capI), *Js = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)capJ);
+  int64_t bufcap = 1024;
+  int32_t *buf = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)bufcap);
+  for (int32_t k = 0; k < n; ++k) {
+    for (int side = 0; side < 2; ++side) {
+      const int64_t bound = est_bound(rp, ci, cp, cr, k, side == 0);   /* candidate count */
+      if (bound > bufcap) { free(buf); bufcap = 2 * bound; buf = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)bufcap); }
+      const int32_t m = est_set(n, rp, ci, val, cp, cr, cmap, diag, k, tau, side == 0, buf);
+      int64_t *used = side == 0 ? &usedI : &usedJ, *cap = side == 0 ? &capI : &capJ;
+      int32_t **S = side == 0 ? &Is : &Js;
+      if (*used + m > *cap) {
+        *cap = 2 * (*used + m);
+        *S = (int32_t *)realloc(*S, sizeof(int32_t) * (size_t)*cap);
+      }
+      memcpy(*S + *used, buf, sizeof(int32_t) * (size_t)m);
+      *used += m;
+      (side == 0 ? Ip : Jp)[k + 1] = *used;
+    }
+  }
+  /* greedy block growing */
+  char *inI = (char *)xcalloc((size_t)n, 1), *inJ = (char *)xcalloc((size_t)n, 1);
+  int32_t *listI = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)n), *listJ = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)n);
+  int32_t nb = 0, k0 = 0;
+  while (k0 < n) {
+    int32_t l = 1, nI = 0, nJ = 0;
+    int64_t sc = (Ip[k0 + 1] - Ip[k0]) + (Jp[k0 + 1] - Jp[k0]) + 1;     /* scalar count c' */
+    for (int64_t p = Ip[k0]; p < Ip[k0 + 1]; ++p) if (!inI[Is[p]]) { inI[Is[p]] = 1; listI[nI++] = Is[p]; }
+    for (int64_t p = Jp[k0]; p < Jp[k0 + 1]; ++p) if (!inJ[Js[p]]) { inJ[Js[p]] = 1; listJ[nJ++] = Js[p]; }
+    while (k0 + l < n && l + 1 <= max_size) {
+      const int32_t t = k0 + l;
+      /* unions with column t's sets, counted outside the grown block [k0, k0+l+1) */
+      int64_t r = 0, s = 0;
+      for (int32_t x = 0; x < nI; ++x) r += listI[x] > t;
+      for (int32_t x = 0; x < nJ; ++x) s += listJ[x] > t;
+      for (int64_t p = Ip[t]; p < Ip[t + 1]; ++p) if (!inI[Is[p]] && Is[p] > t) r++;
+      for (int64_t p = Jp[t]; p < Jp[t + 1]; ++p) if (!inJ[Js[p]] && Js[p] > t) s++;
+      const int64_t l1 = l + 1;
+      const int64_t f = (r + s + l1) * l1;
+      const int64_t c2 = sc + (Ip[t + 1] - Ip[t]) + (Jp[t + 1] - Jp[t]) + 1;
+      if (!(3 * f <= 4 * c2 || f <= c2 + 4 * l1)) break;
+      sc = c2;
+      for (int64_t p = Ip[t]; p < Ip[t + 1]; ++p) if (!inI[Is[p]]) { inI[Is[p]] = 1; listI[nI++] = Is[p]; }
+      for (int64_t p = Jp[t]; p < Jp[t + 1]; ++p) if (!inJ[Js[p]]) { inJ[Js[p]] = 1; listJ[nJ++] = Js[p]; }
+      ++l;
+    }
+    for (int32_t x = 0; x < nI; ++x) inI[listI[x]] = 0;
+    for (int32_t x = 0; x < nJ; ++x) inJ[listJ[x]] = 0;
+    out[nb++] = l;
+    k0 += l;
+  }
+  free(cp); free(cr); free(cmap); free(diag); free(Ip); free(Jp); free(Is); free(Js); free(buf);
+  free(inI); free(inJ); free(listI); free(listJ);
+  return nb;
+}

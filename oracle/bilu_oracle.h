@@ -87,6 +87,17 @@ int orc_aggregate_test(int64_t p, int64_t q, int64_t r, int64_t s, int64_t t,
                        int64_t r2, int64_t s2, int64_t t2, int64_t u, int64_t v,
                        int64_t max_block);
 
+/* ILU(1,tau) initial block estimate of Sec. 3.4 (R20) on an
+ * already-permuted CSR matrix; out receives the block sizes (capacity n).  Returns the number
+ * of blocks, -1 on a bad argument. */
+int32_t orc_ilu1_blocks(int32_t n, const int64_t *rp, const int32_t *ci, const double *val, double tau,
+                        int32_t max_size, int32_t *out);
+
+/* One estimated set of Sec. 3.4 (lower = 1: I~_k of column k of L, 0: J~_k of row k of U),
+ * ascending in out (capacity n); returns its size, -1 on a bad argument. */
+int32_t orc_ilu1_set(int32_t n, const int64_t *rp, const int32_t *ci, const double *val, double tau, int32_t k,
+                     int32_t lower, int32_t *out);
+
 void orc_free(orc_factor *f);
 
 #ifdef __cplusplus

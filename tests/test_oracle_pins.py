@@ -401,3 +401,91 @@ def test_perturbation_singular_block_bounded_modification():
     pmax = np.abs(L @ P @ U)[4:6, 4:6].max()
     assert np.abs(E[mask]).max() > 0
     assert np.abs(E[mask]).max() <= 3 * (rho * pmax * pmax + tp * alpha)
+
+
+# ------------------------------------------------------------ ILU(1,tau) block estimate (Sec. 3.4)
+def _csr(D):
+    import scipy.sparse as sp
+    A = sp.csr_matrix(np.asarray(D, dtype=np.float64))
+    A.sort_indices()
+    return A.indptr, A.indices, A.data
+
+
+def test_ilu1_sets_hand_trace():
+    """Hand trace of PAPER.md:1178-1198 on a 4x4 unsymmetric matrix (tests/golden/ilu1_hand_4x4.json).
+
+    tau=0.5: I~_1 = {2} only through the ILU(1) fill a_21 = -a_20 a_01 / a_00 (|5*1| >= .5|2*4|);
+    the direct a_31 = .1 < .5*4 is dropped.  J~_2 = {3} only through the fill of row 2 via i=0
+    (|a_20 a_03| = 5 >= .5|a_00 a_22|).  tau=0.625 sits exactly on |5| = tau*8 (kept, ">="), and
+    J~_0 loses a_01 = a_03 = 1 < 1.25.  tau=0.63 drops the fill.  tau=0.01 keeps a_31.
+    Using a_kj instead of a_jk in the fill (a transposed operand) gives I~_1 = {} at tau=0.5."""
+    g = json.load(open(os.path.join(GOLD, "ilu1_hand_4x4.json")))
+    ip, ix, dv = _csr(g["A"])
+    for c in g["cases"]:
+        for k in range(4):
+            assert list(oracle.ilu1_set(ip, ix, dv, c["tau"], k, True)) == c["I"][k], (c["tau"], k)
+            assert list(oracle.ilu1_set(ip, ix, dv, c["tau"], k, False)) == c["J"][k], (c["tau"], k)
+        if "blocks_max8" in c:
+            # k0=0: t=1 f=8,c'=7 (24<=28); t=2 f=12,c'=9 (36<=36); t=3 f=16 <= c'+16 = 26
+            assert list(oracle.ilu1_blocks(ip, ix, dv, c["tau"], 8)) == c["blocks_max8"]
+            assert list(oracle.ilu1_blocks(ip, ix, dv, c["tau"], 2)) == c["blocks_max2"]
+
+
+def test_ilu1_identity_blocks_of_five():
+    """Identity: f_{l+1} = (l+1)^2, c' = l+1, so l+1 <= 5 (SURVEY S:303 / §8c: f6 = 36 > 6+24)."""
+    n = 23
+    ip, ix, dv = np.arange(n + 1), np.arange(n), np.ones(n)
+    assert list(oracle.ilu1_blocks(ip, ix, dv, 1e-2, 128)) == [5, 5, 5, 5, 3]
+    assert list(oracle.ilu1_blocks(ip, ix, dv, 1e-2, 3)) == [3] * 7 + [2]      # the max_size cap
+    assert list(oracle.ilu1_blocks(ip, ix, dv, 1e-2, 1)) == [1] * n
+
+
+def test_ilu1_tridiagonal_hand_trace():
+    """Tridiagonal(-1, 4, -1), n=8, tau=.1: I~_k = J~_k = {k+1}.  From k0=0 the block keeps r=s=1:
+    f = 8,15,24,35 against c' = 6,9,12,15 (4/3 test or c'+4(l+1)) -> l=5; t=5: f=48 > 18+24.
+    From k0=5: f=8 <= 4/3*6, then r=s=0, f=9 <= 4/3*7 -> [5, 3].  Not removing the in-block
+    entries from r, s would stop the first block at 2 (t=2: f=27 > 9+12)."""
+    import scipy.sparse as sp
+    T = sp.diags([-np.ones(7), 4 * np.ones(8), -np.ones(7)], [-1, 0, 1]).tocsr()
+    T.sort_indices()
+    assert list(oracle.ilu1_blocks(T.indptr, T.indices, T.data, 0.1, 8)) == [5, 3]
+
+
+def test_ilu1_star_fill_path_theorem():
+    """Dense first row/column + diagonal (a star eliminated centre-first): every fill path has one
+    intermediate vertex (0), so with tau=0 the ILU(1) estimate is the exact LU pattern: I~_k =
+    J~_k = {k+1..n-1} (fill-path theorem, Rose-Tarjan)."""
+    rng = np.random.default_rng(3)
+    n = 9
+    D = np.diag(rng.uniform(5, 6, n))
+    D[0, 1:] = rng.uniform(0.5, 1, n - 1)
+    D[1:, 0] = rng.uniform(0.5, 1, n - 1)
+    ip, ix, dv = _csr(D)
+    for k in range(n):
+        assert list(oracle.ilu1_set(ip, ix, dv, 0.0, k, True)) == list(range(k + 1, n))
+        assert list(oracle.ilu1_set(ip, ix, dv, 0.0, k, False)) == list(range(k + 1, n))
+
+
+def test_ilu1_sets_inside_exact_lu_pattern_and_monotone():
+    """tau=0: pattern(A) below/right of k  <=  I~_k, J~_k  <=  pattern of the exact (no pivoting) LU
+    factors (generic values: no cancellation); the sets shrink as tau grows."""
+    rng = np.random.default_rng(11)
+    n = 40
+    M = (rng.random((n, n)) < 0.08) * rng.uniform(-1, 1, (n, n))
+    M += np.diag(np.abs(M).sum(1) + 1.0)
+    P, Lf, Uf = sla.lu(M)
+    assert np.allclose(P, np.eye(n))          # diagonally dominant: no row exchanges
+    ip, ix, dv = _csr(M)
+    for k in range(n):
+        lo = set(oracle.ilu1_set(ip, ix, dv, 0.0, k, True))
+        up = set(oracle.ilu1_set(ip, ix, dv, 0.0, k, False))
+        assert set(np.nonzero(M[k + 1:, k])[0] + k + 1) <= lo <= set(np.nonzero(np.abs(Lf[k + 1:, k]) > 0)[0] + k + 1)
+        assert set(np.nonzero(M[k, k + 1:])[0] + k + 1) <= up <= set(np.nonzero(np.abs(Uf[k, k + 1:]) > 0)[0] + k + 1)
+        prev_lo, prev_up = lo, up
+        for tau in (1e-3, 1e-2, 1e-1, 1.0):
+            lo_t = set(oracle.ilu1_set(ip, ix, dv, tau, k, True))
+            up_t = set(oracle.ilu1_set(ip, ix, dv, tau, k, False))
+            assert lo_t <= prev_lo and up_t <= prev_up
+            prev_lo, prev_up = lo_t, up_t
+    b = oracle.ilu1_blocks(ip, ix, dv, 1e-2, 8)
+    assert b.sum() == n and b.min() >= 1 and b.max() <= 8
