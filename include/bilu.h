@@ -239,6 +239,27 @@ bilu_status bilu_factor_separators(bilu_ctx *h, bilu_factor_stats *st);
 void bilu_destroy(bilu_ctx *h);
 
 const char *bilu_status_string(bilu_status s);
+/*
+ * bilu_ilu1_blocks -- initial block partition by the ILU(1,tau) simulation of Sec. 3.4
+ * (readings in DESIGN.md R20), computed on the device.
+ *   n, row_ptr, col_idx, val, perm   HOST, as in bilu_analyze (val required); the estimate
+ *                works on Ã = A(perm, perm)
+ *   tau          drop tolerance of the simulation (>= 0)
+ *   max_size     cap on a block (1..128; BASELINE: "initial block size up to 8")
+ *   device, stream   CUDA device ordinal and cudaStream_t (NULL = legacy default stream)
+ *   block_sizes  HOST, int32[n] (capacity n): receives the partition of Ã, sum = n
+ *   n_blocks     receives the number of blocks
+ *   n_kernel_launches   optional (may be NULL): kernels launched
+ * Column k of L is estimated as I~_k = {i>k : |a_ik| >= tau|a_kk|} u {i>k : exists j<k,
+ * |a_ij a_jk| >= tau|a_jj a_kk|} (and row k of U symmetrically); a block grows from k0 while
+ * f_{l+1} <= 4/3 c' or f_{l+1} <= c' + 4(l+1).  Result identical to the oracle's.  Synchronous;
+ * device memory is allocated and freed inside.  Errors: BILU_ERR_ARG (bad CSR / perm / tau /
+ * max_size), BILU_ERR_OOM, BILU_ERR_CUDA, BILU_ERR_NOT_BUILT.
+ */
+bilu_status bilu_ilu1_blocks(int32_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
+                             const int32_t *perm, double tau, int32_t max_size, int32_t device, void *stream,
+                             int32_t *block_sizes, int32_t *n_blocks, int32_t *n_kernel_launches);
+
 const char *bilu_last_error(const bilu_ctx *h);
 
 /* Number of kernels the library launched since the context was created

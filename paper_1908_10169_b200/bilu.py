@@ -22,7 +22,7 @@ ABI_SYMBOLS = ["bilu_options_default", "bilu_analyze", "bilu_set_values", "bilu_
                "bilu_apply", "bilu_export", "bilu_factor_view_free", "bilu_destroy",
                "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm", "bilu_diag_tsgemm",
                "bilu_dist_setup", "bilu_factor_local", "bilu_interface_pack", "bilu_interface_unpack",
-               "bilu_factor_separators", "bilu_gmres"]
+               "bilu_factor_separators", "bilu_gmres", "bilu_ilu1_blocks"]
 
 
 class BiluError(RuntimeError):
@@ -132,6 +132,8 @@ def load_library():
     lib.bilu_gmres.restype = ctypes.c_int
     lib.bilu_factor_separators.argtypes = [P, ctypes.POINTER(FactorStats)]
     lib.bilu_factor_separators.restype = ctypes.c_int
+    lib.bilu_ilu1_blocks.argtypes = [ctypes.c_int32, P, P, P, P, D, ctypes.c_int32, ctypes.c_int32, P, P, P, P]
+    lib.bilu_ilu1_blocks.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -337,3 +339,23 @@ def diag_dgemm(A, B, C, alpha=1.0, beta=0.0, stream=0, tall_skinny=False):
                              B.stride(0), C.stride(0), ctypes.c_void_p(stream))
     if rc != 0:
         raise BiluError(rc, "bilu_diag_dgemm failed")
+
+
+def ilu1_blocks(indptr, indices, data, tau, max_size=8, perm=None, device=0, stream=0):
+    """bilu_ilu1_blocks: the ILU(1,tau) initial block partition of Sec. 3.4,
+    computed on the device for Ã = A(perm, perm).  Returns (block_sizes int32 array, kernels launched)."""
+    lib = load_library()
+    ip = _arr(indptr, np.int64)
+    ix = _arr(indices, np.int32)
+    dv = _arr(data, np.float64)
+    n = len(ip) - 1
+    pm = None if perm is None else _arr(perm, np.int32)
+    out = np.zeros(max(n, 1), dtype=np.int32)
+    nb = ctypes.c_int32(0)
+    nl = ctypes.c_int32(0)
+    rc = lib.bilu_ilu1_blocks(n, ip.ctypes.data, ix.ctypes.data, dv.ctypes.data,
+                              None if pm is None else pm.ctypes.data, float(tau), int(max_size), int(device),
+                              ctypes.c_void_p(stream), out.ctypes.data, ctypes.byref(nb), ctypes.byref(nl))
+    if rc != 0:
+        raise BiluError(rc, lib.bilu_last_error(None).decode())
+    return out[: nb.value].copy(), nl.value

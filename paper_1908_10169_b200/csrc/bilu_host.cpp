@@ -62,6 +62,9 @@ extern "C" int bilu_merge_nchunks(int N);
 extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
                                         cudaStream_t st);
 extern "C" cudaError_t bilu_launch_apply(const ApplyArgs &A, int grid, int backward, cudaStream_t st);
+extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci, const double *val, double tau,
+                                     int max_size, int sms, cudaStream_t st, int32_t *h_sizes, int32_t *nblocks,
+                                     int *launches);
 }  // namespace bilu
 
 // Final (post-aggregation) factor: per final block F, descriptors into the
@@ -247,6 +250,48 @@ extern "C" void bilu_destroy(bilu_ctx *h) {
   delete h;
 }
 
+// --------------------------------------------------------------- CSR / permutation input
+// Validates a host CSR (sorted, duplicate-free rows) and a permutation (NULL = identity).
+static bilu_status check_csr_perm(const char *fn, int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                                  const int32_t *perm, std::vector<int32_t> &pm, std::vector<int32_t> &ipm) {
+  if (row_ptr[0] != 0) { set_err(nullptr, "%s: row_ptr[0] != 0", fn); return BILU_ERR_ARG; }
+  for (int32_t i = 0; i < n; ++i) {
+    if (row_ptr[i + 1] < row_ptr[i]) { set_err(nullptr, "%s: row_ptr decreases at row %d", fn, i); return BILU_ERR_ARG; }
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      if (col_idx[p] < 0 || col_idx[p] >= n) { set_err(nullptr, "%s: column index out of range in row %d", fn, i); return BILU_ERR_ARG; }
+      if (p > row_ptr[i] && col_idx[p] <= col_idx[p - 1]) { set_err(nullptr, "%s: row %d not strictly increasing (unsorted or duplicate)", fn, i); return BILU_ERR_ARG; }
+    }
+  }
+  pm.assign(n, 0);
+  ipm.assign(n, -1);
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t p = perm ? perm[i] : i;
+    if (p < 0 || p >= n || ipm[p] != -1) { set_err(nullptr, "%s: perm is not a bijection (position %d)", fn, i); return BILU_ERR_ARG; }
+    pm[i] = p; ipm[p] = i;
+  }
+  return BILU_OK;
+}
+
+// Ã = A(pm, pm) in CSR with sorted rows; map[q] = position of Ã's entry q in A's arrays.
+static void permute_csr(int32_t n, const int64_t *row_ptr, const int32_t *col_idx, const std::vector<int32_t> &pm,
+                        const std::vector<int32_t> &ipm, std::vector<int64_t> &rp, std::vector<int32_t> &ci,
+                        std::vector<int64_t> &map) {
+  const int64_t nnz = row_ptr[n];
+  rp.assign(n + 1, 0);
+  for (int32_t i = 0; i < n; ++i) rp[i + 1] = rp[i] + (row_ptr[pm[i] + 1] - row_ptr[pm[i]]);
+  ci.resize(nnz);
+  map.resize(nnz);
+  std::vector<std::pair<int32_t, int64_t>> tmp;
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t o = pm[i];
+    tmp.clear();
+    for (int64_t p = row_ptr[o]; p < row_ptr[o + 1]; ++p) tmp.emplace_back(ipm[col_idx[p]], p);
+    std::sort(tmp.begin(), tmp.end());
+    int64_t q = rp[i];
+    for (auto &t : tmp) { ci[q] = t.first; map[q] = t.second; ++q; }
+  }
+}
+
 // --------------------------------------------------------------- analyze
 extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
                                     const double *val, const int32_t *perm,
@@ -273,23 +318,12 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     set_err(nullptr, "bilu_analyze: world > 1 is not supported by this build");
     return BILU_ERR_ARG;
   }
-  // ---- validate CSR
-  if (row_ptr[0] != 0) { set_err(nullptr, "bilu_analyze: row_ptr[0] != 0"); return BILU_ERR_ARG; }
-  for (int32_t i = 0; i < n; ++i) {
-    if (row_ptr[i + 1] < row_ptr[i]) { set_err(nullptr, "bilu_analyze: row_ptr decreases at row %d", i); return BILU_ERR_ARG; }
-    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
-      if (col_idx[p] < 0 || col_idx[p] >= n) { set_err(nullptr, "bilu_analyze: column index out of range in row %d", i); return BILU_ERR_ARG; }
-      if (p > row_ptr[i] && col_idx[p] <= col_idx[p - 1]) { set_err(nullptr, "bilu_analyze: row %d not strictly increasing (unsorted or duplicate)", i); return BILU_ERR_ARG; }
-    }
+  std::vector<int32_t> pm, ipm;
+  {
+    bilu_status st = check_csr_perm("bilu_analyze", n, row_ptr, col_idx, perm, pm, ipm);
+    if (st != BILU_OK) return st;
   }
   const int64_t nnz = row_ptr[n];
-  // ---- validate permutation
-  std::vector<int32_t> pm(n), ipm(n, -1);
-  for (int32_t i = 0; i < n; ++i) {
-    int32_t p = perm ? perm[i] : i;
-    if (p < 0 || p >= n || ipm[p] != -1) { set_err(nullptr, "bilu_analyze: perm is not a bijection (position %d)", i); return BILU_ERR_ARG; }
-    pm[i] = p; ipm[p] = i;
-  }
   // ---- validate partition
   std::vector<int32_t> bstart(n_blocks + 1, 0);
   int max_b = 0;
@@ -319,21 +353,9 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, opt.device);
 
   // ---- Ã = A(perm, perm), CSR (rows sorted)
-  std::vector<int64_t> rp(n + 1, 0);
-  for (int32_t i = 0; i < n; ++i) rp[i + 1] = rp[i] + (row_ptr[pm[i] + 1] - row_ptr[pm[i]]);
-  std::vector<int32_t> ci(nnz);
-  h->map_csr.resize(nnz);
-  {
-    std::vector<std::pair<int32_t, int64_t>> tmp;
-    for (int32_t i = 0; i < n; ++i) {
-      int32_t o = pm[i];
-      tmp.clear();
-      for (int64_t p = row_ptr[o]; p < row_ptr[o + 1]; ++p) tmp.emplace_back(ipm[col_idx[p]], p);
-      std::sort(tmp.begin(), tmp.end());
-      int64_t q = rp[i];
-      for (auto &t : tmp) { ci[q] = t.first; h->map_csr[q] = t.second; ++q; }
-    }
-  }
+  std::vector<int64_t> rp;
+  std::vector<int32_t> ci;
+  permute_csr(n, row_ptr, col_idx, pm, ipm, rp, ci, h->map_csr);
   // ---- block graph of sym(Ã): successors > K and pending counts
   std::vector<int32_t> block_of(n);
   for (int32_t K = 0; K < n_blocks; ++K)
@@ -1552,5 +1574,57 @@ extern "C" bilu_status bilu_apply(bilu_ctx *h, const double *x, double *y, void 
   }
   CUDA_TRY(h, bilu_launch_permute(y, h->d_y, h->d_perm, h->n, 1, st));
   h->launches += 4;
+  return BILU_OK;
+}
+
+// --------------------------------------------------------------- ILU(1,tau) initial blocking
+extern "C" bilu_status bilu_ilu1_blocks(int32_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
+                                        const int32_t *perm, double tau, int32_t max_size, int32_t device,
+                                        void *stream, int32_t *block_sizes, int32_t *n_blocks,
+                                        int32_t *n_kernel_launches) {
+  if (n_blocks) *n_blocks = 0;
+  if (n < 1 || !row_ptr || !col_idx || !val || !block_sizes || !n_blocks) {
+    set_err(nullptr, "bilu_ilu1_blocks: null pointer or n < 1");
+    return BILU_ERR_ARG;
+  }
+  if (!(tau >= 0.0) || max_size < 1 || max_size > 128) {
+    set_err(nullptr, "bilu_ilu1_blocks: need tau >= 0 and max_size in [1,128] (got %g, %d)", tau, max_size);
+    return BILU_ERR_ARG;
+  }
+  if (n >= (1 << 30)) { set_err(nullptr, "bilu_ilu1_blocks: n must be < 2^30"); return BILU_ERR_ARG; }
+  std::vector<int32_t> pm, ipm;
+  bilu_status st = check_csr_perm("bilu_ilu1_blocks", n, row_ptr, col_idx, perm, pm, ipm);
+  if (st != BILU_OK) return st;
+  std::vector<int64_t> rp, map;
+  std::vector<int32_t> ci;
+  permute_csr(n, row_ptr, col_idx, pm, ipm, rp, ci, map);
+  const int64_t nnz = rp[n];
+  std::vector<double> v(nnz);
+  for (int64_t q = 0; q < nnz; ++q) v[q] = val[map[q]];
+  if (cudaSetDevice(device) != cudaSuccess) {
+    set_err(nullptr, "bilu_ilu1_blocks: cannot use CUDA device %d", device);
+    return BILU_ERR_NOT_BUILT;
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t *d_rp = nullptr;
+  int32_t *d_ci = nullptr;
+  double *d_v = nullptr;
+  cudaError_t e = cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_v, sizeof(double) * (nnz > 0 ? nnz : 1));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_rp, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(d_ci, ci.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(d_v, v.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, s);
+  int launches = 0;
+  if (e == cudaSuccess) e = bilu_ilu1_run(n, d_rp, d_ci, d_v, tau, max_size, sms, s, block_sizes, n_blocks, &launches);
+  cudaStreamSynchronize(s);
+  cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_v);
+  if (n_kernel_launches) *n_kernel_launches = launches;
+  if (e != cudaSuccess) {
+    set_err(nullptr, "bilu_ilu1_blocks: %s", cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? BILU_ERR_OOM : BILU_ERR_CUDA;
+  }
   return BILU_OK;
 }
