@@ -1,7 +1,8 @@
 // bilu_blocking.cu -- the ILU(1,tau) initial block estimate of Sec. 3.4 (PAPER.md:1171-1242,
 // DESIGN.md R20) on the device: the input of bilu_analyze's block partition.
 //
-//  1. CSC of the (already permuted) matrix and its diagonal (count / scan / scatter; the order
+//  0. Ã = A(perm, perm) on the device (rows left unsorted).
+//  1. CSC of Ã and its diagonal (count / scan / scatter; the order
 //     inside a column is irrelevant: only sets are built from it).
 //  2. Estimated patterns I~_k (column k of L) and J~_k (row k of U), one warp per step k:
 //     the direct entries |a_ik| >= tau |a_kk| plus the ILU(1) fill |a_ij a_jk| >= tau |a_jj a_kk|
@@ -310,6 +311,24 @@ __global__ void csc_fill_kernel(int n, const int64_t *rp, const int32_t *ci, con
   }
 }
 
+// ---- Ã = A(pm, pm) without sorting the rows (only sets are built from them)
+__global__ void perm_len_kernel(int n, const int64_t *rp, const int32_t *pm, int64_t *len) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    len[i] = rp[pm[i] + 1] - rp[pm[i]];
+}
+__global__ void perm_rows_kernel(int n, const int64_t *rp, const int32_t *ci, const double *val, const int32_t *pm,
+                                 const int32_t *ipm, const int64_t *nrp, int32_t *nci, double *nval) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  for (int i = gw; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    const int o = pm[i];
+    const int64_t src = rp[o], dst = nrp[i], m = rp[o + 1] - src;
+    for (int64_t x = lane; x < m; x += 32) {
+      nci[dst + x] = ipm[ci[src + x]];
+      nval[dst + x] = val[src + x];
+    }
+  }
+}
+
 // ---- exclusive scan of int64 (out has n+1 entries; out[n] = total)
 __global__ void __launch_bounds__(256) scan_tiles_kernel(const int64_t *in, int64_t n, int64_t *part) {
   __shared__ int64_t sw[8];
@@ -459,14 +478,26 @@ cudaError_t build_sets(const EstArgs &E, int grid, int sms, int64_t **off_o, int
 
 // Runs the whole estimate on the permuted CSR already on the device.  h_sizes (HOST,
 // capacity n) receives the block sizes, *nblocks their number; *launches the kernels run.
-extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci, const double *val, double tau,
-                                     int max_size, int sms, cudaStream_t st, int32_t *h_sizes, int32_t *nblocks,
-                                     int *launches) {
+// pm / ipm (device, may be NULL = identity): the estimate runs on Ã = A(pm, pm).
+extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci, const double *val,
+                                     const int32_t *pm, const int32_t *ipm, double tau, int max_size, int sms,
+                                     cudaStream_t st, int32_t *h_sizes, int32_t *nblocks, int *launches) {
   Pool pool;
   *launches = 0;
   int64_t nnz = 0;
   cudaError_t e = cudaMemcpyAsync(&nnz, rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess || (e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  if (pm) {
+    int64_t *len = pool.get<int64_t>(n), *nrp = pool.get<int64_t>(n + 1);
+    int32_t *nci = pool.get<int32_t>(nnz);
+    double *nval = pool.get<double>(nnz);
+    if (pool.err != cudaSuccess) return pool.err;
+    perm_len_kernel<<<sms * 4, 256, 0, st>>>(n, rp, pm, len);
+    if ((e = scan_excl(len, n, nrp, pool, st)) != cudaSuccess) return e;
+    perm_rows_kernel<<<sms * 8, 256, 0, st>>>(n, rp, ci, val, pm, ipm, nrp, nci, nval);
+    *launches += 5;
+    rp = nrp; ci = nci; val = nval;
+  }
   // 1. CSC
   unsigned long long *colcnt = pool.get<unsigned long long>(n);
   int64_t *cp = pool.get<int64_t>(n + 1);

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <chrono>
 #include <ctime>
 #include <unistd.h>
 
@@ -35,6 +36,8 @@ extern "C" cudaError_t bilu_launch_permute(double *y, const double *x, const int
                                            int32_t n, int inverse, cudaStream_t st);
 extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_t st);
 extern "C" int bilu_merge_plan_launches();
+extern "C" int bilu_merge_test_grid(int grid);
+extern "C" cudaError_t bilu_merge_bound(const MergeArgs &M, unsigned long long *out, int sms, cudaStream_t st);
 extern "C" int bilu_heavyctx_size();
 extern "C" cudaError_t bilu_launch_spmv(int n, const int64_t *rp, const int32_t *ci, const double *val, const double *x,
                                         double *y, int lpr, int sms, cudaStream_t st);
@@ -62,9 +65,9 @@ extern "C" int bilu_merge_nchunks(int N);
 extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
                                         cudaStream_t st);
 extern "C" cudaError_t bilu_launch_apply(const ApplyArgs &A, int grid, int backward, cudaStream_t st);
-extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci, const double *val, double tau,
-                                     int max_size, int sms, cudaStream_t st, int32_t *h_sizes, int32_t *nblocks,
-                                     int *launches);
+extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci, const double *val,
+                                     const int32_t *pm, const int32_t *ipm, double tau, int max_size, int sms,
+                                     cudaStream_t st, int32_t *h_sizes, int32_t *nblocks, int *launches);
 }  // namespace bilu
 
 // Final (post-aggregation) factor: per final block F, descriptors into the
@@ -113,6 +116,8 @@ struct bilu_ctx {
   unsigned long long cur[4] = {0, 0, 0, 0};      // arena cursors after phase A + unpacks
   unsigned long long qhead0 = 0, ctrl_init[CTRL_COUNT * CS];
   int32_t *d_own_ready = nullptr; int32_t n_own_ready = 0;
+  unsigned long long *d_mbound = nullptr;           // merge test: widest window
+  unsigned char *d_mhbig = nullptr; int64_t mhbig_cap = 0;   // merge test: per-CTA global tables
   double flops_local = 0.0, t_local_ms = 0.0;
   double *d_alpha = nullptr;
   // GMRES: A's CSR structure (original ordering) and the Krylov workspace
@@ -745,6 +750,25 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
     M.Ucol_off = F.Ucol_off; M.Uc = F.Uc; M.Uval_off = F.Uval_off;
     M.D = F.D; M.D_off = F.D_off;
     M.work_ints = h->merge_work_ints;
+    {   // windows too wide for the test's shared-memory table use per-CTA global tables
+      M.Lidx = F.Lidx; M.Uidx = F.Uidx;
+      if (!h->d_mbound) CUDA_TRY(h, dalloc(h, &h->d_mbound, 1));
+      CUDA_TRY(h, bilu_merge_bound(M, h->d_mbound, h->sms, h->stream));
+      launches += 1;
+      unsigned long long mx = 0;
+      CUDA_TRY(h, cudaMemcpyAsync(&mx, h->d_mbound, sizeof(mx), cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      int64_t cap = 64;
+      while (cap < 2 * (int64_t)mx) cap <<= 1;
+      if (cap > 8192 && cap > h->mhbig_cap) {
+        if (h->d_mhbig) dfree(h, h->d_mhbig);
+        h->d_mhbig = nullptr;
+        CUDA_TRY(h, dalloc(h, &h->d_mhbig, (size_t)bilu_merge_test_grid(h->grid) * 9 * (size_t)cap));
+        h->mhbig_cap = cap;
+      }
+      M.hbig = h->d_mhbig;
+      M.hbig_cap = h->mhbig_cap;
+    }
     unsigned long long tot[16];
     for (int attempt = 0;; ++attempt) {
       M.Lidx = F.Lidx; M.Uidx = F.Uidx; M.Lval = F.Lval; M.Uval = F.Uval;
@@ -1592,15 +1616,11 @@ extern "C" bilu_status bilu_ilu1_blocks(int32_t n, const int64_t *row_ptr, const
     return BILU_ERR_ARG;
   }
   if (n >= (1 << 30)) { set_err(nullptr, "bilu_ilu1_blocks: n must be < 2^30"); return BILU_ERR_ARG; }
+  const auto t_host0 = std::chrono::steady_clock::now();
   std::vector<int32_t> pm, ipm;
   bilu_status st = check_csr_perm("bilu_ilu1_blocks", n, row_ptr, col_idx, perm, pm, ipm);
   if (st != BILU_OK) return st;
-  std::vector<int64_t> rp, map;
-  std::vector<int32_t> ci;
-  permute_csr(n, row_ptr, col_idx, pm, ipm, rp, ci, map);
-  const int64_t nnz = rp[n];
-  std::vector<double> v(nnz);
-  for (int64_t q = 0; q < nnz; ++q) v[q] = val[map[q]];
+  const int64_t nnz = row_ptr[n];
   if (cudaSetDevice(device) != cudaSuccess) {
     set_err(nullptr, "bilu_ilu1_blocks: cannot use CUDA device %d", device);
     return BILU_ERR_NOT_BUILT;
@@ -1609,18 +1629,31 @@ extern "C" bilu_status bilu_ilu1_blocks(int32_t n, const int64_t *row_ptr, const
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaStream_t s = (cudaStream_t)stream;
   int64_t *d_rp = nullptr;
-  int32_t *d_ci = nullptr;
+  int32_t *d_ci = nullptr, *d_pm = nullptr, *d_ipm = nullptr;
   double *d_v = nullptr;
   cudaError_t e = cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1));
   if (e == cudaSuccess) e = cudaMalloc(&d_ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
   if (e == cudaSuccess) e = cudaMalloc(&d_v, sizeof(double) * (nnz > 0 ? nnz : 1));
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_rp, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(d_ci, ci.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(d_v, v.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && perm) e = cudaMalloc(&d_pm, sizeof(int32_t) * n);
+  if (e == cudaSuccess && perm) e = cudaMalloc(&d_ipm, sizeof(int32_t) * n);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(d_ci, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(d_v, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && perm) e = cudaMemcpyAsync(d_pm, pm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && perm) e = cudaMemcpyAsync(d_ipm, ipm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s);
   int launches = 0;
-  if (e == cudaSuccess) e = bilu_ilu1_run(n, d_rp, d_ci, d_v, tau, max_size, sms, s, block_sizes, n_blocks, &launches);
   cudaStreamSynchronize(s);
-  cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_v);
+  const auto t_dev0 = std::chrono::steady_clock::now();
+  if (e == cudaSuccess)
+    e = bilu_ilu1_run(n, d_rp, d_ci, d_v, d_pm, d_ipm, tau, max_size, sms, s, block_sizes, n_blocks, &launches);
+  cudaStreamSynchronize(s);
+  if (getenv("BILU_VERBOSE")) {
+    const auto t_dev1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[bilu] ilu1_blocks: host validate+upload %.2f ms, device permute+estimate %.2f ms (%d launches)\n",
+            std::chrono::duration<double, std::milli>(t_dev0 - t_host0).count(),
+            std::chrono::duration<double, std::milli>(t_dev1 - t_dev0).count(), launches);
+  }
+  cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_v); cudaFree(d_pm); cudaFree(d_ipm);
   if (n_kernel_launches) *n_kernel_launches = launches;
   if (e != cudaSuccess) {
     set_err(nullptr, "bilu_ilu1_blocks: %s", cudaGetErrorString(e));

@@ -146,6 +146,9 @@ struct MergeArgs {
   int *work; int64_t work_ints;  // per-CTA workspace (ints)
   double *flops;          // [1]
   int *ovf;               // [1]
+  // test windows wider than the shared-memory hash table: per-CTA global tables of hbig_cap
+  // slots (keys int32, dmin int32, flag uint8), bytes per CTA = 9 * hbig_cap
+  unsigned char *hbig; int64_t hbig_cap;
 };
 
 // Apply (forward/backward block triangular solves) -- dataflow over final blocks.

@@ -114,14 +114,14 @@ struct TestSide {
 };
 
 // Per distinct key x of the window's lists: dmin(x) = smallest d >= 1 with x in l_d and
-// whether x is in l_0, from an open-addressing hash table in shared memory (O(total list
-// length) per block); windows with more entries than the table holds use binary searches
-// in the (global) lists instead.
-constexpr int TEST_HT = 8192;      // hash slots (power of two)
+// whether x is in l_0, from an open-addressing hash table (O(total list length) per block):
+// in shared memory when 2 * total <= TEST_HT, else in the CTA's global-memory table
+// (M.hbig, sized by merge_bound_kernel for the widest window).
+constexpr int TEST_HT = 8192;      // shared hash slots (power of two)
 
 __device__ __forceinline__ unsigned t_hash(int key, unsigned mask) { return ((unsigned)key * 0x9E3779B1u) >> 5 & mask; }
 
-__device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *hkeys, int *hdmin, uint8_t *hflag,
+__device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *s_hkeys, int *s_hdmin, uint8_t *s_hflag,
                           int *s_len, int *s_off, const int **s_ptr, TestSide &R) {
   const int tid = threadIdx.x;
   const int s_k = M.bstart[k], e_k = M.bstart[k + 1];
@@ -157,50 +157,41 @@ __device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *hkey
   }
   __syncthreads();
   const int total = s_off[W + 1];
-  if (2 * total <= TEST_HT) {
-    unsigned hs = 64;
-    while (hs < 2u * (unsigned)total) hs <<= 1;
-    const unsigned mask = hs - 1;
-    for (unsigned h = tid; h < hs; h += TEST_T) { hkeys[h] = -1; hdmin[h] = 255; hflag[h] = 0; }
-    __syncthreads();
-    for (int x = tid; x < total; x += TEST_T) {
-      int lo = 0, hi = W;
-      while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= x) lo = mid; else hi = mid - 1; }
-      const int d = lo;
-      const int key = s_ptr[d][x - s_off[d]];
-      unsigned h = t_hash(key, mask);
-      while (true) {
-        const int old = atomicCAS(&hkeys[h], -1, key);
-        if (old == -1 || old == key) break;
-        h = (h + 1) & mask;
-      }
-      if (d == 0) hflag[h] = 1;
-      else atomicMin(&hdmin[h], d);
+  unsigned hs = 64;
+  while (hs < 2u * (unsigned)total) hs <<= 1;
+  int *hkeys = s_hkeys, *hdmin = s_hdmin;
+  uint8_t *hflag = s_hflag;
+  if (hs > (unsigned)TEST_HT) {      // the CTA's global table (capacity checked by the host's bound)
+    unsigned char *base = M.hbig + (size_t)blockIdx.x * 9 * (size_t)M.hbig_cap;
+    hkeys = (int *)base;
+    hdmin = hkeys + M.hbig_cap;
+    hflag = (uint8_t *)(hdmin + M.hbig_cap);
+  }
+  const unsigned mask = hs - 1;
+  for (unsigned h = tid; h < hs; h += TEST_T) { hkeys[h] = -1; hdmin[h] = 255; hflag[h] = 0; }
+  __syncthreads();
+  for (int x = tid; x < total; x += TEST_T) {
+    int lo = 0, hi = W;
+    while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= x) lo = mid; else hi = mid - 1; }
+    const int d = lo;
+    const int key = s_ptr[d][x - s_off[d]];
+    unsigned h = t_hash(key, mask);
+    while (true) {
+      const int old = atomicCAS(&hkeys[h], -1, key);
+      if (old == -1 || old == key) break;
+      h = (h + 1) & mask;
     }
-    __syncthreads();
-    for (unsigned h = tid; h < hs; h += TEST_T) {
-      const int key = hkeys[h], d = hdmin[h];
-      if (key < 0 || d > W) continue;
-      if (key < e_k) atomicAdd(&R.r[d], 1);
-      else {
-        atomicAdd(&R.s[d], 1);
-        if (!hflag[h]) atomicAdd(&R.u[d], 1);
-      }
-    }
-  } else {
-    for (int x = s_len[0] + tid; x < total; x += TEST_T) {
-      int lo = 1, hi = W;
-      while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (s_off[mid] <= x) lo = mid; else hi = mid - 1; }
-      const int d = lo;
-      const int key = s_ptr[d][x - s_off[d]];
-      bool first = true;
-      for (int d2 = 1; d2 < d && first; ++d2) first = !m_contains(s_ptr[d2], s_len[d2], key);
-      if (!first) continue;
-      if (key < e_k) atomicAdd(&R.r[d], 1);
-      else {
-        atomicAdd(&R.s[d], 1);
-        if (!m_contains(s_ptr[0], s_len[0], key)) atomicAdd(&R.u[d], 1);
-      }
+    if (d == 0) hflag[h] = 1;
+    else atomicMin(&hdmin[h], d);
+  }
+  __syncthreads();
+  for (unsigned h = tid; h < hs; h += TEST_T) {
+    const int key = hkeys[h], d = hdmin[h];
+    if (key < 0 || d > W) continue;
+    if (key < e_k) atomicAdd(&R.r[d], 1);
+    else {
+      atomicAdd(&R.s[d], 1);
+      if (!hflag[h]) atomicAdd(&R.u[d], 1);
     }
   }
   __syncthreads();
@@ -209,6 +200,30 @@ __device__ void test_side(const MergeArgs &M, int k, int W, bool rows, int *hkey
     for (int d = 1; d <= W; ++d) { r += R.r[d]; s += R.s[d]; u += R.u[d]; R.r[d] = r; R.s[d] = s; R.u[d] = u; }
   }
   __syncthreads();
+}
+
+// widest test window: max over k and both sides of the window's total list length
+__global__ void __launch_bounds__(256) merge_bound_kernel(MergeArgs M, unsigned long long *out) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int k = gw; k < M.N; k += nw) {
+    const int W = (int)(M.wofs[k + 1] - M.wofs[k]) - 1;
+    if (W <= 0) continue;
+    const int s_k = M.bstart[k];
+    long long tl = 0, tu = 0;
+    for (int d = lane; d <= W; d += 32) {
+      const int j = k - d;
+      const int ml = M.Lm[j], mu = M.Uc[j];
+      tl += ml - m_lbound(M.Lidx + M.Lrow_off[j], 0, ml, s_k);
+      tu += mu - m_lbound(M.Uidx + M.Ucol_off[j], 0, mu, s_k);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tl += __shfl_xor_sync(0xffffffffu, tl, o);
+      tu += __shfl_xor_sync(0xffffffffu, tu, o);
+    }
+    if (lane == 0) atomicMax(out, (unsigned long long)(tl > tu ? tl : tu));
+  }
 }
 
 __global__ void __launch_bounds__(TEST_T) merge_test_kernel(MergeArgs M) {
@@ -681,7 +696,7 @@ extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_
   const int tsmem = TEST_HT * 9;
   cudaError_t e = cudaFuncSetAttribute(merge_test_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
   if (e != cudaSuccess) return e;
-  merge_test_kernel<<<grid * 3, TEST_T, tsmem, st>>>(M);
+  merge_test_kernel<<<grid * 3, TEST_T, tsmem, st>>>(M);   // bilu_merge_test_grid
   if (nchunks > 0) merge_chunkmap_kernel<<<nchunks, 128, 0, st>>>(M);
   merge_scan_kernel<<<1, 1024, 0, st>>>(M, nchunks);
   merge_offsets_kernel<<<1, 1024, 0, st>>>(M);
@@ -689,6 +704,13 @@ extern "C" cudaError_t bilu_merge_plan(const MergeArgs &M, int grid, cudaStream_
 }
 
 extern "C" int bilu_merge_plan_launches() { return 4; }
+extern "C" int bilu_merge_test_grid(int grid) { return grid * 3; }
+
+extern "C" cudaError_t bilu_merge_bound(const MergeArgs &M, unsigned long long *out, int sms, cudaStream_t st) {
+  cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+  merge_bound_kernel<<<sms * 8, 256, 0, st>>>(M, out);
+  return cudaGetLastError();
+}
 extern "C" int bilu_merge_nchunks(int N) { return N > 1 ? (N - 1 + SCAN_CHUNK - 1) / SCAN_CHUNK : 0; }
 
 extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
