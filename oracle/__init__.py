@@ -94,6 +94,9 @@ def _load():
         lib.orc_ilu1_set.restype = ctypes.c_int32
         lib.orc_ilu1_set.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
+        lib.orc_cosine_blocks.restype = ctypes.c_int32
+        lib.orc_cosine_blocks.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                          ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
         lib.orc_bilu_apply.restype = ctypes.c_int
         lib.orc_bilu_apply.argtypes = [ctypes.POINTER(_Factor), ctypes.c_void_p, ctypes.c_void_p]
         lib.orc_aggregate_test.restype = ctypes.c_int
@@ -306,3 +309,18 @@ def ilu1_set(indptr, indices, data, tau, k, lower=True) -> np.ndarray:
     if m < 0:
         raise OracleError("bad argument")
     return out[:m].copy()
+
+
+def cosine_blocks(indptr, indices, tau=0.8, max_size=128):
+    """Cosine-based blocking of Sec. 3.2 (R21): (q new->old, group sizes)."""
+    lib = _load()
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    indices = np.ascontiguousarray(indices, dtype=np.int32)
+    n = len(indptr) - 1
+    q = np.zeros(n, dtype=np.int32)
+    sizes = np.zeros(n, dtype=np.int32)
+    nb = lib.orc_cosine_blocks(n, indptr.ctypes.data, indices.ctypes.data, float(tau), int(max_size),
+                               q.ctypes.data, sizes.ctypes.data)
+    if nb < 0:
+        raise OracleError("bad argument")
+    return q, sizes[:nb].copy()

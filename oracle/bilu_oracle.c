@@ -944,3 +944,91 @@ int32_t orc_ilu1_blocks(int32_t n, const int64_t *rp, const int32_t *ci, const d
   free(inI); free(inJ); free(listI); free(listJ);
   return nb;
 }
+
+/* ---------------- cosine-based blocking (Sec. 3.2; R21) ----------------
+ * Pattern vectors c_i of the rows of A; rows i, j are grouped when
+ *   nz(a_i n a_j)^2 >= tau nz(a_i) nz(a_j)
+ * scanning i = 0, 1, ... : an unassigned row i opens a group and takes every unassigned j > i
+ * with (A A^T)_ij != 0 that passes the test, in increasing j, until the group has max_size rows
+ * (Saad's greedy over the upper triangle of A A^T).  Rows / columns with more
+ * than mu + 2 sigma nonzeros (mu = nnz/n, sigma the population standard deviation of the row /
+ * column counts) are ignored: an ignored column does not count in nz(.) or in
+ * the intersections, an ignored row forms its own group.  The mu + 2 sigma test is evaluated in
+ * exact integers: c > mu + 2 sigma  <=>  n c - S1 > 0 and (n c - S1)^2 > 4 (n S2 - S1^2).
+ * Output: q (new -> old, groups in the order of their first row, rows ascending inside) and the
+ * group sizes; returns the number of groups, -1 on a bad argument. */
+static int cos_heavy(int64_t c, int64_t n, int64_t S1, int64_t S2) {
+  const __int128 a = (__int128)n * c - S1;
+  if (a <= 0) return 0;
+  return a * a > (__int128)4 * ((__int128)n * S2 - (__int128)S1 * S1);
+}
+
+int32_t orc_cosine_blocks(int32_t n, const int64_t *rp, const int32_t *ci, double tau, int32_t max_size,
+                          int32_t *q, int32_t *sizes) {
+  if (n < 1 || !rp || !ci || !q || !sizes || max_size < 1 || !(tau >= 0.0)) return -1;
+  const int64_t nnz = rp[n];
+  int64_t *rc = (int64_t *)xcalloc((size_t)n, sizeof(int64_t)), *cc = (int64_t *)xcalloc((size_t)n, sizeof(int64_t));
+  for (int32_t i = 0; i < n; ++i) rc[i] = rp[i + 1] - rp[i];
+  for (int64_t p = 0; p < nnz; ++p) cc[ci[p]]++;
+  int64_t S1r = 0, S2r = 0, S1c = 0, S2c = 0;
+  for (int32_t i = 0; i < n; ++i) { S1r += rc[i]; S2r += rc[i] * rc[i]; S1c += cc[i]; S2c += cc[i] * cc[i]; }
+  char *row_ign = (char *)xcalloc((size_t)n, 1), *col_ign = (char *)xcalloc((size_t)n, 1);
+  for (int32_t i = 0; i < n; ++i) {
+    row_ign[i] = (char)cos_heavy(rc[i], n, S1r, S2r);
+    col_ign[i] = (char)cos_heavy(cc[i], n, S1c, S2c);
+  }
+  /* nz(a_i) over the columns kept; CSC of the kept columns */
+  int64_t *nz = (int64_t *)xcalloc((size_t)n, sizeof(int64_t));
+  int64_t *cp = (int64_t *)xcalloc((size_t)n + 1, sizeof(int64_t));
+  for (int32_t i = 0; i < n; ++i)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+      if (!col_ign[ci[p]]) { nz[i]++; cp[ci[p] + 1]++; }
+  for (int32_t j = 0; j < n; ++j) cp[j + 1] += cp[j];
+  int32_t *cr = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)(cp[n] > 0 ? cp[n] : 1));
+  int64_t *fill = (int64_t *)xmalloc(sizeof(int64_t) * (size_t)n);
+  for (int32_t j = 0; j < n; ++j) fill[j] = cp[j];
+  for (int32_t i = 0; i < n; ++i)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+      if (!col_ign[ci[p]]) cr[fill[ci[p]]++] = i;          /* rows ascending in each column */
+  int32_t *group = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)n);
+  for (int32_t i = 0; i < n; ++i) group[i] = -1;
+  int64_t *cnt = (int64_t *)xcalloc((size_t)n, sizeof(int64_t));
+  int32_t *touched = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)n);
+  int32_t nb = 0, pos = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    if (group[i] >= 0) continue;
+    group[i] = nb;
+    q[pos++] = i;
+    int32_t size = 1;
+    if (!row_ign[i] && nz[i] > 0) {
+      /* nz(a_i n a_j) for every j > i sharing a kept column: row i of A A^T */
+      int32_t nt = 0;
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t c = ci[p];
+        if (col_ign[c]) continue;
+        for (int64_t x = cp[c]; x < cp[c + 1]; ++x) {
+          const int32_t j = cr[x];
+          if (j <= i) continue;
+          if (cnt[j] == 0) touched[nt++] = j;
+          cnt[j]++;
+        }
+      }
+      qsort(touched, (size_t)nt, sizeof(int32_t), cmp_int);
+      for (int32_t t = 0; t < nt; ++t) {
+        const int32_t j = touched[t];
+        const int64_t c = cnt[j];
+        cnt[j] = 0;
+        if (size >= max_size || group[j] >= 0 || row_ign[j]) continue;
+        if ((double)c * (double)c >= tau * ((double)nz[i] * (double)nz[j])) {
+          group[j] = nb;
+          q[pos++] = j;
+          size++;
+        }
+      }
+    }
+    sizes[nb++] = size;
+  }
+  free(rc); free(cc); free(row_ign); free(col_ign); free(nz); free(cp); free(cr); free(fill); free(group);
+  free(cnt); free(touched);
+  return nb;
+}

@@ -98,6 +98,12 @@ int32_t orc_ilu1_blocks(int32_t n, const int64_t *rp, const int32_t *ci, const d
 int32_t orc_ilu1_set(int32_t n, const int64_t *rp, const int32_t *ci, const double *val, double tau, int32_t k,
                      int32_t lower, int32_t *out);
 
+/* Cosine-based blocking of Sec. 3.2 (R21) on the pattern of A:
+ * q (capacity n) receives the grouping permutation (new -> old), sizes (capacity n) the group
+ * sizes; returns the number of groups, -1 on a bad argument. */
+int32_t orc_cosine_blocks(int32_t n, const int64_t *rp, const int32_t *ci, double tau, int32_t max_size,
+                          int32_t *q, int32_t *sizes);
+
 void orc_free(orc_factor *f);
 
 #ifdef __cplusplus

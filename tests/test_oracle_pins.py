@@ -489,3 +489,66 @@ def test_ilu1_sets_inside_exact_lu_pattern_and_monotone():
             prev_lo, prev_up = lo_t, up_t
     b = oracle.ilu1_blocks(ip, ix, dv, 1e-2, 8)
     assert b.sum() == n and b.min() >= 1 and b.max() <= 8
+
+
+# ------------------------------------------------------------ cosine-based blocking (Sec. 3.2)
+def _pattern_csr(rows, n):
+    ip = np.zeros(n + 1, dtype=np.int64)
+    for i, r in enumerate(rows):
+        ip[i + 1] = ip[i] + len(r)
+    return ip, np.concatenate([np.asarray(sorted(r), dtype=np.int32) for r in rows])
+
+
+def test_cosine_hand_trace():
+    """Hand trace of PAPER.md:934-947 on a 6x6 pattern (tests/golden/cosine_hand_6x6.json).
+    No row/column exceeds mu + 2 sigma (rows: mu=3, 4 sigma^2 = 240/36; columns: 48/36).
+    tau=.8: row 0 (nz 4) takes row 2 on the equality 4^2 = .8*4*5 but not row 1 (3^2 < 9.6);
+    rows 3,4: 2^2 < .8*2*3.  tau=.75: 3^2 >= .75*12 also takes row 1.  max_size=2 stops the
+    first group after row 1, and row 2 (with rows 3, 4: 1 < 7.5, 4 < 11.25) stays alone.
+    Grouping columns instead of rows (a transposed operand) gives {0,1,2} at tau=.8."""
+    g = json.load(open(os.path.join(GOLD, "cosine_hand_6x6.json")))
+    ip, ix = _pattern_csr(g["rows"], 6)
+    for c in g["cases"]:
+        q, s = oracle.cosine_blocks(ip, ix, c["tau"], c["max_size"])
+        assert list(q) == c["q"] and list(s) == c["sizes"], c
+
+
+def test_cosine_ignores_dense_rows_and_columns():
+    """Arrow pattern (dense row 0 and column 0 + diagonal), n=10, tau=.2: row/column 0 have
+    10 > mu + 2 sigma nonzeros (mu = 2.8, sigma = 2.4) and are ignored; the other rows then share
+    no kept column, so every group is a singleton.  Keeping column 0 would put rows 1.. together
+    (1^2 >= .2*2*2)."""
+    n = 10
+    rows = [list(range(n))] + [[0, i] for i in range(1, n)]
+    ip, ix = _pattern_csr(rows, n)
+    q, s = oracle.cosine_blocks(ip, ix, 0.2, 128)
+    assert list(s) == [1] * n and list(q) == list(range(n))
+
+
+def test_cosine_cap_identical_rows():
+    """Identical rows (sigma = 0, nothing ignored): the first row takes the next ones up to max_size."""
+    n = 10
+    ip, ix = _pattern_csr([list(range(n))] * n, n)
+    q, s = oracle.cosine_blocks(ip, ix, 0.8, 4)
+    assert list(s) == [4, 4, 2] and list(q) == list(range(n))
+
+
+def test_cosine_recovers_permuted_block_diagonal():
+    """Dense diagonal blocks [3,1,4,2,5] under a random symmetric permutation: rows of one block
+    have identical patterns (cosine 1) and rows of different blocks share no column, so the
+    groups are exactly the blocks, in the order of their first row."""
+    sizes = [3, 1, 4, 2, 5]
+    n = sum(sizes)
+    lab = np.repeat(np.arange(len(sizes)), sizes)
+    perm = np.random.default_rng(4).permutation(n)          # new row r = old row perm[r]
+    lab_new = lab[perm]
+    rows = [list(np.nonzero(lab_new == lab_new[r])[0]) for r in range(n)]
+    ip, ix = _pattern_csr(rows, n)
+    q, s = oracle.cosine_blocks(ip, ix, 0.8, 128)
+    groups, seen = [], set()
+    for r in range(n):
+        if lab_new[r] not in seen:
+            seen.add(lab_new[r])
+            groups.append(list(np.nonzero(lab_new == lab_new[r])[0]))
+    assert list(s) == [len(g) for g in groups]
+    assert list(q) == [x for g in groups for x in g]
