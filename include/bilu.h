@@ -260,6 +260,26 @@ bilu_status bilu_ilu1_blocks(int32_t n, const int64_t *row_ptr, const int32_t *c
                              const int32_t *perm, double tau, int32_t max_size, int32_t device, void *stream,
                              int32_t *block_sizes, int32_t *n_blocks, int32_t *n_kernel_launches);
 
+/*
+ * bilu_cosine_blocks -- cosine-based initial blocking of Sec. 3.2 (readings
+ * in DESIGN.md R21), computed on the device from the pattern of A.
+ *   n, row_ptr, col_idx   HOST CSR of A as in bilu_analyze (values are not used)
+ *   tau          similarity threshold in [0,1] (the paper's 0.8)
+ *   max_size     cap on a group (1..128)
+ *   device, stream   CUDA device ordinal and cudaStream_t (NULL = legacy default stream)
+ *   q            HOST, int32[n]: the grouping permutation Q (new -> old), Ã = A(q, q)
+ *   block_sizes  HOST, int32[n] (capacity n): group sizes in Q's order, sum = n
+ *   n_blocks     receives the number of groups
+ *   n_kernel_launches   optional (may be NULL)
+ * Rows i, j join when nz(a_i n a_j)^2 >= tau nz(a_i) nz(a_j); rows / columns with more than
+ * mu + 2 sigma nonzeros are ignored; groups follow Saad's greedy in row order.  Result identical
+ * to the oracle's.  Synchronous; device memory allocated and freed inside.  Errors: BILU_ERR_ARG
+ * (bad CSR / tau / max_size), BILU_ERR_OOM, BILU_ERR_CUDA, BILU_ERR_NOT_BUILT.
+ */
+bilu_status bilu_cosine_blocks(int32_t n, const int64_t *row_ptr, const int32_t *col_idx, double tau, int32_t max_size,
+                               int32_t device, void *stream, int32_t *q, int32_t *block_sizes, int32_t *n_blocks,
+                               int32_t *n_kernel_launches);
+
 const char *bilu_last_error(const bilu_ctx *h);
 
 /* Number of kernels the library launched since the context was created

@@ -22,7 +22,8 @@ ABI_SYMBOLS = ["bilu_options_default", "bilu_analyze", "bilu_set_values", "bilu_
                "bilu_apply", "bilu_export", "bilu_factor_view_free", "bilu_destroy",
                "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm", "bilu_diag_tsgemm",
                "bilu_dist_setup", "bilu_factor_local", "bilu_interface_pack", "bilu_interface_unpack",
-               "bilu_factor_separators", "bilu_gmres", "bilu_ilu1_blocks"]
+               "bilu_factor_separators", "bilu_gmres", "bilu_ilu1_blocks",
+               "bilu_cosine_blocks"]
 
 
 class BiluError(RuntimeError):
@@ -134,6 +135,8 @@ def load_library():
     lib.bilu_factor_separators.restype = ctypes.c_int
     lib.bilu_ilu1_blocks.argtypes = [ctypes.c_int32, P, P, P, P, D, ctypes.c_int32, ctypes.c_int32, P, P, P, P]
     lib.bilu_ilu1_blocks.restype = ctypes.c_int
+    lib.bilu_cosine_blocks.argtypes = [ctypes.c_int32, P, P, D, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P]
+    lib.bilu_cosine_blocks.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -359,3 +362,22 @@ def ilu1_blocks(indptr, indices, data, tau, max_size=8, perm=None, device=0, str
     if rc != 0:
         raise BiluError(rc, lib.bilu_last_error(None).decode())
     return out[: nb.value].copy(), nl.value
+
+
+def cosine_blocks(indptr, indices, tau=0.8, max_size=128, device=0, stream=0):
+    """bilu_cosine_blocks: cosine-based blocking of Sec. 3.2 on the device.
+    Returns (q new->old int32 array, block sizes int32 array, kernels launched)."""
+    lib = load_library()
+    ip = _arr(indptr, np.int64)
+    ix = _arr(indices, np.int32)
+    n = len(ip) - 1
+    q = np.zeros(max(n, 1), dtype=np.int32)
+    out = np.zeros(max(n, 1), dtype=np.int32)
+    nb = ctypes.c_int32(0)
+    nl = ctypes.c_int32(0)
+    rc = lib.bilu_cosine_blocks(n, ip.ctypes.data, ix.ctypes.data, float(tau), int(max_size), int(device),
+                                ctypes.c_void_p(stream), q.ctypes.data, out.ctypes.data, ctypes.byref(nb),
+                                ctypes.byref(nl))
+    if rc != 0:
+        raise BiluError(rc, lib.bilu_last_error(None).decode())
+    return q[:n].copy(), out[: nb.value].copy(), nl.value

@@ -384,6 +384,278 @@ __global__ void __launch_bounds__(256) scan_apply_kernel(const int64_t *in, int6
   }
 }
 
+// ================================================================ cosine-based blocking
+// Sec. 3.2 (R21): rows i, j with nz(a_i n a_j)^2 >= tau nz(a_i) nz(a_j)
+// are grouped by Saad's greedy (rows in increasing order, an unassigned row takes the unassigned
+// j > i that pass, up to max_size).  On the device: the pairs that pass (one warp per row i, the
+// row of A A^T in a count hash), then the greedy as a fixed point: j is decided once every
+// smaller neighbour is: it joins the first leader i among them whose earlier joiners leave room
+// (its slot = 1 + their number), else it leads.  Decisions only read decided states, so the
+// in-place rounds are deterministic; a one-thread sweep in index order finishes long chains.
+
+// exact "count > mu + 2 sigma" (population sigma): n c - S1 > 0 and (n c - S1)^2 > 4 (n S2 - S1^2)
+__device__ __forceinline__ int cos_heavy_dev(long long c, long long n, long long S1, long long S2) {
+  const __int128 a = (__int128)n * c - S1;
+  if (a <= 0) return 0;
+  return a * a > (__int128)4 * ((__int128)n * S2 - (__int128)S1 * S1);
+}
+
+// S[0..3] = sum rc, sum rc^2, sum cc, sum cc^2 (integers: exact in any order)
+__global__ void cos_stats_kernel(int n, const int64_t *rp, const unsigned long long *cc, unsigned long long *S) {
+  unsigned long long a = 0, b = 0, c = 0, d = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long r = (unsigned long long)(rp[i + 1] - rp[i]), k = cc[i];
+    a += r; b += r * r; c += k; d += k * k;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o); b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o); d += __shfl_xor_sync(0xffffffffu, d, o);
+  }
+  if ((threadIdx.x & 31) == 0) { atomicAdd(S, a); atomicAdd(S + 1, b); atomicAdd(S + 2, c); atomicAdd(S + 3, d); }
+}
+
+// ignore flags; kept-column counts (for the kept CSC) and nz(a_i) over kept columns
+__global__ void cos_flags_kernel(int n, const int64_t *rp, const int32_t *ci, const unsigned long long *cc,
+                                 const unsigned long long *S, uint8_t *rign, uint8_t *cign, int64_t *kcnt,
+                                 int64_t *nz) {
+  const long long S1r = (long long)S[0], S2r = (long long)S[1], S1c = (long long)S[2], S2c = (long long)S[3];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    rign[i] = (uint8_t)cos_heavy_dev(rp[i + 1] - rp[i], n, S1r, S2r);
+    const int ig = cos_heavy_dev((long long)cc[i], n, S1c, S2c);
+    cign[i] = (uint8_t)ig;
+    kcnt[i] = ig ? 0 : (int64_t)cc[i];
+  }
+}
+__global__ void cos_nz_kernel(int n, const int64_t *rp, const int32_t *ci, const uint8_t *cign, int64_t *nz) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  for (int i = gw; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    int64_t c = 0;
+    for (int64_t p = rp[i] + lane; p < rp[i + 1]; p += 32) c += !cign[ci[p]];
+    c = warp_sum64(c);
+    if (lane == 0) nz[i] = c;
+  }
+}
+__global__ void cos_csc_kernel(int n, const int64_t *rp, const int32_t *ci, const uint8_t *cign,
+                               unsigned long long *cur, int32_t *cr) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  for (int i = gw; i < n; i += (gridDim.x * blockDim.x) >> 5)
+    for (int64_t p = rp[i] + lane; p < rp[i + 1]; p += 32) {
+      const int32_t c = ci[p];
+      if (!cign[c]) cr[atomicAdd(cur + c, 1ull)] = i;
+    }
+}
+
+struct CosArgs {
+  int n;
+  const int64_t *rp; const int32_t *ci;     // A
+  const int64_t *cp; const int32_t *cr;     // kept columns
+  const uint8_t *rign, *cign;
+  const int64_t *nz;
+  double tau;
+};
+
+__device__ __forceinline__ int64_t cos_bound(const CosArgs &C, int i, int lane) {
+  int64_t b = 0;
+  for (int64_t p = C.rp[i] + lane; p < C.rp[i + 1]; p += 32) {
+    const int32_t c = C.ci[p];
+    if (!C.cign[c]) b += C.cp[c + 1] - C.cp[c];
+  }
+  return warp_sum64(b);
+}
+
+// row i of A A^T (j > i, kept rows) in T (keys) / V (counts), both cleared; returns nothing
+__device__ void cos_row(const CosArgs &C, int i, Table T, int32_t *V, int lane) {
+  for (int64_t p = C.rp[i]; p < C.rp[i + 1]; ++p) {
+    const int32_t c = C.ci[p];
+    if (C.cign[c]) continue;
+    for (int64_t x = C.cp[c] + lane; x < C.cp[c + 1]; x += 32) {
+      const int32_t j = C.cr[x];
+      if (j <= i || C.rign[j]) continue;
+      uint32_t s = slot0(j, T.mask);
+      while (true) {
+        const int32_t old = atomicCAS(T.t + s, -1, j);
+        if (old == -1 || old == j) break;
+        s = (s + 1) & T.mask;
+      }
+      atomicAdd(V + s, 1);
+    }
+  }
+  __syncwarp();
+}
+
+// passing j of the table, written to out (arbitrary order); returns their number
+__device__ int cos_emit(const CosArgs &C, int i, Table T, const int32_t *V, int32_t *out, int lane) {
+  const double ni = (double)C.nz[i];
+  int base = 0;
+  for (uint32_t s0 = 0; s0 <= T.mask; s0 += 32) {
+    const int32_t j = T.t[s0 + lane];
+    bool ok = false;
+    if (j >= 0) {
+      const double c = (double)V[s0 + lane];
+      ok = c * c >= C.tau * (ni * (double)C.nz[j]);
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, ok);
+    if (ok && out) out[base + __popc(b & ((1u << lane) - 1u))] = j;
+    base += __popc(b);
+  }
+  return base;
+}
+
+// src[0..m) distinct -> dst ascending (rank sort, one warp)
+__device__ void rank_sort_copy(const int32_t *src, int32_t *dst, int m, int lane) {
+  for (int x = lane; x < m; x += 32) {
+    const int32_t v = src[x];
+    int r = 0;
+    for (int y = 0; y < m; ++y) r += src[y] < v;
+    dst[r] = v;
+  }
+}
+
+struct CosOut {
+  int64_t *cnt; const int64_t *off; int32_t *tmp; int32_t *up;
+  int32_t *ovf_list; int *ovf_n; unsigned long long *ovf_max;
+};
+
+template <bool WRITE>
+__device__ void cos_one(const CosArgs &C, const CosOut &O, int i, Table T, int32_t *V, int lane) {
+  t_clear(T, lane);
+  for (uint32_t x = lane; x <= T.mask; x += 32) V[x] = 0;
+  __syncwarp();
+  cos_row(C, i, T, V, lane);
+  if (!WRITE) {
+    const int m = cos_emit(C, i, T, V, nullptr, lane);
+    if (lane == 0) O.cnt[i] = m;
+  } else {
+    const int m = cos_emit(C, i, T, V, O.tmp + O.off[i], lane);
+    __syncwarp();
+    rank_sort_copy(O.tmp + O.off[i], O.up + O.off[i], m, lane);
+  }
+  __syncwarp();
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(BT) cos_pairs_kernel(CosArgs C, CosOut O) {
+  extern __shared__ int32_t s_tab[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int CAP = SET_CAP / 2;
+  const Table T{s_tab + w * 2 * CAP, CAP - 1};
+  int32_t *V = s_tab + w * 2 * CAP + CAP;
+  for (int i = blockIdx.x * BW + w; i < C.n; i += gridDim.x * BW) {
+    if (C.rign[i] || C.nz[i] == 0) { if (!WRITE && lane == 0) O.cnt[i] = 0; continue; }
+    const int64_t b = cos_bound(C, i, lane);
+    if (2 * b > CAP) {
+      if (!WRITE && lane == 0) { O.ovf_list[atomicAdd(O.ovf_n, 1)] = i; atomicMax(O.ovf_max, (unsigned long long)b); }
+      continue;
+    }
+    cos_one<WRITE>(C, O, i, T, V, lane);
+  }
+}
+template <bool WRITE>
+__global__ void __launch_bounds__(BT) cos_pairs_big_kernel(CosArgs C, CosOut O, int nlist, int32_t *region, uint32_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * BT + threadIdx.x) >> 5, nw = gridDim.x * BW;
+  const Table T{region + (int64_t)gw * 2 * cap, cap - 1};
+  int32_t *V = region + (int64_t)gw * 2 * cap + cap;
+  for (int x = gw; x < nlist; x += nw) cos_one<WRITE>(C, O, O.ovf_list[x], T, V, lane);
+}
+
+// lower lists: low(j) = { i < j : j in up(i) }
+__global__ void cos_low_count_kernel(int n, const int64_t *uoff, const int32_t *up, unsigned long long *lcnt) {
+  const int64_t tot = uoff[n];
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < tot; p += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(lcnt + up[p], 1ull);
+}
+__global__ void cos_low_fill_kernel(int n, const int64_t *uoff, const int32_t *up, unsigned long long *cur, int32_t *tmp) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  for (int i = gw; i < n; i += (gridDim.x * blockDim.x) >> 5)
+    for (int64_t p = uoff[i] + lane; p < uoff[i + 1]; p += 32) tmp[atomicAdd(cur + up[p], 1ull)] = i;
+}
+__global__ void cos_low_sort_kernel(int n, const int64_t *loff, const int32_t *tmp, int32_t *low) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  for (int j = gw; j < n; j += (gridDim.x * blockDim.x) >> 5)
+    rank_sort_copy(tmp + loff[j], low + loff[j], (int)(loff[j + 1] - loff[j]), lane);
+}
+
+struct CosGreedy {
+  int n, max_size;
+  const int64_t *uoff; const int32_t *up;    // up(i) ascending
+  const int64_t *loff; const int32_t *low;   // low(j) ascending
+  int32_t *state;                            // -2 undecided, -1 leader, >= 0 leader it joined
+  int32_t *slot;                             // rank inside the group
+  int *progress;
+};
+
+// one decision attempt for j (undecided); returns 1 if decided
+__device__ int cos_decide(const CosGreedy &G, int j) {
+  volatile int32_t *st = G.state;
+  for (int64_t p = G.loff[j]; p < G.loff[j + 1]; ++p) {
+    const int i = G.low[p];
+    const int si = st[i];
+    if (si == -2) return 0;
+    if (si >= 0) continue;                   // i joined a group: it claims nobody
+    int cnt = 0;                             // earlier joiners of i
+    for (int64_t x = G.uoff[i]; x < G.uoff[i + 1]; ++x) {
+      const int jj = G.up[x];
+      if (jj >= j) break;
+      const int sj = st[jj];
+      if (sj == -2) return 0;
+      cnt += (sj == i);
+    }
+    if (cnt < G.max_size - 1) {
+      G.slot[j] = cnt + 1;
+      __threadfence();
+      st[j] = i;
+      return 1;
+    }
+  }
+  G.slot[j] = 0;
+  __threadfence();
+  st[j] = -1;
+  return 1;
+}
+
+__global__ void cos_init_kernel(int n, int32_t *state) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) state[j] = -2;
+}
+
+__global__ void cos_round_kernel(CosGreedy G) {
+  int done = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < G.n; j += gridDim.x * blockDim.x)
+    if (((volatile int32_t *)G.state)[j] == -2) done += cos_decide(G, j);
+  if (done) atomicAdd(G.progress, done);
+}
+__global__ void cos_undecided_kernel(int n, const int32_t *state, int64_t *flag) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) flag[j] = state[j] == -2;
+}
+__global__ void cos_list_kernel(int n, const int64_t *flag, const int64_t *pos, int32_t *list) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    if (flag[j]) list[pos[j]] = j;
+}
+// one thread over the undecided rows in index order: every dependency is decided first
+__global__ void cos_sweep_kernel(CosGreedy G, const int32_t *list, const int64_t *m) {
+  for (int64_t x = 0; x < *m; ++x) cos_decide(G, list[x]);
+}
+
+// groups: leaders numbered in index order; size = 1 + joiners; q[gstart[g] + slot[j]] = j
+__global__ void cos_leader_kernel(int n, const int32_t *state, int64_t *lead) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) lead[j] = state[j] == -1;
+}
+__global__ void cos_size_kernel(int n, const int32_t *state, const int64_t *gid, unsigned long long *gsize) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    atomicAdd(gsize + gid[state[j] == -1 ? j : state[j]], 1ull);
+}
+__global__ void cos_place_kernel(int n, const int32_t *state, const int32_t *slot, const int64_t *gid,
+                                 const int64_t *gstart, int32_t *q) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int L = state[j] == -1 ? j : state[j];
+    q[gstart[gid[L]] + slot[j]] = j;
+  }
+}
+__global__ void cos_sizes_kernel(int nb, const unsigned long long *gsize, int32_t *sizes) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < nb; g += gridDim.x * blockDim.x) sizes[g] = (int32_t)gsize[g];
+}
+
 // ---------------------------------------------------------------- host orchestration
 namespace {
 struct Pool {
@@ -572,6 +844,149 @@ extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci
   cudaMemcpyAsync(&nb, cbase + nch, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
   if (nb < 1 || nb > n) return cudaErrorUnknown;
+  cudaMemcpyAsync(h_sizes, sizes, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  *nblocks = (int32_t)nb;
+  return cudaGetLastError();
+}
+
+// Cosine-based blocking of the pattern of A (device CSR).  h_q (HOST, n): the grouping
+// permutation (new -> old); h_sizes (HOST, capacity n): group sizes; *nblocks their number.
+extern "C" cudaError_t bilu_cosine_run(int n, const int64_t *rp, const int32_t *ci, double tau, int max_size, int sms,
+                                       cudaStream_t st, int32_t *h_q, int32_t *h_sizes, int32_t *nblocks,
+                                       int *launches, int *rounds) {
+  Pool pool;
+  *launches = 0;
+  *rounds = 0;
+  int64_t nnz = 0;
+  cudaError_t e = cudaMemcpyAsync(&nnz, rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess || (e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  const int egrid = sms * 8;
+  unsigned long long *cc = pool.get<unsigned long long>(n), *S = pool.get<unsigned long long>(4);
+  uint8_t *rign = pool.get<uint8_t>(n), *cign = pool.get<uint8_t>(n);
+  int64_t *kcnt = pool.get<int64_t>(n), *nz = pool.get<int64_t>(n), *cp = pool.get<int64_t>(n + 1);
+  int32_t *cr = pool.get<int32_t>(nnz);
+  if (pool.err != cudaSuccess) return pool.err;
+  cudaMemsetAsync(cc, 0, sizeof(unsigned long long) * n, st);
+  cudaMemsetAsync(S, 0, sizeof(unsigned long long) * 4, st);
+  csc_count_kernel<<<egrid, 256, 0, st>>>(n, rp, ci, cc);
+  cos_stats_kernel<<<egrid, 256, 0, st>>>(n, rp, cc, S);
+  cos_flags_kernel<<<egrid, 256, 0, st>>>(n, rp, ci, cc, S, rign, cign, kcnt, nz);
+  cos_nz_kernel<<<egrid, 256, 0, st>>>(n, rp, ci, cign, nz);
+  if ((e = scan_excl(kcnt, n, cp, pool, st)) != cudaSuccess) return e;
+  cudaMemcpyAsync(cc, cp, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st);
+  cos_csc_kernel<<<egrid, 256, 0, st>>>(n, rp, ci, cign, cc, cr);
+  *launches += 8;
+  const CosArgs C{n, rp, ci, cp, cr, rign, cign, nz, tau};
+  // similar pairs: count, scan, write (+ global-table fallback)
+  int64_t *cnt = pool.get<int64_t>(n), *uoff = pool.get<int64_t>(n + 1);
+  int32_t *list = pool.get<int32_t>(n);
+  int *d_novf = pool.get<int>(1);
+  unsigned long long *d_max = pool.get<unsigned long long>(1);
+  if (pool.err != cudaSuccess) return pool.err;
+  cudaMemsetAsync(d_novf, 0, sizeof(int), st);
+  cudaMemsetAsync(d_max, 0, sizeof(unsigned long long), st);
+  CosOut O{cnt, uoff, nullptr, nullptr, list, d_novf, d_max};
+  static bool attr = false;
+  const int smem = BW * SET_CAP * (int)sizeof(int32_t);
+  if (!attr) {
+    cudaFuncSetAttribute(cos_pairs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(cos_pairs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int grid = sms * 3;
+  cos_pairs_kernel<false><<<grid, BT, smem, st>>>(C, O);
+  ++*launches;
+  int novf = 0;
+  unsigned long long mx = 0;
+  cudaMemcpyAsync(&novf, d_novf, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&mx, d_max, sizeof(mx), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  int32_t *region = nullptr;
+  uint32_t cap = 0;
+  int bgrid = 0;
+  if (novf > 0) {
+    cap = pow2_at_least(2 * (int64_t)mx);
+    int64_t warps = ((int64_t)1 << 27) / cap;
+    warps = warps < 1 ? 1 : warps;
+    warps = warps > (int64_t)sms * BW * 4 ? (int64_t)sms * BW * 4 : warps;
+    warps = warps > novf ? novf : warps;
+    bgrid = (int)((warps + BW - 1) / BW);
+    region = pool.get<int32_t>((int64_t)bgrid * BW * 2 * cap);
+    if (!region) return pool.err;
+    cos_pairs_big_kernel<false><<<bgrid, BT, 0, st>>>(C, O, novf, region, cap);
+    ++*launches;
+  }
+  if ((e = scan_excl(cnt, n, uoff, pool, st)) != cudaSuccess) return e;
+  *launches += 3;
+  int64_t npairs = 0;
+  cudaMemcpyAsync(&npairs, uoff + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  int32_t *tmp = pool.get<int32_t>(npairs), *up = pool.get<int32_t>(npairs), *low = pool.get<int32_t>(npairs);
+  int64_t *loff = pool.get<int64_t>(n + 1);
+  unsigned long long *lcnt = pool.get<unsigned long long>(n);
+  if (pool.err != cudaSuccess) return pool.err;
+  O.tmp = tmp; O.up = up;
+  cos_pairs_kernel<true><<<grid, BT, smem, st>>>(C, O);
+  ++*launches;
+  if (novf > 0) { cos_pairs_big_kernel<true><<<bgrid, BT, 0, st>>>(C, O, novf, region, cap); ++*launches; }
+  cudaMemsetAsync(lcnt, 0, sizeof(unsigned long long) * n, st);
+  cos_low_count_kernel<<<egrid, 256, 0, st>>>(n, uoff, up, lcnt);
+  if ((e = scan_excl((const int64_t *)lcnt, n, loff, pool, st)) != cudaSuccess) return e;
+  cudaMemcpyAsync(lcnt, loff, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st);
+  cos_low_fill_kernel<<<egrid, 256, 0, st>>>(n, uoff, up, lcnt, tmp);
+  cos_low_sort_kernel<<<egrid, 256, 0, st>>>(n, loff, tmp, low);
+  *launches += 6;
+  // greedy fixed point
+  int32_t *state = pool.get<int32_t>(n), *slot = pool.get<int32_t>(n);
+  int *progress = pool.get<int>(1);
+  if (pool.err != cudaSuccess) return pool.err;
+  cos_init_kernel<<<egrid, 256, 0, st>>>(n, state);
+  ++*launches;
+  const CosGreedy G{n, max_size, uoff, up, loff, low, state, slot, progress};
+  int64_t decided = 0;
+  const int rgrid = (int)(((int64_t)n + 255) / 256 < (int64_t)sms * 16 ? ((int64_t)n + 255) / 256 : (int64_t)sms * 16);
+  while (decided < n) {
+    cudaMemsetAsync(progress, 0, sizeof(int), st);
+    cos_round_kernel<<<rgrid, 256, 0, st>>>(G);
+    ++*launches;
+    ++*rounds;
+    int pr = 0;
+    cudaMemcpyAsync(&pr, progress, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    decided += pr;
+    if (decided < n && (*rounds >= 64 || pr < (n - decided) / 64)) {   // long chains: finish in order
+      int64_t *flag = pool.get<int64_t>(n), *pos = pool.get<int64_t>(n + 1);
+      int32_t *ulist = pool.get<int32_t>(n);
+      if (pool.err != cudaSuccess) return pool.err;
+      cos_undecided_kernel<<<egrid, 256, 0, st>>>(n, state, flag);
+      if ((e = scan_excl(flag, n, pos, pool, st)) != cudaSuccess) return e;
+      cos_list_kernel<<<egrid, 256, 0, st>>>(n, flag, pos, ulist);
+      cos_sweep_kernel<<<1, 1, 0, st>>>(G, ulist, pos + n);
+      *launches += 6;
+      break;
+    }
+  }
+  // groups
+  int64_t *lead = pool.get<int64_t>(n), *gid = pool.get<int64_t>(n + 1);
+  if (pool.err != cudaSuccess) return pool.err;
+  cos_leader_kernel<<<egrid, 256, 0, st>>>(n, state, lead);
+  if ((e = scan_excl(lead, n, gid, pool, st)) != cudaSuccess) return e;
+  int64_t nb = 0;
+  cudaMemcpyAsync(&nb, gid + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  if (nb < 1 || nb > n) return cudaErrorUnknown;
+  unsigned long long *gsize = pool.get<unsigned long long>(nb);
+  int64_t *gstart = pool.get<int64_t>(nb + 1);
+  int32_t *q = pool.get<int32_t>(n), *sizes = pool.get<int32_t>(nb);
+  if (pool.err != cudaSuccess) return pool.err;
+  cudaMemsetAsync(gsize, 0, sizeof(unsigned long long) * nb, st);
+  cos_size_kernel<<<egrid, 256, 0, st>>>(n, state, gid, gsize);
+  if ((e = scan_excl((const int64_t *)gsize, nb, gstart, pool, st)) != cudaSuccess) return e;
+  cos_place_kernel<<<egrid, 256, 0, st>>>(n, state, slot, gid, gstart, q);
+  cos_sizes_kernel<<<egrid, 256, 0, st>>>((int)nb, gsize, sizes);
+  *launches += 8;
+  cudaMemcpyAsync(h_q, q, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(h_sizes, sizes, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
   *nblocks = (int32_t)nb;

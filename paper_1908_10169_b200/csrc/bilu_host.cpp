@@ -68,6 +68,9 @@ extern "C" cudaError_t bilu_launch_apply(const ApplyArgs &A, int grid, int backw
 extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci, const double *val,
                                      const int32_t *pm, const int32_t *ipm, double tau, int max_size, int sms,
                                      cudaStream_t st, int32_t *h_sizes, int32_t *nblocks, int *launches);
+extern "C" cudaError_t bilu_cosine_run(int n, const int64_t *rp, const int32_t *ci, double tau, int max_size, int sms,
+                                       cudaStream_t st, int32_t *h_q, int32_t *h_sizes, int32_t *nblocks,
+                                       int *launches, int *rounds);
 }  // namespace bilu
 
 // Final (post-aggregation) factor: per final block F, descriptors into the
@@ -1657,6 +1660,50 @@ extern "C" bilu_status bilu_ilu1_blocks(int32_t n, const int64_t *row_ptr, const
   if (n_kernel_launches) *n_kernel_launches = launches;
   if (e != cudaSuccess) {
     set_err(nullptr, "bilu_ilu1_blocks: %s", cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? BILU_ERR_OOM : BILU_ERR_CUDA;
+  }
+  return BILU_OK;
+}
+
+// --------------------------------------------------------------- cosine-based blocking
+extern "C" bilu_status bilu_cosine_blocks(int32_t n, const int64_t *row_ptr, const int32_t *col_idx, double tau,
+                                          int32_t max_size, int32_t device, void *stream, int32_t *q,
+                                          int32_t *block_sizes, int32_t *n_blocks, int32_t *n_kernel_launches) {
+  if (n_blocks) *n_blocks = 0;
+  if (n < 1 || !row_ptr || !col_idx || !q || !block_sizes || !n_blocks) {
+    set_err(nullptr, "bilu_cosine_blocks: null pointer or n < 1");
+    return BILU_ERR_ARG;
+  }
+  if (!(tau >= 0.0 && tau <= 1.0) || max_size < 1 || max_size > 128) {
+    set_err(nullptr, "bilu_cosine_blocks: need tau in [0,1] and max_size in [1,128] (got %g, %d)", tau, max_size);
+    return BILU_ERR_ARG;
+  }
+  if (n >= (1 << 30)) { set_err(nullptr, "bilu_cosine_blocks: n must be < 2^30"); return BILU_ERR_ARG; }
+  std::vector<int32_t> pm, ipm;
+  bilu_status st = check_csr_perm("bilu_cosine_blocks", n, row_ptr, col_idx, nullptr, pm, ipm);
+  if (st != BILU_OK) return st;
+  const int64_t nnz = row_ptr[n];
+  if (cudaSetDevice(device) != cudaSuccess) {
+    set_err(nullptr, "bilu_cosine_blocks: cannot use CUDA device %d", device);
+    return BILU_ERR_NOT_BUILT;
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t *d_rp = nullptr;
+  int32_t *d_ci = nullptr;
+  cudaError_t e = cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(d_ci, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s);
+  int launches = 0, rounds = 0;
+  if (e == cudaSuccess) e = bilu_cosine_run(n, d_rp, d_ci, tau, max_size, sms, s, q, block_sizes, n_blocks, &launches, &rounds);
+  cudaStreamSynchronize(s);
+  cudaFree(d_rp); cudaFree(d_ci);
+  if (getenv("BILU_VERBOSE")) fprintf(stderr, "[bilu] cosine_blocks: %d launches, %d greedy rounds\n", launches, rounds);
+  if (n_kernel_launches) *n_kernel_launches = launches;
+  if (e != cudaSuccess) {
+    set_err(nullptr, "bilu_cosine_blocks: %s", cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? BILU_ERR_OOM : BILU_ERR_CUDA;
   }
   return BILU_OK;

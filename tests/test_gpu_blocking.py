@@ -141,3 +141,110 @@ def test_factor_from_estimated_blocks(name):
     assert st["n_blocks_init"] == len(bs)
     r = compare_factors(gf, of, 1e-10)
     assert not r["problems"], r["problems"][:5]
+
+
+# ------------------------------------------------------------ cosine-based blocking (Sec. 3.2)
+def cos_both(ip, ix, tau=0.8, max_size=128):
+    from paper_1908_10169_b200 import cosine_blocks
+    q, s, nl = cosine_blocks(ip, ix, tau, max_size)
+    oq, os_ = oracle.cosine_blocks(ip, ix, tau, max_size)
+    assert nl > 0
+    assert np.array_equal(np.sort(q), np.arange(len(ip) - 1))
+    assert len(s) == len(os_) and np.array_equal(s, os_), (len(s), len(os_))
+    assert np.array_equal(q, oq)
+    return q, s
+
+
+def _rows_csr(rows, n):
+    ip = np.zeros(n + 1, dtype=np.int64)
+    for i, r in enumerate(rows):
+        ip[i + 1] = ip[i] + len(r)
+    return ip, np.concatenate([np.asarray(sorted(set(r)), dtype=np.int32) for r in rows])
+
+
+def test_cosine_pins():
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cosine_hand_6x6.json")))
+    ip, ix = _rows_csr(g["rows"], 6)
+    for c in g["cases"]:
+        q, s = cos_both(ip, ix, c["tau"], c["max_size"])
+        assert list(q) == c["q"] and list(s) == c["sizes"]
+    n = 10
+    ip, ix = _rows_csr([list(range(n))] + [[0, i] for i in range(1, n)], n)
+    q, s = cos_both(ip, ix, 0.2)
+    assert list(s) == [1] * n
+    ip, ix = _rows_csr([list(range(n))] * n, n)
+    q, s = cos_both(ip, ix, 0.8, 4)
+    assert list(s) == [4, 4, 2]
+
+
+def _dup_pattern(n, seed, deg=6, dup=0.6, noise=0.3):
+    """rows copied (with noise) from a few earlier rows: groups of similar rows"""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(n):
+        if i > 0 and rng.random() < dup:
+            src = rows[max(0, i - int(rng.integers(1, 4)))]
+            r = [c for c in src if rng.random() > noise * 0.3]
+            if rng.random() < noise:
+                r.append(int(rng.integers(0, n)))
+        else:
+            r = list(rng.integers(0, n, size=int(rng.integers(1, deg + 1))))
+        rows.append(sorted(set(r + [i])))
+    return _rows_csr(rows, n)
+
+
+@pytest.mark.parametrize("n", [1, 2, 255, 257, 1000, 5000])
+@pytest.mark.parametrize("max_size", [1, 2, 4, 128])
+def test_cosine_ragged_random(n, max_size):
+    ip, ix = _dup_pattern(n, n + max_size)
+    for tau in (0.3, 0.5, 0.8):
+        cos_both(ip, ix, tau, max_size)
+
+
+def test_cosine_band_long_chain():
+    """Band of half-width 6: consecutive rows share 12 of 13 columns, so the greedy's dependency
+    chain runs through the whole matrix (exercises the in-order sweep after the rounds stall)."""
+    n, w = 3000, 6
+    rows = [list(range(max(0, i - w), min(n, i + w + 1))) for i in range(n)]
+    ip, ix = _rows_csr(rows, n)
+    for ms in (3, 128):
+        cos_both(ip, ix, 0.8, ms)
+
+
+def test_cosine_overflow_block_rows():
+    P = config4(nblocks=150)
+    q, s = cos_both(P.indptr, P.indices, 0.8, 128)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_cosine_full_configs(name):
+    P = {"c2": config2, "c3": config3, "c5": config5}[name]()
+    q, s = cos_both(P.indptr, P.indices, 0.8, 128)
+    if name == "c3":
+        assert len(s) == P.n // 3 and set(s) == {3}      # the nodal 3x3 blocks (PAPER.md Ex. 3.2's role)
+
+
+def test_cosine_bad_arguments():
+    from paper_1908_10169_b200 import BiluError, cosine_blocks
+    ip, ix = np.arange(4), np.arange(3)
+    with pytest.raises(BiluError):
+        cosine_blocks(ip, ix, 1.5, 8)
+    with pytest.raises(BiluError):
+        cosine_blocks(ip, ix, 0.8, 0)
+    with pytest.raises(BiluError):
+        cosine_blocks(np.array([0, 2, 2, 3]), np.array([1, 0, 2]), 0.8, 8)
+
+
+def test_factor_from_cosine_blocks():
+    """Q and the groups feed bilu_analyze (perm = Q): parity with the oracle on the same input."""
+    from paper_1908_10169_b200 import BILU, cosine_blocks
+    P = config3(N=10)
+    q, s, _ = cosine_blocks(P.indptr, P.indices, 0.8, 128)
+    g = BILU(P.indptr, P.indices, P.data, s, perm=q)
+    st = g.factor(P.tau)
+    gf = g.export()
+    pip, pix, pdv = oracle.permute_csr(P.indptr, P.indices, P.data, q)
+    of = oracle.factor(pip, pix, pdv, s, P.tau, aggregate=True, overrides=overrides_from_near(gf.near))
+    r = compare_factors(gf, of, 1e-10)
+    assert not r["problems"], r["problems"][:5]
