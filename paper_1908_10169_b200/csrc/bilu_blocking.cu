@@ -101,30 +101,46 @@ __device__ int64_t set_bound(const EstArgs &E, int k, int lane) {
 }
 
 // I~_k (LOWER: column k, through the CSC) or J~_k (row k, through the CSR) into T (cleared);
-// returns the set size.  PAPER.md:1183-1198; the products are the oracle's (R20).
+// returns the set size.  PAPER.md:1183-1198; the products are the oracle's (R20).  With a
+// limit (optimistic shared-memory attempt) the build stops once the distinct keys, counted in
+// *nkeys, reach it (<= half the table, overshoot < 32): returns -1 then.
 template <bool LOWER>
-__device__ int build_set(const EstArgs &E, int k, Table T, int lane) {
+__device__ int build_set(const EstArgs &E, int k, Table T, int lane, int *nkeys = nullptr, int limit = 0) {
   const int64_t *P = LOWER ? E.cp : E.rp;
   const int32_t *X = LOWER ? E.cr : E.ci;
   const double *V = LOWER ? E.cv : E.val;
+  volatile int *vk = nkeys;
   const double akk = E.diag[k];
   const double thr = E.tau * fabs(akk);
   int64_t cnt = 0;
   for (int64_t p = P[k] + lane; p < P[k + 1]; p += 32) {
     const int32_t x = X[p];
-    if (x > k && fabs(V[p]) >= thr) cnt += t_insert(T, x);
-  }
-  for (int64_t p = P[k]; p < P[k + 1]; ++p) {          // j < k with a_jk != 0 (resp. i < k, a_ki != 0)
-    const int32_t j = X[p];
-    if (j >= k) continue;
-    const double ajk = V[p];
-    const double thr2 = E.tau * fabs(E.diag[j] * akk);
-    for (int64_t q = P[j] + lane; q < P[j + 1]; q += 32) {
-      const int32_t x = X[q];
-      if (x > k && fabs(V[q] * ajk) >= thr2) cnt += t_insert(T, x);
+    if (x > k && fabs(V[p]) >= thr) {
+      const int nw = t_insert(T, x);
+      cnt += nw;
+      if (limit && nw) atomicAdd(nkeys, 1);
     }
   }
   __syncwarp();
+  for (int64_t p = P[k]; p < P[k + 1]; ++p) {          // j < k with a_jk != 0 (resp. i < k, a_ki != 0)
+    const int32_t j = X[p];
+    if (j >= k) continue;
+    if (limit && *vk >= limit) return -1;
+    const double ajk = V[p];
+    const double thr2 = E.tau * fabs(E.diag[j] * akk);
+    for (int64_t q = P[j] + lane; q < P[j + 1]; q += 32) {
+      if (limit && *vk >= limit) break;
+      const int32_t x = X[q];
+      if (x > k && fabs(V[q] * ajk) >= thr2) {
+        const int nw = t_insert(T, x);
+        cnt += nw;
+        if (limit && nw) atomicAdd(nkeys, 1);
+      }
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  if (limit && *vk >= limit) return -1;
   return (int)warp_sum64(cnt);
 }
 
@@ -137,22 +153,29 @@ struct SetOut {
   unsigned long long *ovf_max;
 };
 
+// steps whose candidate bound exceeds half the table are tried optimistically (candidates
+// repeat); a step whose distinct keys do not fit goes to the global tables
 template <bool LOWER, bool WRITE>
 __global__ void __launch_bounds__(BT) sets_kernel(EstArgs E, SetOut O) {
   extern __shared__ int32_t s_tab[];
+  __shared__ int s_nkeys[BW];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const Table T{s_tab + w * SET_CAP, SET_CAP - 1};
   for (int k = blockIdx.x * BW + w; k < E.n; k += gridDim.x * BW) {
     const int64_t b = set_bound<LOWER>(E, k, lane);
-    if (2 * b > SET_CAP) {
+    const int limit = 2 * b > SET_CAP ? SET_CAP / 2 : 0;
+    t_clear(T, lane);
+    if (lane == 0) s_nkeys[w] = 0;
+    __syncwarp();
+    const int c = build_set<LOWER>(E, k, T, lane, s_nkeys + w, limit);
+    if (c < 0) {
       if (!WRITE && lane == 0) {
         O.ovf_list[atomicAdd(O.ovf_n, 1)] = k;
         atomicMax(O.ovf_max, (unsigned long long)b);
       }
+      __syncwarp();
       continue;
     }
-    t_clear(T, lane);
-    const int c = build_set<LOWER>(E, k, T, lane);
     if (WRITE) t_emit(T, O.out + O.off[k], lane);
     else if (lane == 0) O.cnt[k] = c;
     __syncwarp();
@@ -464,24 +487,32 @@ __device__ __forceinline__ int64_t cos_bound(const CosArgs &C, int i, int lane) 
   return warp_sum64(b);
 }
 
-// row i of A A^T (j > i, kept rows) in T (keys) / V (counts), both cleared; returns nothing
-__device__ void cos_row(const CosArgs &C, int i, Table T, int32_t *V, int lane) {
+// row i of A A^T (j > i, kept rows) in T (keys) / V (counts), both cleared.  With a limit
+// (optimistic shared-memory attempt) the distinct keys are counted in *nkeys and the build
+// stops once they reach the limit (<= half the table, overshoot < 32): returns 0 then.
+__device__ int cos_row(const CosArgs &C, int i, Table T, int32_t *V, int lane, int *nkeys, int limit) {
+  volatile int *vk = nkeys;
   for (int64_t p = C.rp[i]; p < C.rp[i + 1]; ++p) {
     const int32_t c = C.ci[p];
     if (C.cign[c]) continue;
     for (int64_t x = C.cp[c] + lane; x < C.cp[c + 1]; x += 32) {
+      if (limit && *vk >= limit) break;
       const int32_t j = C.cr[x];
       if (j <= i || C.rign[j]) continue;
       uint32_t s = slot0(j, T.mask);
       while (true) {
         const int32_t old = atomicCAS(T.t + s, -1, j);
-        if (old == -1 || old == j) break;
+        if (old == -1) { if (limit) atomicAdd(nkeys, 1); break; }
+        if (old == j) break;
         s = (s + 1) & T.mask;
       }
       atomicAdd(V + s, 1);
     }
+    __syncwarp();
+    if (limit && *vk >= limit) return 0;
   }
   __syncwarp();
+  return 1;
 }
 
 // passing j of the table, written to out (arbitrary order); returns their number
@@ -517,12 +548,14 @@ struct CosOut {
   int32_t *ovf_list; int *ovf_n; unsigned long long *ovf_max;
 };
 
+// returns 0 if the optimistic attempt (limit > 0) overflowed
 template <bool WRITE>
-__device__ void cos_one(const CosArgs &C, const CosOut &O, int i, Table T, int32_t *V, int lane) {
+__device__ int cos_one(const CosArgs &C, const CosOut &O, int i, Table T, int32_t *V, int lane, int *nkeys, int limit) {
   t_clear(T, lane);
   for (uint32_t x = lane; x <= T.mask; x += 32) V[x] = 0;
+  if (lane == 0 && nkeys) *nkeys = 0;
   __syncwarp();
-  cos_row(C, i, T, V, lane);
+  if (!cos_row(C, i, T, V, lane, nkeys, limit)) return 0;
   if (!WRITE) {
     const int m = cos_emit(C, i, T, V, nullptr, lane);
     if (lane == 0) O.cnt[i] = m;
@@ -532,11 +565,15 @@ __device__ void cos_one(const CosArgs &C, const CosOut &O, int i, Table T, int32
     rank_sort_copy(O.tmp + O.off[i], O.up + O.off[i], m, lane);
   }
   __syncwarp();
+  return 1;
 }
 
+// rows whose candidate bound exceeds half the shared table are tried optimistically (most of
+// their candidates repeat); a row whose distinct keys do not fit goes to the global tables
 template <bool WRITE>
 __global__ void __launch_bounds__(BT) cos_pairs_kernel(CosArgs C, CosOut O) {
   extern __shared__ int32_t s_tab[];
+  __shared__ int s_nkeys[BW];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   constexpr int CAP = SET_CAP / 2;
   const Table T{s_tab + w * 2 * CAP, CAP - 1};
@@ -544,11 +581,11 @@ __global__ void __launch_bounds__(BT) cos_pairs_kernel(CosArgs C, CosOut O) {
   for (int i = blockIdx.x * BW + w; i < C.n; i += gridDim.x * BW) {
     if (C.rign[i] || C.nz[i] == 0) { if (!WRITE && lane == 0) O.cnt[i] = 0; continue; }
     const int64_t b = cos_bound(C, i, lane);
-    if (2 * b > CAP) {
+    const int limit = 2 * b > CAP ? CAP / 2 : 0;
+    if (!cos_one<WRITE>(C, O, i, T, V, lane, s_nkeys + w, limit)) {
       if (!WRITE && lane == 0) { O.ovf_list[atomicAdd(O.ovf_n, 1)] = i; atomicMax(O.ovf_max, (unsigned long long)b); }
-      continue;
+      __syncwarp();
     }
-    cos_one<WRITE>(C, O, i, T, V, lane);
   }
 }
 template <bool WRITE>
@@ -557,7 +594,7 @@ __global__ void __launch_bounds__(BT) cos_pairs_big_kernel(CosArgs C, CosOut O, 
   const int gw = (blockIdx.x * BT + threadIdx.x) >> 5, nw = gridDim.x * BW;
   const Table T{region + (int64_t)gw * 2 * cap, cap - 1};
   int32_t *V = region + (int64_t)gw * 2 * cap + cap;
-  for (int x = gw; x < nlist; x += nw) cos_one<WRITE>(C, O, O.ovf_list[x], T, V, lane);
+  for (int x = gw; x < nlist; x += nw) cos_one<WRITE>(C, O, O.ovf_list[x], T, V, lane, nullptr, 0);
 }
 
 // lower lists: low(j) = { i < j : j in up(i) }
@@ -658,20 +695,36 @@ __global__ void cos_sizes_kernel(int nb, const unsigned long long *gsize, int32_
 
 // ---------------------------------------------------------------- host orchestration
 namespace {
+// scratch from the stream-ordered allocator: repeated calls reuse the device's pool instead of
+// paying cudaMalloc / cudaFree (which synchronise) for GB-sized arrays
 struct Pool {
   std::vector<void *> ptrs;
+  cudaStream_t st;
   cudaError_t err = cudaSuccess;
+  explicit Pool(cudaStream_t s) : st(s) {
+    static bool once = false;
+    if (!once) {
+      int dev = 0;
+      cudaMemPool_t mp;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+        uint64_t keep = (uint64_t)8 << 30;          // retain up to 8 GiB between calls
+        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      once = true;
+    }
+  }
   template <class T>
   T *get(int64_t count) {
     void *p = nullptr;
     if (err != cudaSuccess) return nullptr;
-    err = cudaMalloc(&p, (size_t)(count > 0 ? count : 1) * sizeof(T));
+    err = cudaMallocAsync(&p, (size_t)(count > 0 ? count : 1) * sizeof(T), st);
     if (err != cudaSuccess) return nullptr;
     ptrs.push_back(p);
     return (T *)p;
   }
   ~Pool() {
-    for (void *p : ptrs) cudaFree(p);
+    for (void *p : ptrs) cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
   }
 };
 
@@ -754,7 +807,7 @@ cudaError_t build_sets(const EstArgs &E, int grid, int sms, int64_t **off_o, int
 extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci, const double *val,
                                      const int32_t *pm, const int32_t *ipm, double tau, int max_size, int sms,
                                      cudaStream_t st, int32_t *h_sizes, int32_t *nblocks, int *launches) {
-  Pool pool;
+  Pool pool(st);
   *launches = 0;
   int64_t nnz = 0;
   cudaError_t e = cudaMemcpyAsync(&nnz, rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
@@ -855,7 +908,7 @@ extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci
 extern "C" cudaError_t bilu_cosine_run(int n, const int64_t *rp, const int32_t *ci, double tau, int max_size, int sms,
                                        cudaStream_t st, int32_t *h_q, int32_t *h_sizes, int32_t *nblocks,
                                        int *launches, int *rounds) {
-  Pool pool;
+  Pool pool(st);
   *launches = 0;
   *rounds = 0;
   int64_t nnz = 0;

@@ -10,7 +10,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402  (test infrastructure: timed beside the device path)
 from inputs.configs import make_config  # noqa: E402
-from paper_1908_10169_b200 import BILU, ilu1_blocks  # noqa: E402
+from paper_1908_10169_b200 import BILU, cosine_blocks, ilu1_blocks  # noqa: E402
 
 for name in sys.argv[1:] or ["c2"]:
     P = make_config(name)
@@ -28,6 +28,19 @@ for name in sys.argv[1:] or ["c2"]:
     print("%s n=%d nnz=%d estimate: device API %.1f ms (min of 3 after warm-up, %d launches), oracle %.0f ms; "
           "%d blocks, sizes %s" % (name, P.n, len(ix), 1e3 * min(ts[1:]), nl, 1e3 * to, len(bs),
                                    np.bincount(bs).tolist()), flush=True)
+    ts = []
+    for _ in range(4):
+        t = time.perf_counter()
+        cq, cs, cl = cosine_blocks(P.indptr, P.indices, 0.8, 128)
+        ts.append(time.perf_counter() - t)
+    t = time.perf_counter()
+    oq, os_ = oracle.cosine_blocks(P.indptr, P.indices, 0.8, 128)
+    to = time.perf_counter() - t
+    assert np.array_equal(cq, oq) and np.array_equal(cs, os_)
+    print("%s cosine blocking: device API %.1f ms (%d launches), oracle %.0f ms; %d groups, sizes %s" % (
+        name, 1e3 * min(ts[1:]), cl, 1e3 * to, len(cs), np.bincount(cs).tolist()[:10]), flush=True)
+    if os.environ.get("EST_NO_FACTOR"):
+        continue
     for label, blocks in (("stand-in", P.block_sizes), ("ilu1", bs)):
         g = BILU(P.indptr, P.indices, P.data, blocks, perm=P.perm)
         for _ in range(2):
