@@ -235,6 +235,28 @@ bilu_status bilu_interface_pack(bilu_ctx *h, void *dst, int64_t capacity, int64_
 bilu_status bilu_interface_unpack(bilu_ctx *h, const void *buf, int64_t bytes);
 bilu_status bilu_factor_separators(bilu_ctx *h, bilu_factor_stats *st);
 
+/*
+ * Distributed preconditioner application y = (L D^{-1} U)^{-1} x over the ranks' factors
+ * (after bilu_factor_separators).  The forward sweep L w = x splits at
+ * the ND separators: a subtree block's L rows lie in its own subtree and in separator rows,
+ * a separator block's only in later separators (PAPER.md:164-171 dependency, ND order), so
+ *   bilu_apply_dist_begin   forward sweep over this rank's subtree blocks; writes this rank's
+ *                           contributions to the separator rows (contrib)
+ *   (caller)                contrib_sum = sum of every rank's contrib (one all-reduce)
+ *   bilu_apply_dist_end     forward sweep over the separator blocks (replicated), D multiply
+ *                           and backward sweep over separator + own subtree blocks; y receives
+ *                           this rank's subtree rows, the separator rows if write_separators,
+ *                           and 0 elsewhere, so the ranks' y sum to the full result.
+ *   x, y        DEVICE, double[n], A's original ordering; x the same on every rank
+ *   contrib, contrib_sum   DEVICE, double[m], m from bilu_dist_separator_rows
+ * Errors: BILU_ERR_STATE (not a distributed context, not factored, end before begin),
+ * BILU_ERR_ARG, BILU_ERR_CUDA.  Asynchronous on stream (NULL = the context's stream).
+ */
+bilu_status bilu_dist_separator_rows(bilu_ctx *h, int64_t *m);
+bilu_status bilu_apply_dist_begin(bilu_ctx *h, const double *x, double *contrib, void *stream);
+bilu_status bilu_apply_dist_end(bilu_ctx *h, const double *contrib_sum, double *y, int32_t write_separators,
+                                void *stream);
+
 /* Destroys the context and frees all device memory.  NULL-safe. */
 void bilu_destroy(bilu_ctx *h);
 

@@ -23,7 +23,7 @@ ABI_SYMBOLS = ["bilu_options_default", "bilu_analyze", "bilu_set_values", "bilu_
                "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm", "bilu_diag_tsgemm",
                "bilu_dist_setup", "bilu_factor_local", "bilu_interface_pack", "bilu_interface_unpack",
                "bilu_factor_separators", "bilu_gmres", "bilu_ilu1_blocks",
-               "bilu_cosine_blocks"]
+               "bilu_cosine_blocks", "bilu_dist_separator_rows", "bilu_apply_dist_begin", "bilu_apply_dist_end"]
 
 
 class BiluError(RuntimeError):
@@ -137,6 +137,12 @@ def load_library():
     lib.bilu_ilu1_blocks.restype = ctypes.c_int
     lib.bilu_cosine_blocks.argtypes = [ctypes.c_int32, P, P, D, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P]
     lib.bilu_cosine_blocks.restype = ctypes.c_int
+    lib.bilu_dist_separator_rows.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
+    lib.bilu_dist_separator_rows.restype = ctypes.c_int
+    lib.bilu_apply_dist_begin.argtypes = [P, P, P, P]
+    lib.bilu_apply_dist_begin.restype = ctypes.c_int
+    lib.bilu_apply_dist_end.argtypes = [P, P, P, ctypes.c_int32, P]
+    lib.bilu_apply_dist_end.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -263,6 +269,28 @@ class BILU:
         self._check(rc, st.breakdown_block)
         self.stats = st.as_dict()
         return self.stats
+
+    def apply_dist_begin(self, x):
+        """bilu_apply_dist_begin: forward sweep over this rank's subtrees; returns this rank's
+        separator-row contributions (CUDA float64 tensor) to be summed over the ranks."""
+        import torch
+        m = ctypes.c_int64(0)
+        self._check(self.lib.bilu_dist_separator_rows(self.h, ctypes.byref(m)))
+        x = x.contiguous()
+        contrib = torch.empty(max(m.value, 1), dtype=torch.float64, device=x.device)[: m.value]
+        self._check(self.lib.bilu_apply_dist_begin(self.h, ctypes.c_void_p(x.data_ptr()),
+                                                   ctypes.c_void_p(contrib.data_ptr()), None))
+        return contrib
+
+    def apply_dist_end(self, contrib_sum, write_separators: bool):
+        """bilu_apply_dist_end: separator sweeps and the backward sweep; returns this rank's
+        share of y (own subtree rows, separator rows if write_separators, 0 elsewhere)."""
+        import torch
+        contrib_sum = contrib_sum.contiguous()
+        y = torch.empty(self.n, dtype=torch.float64, device=contrib_sum.device)
+        self._check(self.lib.bilu_apply_dist_end(self.h, ctypes.c_void_p(contrib_sum.data_ptr()),
+                                                 ctypes.c_void_p(y.data_ptr()), int(bool(write_separators)), None))
+        return y
 
     def gmres(self, b, restart=30, tol=1e-8, max_restarts=100):
         """Solve A x = b on the device (bilu_gmres); b a CUDA float64 tensor in A's ordering.

@@ -29,7 +29,7 @@ __device__ __forceinline__ int a_pop_warp(const ApplyArgs &A) {
   int F = -1;
   if ((threadIdx.x & 31) == 0) {
     const unsigned long long idx = atomicAdd(&A.ctrl[1], 1ull);
-    if (idx < (unsigned long long)A.nF) {
+    if (idx < (unsigned long long)A.ntarget) {
       while ((F = a_ld_vol(&A.queue[idx])) < 0) __nanosleep(20);
     }
   }
@@ -137,6 +137,48 @@ __global__ void __launch_bounds__(AT) apply_bwd_kernel(ApplyArgs A) {
     __syncwarp();
     a_release_warp(A, A.bs_ptr, A.bs, F);
   }
+}
+
+// ---- distributed apply (bilu_apply_dist_begin / _end): separator rows of the permuted vectors
+__global__ void sep_gather_kernel(int m, const int32_t *idx, const double *src, double *out) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < m; x += gridDim.x * blockDim.x) out[x] = src[idx[x]];
+}
+// out = w[sep] - x[sep]: this rank's (negated) contributions L_J w_J to the separator rows
+__global__ void sep_contrib_kernel(int m, const int32_t *idx, const double *w, const double *xsep, double *out) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < m; x += gridDim.x * blockDim.x) out[x] = w[idx[x]] - xsep[x];
+}
+// w[sep] = x[sep] + (sum over ranks of the contributions)
+__global__ void sep_set_kernel(int m, const int32_t *idx, const double *xsep, const double *sum, double *w) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < m; x += gridDim.x * blockDim.x) w[idx[x]] = xsep[x] + sum[x];
+}
+// y[perm[i]] = y_perm[i] on the rows this rank reports (mask 1: own subtree, 2: separator if
+// write_sep), 0 elsewhere: the ranks' outputs sum to the full vector
+__global__ void permute_out_masked_kernel(int n, const int32_t *perm, const uint8_t *mask, int write_sep,
+                                          const double *yp, double *y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int m = mask[i];
+    y[perm[i]] = (m == 1 || (m == 2 && write_sep)) ? yp[i] : 0.0;
+  }
+}
+
+extern "C" cudaError_t bilu_launch_sep_gather(int m, const int32_t *idx, const double *src, double *out, cudaStream_t st) {
+  if (m > 0) sep_gather_kernel<<<(m + 255) / 256, 256, 0, st>>>(m, idx, src, out);
+  return cudaGetLastError();
+}
+extern "C" cudaError_t bilu_launch_sep_contrib(int m, const int32_t *idx, const double *w, const double *xsep,
+                                               double *out, cudaStream_t st) {
+  if (m > 0) sep_contrib_kernel<<<(m + 255) / 256, 256, 0, st>>>(m, idx, w, xsep, out);
+  return cudaGetLastError();
+}
+extern "C" cudaError_t bilu_launch_sep_set(int m, const int32_t *idx, const double *xsep, const double *sum, double *w,
+                                           cudaStream_t st) {
+  if (m > 0) sep_set_kernel<<<(m + 255) / 256, 256, 0, st>>>(m, idx, xsep, sum, w);
+  return cudaGetLastError();
+}
+extern "C" cudaError_t bilu_launch_permute_out_masked(int n, const int32_t *perm, const uint8_t *mask, int write_sep,
+                                                      const double *yp, double *y, cudaStream_t st) {
+  permute_out_masked_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, perm, mask, write_sep, yp, y);
+  return cudaGetLastError();
 }
 
 extern "C" cudaError_t bilu_launch_apply(const ApplyArgs &A, int grid, int backward, cudaStream_t st) {

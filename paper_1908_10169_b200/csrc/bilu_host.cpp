@@ -65,6 +65,13 @@ extern "C" int bilu_merge_nchunks(int N);
 extern "C" cudaError_t bilu_merge_arith(const MergeArgs &M, double *dwork, int64_t dwork_per_cta, int grid,
                                         cudaStream_t st);
 extern "C" cudaError_t bilu_launch_apply(const ApplyArgs &A, int grid, int backward, cudaStream_t st);
+extern "C" cudaError_t bilu_launch_sep_gather(int m, const int32_t *idx, const double *src, double *out, cudaStream_t st);
+extern "C" cudaError_t bilu_launch_sep_contrib(int m, const int32_t *idx, const double *w, const double *xsep,
+                                               double *out, cudaStream_t st);
+extern "C" cudaError_t bilu_launch_sep_set(int m, const int32_t *idx, const double *xsep, const double *sum, double *w,
+                                           cudaStream_t st);
+extern "C" cudaError_t bilu_launch_permute_out_masked(int n, const int32_t *perm, const uint8_t *mask, int write_sep,
+                                                      const double *yp, double *y, cudaStream_t st);
 extern "C" cudaError_t bilu_ilu1_run(int n, const int64_t *rp, const int32_t *ci, const double *val,
                                      const int32_t *pm, const int32_t *ipm, double tau, int max_size, int sms,
                                      cudaStream_t st, int32_t *h_sizes, int32_t *nblocks, int *launches);
@@ -168,6 +175,14 @@ struct bilu_ctx {
   int32_t *d_q_f0 = nullptr, *d_q_b0 = nullptr;
   int32_t nq_f0 = 0, nq_b0 = 0;
   unsigned long long nq_f0_ull = 0, nq_b0_ull = 0;
+  int32_t nt_f0 = 0, nt_b0 = 0;                      // blocks per sweep (nF unless distributed)
+  // distributed apply: forward over the separator blocks (phase 2), separator rows, row mask
+  int32_t *d_cnt_f2 = nullptr, *d_q_f2 = nullptr; int32_t nq_f2 = 0, nt_f2 = 0;
+  unsigned long long nq_f2_ull = 0;
+  int32_t *d_seprows = nullptr; int32_t nsep_rows = 0;
+  double *d_xsep = nullptr;
+  uint8_t *d_rowmask = nullptr;
+  bool dist_apply_begun = false;
   double *d_w = nullptr, *d_y = nullptr;
 };
 
@@ -1498,9 +1513,20 @@ static bilu_status build_apply(bilu_ctx *h) {
   CUDA_TRY(h, cudaStreamSynchronize(st));
   std::vector<int32_t> fbo(n);
   for (int F = 0; F < nF; ++F) for (int i = fb[F]; i < fb[F + 1]; ++i) fbo[i] = F;
+  // distributed: role of every final block (1 own subtree, 2 separator, 0 another rank's);
+  // only own and separator blocks take part in this rank's sweeps
+  std::vector<uint8_t> role(nF, 1);
+  if (h->dist) {
+    for (int F = 0; F < nF; ++F) {
+      const int K = (int)(std::upper_bound(h->bstart.begin(), h->bstart.end(), fb[F]) - h->bstart.begin()) - 1;
+      const int o = h->owner[K];
+      role[F] = o == h->rank ? 1 : (o < 0 ? 2 : 0);
+    }
+  }
   // forward: target T pulls (J, r0, r1) for every J with L rows in T
   std::vector<int32_t> fl_cnt(nF + 1, 0), fs_ptr(nF + 1, 0), bs_cnt(nF + 1, 0), cnt_b(nF, 0);
   for (int J = 0; J < nF; ++J) {
+    if (!role[J]) continue;
     const int32_t *r = Li.data() + Lro[J];
     for (int p = 0; p < Lm[J]; ++p) if (p == 0 || fbo[r[p]] != fbo[r[p - 1]]) { fl_cnt[fbo[r[p]] + 1]++; fs_ptr[J + 1]++; }
     const int32_t *c = Ui.data() + Uco[J];
@@ -1516,6 +1542,7 @@ static bilu_status build_apply(bilu_ctx *h) {
   std::vector<int32_t> fl_rec(3 * (size_t)fl_ptr[nF] + 3), fs(fs_ptr[nF] + 1), bs(bs_ptr[nF] + 1);
   std::vector<int32_t> flf(fl_ptr.begin(), fl_ptr.end() - 1), bsf(bs_ptr.begin(), bs_ptr.end() - 1);
   for (int J = 0; J < nF; ++J) {
+    if (!role[J]) continue;
     const int32_t *r = Li.data() + Lro[J];
     int xs = fs_ptr[J];
     for (int p = 0; p < Lm[J];) {
@@ -1534,9 +1561,48 @@ static bilu_status build_apply(bilu_ctx *h) {
       q = q1;
     }
   }
-  std::vector<int32_t> qf, qb;
+  std::vector<int32_t> qf, qb, qf2, cnt_f2;
+  int nt_f = nF, nt_b = nF, nt_f2 = 0;
+  if (h->dist) {
+    // forward phase 1: own blocks (their contributors are own blocks); phase 2: separators,
+    // counting separator contributors only; backward: own + separators.  Blocks outside a
+    // phase never reach zero.
+    const int32_t BIG = 1 << 30;
+    cnt_f2.assign(nF, BIG);
+    for (int F = 0; F < nF; ++F) {
+      if (role[F] != 2) continue;
+      int c = 0;
+      for (int x = fl_ptr[F]; x < fl_ptr[F + 1]; ++x) c += role[fl_rec[3 * x]] == 2;
+      cnt_f2[F] = c;
+      if (c == 0) qf2.push_back(F);
+    }
+    nt_f = nt_f2 = nt_b = 0;
+    for (int F = 0; F < nF; ++F) {
+      nt_f += role[F] == 1; nt_f2 += role[F] == 2; nt_b += role[F] != 0;
+      if (role[F] != 1) cnt_f[F] += BIG;
+      if (role[F] == 0) cnt_b[F] += BIG;
+    }
+    std::vector<int32_t> seprows;
+    std::vector<uint8_t> rmask(n, 0);
+    for (int F = 0; F < nF; ++F)
+      for (int i = fb[F]; i < fb[F + 1]; ++i) {
+        rmask[i] = role[F];
+        if (role[F] == 2) seprows.push_back(i);
+      }
+    dfree(h, h->d_seprows); dfree(h, h->d_xsep); dfree(h, h->d_rowmask);
+    h->nsep_rows = (int32_t)seprows.size();
+    CUDA_TRY(h, dalloc(h, &h->d_seprows, std::max<size_t>(seprows.size(), 1)));
+    CUDA_TRY(h, dalloc(h, &h->d_xsep, std::max<size_t>(seprows.size(), 1)));
+    CUDA_TRY(h, dalloc(h, &h->d_rowmask, (size_t)n));
+    if (!seprows.empty()) CUDA_TRY(h, cudaMemcpy(h->d_seprows, seprows.data(), seprows.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(h, cudaMemcpy(h->d_rowmask, rmask.data(), (size_t)n, cudaMemcpyHostToDevice));
+  }
   for (int F = 0; F < nF; ++F) if (cnt_f[F] == 0) qf.push_back(F);
   for (int F = nF - 1; F >= 0; --F) if (cnt_b[F] == 0) qb.push_back(F);
+  h->nt_f0 = nt_f; h->nt_b0 = nt_b; h->nt_f2 = nt_f2;
+  dfree(h, h->d_cnt_f2); dfree(h, h->d_q_f2);
+  h->nq_f2 = (int32_t)qf2.size();
+  h->nq_f2_ull = (unsigned long long)h->nq_f2;
   dfree(h, h->d_fl_ptr); dfree(h, h->d_fl_rec); dfree(h, h->d_fs_ptr); dfree(h, h->d_fs);
   dfree(h, h->d_bs_ptr); dfree(h, h->d_bs); dfree(h, h->d_cnt_f0); dfree(h, h->d_cnt_b0);
   dfree(h, h->d_q_f0); dfree(h, h->d_q_b0);
@@ -1549,7 +1615,7 @@ static bilu_status build_apply(bilu_ctx *h) {
   if ((bs_ = up(h->d_fl_ptr, fl_ptr)) || (bs_ = up(h->d_fl_rec, fl_rec)) || (bs_ = up(h->d_fs_ptr, fs_ptr)) ||
       (bs_ = up(h->d_fs, fs)) || (bs_ = up(h->d_bs_ptr, bs_ptr)) || (bs_ = up(h->d_bs, bs)) ||
       (bs_ = up(h->d_cnt_f0, cnt_f)) || (bs_ = up(h->d_cnt_b0, cnt_b)) || (bs_ = up(h->d_q_f0, qf)) ||
-      (bs_ = up(h->d_q_b0, qb)))
+      (bs_ = up(h->d_q_b0, qb)) || (bs_ = up(h->d_cnt_f2, cnt_f2)) || (bs_ = up(h->d_q_f2, qf2)))
     return bs_;
   h->nq_f0 = (int32_t)qf.size(); h->nq_b0 = (int32_t)qb.size();
   h->nq_f0_ull = (unsigned long long)h->nq_f0; h->nq_b0_ull = (unsigned long long)h->nq_b0;
@@ -1573,34 +1639,92 @@ static bilu_status build_apply(bilu_ctx *h) {
   return BILU_OK;
 }
 
+// one dataflow sweep over ntarget blocks, starting from the counters cnt0 and ready queue q0
+static bilu_status run_sweep(bilu_ctx *h, const int32_t *cnt0, const int32_t *q0, int nq,
+                             const unsigned long long *nq_ull, int ntarget, int backward, cudaStream_t st) {
+  ApplyArgs &A = h->AA;
+  const int nF = h->fin.nF;
+  if (ntarget <= 0) return BILU_OK;
+  A.ntarget = ntarget;
+  const int grid = std::max(1, std::min((ntarget + 15) / 16, h->sms * 2));   // 16 warp-workers per CTA
+  CUDA_TRY(h, cudaMemcpyAsync(A.cnt, cnt0, nF * 4, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(h, cudaMemsetAsync(A.queue, 0xFF, nF * 4, st));
+  if (nq) CUDA_TRY(h, cudaMemcpyAsync(A.queue, q0, nq * 4, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(h, cudaMemsetAsync(A.ctrl, 0, 4 * sizeof(unsigned long long), st));
+  CUDA_TRY(h, cudaMemcpyAsync(A.ctrl, nq_ull, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h, bilu_launch_apply(A, grid, backward, st));
+  h->launches += 1;
+  return BILU_OK;
+}
+
 extern "C" bilu_status bilu_apply(bilu_ctx *h, const double *x, double *y, void *stream) {
-  if (h && h->dist) { set_err(h, "bilu_apply: distributed factors are spread over the ranks (not supported)"); return BILU_ERR_STATE; }
+  if (h && h->dist) {
+    set_err(h, "bilu_apply: distributed factors are spread over the ranks (use bilu_apply_dist_begin/_end)");
+    return BILU_ERR_STATE;
+  }
   if (!h || !x || !y) { set_err(h, "bilu_apply: null argument"); return BILU_ERR_ARG; }
   if (x == y) { set_err(h, "bilu_apply: x and y may not alias"); return BILU_ERR_ARG; }
   if (!h->factored) { set_err(h, "bilu_apply: no factorization"); return BILU_ERR_STATE; }
   cudaSetDevice(h->opt.device);
   if (!h->apply_ready) { bilu_status s = build_apply(h); if (s != BILU_OK) return s; }
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
-  ApplyArgs &A = h->AA;
-  const int nF = h->fin.nF;
-  const int grid = std::max(1, std::min((nF + 15) / 16, h->sms * 2));   // 16 warp-workers per CTA
   CUDA_TRY(h, bilu_launch_permute(h->d_w, x, h->d_perm, h->n, 0, st));
   const int only = getenv("BILU_APPLY_ONLY") ? atoi(getenv("BILU_APPLY_ONLY")) : -1;   // diagnostics
-  for (int pass = 0; pass < 2; ++pass) {
-    if (only >= 0 && pass != only) continue;
-    const int32_t *cnt0 = pass ? h->d_cnt_b0 : h->d_cnt_f0;
-    const int32_t *q0 = pass ? h->d_q_b0 : h->d_q_f0;
-    const int nq = pass ? h->nq_b0 : h->nq_f0;
-    CUDA_TRY(h, cudaMemcpyAsync(A.cnt, cnt0, nF * 4, cudaMemcpyDeviceToDevice, st));
-    CUDA_TRY(h, cudaMemsetAsync(A.queue, 0xFF, nF * 4, st));
-    if (nq) CUDA_TRY(h, cudaMemcpyAsync(A.queue, q0, nq * 4, cudaMemcpyDeviceToDevice, st));
-    CUDA_TRY(h, cudaMemsetAsync(A.ctrl, 0, 4 * sizeof(unsigned long long), st));
-    CUDA_TRY(h, cudaMemcpyAsync(A.ctrl, pass ? &h->nq_b0_ull : &h->nq_f0_ull, sizeof(unsigned long long),
-                                cudaMemcpyHostToDevice, st));
-    CUDA_TRY(h, bilu_launch_apply(A, grid, pass, st));
-  }
+  bilu_status s;
+  if (only != 1 && (s = run_sweep(h, h->d_cnt_f0, h->d_q_f0, h->nq_f0, &h->nq_f0_ull, h->nt_f0, 0, st)) != BILU_OK)
+    return s;
+  if (only != 0 && (s = run_sweep(h, h->d_cnt_b0, h->d_q_b0, h->nq_b0, &h->nq_b0_ull, h->nt_b0, 1, st)) != BILU_OK)
+    return s;
   CUDA_TRY(h, bilu_launch_permute(y, h->d_y, h->d_perm, h->n, 1, st));
-  h->launches += 4;
+  h->launches += 2;
+  return BILU_OK;
+}
+
+// ---- distributed apply: phase 1 (own subtrees) / exchange by the caller / phases 2-3
+static bilu_status dist_apply_check(bilu_ctx *h, const char *fn) {
+  if (!h) { set_err(nullptr, "%s: null context", fn); return BILU_ERR_ARG; }
+  if (!h->dist) { set_err(h, "%s: not a distributed context (use bilu_apply)", fn); return BILU_ERR_STATE; }
+  if (!h->factored) { set_err(h, "%s: bilu_factor_separators has not run", fn); return BILU_ERR_STATE; }
+  cudaSetDevice(h->opt.device);
+  if (!h->apply_ready) { bilu_status s = build_apply(h); if (s != BILU_OK) return s; }
+  return BILU_OK;
+}
+
+extern "C" bilu_status bilu_dist_separator_rows(bilu_ctx *h, int64_t *m) {
+  bilu_status s = dist_apply_check(h, "bilu_dist_separator_rows");
+  if (s != BILU_OK) return s;
+  if (!m) { set_err(h, "bilu_dist_separator_rows: null argument"); return BILU_ERR_ARG; }
+  *m = h->nsep_rows;
+  return BILU_OK;
+}
+
+extern "C" bilu_status bilu_apply_dist_begin(bilu_ctx *h, const double *x, double *contrib, void *stream) {
+  bilu_status s = dist_apply_check(h, "bilu_apply_dist_begin");
+  if (s != BILU_OK) return s;
+  if (!x || (!contrib && h->nsep_rows > 0)) { set_err(h, "bilu_apply_dist_begin: null argument"); return BILU_ERR_ARG; }
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  CUDA_TRY(h, bilu_launch_permute(h->d_w, x, h->d_perm, h->n, 0, st));
+  CUDA_TRY(h, bilu_launch_sep_gather(h->nsep_rows, h->d_seprows, h->d_w, h->d_xsep, st));
+  if ((s = run_sweep(h, h->d_cnt_f0, h->d_q_f0, h->nq_f0, &h->nq_f0_ull, h->nt_f0, 0, st)) != BILU_OK) return s;
+  CUDA_TRY(h, bilu_launch_sep_contrib(h->nsep_rows, h->d_seprows, h->d_w, h->d_xsep, contrib, st));
+  h->launches += 3;
+  h->dist_apply_begun = true;
+  return BILU_OK;
+}
+
+extern "C" bilu_status bilu_apply_dist_end(bilu_ctx *h, const double *contrib_sum, double *y, int32_t write_separators,
+                                           void *stream) {
+  bilu_status s = dist_apply_check(h, "bilu_apply_dist_end");
+  if (s != BILU_OK) return s;
+  if (!y || (!contrib_sum && h->nsep_rows > 0)) { set_err(h, "bilu_apply_dist_end: null argument"); return BILU_ERR_ARG; }
+  if (!h->dist_apply_begun) { set_err(h, "bilu_apply_dist_end: bilu_apply_dist_begin has not run"); return BILU_ERR_STATE; }
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  CUDA_TRY(h, bilu_launch_sep_set(h->nsep_rows, h->d_seprows, h->d_xsep, contrib_sum, h->d_w, st));
+  if ((s = run_sweep(h, h->d_cnt_f2, h->d_q_f2, h->nq_f2, &h->nq_f2_ull, h->nt_f2, 0, st)) != BILU_OK) return s;
+  if ((s = run_sweep(h, h->d_cnt_b0, h->d_q_b0, h->nq_b0, &h->nq_b0_ull, h->nt_b0, 1, st)) != BILU_OK) return s;
+  CUDA_TRY(h, bilu_launch_permute_out_masked(h->n, h->d_perm, h->d_rowmask, write_separators, h->d_y, y, st));
+  h->launches += 2;
+  h->dist_apply_begun = false;
   return BILU_OK;
 }
 

@@ -167,6 +167,7 @@ struct ApplyArgs {
   int32_t *queue;                 // [nF]
   unsigned long long *ctrl;       // [4]: qhead, qtail
   double *w, *y;                  // permuted work vectors
+  int ntarget;                    // blocks this sweep processes (nF; a rank's share when distributed)
 };
 
 // packed interface blocks exchanged between ranks (bilu_interface_pack/unpack)

@@ -14,6 +14,10 @@ partition; the top-level ND subtrees are assigned to ranks (`partition_owner`), 
   phase B   bilu_factor_separators  every rank factors the separator blocks (replicated),
                                     then aggregates within its own blocks
 
+The preconditioner is applied the same way (`apply_distributed`): forward sweep over the
+own subtrees, one all-reduce of the separator-row contributions, the separator sweeps
+(replicated) and the backward sweep over own subtree blocks, one all-reduce assembling y.
+
 torch.distributed is the transport only (plumbing); every arithmetic step runs in the
 library's kernels.
 """
@@ -78,3 +82,15 @@ def factor_distributed(g, tau, group=None, timer=None):
     if timer:
         timer("separators")
     return st, int(mine.numel()), recv
+
+
+def apply_distributed(g, x, group=None):
+    """y = M^{-1} x with the ranks' distributed factors (`g` after factor_distributed; x the
+    same CUDA float64 vector on every rank).  Two all-reduces: the separator contributions of
+    the forward sweep, and the assembly of y from the ranks' disjoint shares."""
+    import torch.distributed as dist
+    contrib = g.apply_dist_begin(x)
+    dist.all_reduce(contrib, group=group)
+    y = g.apply_dist_end(contrib, write_separators=dist.get_rank(group) == 0)
+    dist.all_reduce(y, group=group)
+    return y

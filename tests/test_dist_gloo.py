@@ -78,3 +78,60 @@ def test_partition_of_nd_orderings_separates():
     oa, ob = owner[a], owner[b]
     assert not np.any((oa >= 0) & (ob >= 0) & (oa != ob))
     assert not np.any((oa == -1) & (ob >= 0) & (a != b))
+
+
+class _FakeRankCtx:
+    """Stands in for a rank's BILU context on CPU: a 6-row problem, rows 0-1 owned by rank 0,
+    rows 2-3 by rank 1, rows 4-5 separators.  begin returns rank-specific contributions; end
+    checks it received their sum and returns its share of y."""
+    def __init__(self, rank):
+        self.rank = rank
+        self.n = 6
+
+    def apply_dist_begin(self, x):
+        import torch
+        return torch.tensor([1.0 + self.rank, 10.0 * (self.rank + 1)], dtype=torch.float64) + x[4:6]
+
+    def apply_dist_end(self, s, write_separators):
+        import torch
+        self.got = s.clone()
+        y = torch.zeros(6, dtype=torch.float64)
+        own = slice(0, 2) if self.rank == 0 else slice(2, 4)
+        y[own] = float(self.rank + 1)
+        if write_separators:
+            y[4:6] = s
+        return y
+
+
+def _apply_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1908_10169_b200.dist import apply_distributed
+    g = _FakeRankCtx(rank)
+    x = torch.arange(6, dtype=torch.float64)
+    y = apply_distributed(g, x)
+    out.put((rank, g.got.tolist(), y.tolist()))
+    dist.destroy_process_group()
+
+
+def test_apply_distributed_gloo_world2():
+    """apply_distributed: one all-reduce of the separator contributions (every rank gets the
+    sum), disjoint shares of y (separators from rank 0 only) summed into the full vector."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_apply_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    s = [1.0 + 2.0 + 4 + 4, 10.0 + 20.0 + 5 + 5]
+    for rank, recv, y in got:
+        assert recv == s
+        assert y == [1.0, 1.0, 2.0, 2.0] + s

@@ -111,3 +111,61 @@ def test_simulated_ranks_c2_full_size_four_ranks():
         present = {int(bst[K]) for K in range(len(owner)) if owner[K] in (r, -1)}
         res = compare_present_blocks(f, of, present)
         assert not res["problems"], (r, res["problems"][:3])
+
+
+def _dist_apply_simulated(ctxs, x):
+    """bilu_apply_dist_begin on every rank, the sum of the contributions (the all-reduce),
+    bilu_apply_dist_end on every rank (separators written by rank 0), the sum of the shares."""
+    contribs = [g.apply_dist_begin(x) for g in ctxs]
+    total = sum(c.clone() for c in contribs) if contribs[0].numel() else contribs[0]
+    ys = [g.apply_dist_end(total, write_separators=(r == 0)) for r, g in enumerate(ctxs)]
+    return sum(ys)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_distributed_apply_matches_oracle_c5(world):
+    """NEXT-1 multi-GPU apply: the ranks' two-phase sweeps give the oracle's M^{-1} x for the
+    factorization with the same segments."""
+    import torch
+    P = config5(N=20, top_levels=2)
+    owner, ctxs, stats, bufs = run_simulated(P, world)
+    exports = [g.export() for g in ctxs]
+    near = {tuple(int(x) for x in row) for f in exports for row in np.asarray(f.near)}
+    ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
+    of = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
+    rng = np.random.default_rng(world)
+    for xv in (np.ones(P.n), rng.standard_normal(P.n)):
+        y = _dist_apply_simulated(ctxs, torch.tensor(xv, device="cuda")).cpu().numpy()
+        yp = oracle.apply(of, xv[P.perm])
+        want = np.empty(P.n)
+        want[P.perm] = yp
+        err = np.abs(y - want).max() / np.abs(want).max()
+        assert err < 1e-10, err
+    for g in ctxs:       # the single-context apply refuses distributed factors
+        from paper_1908_10169_b200 import BiluError
+        with pytest.raises(BiluError):
+            g.apply(0, 0)
+
+
+def test_distributed_apply_c2_two_subtrees():
+    import torch
+    P = config2(N=24, leaf=128, top_levels=1)
+    owner, ctxs, stats, bufs = run_simulated(P, 2)
+    exports = [g.export() for g in ctxs]
+    near = {tuple(int(x) for x in row) for f in exports for row in np.asarray(f.near)}
+    ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
+    of = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
+    xv = np.random.default_rng(7).standard_normal(P.n)
+    y = _dist_apply_simulated(ctxs, torch.tensor(xv, device="cuda")).cpu().numpy()
+    want = np.empty(P.n)
+    want[P.perm] = oracle.apply(of, xv[P.perm])
+    assert np.abs(y - want).max() / np.abs(want).max() < 1e-10
+
+
+def test_distributed_apply_order_errors():
+    import torch
+    from paper_1908_10169_b200 import BiluError
+    P = config5(N=12, top_levels=1)
+    owner, ctxs, stats, bufs = run_simulated(P, 2)
+    with pytest.raises(BiluError):       # end before begin
+        ctxs[0].apply_dist_end(torch.zeros(max(1, P.n), dtype=torch.float64, device="cuda"), True)
