@@ -50,6 +50,33 @@ out = {"config": name, "world": world, "phaseA_ms_per_rank": [round(x, 2) for x 
        "phaseB_ms": round(max(tb), 2), "exchange_bytes_per_rank": nbytes,
        "exchange_ms_projected_nvlink": round(t_ex, 4), "projected_ms": round(proj, 2),
        "single_gpu_ms": round(t1, 2), "projected_speedup": round(t1 / proj, 3)}
+# distributed apply: each rank's begin / end timed alone (CUDA events), the two all-reduces
+# projected (separator contributions, then y) at NVLink bandwidth + 15 us latency each
+def ev_time(fn):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    r = fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b), r
+
+
+x = torch.ones(P.n, dtype=torch.float64, device="cuda")
+for _ in range(2):
+    tbeg, contribs = zip(*[ev_time(lambda g=g: g.apply_dist_begin(x)) for g in ctxs])
+    total = sum(c.clone() for c in contribs)
+    tend, ys = zip(*[ev_time(lambda r=r, g=g: g.apply_dist_end(total, r == 0)) for r, g in enumerate(ctxs)])
+y_dist = sum(ys)
+m = contribs[0].numel()
+t_ar = 2 * 15e-3 + (m * 8 + P.n * 8) / 900e9 * 1e3
+ya = torch.empty_like(x)
+for _ in range(3):
+    t_single_apply, _ = ev_time(lambda: single.apply(x.data_ptr(), ya.data_ptr()))
+out.update({"apply_begin_ms_per_rank": [round(v, 3) for v in tbeg], "apply_end_ms_per_rank": [round(v, 3) for v in tend],
+            "apply_separator_rows": m, "apply_allreduce_ms_projected": round(t_ar, 4),
+            "apply_projected_ms": round(max(tbeg) + t_ar + max(tend), 3),
+            "apply_single_gpu_ms": round(t_single_apply, 3)})
 if check:
     import oracle
     from tests.parity import compare_present_blocks
@@ -66,4 +93,8 @@ if check:
         probs += res["problems"][:2]
     out["parity_max_rel"] = worst
     out["parity_problems"] = probs
+    xv = np.ones(P.n)
+    want = np.empty(P.n)
+    want[P.perm] = oracle.apply(of, xv[P.perm])
+    out["apply_parity_max_rel"] = float(np.abs(y_dist.cpu().numpy() - want).max() / np.abs(want).max())
 print(json.dumps(out), flush=True)
