@@ -1652,8 +1652,24 @@ static bilu_status run_sweep(bilu_ctx *h, const int32_t *cnt0, const int32_t *q0
   if (nq) CUDA_TRY(h, cudaMemcpyAsync(A.queue, q0, nq * 4, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(A.ctrl, 0, 4 * sizeof(unsigned long long), st));
   CUDA_TRY(h, cudaMemcpyAsync(A.ctrl, nq_ull, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+  const char *prof_path = getenv("BILU_APPLY_PROF");   // diagnostics: per-block times to <path>.<sweep>
+  unsigned long long *d_prof = nullptr;
+  if (prof_path) {
+    CUDA_TRY(h, cudaMalloc(&d_prof, sizeof(unsigned long long) * 3 * nF));
+    CUDA_TRY(h, cudaMemsetAsync(d_prof, 0, sizeof(unsigned long long) * 3 * nF, st));
+  }
+  A.prof = d_prof;
   CUDA_TRY(h, bilu_launch_apply(A, grid, backward, st));
+  A.prof = nullptr;
   h->launches += 1;
+  if (prof_path) {
+    std::vector<unsigned long long> t(3 * (size_t)nF);
+    CUDA_TRY(h, cudaMemcpyAsync(t.data(), d_prof, t.size() * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    cudaFree(d_prof);
+    std::string fn = std::string(prof_path) + (backward ? ".bwd" : ".fwd");
+    if (FILE *fp = fopen(fn.c_str(), "wb")) { fwrite(t.data(), 8, t.size(), fp); fclose(fp); }
+  }
   return BILU_OK;
 }
 

@@ -168,6 +168,7 @@ struct ApplyArgs {
   unsigned long long *ctrl;       // [4]: qhead, qtail
   double *w, *y;                  // permuted work vectors
   int ntarget;                    // blocks this sweep processes (nF; a rank's share when distributed)
+  unsigned long long *prof;       // diagnostics (BILU_APPLY_PROF): per block popped/computed/released times, or NULL
 };
 
 // packed interface blocks exchanged between ranks (bilu_interface_pack/unpack)
