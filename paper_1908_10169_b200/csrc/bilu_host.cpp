@@ -127,6 +127,7 @@ struct bilu_ctx {
   unsigned long long qhead0 = 0, ctrl_init[CTRL_COUNT * CS];
   int32_t *d_own_ready = nullptr; int32_t n_own_ready = 0;
   unsigned long long *d_mbound = nullptr;           // merge test: widest window
+  int *d_mticket = nullptr;                          // merge arith: dynamic block ticket
   unsigned char *d_mhbig = nullptr; int64_t mhbig_cap = 0;   // merge test: per-CTA global tables
   double flops_local = 0.0, t_local_ms = 0.0;
   double *d_alpha = nullptr;
@@ -837,6 +838,9 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       int ovf = 0;
       CUDA_TRY(h, cudaMemsetAsync(M.ovf, 0, sizeof(int), h->stream));
       CUDA_TRY(h, cudaMemsetAsync(M.flops, 0, sizeof(double), h->stream));
+      if (!h->d_mticket) CUDA_TRY(h, dalloc(h, &h->d_mticket, 1));
+      CUDA_TRY(h, cudaMemsetAsync(h->d_mticket, 0, sizeof(int), h->stream));
+      M.ticket = h->d_mticket;
       CUDA_TRY(h, bilu_merge_arith(M, h->d_mdwork, h->merge_dwork, mgrid, h->stream));
       launches += 1;
       CUDA_TRY(h, cudaMemcpyAsync(&mfl, M.flops, sizeof(double), cudaMemcpyDeviceToHost, h->stream));

@@ -149,6 +149,7 @@ struct MergeArgs {
   // test windows wider than the shared-memory hash table: per-CTA global tables of hbig_cap
   // slots (keys int32, dmin int32, flag uint8), bytes per CTA = 9 * hbig_cap
   unsigned char *hbig; int64_t hbig_cap;
+  int *ticket;            // [1] merge_arith: next final block (dynamic, heaviest-first order)
 };
 
 // Apply (forward/backward block triangular solves) -- dataflow over final blocks.

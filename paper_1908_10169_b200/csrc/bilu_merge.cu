@@ -523,7 +523,15 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
   double *gbase = dwork + (size_t)blockIdx.x * dwork_per_cta;
   int *gkeys = M.work + (size_t)blockIdx.x * M.work_ints;
   double flops = 0.0;
-  for (int F = blockIdx.x; F < nF; F += gridDim.x) {
+  __shared__ int s_F;
+  while (true) {
+    // dynamic assignment, last final block first: the separator runs (largest P, widest
+    // unions) sit at the end of the ordering and start before the cheap copies
+    __syncthreads();
+    if (tid == 0) s_F = nF - 1 - atomicAdd(M.ticket, 1);
+    __syncthreads();
+    const int F = s_F;
+    if (F < 0) break;
     const int a = M.first[F], k = M.first[F + 1] - 1;
     const int sa = M.bstart[a], ek = M.bstart[k + 1];
     const int P = ek - sa;
