@@ -772,6 +772,8 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
     {   // windows too wide for the test's shared-memory table use per-CTA global tables
       M.Lidx = F.Lidx; M.Uidx = F.Uidx;
       if (!h->d_mbound) CUDA_TRY(h, dalloc(h, &h->d_mbound, 1));
+      if (!h->d_mticket) CUDA_TRY(h, dalloc(h, &h->d_mticket, 1));
+      M.ticket = h->d_mticket;
       CUDA_TRY(h, bilu_merge_bound(M, h->d_mbound, h->sms, h->stream));
       launches += 1;
       unsigned long long mx = 0;
@@ -795,6 +797,7 @@ static bilu_status finalize(bilu_ctx *h, const unsigned long long *ctrl, bilu_fa
       CUDA_TRY(h, cudaMemcpyAsync(M.tot, cur, sizeof(cur), cudaMemcpyHostToDevice, h->stream));
       CUDA_TRY(h, cudaMemsetAsync(M.ovf, 0, sizeof(int), h->stream));
       CUDA_TRY(h, cudaMemsetAsync(M.flops, 0, sizeof(double), h->stream));
+      CUDA_TRY(h, cudaMemsetAsync(h->d_mticket, 0, sizeof(int), h->stream));
       CUDA_TRY(h, bilu_merge_plan(M, h->grid, h->stream));
       launches += bilu_merge_plan_launches();
       int ovf = 0;

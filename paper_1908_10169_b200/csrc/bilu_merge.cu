@@ -236,7 +236,14 @@ __global__ void __launch_bounds__(TEST_T) merge_test_kernel(MergeArgs M) {
   __shared__ TestSide SR, SC;
   __shared__ uint32_t s_mask[4];
   const int tid = threadIdx.x;
-  for (int k = blockIdx.x; k < M.N; k += gridDim.x) {
+  __shared__ int s_k;
+  while (true) {
+    // dynamic assignment, last block first (the separators' wide windows start early)
+    __syncthreads();
+    if (tid == 0) s_k = M.N - 1 - atomicAdd(M.ticket, 1);
+    __syncthreads();
+    const int k = s_k;
+    if (k < 0) break;
     if (tid < 4) s_mask[tid] = 0u;
     const int W = (int)(M.wofs[k + 1] - M.wofs[k]) - 1;     // the host's window (same rule)
     __syncthreads();
