@@ -280,6 +280,25 @@ def main():
     t_kern = allreduce_max(float(np.mean(kern_ms)), world)
     value = (world if world == 1 else 1) / (t_step * 1e-3)   # N > 1: one factorization per step
 
+    # ---------------- distributed preconditioner apply (all ranks; reported by rank 0)
+    dist_apply = None
+    if use_dist and not args.no_solve:
+        from paper_1908_10169_b200.dist import apply_distributed
+        xb = torch.ones(P.n, dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            apply_distributed(g, xb)
+        barrier(world)
+        torch.cuda.synchronize()
+        ea0, ea1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea0.record()
+        for _ in range(5):
+            yb = apply_distributed(g, xb)
+        ea1.record()
+        torch.cuda.synchronize()
+        dist_apply = {"dist_apply_ms": allreduce_max(ea0.elapsed_time(ea1) / 5, world),
+                      "y_sum": float(yb.sum().item()),
+                      "note": "bilu_apply_dist_begin/_end + 2 all-reduces, device time, max over ranks"}
+
     # ---------------- e2e through the C-ABI with host buffers
     e2e = None
     if not args.no_e2e:
@@ -352,6 +371,8 @@ def main():
             out["solve"] = {"gmres_iterations": int(sst["iterations"]), "converged": bool(sst["converged"]),
                             "rel_residual": sst["rel_residual"], "gmres_ms": sst["t_solve_ms"],
                             "apply_ms": ea0.elapsed_time(ea1) / 5}
+        if dist_apply is not None:
+            out["solve"] = dist_apply
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(P)
         print(json.dumps(out), flush=True)
