@@ -379,3 +379,36 @@ def test_device_gmres_matches_host_gmres(cfg):
     xh, it_h, ok_h, _ = gmres(A.dot, np.ones(P.n), precond=m_gpu, restart=30, tol=1e-8)
     assert ok_h and abs(st["iterations"] - it_h) <= 1
     assert np.abs(xs - xh).max() <= 1e-6 * np.abs(xh).max()
+
+
+@pytest.mark.parametrize("agg", [False, True])
+def test_apply_heavy_blocks_split_over_warps(agg):
+    """Blocks with wide panels (b >= 32, >= 16K panel entries) are applied by several warps of
+    a CTA (forward: 64-row parts pushing into w; backward: 128-column parts accumulating into
+    the owner's z).  Block 0 (b=64) couples densely to all 2000 later rows/columns, a middle
+    block (b=48) to everything after it; the apply must match the oracle's (L P U)^{-1} x."""
+    import torch
+    rng = np.random.default_rng(17)
+    n0, nmid, nrest = 64, 48, 2000
+    n = n0 + nrest
+    A = sp.random(n, n, density=3.0 / n, random_state=17, format="lil")
+    A[:n0, n0:] = rng.uniform(-0.1, 0.1, (n0, nrest))
+    A[n0:, :n0] = rng.uniform(-0.1, 0.1, (nrest, n0))
+    m0 = n0 + 1000
+    A[m0:m0 + nmid, m0 + nmid:] = rng.uniform(-0.1, 0.1, (nmid, n - m0 - nmid))
+    A[m0 + nmid:, m0:m0 + nmid] = rng.uniform(-0.1, 0.1, (n - m0 - nmid, nmid))
+    A = A.tocsr()
+    A.setdiag(0.0)
+    A.eliminate_zeros()
+    A = (A + sp.diags(1.5 * np.asarray(abs(A).sum(axis=1)).ravel() + 1.0)).tocsr()
+    A.sort_indices()
+    bs = [n0] + [8] * (1000 // 8) + [nmid] + [8] * ((nrest - 1000 - nmid) // 8)
+    assert sum(bs) == n
+    g, st, gf, of = run_pair(A.indptr, A.indices, A.data, bs, 1e-5, agg)
+    Lm = np.diff(gf.Lp)
+    b = np.diff(gf.bstart)
+    assert ((b >= 32) & (Lm * b >= 16384)).sum() >= 2          # the split paths are exercised
+    for x in (np.ones(n), rng.standard_normal(n)):
+        y = g.apply_tensor(torch.tensor(x, device="cuda")).cpu().numpy()
+        yo = oracle.apply(of, x)
+        np.testing.assert_allclose(y, yo, rtol=1e-11, atol=1e-12 * np.abs(yo).max())
