@@ -97,6 +97,9 @@ def _load():
         lib.orc_cosine_blocks.restype = ctypes.c_int32
         lib.orc_cosine_blocks.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                           ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+        lib.orc_mwm.restype = ctypes.c_int
+        lib.orc_mwm.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         lib.orc_bilu_apply.restype = ctypes.c_int
         lib.orc_bilu_apply.argtypes = [ctypes.POINTER(_Factor), ctypes.c_void_p, ctypes.c_void_p]
         lib.orc_aggregate_test.restype = ctypes.c_int
@@ -324,3 +327,23 @@ def cosine_blocks(indptr, indices, tau=0.8, max_size=128):
     if nb < 0:
         raise OracleError("bad argument")
     return q, sizes[:nb].copy()
+
+
+def mwm(indptr, indices, data):
+    """Maximum product transversal + scalings of Sec. 3.1 (R22): (sigma, dl, dr) with
+    sigma[i] the column matched to row i; |dl_i a_ij dr_j| <= 1, = 1 on the matching."""
+    lib = _load()
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    indices = np.ascontiguousarray(indices, dtype=np.int32)
+    data = np.ascontiguousarray(data, dtype=np.float64)
+    n = len(indptr) - 1
+    sigma = np.zeros(n, dtype=np.int32)
+    dl = np.zeros(n)
+    dr = np.zeros(n)
+    rc = lib.orc_mwm(n, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, sigma.ctypes.data,
+                     dl.ctypes.data, dr.ctypes.data)
+    if rc == -2:
+        raise OracleError("structurally singular: no perfect matching")
+    if rc != 0:
+        raise OracleError("bad argument")
+    return sigma, dl, dr

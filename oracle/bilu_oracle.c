@@ -1032,3 +1032,74 @@ int32_t orc_cosine_blocks(int32_t n, const int64_t *rp, const int32_t *ci, doubl
   free(cnt); free(touched);
   return nb;
 }
+
+/* ---------------- maximum weight matching + scaling (Sec. 3.1; R22) ----------------
+ * Maximum product transversal: a permutation sigma maximising prod_i |a_{i,sigma(i)}|, i.e.
+ * minimising sum_i c_{i,sigma(i)} with c_ij = log(cmax_j) - log|a_ij| >= 0 (cmax_j the largest
+ * |a_ij| of column j; MC64's normalisation), over the stored nonzeros only.
+ * Solved by the textbook O(n^3) Hungarian method with potentials u (rows), v (columns) on the
+ * dense cost matrix (missing entries excluded); at the optimum u_i + v_j <= c_ij with equality
+ * on the matching, so with D_l = diag(exp(u_i)) and D_r = diag(exp(v_j) / cmax_j)
+ *   |(D_l A D_r)_ij| <= 1 and |(D_l A D_r)_{i,sigma(i)}| = 1,
+ * and A^ = D_l A D_r Pi has the matched entries on its diagonal (Pi maps column sigma(i) to i).
+ * Test infrastructure for small n (dense O(n^2) memory).  sigma[i] = column matched to row i.
+ * Returns 0, -1 on a bad argument, -2 if A is structurally singular (no perfect matching). */
+int orc_mwm(int32_t n, const int64_t *rp, const int32_t *ci, const double *val, int32_t *sigma, double *dl,
+            double *dr) {
+  if (n < 1 || n > 8192 || !rp || !ci || !val || !sigma || !dl || !dr) return -1;
+  const double INF = HUGE_VAL;
+  double *cmax = (double *)xcalloc((size_t)n, sizeof(double));
+  for (int32_t i = 0; i < n; ++i)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+      if (fabs(val[p]) > cmax[ci[p]]) cmax[ci[p]] = fabs(val[p]);
+  /* dense costs, 1-based as in the textbook statement: c[i][j], i, j = 1..n */
+  double *c = (double *)xmalloc(sizeof(double) * (size_t)(n + 1) * (size_t)(n + 1));
+  for (size_t x = 0; x < (size_t)(n + 1) * (size_t)(n + 1); ++x) c[x] = INF;
+  for (int32_t i = 0; i < n; ++i)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+      if (val[p] != 0.0) c[(size_t)(i + 1) * (n + 1) + ci[p] + 1] = log(cmax[ci[p]]) - log(fabs(val[p]));
+  double *u = (double *)xcalloc((size_t)n + 1, sizeof(double)), *v = (double *)xcalloc((size_t)n + 1, sizeof(double));
+  double *minv = (double *)xmalloc(sizeof(double) * (size_t)(n + 1));
+  int32_t *p = (int32_t *)xcalloc((size_t)n + 1, sizeof(int32_t)), *way = (int32_t *)xcalloc((size_t)n + 1, sizeof(int32_t));
+  char *used = (char *)xmalloc((size_t)n + 1);
+  int rc = 0;
+  for (int32_t i = 1; i <= n && rc == 0; ++i) {
+    p[0] = i;
+    int32_t j0 = 0;
+    for (int32_t j = 0; j <= n; ++j) { minv[j] = INF; used[j] = 0; }
+    do {
+      used[j0] = 1;
+      const int32_t i0 = p[j0];
+      double delta = INF;
+      int32_t j1 = -1;
+      for (int32_t j = 1; j <= n; ++j) {
+        if (used[j]) continue;
+        const double cij = c[(size_t)i0 * (n + 1) + j];
+        if (cij < INF) {
+          const double cur = cij - u[i0] - v[j];
+          if (cur < minv[j]) { minv[j] = cur; way[j] = j0; }
+        }
+        if (minv[j] < delta) { delta = minv[j]; j1 = j; }
+      }
+      if (j1 < 0) { rc = -2; break; }                       /* no augmenting path */
+      for (int32_t j = 0; j <= n; ++j) {
+        if (used[j]) { u[p[j]] += delta; v[j] -= delta; }
+        else minv[j] -= delta;
+      }
+      j0 = j1;
+    } while (p[j0] != 0);
+    if (rc) break;
+    do {
+      const int32_t j1 = way[j0];
+      p[j0] = p[j1];
+      j0 = j1;
+    } while (j0);
+  }
+  if (rc == 0) {
+    for (int32_t j = 1; j <= n; ++j) sigma[p[j] - 1] = j - 1;
+    for (int32_t i = 0; i < n; ++i) dl[i] = exp(u[i + 1]);
+    for (int32_t j = 0; j < n; ++j) dr[j] = exp(v[j + 1]) / cmax[j];
+  }
+  free(cmax); free(c); free(u); free(v); free(minv); free(p); free(way); free(used);
+  return rc;
+}

@@ -104,6 +104,12 @@ int32_t orc_ilu1_set(int32_t n, const int64_t *rp, const int32_t *ci, const doub
 int32_t orc_cosine_blocks(int32_t n, const int64_t *rp, const int32_t *ci, double tau, int32_t max_size,
                           int32_t *q, int32_t *sizes);
 
+/* Maximum product transversal + MC64-style scalings of Sec. 3.1 (DESIGN.md
+ * R22) by the dense O(n^3) Hungarian method (small n): sigma[i] = column matched to row i,
+ * dl, dr the row / column scalings.  Returns 0, -1 bad argument, -2 structurally singular. */
+int orc_mwm(int32_t n, const int64_t *rp, const int32_t *ci, const double *val, int32_t *sigma, double *dl,
+            double *dr);
+
 void orc_free(orc_factor *f);
 
 #ifdef __cplusplus

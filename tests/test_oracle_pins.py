@@ -552,3 +552,62 @@ def test_cosine_recovers_permuted_block_diagonal():
             groups.append(list(np.nonzero(lab_new == lab_new[r])[0]))
     assert list(s) == [len(g) for g in groups]
     assert list(q) == [x for g in groups for x in g]
+
+
+# ------------------------------------------------------------ maximum weight matching (Sec. 3.1)
+def test_mwm_hand_2x2():
+    """[[1,3],[2,1]]: the transversal {a01, a10} (product 6) beats the diagonal (1).  Column maxima
+    (2, 3); the scaled matrix has 1 on the matching: D_l = I, D_r = diag(1/2, 1/3)."""
+    A = np.array([[1.0, 3.0], [2.0, 1.0]])
+    ip, ix, dv = dense_to_csr(A)
+    sigma, dl, dr = oracle.mwm(ip, ix, dv)
+    assert list(sigma) == [1, 0]
+    S = dl[:, None] * A * dr[None, :]
+    np.testing.assert_allclose(S, [[0.5, 1.0], [1.0, 1.0 / 3.0]], rtol=1e-14)
+
+
+def _mwm_random(n, seed):
+    rng = np.random.default_rng(seed)
+    A = (rng.random((n, n)) < 0.08) * rng.standard_normal((n, n)) * np.exp(rng.uniform(-4, 4, (n, n)))
+    A[np.arange(n), rng.permutation(n)] += rng.uniform(0.1, 1.0, n)    # a perfect matching exists
+    return A
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_mwm_optimum_matches_linear_sum_assignment(seed):
+    """The transversal's objective equals scipy's linear_sum_assignment (an independent solver)
+    on the costs c_ij = log(cmax_j) - log|a_ij| (missing entries excluded by a prohibitive cost),
+    and the scalings satisfy |d_l a d_r| <= 1 with equality on the matching."""
+    from scipy.optimize import linear_sum_assignment
+    n = 60
+    A = _mwm_random(n, seed)
+    ip, ix, dv = dense_to_csr(A)
+    sigma, dl, dr = oracle.mwm(ip, ix, dv)
+    assert sorted(sigma) == list(range(n)) and np.all(A[np.arange(n), sigma] != 0)
+    cmax = np.abs(A).max(axis=0)
+    with np.errstate(divide="ignore"):
+        C = np.where(A != 0, np.log(cmax)[None, :] - np.log(np.abs(A)), 1e6)
+    r, c = linear_sum_assignment(C)
+    assert abs(C[np.arange(n), sigma].sum() - C[r, c].sum()) < 1e-9
+    S = np.abs(dl[:, None] * A * dr[None, :])
+    assert S.max() <= 1 + 1e-12
+    np.testing.assert_allclose(S[np.arange(n), sigma], 1.0, rtol=1e-12)
+
+
+def test_mwm_permuted_diagonal_and_singular():
+    """One entry per row and column: the matching is forced and every scaled entry is 1.  A
+    structurally singular pattern (an empty column) has no perfect matching."""
+    rng = np.random.default_rng(2)
+    n = 25
+    perm = rng.permutation(n)
+    A = np.zeros((n, n))
+    A[np.arange(n), perm] = rng.uniform(-5, 5, n)
+    ip, ix, dv = dense_to_csr(A)
+    sigma, dl, dr = oracle.mwm(ip, ix, dv)
+    assert list(sigma) == list(perm)
+    np.testing.assert_allclose(np.abs(dl * A[np.arange(n), perm] * dr[perm]), 1.0, rtol=1e-13)
+    B = _mwm_random(20, 9)
+    B[:, 3] = 0.0
+    ipb, ixb, dvb = dense_to_csr(B)
+    with pytest.raises(oracle.OracleError):
+        oracle.mwm(ipb, ixb, dvb)
