@@ -49,6 +49,7 @@ class _Factor(ctypes.Structure):
         ("n_merges", ctypes.c_int32), ("breakdown_block", ctypes.c_int32),
         ("n_decisions", ctypes.c_int64), ("n_near", ctypes.c_int64),
         ("min_margin", ctypes.c_double), ("n_perturbed", ctypes.c_int64),
+        ("n_override_applied", ctypes.c_int64),
     ]
 
 
@@ -142,6 +143,7 @@ class OracleFactor:
     n_near: int = 0
     min_margin: float = float("inf")
     n_perturbed: int = 0
+    n_override_applied: int = 0
     _keep: object = field(default=None, repr=False)
 
     @property
@@ -209,7 +211,9 @@ def factor(indptr, indices, data, block_sizes, tau, aggregate=True, max_block=12
         bb = f.breakdown_block
         lib.orc_free(ctypes.byref(f))
         raise OracleError({1: "bad argument", 2: "breakdown in block %d" % bb,
-                           3: "out of memory"}.get(rc, "error %d" % rc))
+                           3: "out of memory",
+                           5: "override refused: it names a decision farther than 1e-6 relative from tau "
+                              "(only near-threshold decisions may be replayed, DESIGN.md R15)"}.get(rc, "error %d" % rc))
     nb = f.nblk
     bstart = _np(f.bstart, nb + 1, np.int64)
     Lp = _np(f.Lp, nb + 1, np.int64)
@@ -223,7 +227,7 @@ def factor(indptr, indices, data, block_sizes, tau, aggregate=True, max_block=12
         Uvp=Uvp, Uv=_np(f.Uv, int(Uvp[-1]), np.float64), Dp=Dp,
         Dv=_np(f.Dv, int(Dp[-1]), np.float64), flops=f.flops, t_factor_s=f.t_factor_s,
         n_merges=f.n_merges, n_decisions=f.n_decisions, n_near=f.n_near,
-        min_margin=f.min_margin, n_perturbed=f.n_perturbed)
+        min_margin=f.min_margin, n_perturbed=f.n_perturbed, n_override_applied=f.n_override_applied)
     lib.orc_free(ctypes.byref(f))
     return out
 

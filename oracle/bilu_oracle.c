@@ -244,7 +244,16 @@ typedef struct {
   const orc_override *ov; int64_t nov;
   double tau, near_rel;
   int64_t n_decisions, n_near; double min_margin;
+  int64_t n_applied;      /* overrides that matched a decision                        */
+  int64_t n_refused;      /* overrides of decisions farther than OVR_GUARD from tau   */
 } decider;
+
+/* An override (decision replay, R15) may only flip a decision that is near tau in the
+ * oracle's OWN arithmetic: north_star exempts only decisions within 1e-8 relative of the
+ * threshold; OVR_GUARD leaves two decades for the rounding differences of the two sides.
+ * A GPU-supplied override farther from tau than this is refused and the factorization
+ * fails (status 5), so a margin bug on the GPU cannot make the oracle copy its decisions. */
+#define OVR_GUARD 1e-6
 
 /* Keep iff max_t |x_t| > tau (R1: max-abs norm; R2: ties drop, "<=" in
  * PAPER.md:167,173; R3: the *scaled* row l_ik l_kk^{-1}). */
@@ -258,7 +267,11 @@ static int decide(decider *d, int32_t blk, int32_t side, int32_t idx, double mx)
   }
   if (d->nov) {
     const orc_override *o = find_override(d->ov, d->nov, blk, side, idx);
-    if (o) keep = o->keep != 0;
+    if (o) {
+      if (!(d->tau > 0.0) || !(fabs(mx / d->tau - 1.0) <= OVR_GUARD)) { d->n_refused++; return keep; }
+      keep = o->keep != 0;
+      d->n_applied++;
+    }
   }
   return keep;
 }
@@ -321,7 +334,7 @@ static int factor_impl(int32_t n, const int64_t *row_ptr, const int32_t *col_idx
     qsort(ov, (size_t)n_ovr, sizeof(orc_override), cmp_ovr);
   }
   decider dec; dec.ov = ov; dec.nov = ov ? n_ovr : 0; dec.tau = tau; dec.near_rel = near_rel;
-  dec.n_decisions = 0; dec.n_near = 0; dec.min_margin = INFINITY;
+  dec.n_decisions = 0; dec.n_near = 0; dec.min_margin = INFINITY; dec.n_applied = 0; dec.n_refused = 0;
 
   /* ---- state ---- */
   oblk *B = (oblk *)xcalloc((size_t)nblk, sizeof(oblk));
@@ -697,6 +710,8 @@ static int factor_impl(int32_t n, const int64_t *row_ptr, const int32_t *col_idx
   f->n_decisions = dec.n_decisions;
   f->n_near = dec.n_near;
   f->min_margin = dec.min_margin;
+  f->n_override_applied = dec.n_applied;
+  if (status == 0 && dec.n_refused > 0) status = 5;
 
   for (K = 0; K < nblk; ++K) {
     free(B[K].Li); free(B[K].Lv); free(B[K].Ui); free(B[K].Uv); free(B[K].D);

@@ -46,6 +46,7 @@ typedef struct {
   int64_t n_near;           /* decisions with margin <= near_rel            */
   double  min_margin;       /* min |max/tau - 1| over all decisions         */
   int64_t n_perturbed;      /* pivot blocks modified by the Sec. 3.6 perturbation */
+  int64_t n_override_applied; /* replayed decisions (each within OVR_GUARD of tau) */
 } orc_factor;
 
 /* Sec. 3.6 perturbation parameters (R19); perturb = 0 disables it. */
@@ -56,7 +57,8 @@ typedef struct { int32_t perturb; double tau, rho, cond_max; } orc_perturb;
 typedef struct { int32_t blk, side, idx, keep; } orc_override;
 
 /* Returns 0 on success, 1 bad argument, 2 breakdown (singular pivot block),
- * 3 out of memory.  On success *f owns malloc'd arrays (free with orc_free). */
+ * 3 out of memory, 5 an override names a decision whose margin |max/tau - 1| exceeds
+ * OVR_GUARD = 1e-6 (refused: only near-threshold decisions may be replayed, R15).  On success *f owns malloc'd arrays (free with orc_free). */
 int orc_bilu_factor(int32_t n, const int64_t *row_ptr, const int32_t *col_idx,
                     const double *val, int32_t nblk, const int32_t *bsizes,
                     double tau, int32_t aggregate, int32_t max_block,

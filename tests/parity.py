@@ -45,6 +45,16 @@ def overrides_from_near(near):
     return [tuple(int(x) for x in row) for row in np.asarray(near)]
 
 
+def assert_replay_bounded(of, overrides):
+    """The decision replay (reading R15) may only touch near-threshold decisions: every
+    override matched a decision of the oracle (which refuses, with an error, any override
+    whose own margin exceeds 1e-6), and there are no more overrides than decisions the
+    oracle itself finds within 1e-8 of tau."""
+    n = len(overrides)
+    assert of.n_override_applied == n, (of.n_override_applied, n)
+    assert n <= of.n_near, (n, of.n_near)
+
+
 def dense_LPU(f, n):
     """Dense L, P (= D^{-1} blocks), U of a factor (small n only; test helper)."""
     L = np.eye(n)
@@ -91,3 +101,13 @@ def compare_present_blocks(g, o, present_start, tol=1e-10):
     if worst > tol:
         problems.append("max normwise relative difference %.3e > %.1e" % (worst, tol))
     return {"problems": problems, "max_rel": worst, "checked": checked}
+
+
+def oracle_replay(*args, overrides=None, **kw):
+    """oracle.factor with the GPU's near-threshold decisions replayed (R15), bounded by
+    assert_replay_bounded."""
+    import oracle
+    ov = list(overrides or [])
+    of = oracle.factor(*args, overrides=ov, **kw)
+    assert_replay_bounded(of, ov)
+    return of

@@ -12,7 +12,7 @@ import scipy.sparse as sp
 
 import oracle
 from inputs.configs import config1, config2, config3, config4, config5, dense_to_csr, random_dd
-from tests.parity import compare_factors, overrides_from_near
+from tests.parity import compare_factors, oracle_replay, overrides_from_near
 
 pytestmark = pytest.mark.gpu
 
@@ -137,7 +137,7 @@ def test_factor_from_estimated_blocks(name):
     gf = g.export()
     pip, pix, pdv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm) if P.perm is not None else (
         P.indptr, P.indices, P.data)
-    of = oracle.factor(pip, pix, pdv, bs, P.tau, aggregate=True, overrides=overrides_from_near(gf.near))
+    of = oracle_replay(pip, pix, pdv, bs, P.tau, aggregate=True, overrides=overrides_from_near(gf.near))
     assert st["n_blocks_init"] == len(bs)
     r = compare_factors(gf, of, 1e-10)
     assert not r["problems"], r["problems"][:5]
@@ -245,6 +245,6 @@ def test_factor_from_cosine_blocks():
     st = g.factor(P.tau)
     gf = g.export()
     pip, pix, pdv = oracle.permute_csr(P.indptr, P.indices, P.data, q)
-    of = oracle.factor(pip, pix, pdv, s, P.tau, aggregate=True, overrides=overrides_from_near(gf.near))
+    of = oracle_replay(pip, pix, pdv, s, P.tau, aggregate=True, overrides=overrides_from_near(gf.near))
     r = compare_factors(gf, of, 1e-10)
     assert not r["problems"], r["problems"][:5]

@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 from inputs.configs import config2, config5
-from tests.parity import compare_present_blocks
+from tests.parity import compare_present_blocks, oracle_replay
 
 pytestmark = pytest.mark.gpu
 
@@ -48,7 +48,7 @@ def test_simulated_ranks_match_oracle_c5(world):
     exports = [g.export() for g in ctxs]
     near = {tuple(int(x) for x in row) for f in exports for row in np.asarray(f.near)}
     ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
-    of = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
+    of = oracle_replay(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
     bst = np.concatenate([[0], np.cumsum(P.block_sizes)])
     for r, f in enumerate(exports):
         present = {int(bst[K]) for K in range(len(owner)) if owner[K] in (r, -1)}
@@ -69,7 +69,7 @@ def test_simulated_ranks_c2_two_subtrees():
     exports = [g.export() for g in ctxs]
     near = {tuple(int(x) for x in row) for f in exports for row in np.asarray(f.near)}
     ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
-    of = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
+    of = oracle_replay(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
     bst = np.concatenate([[0], np.cumsum(P.block_sizes)])
     for r, f in enumerate(exports):
         present = {int(bst[K]) for K in range(len(owner)) if owner[K] in (r, -1)}
@@ -105,7 +105,7 @@ def test_simulated_ranks_c2_full_size_four_ranks():
     exports = [g.export() for g in ctxs]
     near = {tuple(int(x) for x in row) for f in exports for row in np.asarray(f.near)}
     ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
-    of = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
+    of = oracle_replay(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
     bst = np.concatenate([[0], np.cumsum(P.block_sizes)])
     for r, f in enumerate(exports):
         present = {int(bst[K]) for K in range(len(owner)) if owner[K] in (r, -1)}
@@ -132,7 +132,7 @@ def test_distributed_apply_matches_oracle_c5(world):
     exports = [g.export() for g in ctxs]
     near = {tuple(int(x) for x in row) for f in exports for row in np.asarray(f.near)}
     ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
-    of = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
+    of = oracle_replay(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
     rng = np.random.default_rng(world)
     for xv in (np.ones(P.n), rng.standard_normal(P.n)):
         y = _dist_apply_simulated(ctxs, torch.tensor(xv, device="cuda")).cpu().numpy()
@@ -154,7 +154,7 @@ def test_distributed_apply_c2_two_subtrees():
     exports = [g.export() for g in ctxs]
     near = {tuple(int(x) for x in row) for f in exports for row in np.asarray(f.near)}
     ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
-    of = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
+    of = oracle_replay(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
     xv = np.random.default_rng(7).standard_normal(P.n)
     y = _dist_apply_simulated(ctxs, torch.tensor(xv, device="cuda")).cpu().numpy()
     want = np.empty(P.n)

@@ -13,7 +13,7 @@ import scipy.sparse as sp
 import oracle
 from harness.gmres import gmres
 from inputs.configs import config1, config2, config3, dense_to_csr, random_dd
-from tests.parity import compare_factors, dense_LPU, overrides_from_near
+from tests.parity import compare_factors, dense_LPU, oracle_replay, overrides_from_near
 
 pytestmark = pytest.mark.gpu
 
@@ -38,7 +38,7 @@ def run_pair(ip, ix, dv, bs, tau, agg=True, perm=None, max_block=128, **kw):
         pip, pix, pdv = oracle.permute_csr(ip, ix, dv, perm)
     else:
         pip, pix, pdv = ip, ix, dv
-    of = oracle.factor(pip, pix, pdv, bs, tau, aggregate=agg, max_block=max_block,
+    of = oracle_replay(pip, pix, pdv, bs, tau, aggregate=agg, max_block=max_block,
                        overrides=overrides_from_near(gf.near))
     return g, st, gf, of
 
@@ -141,7 +141,7 @@ def test_refactor_new_values_and_tau():
     g.set_values(dv2)
     g.factor(3e-3)
     gf = g.export()
-    of = oracle.factor(ip, ix, dv2, bs, 3e-3, overrides=overrides_from_near(gf.near))
+    of = oracle_replay(ip, ix, dv2, bs, 3e-3, overrides=overrides_from_near(gf.near))
     assert_parity(gf, of)
 
 
@@ -304,7 +304,7 @@ def run_pair_pt(ip, ix, dv, bs, tau, agg=True):
              cond_max=PT[2])
     st = g.factor(tau)
     gf = g.export()
-    of = oracle.factor(ip, ix, dv, bs, tau, aggregate=agg, perturb=PT, overrides=overrides_from_near(gf.near))
+    of = oracle_replay(ip, ix, dv, bs, tau, aggregate=agg, perturb=PT, overrides=overrides_from_near(gf.near))
     return g, st, gf, of
 
 
@@ -412,3 +412,26 @@ def test_apply_heavy_blocks_split_over_warps(agg):
         y = g.apply_tensor(torch.tensor(x, device="cuda")).cpu().numpy()
         yo = oracle.apply(of, x)
         np.testing.assert_allclose(y, yo, rtol=1e-11, atol=1e-12 * np.abs(yo).max())
+
+
+@pytest.mark.parametrize("cfg", ["c2r", "c4r", "rand"])
+def test_flop_count_matches_oracle_without_aggregation(cfg):
+    """The GFLOP/s numerator (bilu_factor_stats.flops) equals the oracle's count
+    of the same executed structure: with aggregate = False both count 2 b_J m c per
+    contributor side and 2b^3 + 2b^2(|R_K| + |C_K|) per block over identical candidate
+    sets (integer-valued sums, exact in fp64)."""
+    from inputs.configs import config4
+    if cfg == "c2r":
+        P = config2(N=24, leaf=128)
+        args = (P.indptr, P.indices, P.data, P.block_sizes, P.tau, False, P.perm)
+    elif cfg == "c4r":
+        P = config4(nblocks=80, per_row=4)
+        args = (P.indptr, P.indices, P.data, P.block_sizes, P.tau, False, P.perm)
+    else:
+        A = random_dd(300, 0.05, 9, dominance=1.3)
+        ip, ix, dv = dense_to_csr(A)
+        args = (ip, ix, dv, partition(300, np.random.default_rng(9), 12), 1e-3, False)
+    g, st, gf, of = run_pair(*args)
+    assert_parity(gf, of)
+    assert st["flops"] == of.flops, (st["flops"], of.flops)
+    g.close()

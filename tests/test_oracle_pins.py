@@ -309,7 +309,19 @@ def test_decision_override_replays():
     assert len(f.Li) == 0 and f.n_near == 1 and f.min_margin == 0.0
     ip, ix, dv = dense_to_csr(A)
     g = oracle.factor(ip, ix, dv, [1, 1], 0.01, aggregate=False, overrides=[(0, 0, 1, 1)])
-    assert list(g.Li) == [1]
+    assert list(g.Li) == [1] and g.n_override_applied == 1
+
+
+def test_decision_override_guard():
+    """Replay is bounded (R15): an override of a decision far from tau (here l = 0.5, margin
+    49 at tau = 0.01) is refused with an error instead of being copied into the oracle;
+    an override naming no decision is not applied."""
+    A = np.array([[2.0, 0.0], [1.0, 1.0]])
+    ip, ix, dv = dense_to_csr(A)
+    with pytest.raises(oracle.OracleError, match="override refused"):
+        oracle.factor(ip, ix, dv, [1, 1], 0.01, aggregate=False, overrides=[(0, 0, 1, 0)])
+    g = oracle.factor(ip, ix, dv, [1, 1], 0.01, aggregate=False, overrides=[(1, 0, 5, 1)])
+    assert g.n_override_applied == 0 and list(g.Li) == [1]
 
 
 def test_aggregation_segments_reading_r18():
@@ -611,3 +623,77 @@ def test_mwm_permuted_diagonal_and_singular():
     ipb, ixb, dvb = dense_to_csr(B)
     with pytest.raises(oracle.OracleError):
         oracle.mwm(ipb, ixb, dvb)
+
+
+# ---------------- aggregation counts (Sec. 3.5) pinned by a hand trace ----------------
+def _trace_matrix(g):
+    n = g["n"]
+    L0 = np.eye(n)
+    U0 = np.eye(n)
+    for i, k, v in g["L0"]:
+        L0[i, k] = v
+    for k, j, v in g["U0"]:
+        U0[k, j] = v
+    return L0 @ np.diag(g["pivots"]) @ U0
+
+
+def test_aggregation_counts_hand_trace():
+    """tests/golden/aggregate_trace.json: a 7x7 A = L0 P0 U0 with scalar initial blocks whose
+    factor patterns are known by construction; the counts r,s,t,r',s',t',u,v of every merge
+    test were traced by hand from those patterns.  The trace's merge
+    decisions, and hence the final partition [1,1,5], differ from what a sum instead of a
+    union for u or v, counting the rows of L_{k-1} inside block k in u, dropping r or t'
+    from mu, or strict inequalities would give (the mutants listed in the file)."""
+    g = json.load(open(os.path.join(GOLD, "aggregate_trace.json")))
+    A = _trace_matrix(g)
+    f = fac(A, g["block_sizes"], g["tau"])            # no aggregation: the patterns of L0, U0
+    for K in range(g["n"]):
+        _, _, rows, _, cols, _, _ = f.block(K)
+        assert list(rows) == g["L_rows_per_block"][K] and list(cols) == g["U_cols_per_block"][K]
+    for st in g["steps"]:
+        p, q = st["p"], st["q"]
+        assert st["r"] + st["s"] + st["t"] >= st["u"] >= max(st["s"], st["t"])
+        assert st["u"] == len(st["u_rows"]) and st["v"] == len(st["v_cols"])
+        mu = p * (p + st["r"] + st["s"] + st["r2"] + st["s2"]) + q * (q + st["t"] + st["t2"])
+        nu = (p + q) * (p + q + st["u"] + st["v"])
+        assert (mu, nu) == (st["mu"], st["nu"])
+        assert oracle.aggregate_test(p, q, st["r"], st["s"], st["t"], st["r2"], st["s2"], st["t2"],
+                                     st["u"], st["v"]) == st["merge"]
+    h = fac(A, g["block_sizes"], g["tau"], agg=True)
+    assert list(np.diff(h.bstart)) == g["final_block_sizes"] and h.n_merges == g["n_merges"]
+    # max_block = 3 (R9) stops the run at p + q = 4 (step k = 5); block 5 alone then meets
+    # block 6: p = q = 1, r = 1 (row 6 of L_5), s = t = r' = s' = t' = u = v = 0, mu = 3,
+    # nu = 4 <= mu + 2(p+q) = 7 -> merge: partition [1, 1, 3, 2]
+    m = fac(A, g["block_sizes"], g["tau"], agg=True, max_block=3)
+    assert list(np.diff(m.bstart)) == [1, 1, 3, 2] and m.n_merges == 3
+    # the merged factors represent the same operator (P:1348-1387)
+    L, P, U = dense_LPU(h, g["n"])
+    np.testing.assert_allclose(L @ P @ U, A, atol=1e-13 * np.abs(A).max())
+
+
+def test_perturbation_ill_conditioned_nonsingular_block():
+    """Sec. 3.6: a pivot block that is nonsingular but ill-conditioned is
+    perturbed.  P = [[1, 1], [1, 1 + 1e-13]] has kappa_1 = ||P||_1 ||P^{-1}||_1 ~ 4e13 >
+    cond_max = 1e12 (R19), so every column, then every row, gets its largest entry (the
+    diagonal, preferred when 2|d_jj| >= |d_kj|) moved to d (1 + rho delta) + sign(d) tau_p
+    alpha; with cond_max = 1e20 the same block is inverted unperturbed."""
+    eps = 1e-13
+    A = np.array([[1.0, 1.0], [1.0, 1.0 + eps]])
+    ip, ix, dv = dense_to_csr(A)
+    tp, rho, _ = PT
+    f = oracle.factor(ip, ix, dv, [2], 0.0, aggregate=False, perturb=PT)
+    assert f.n_perturbed == 1
+    alpha = 1.0 + eps
+    Pp = A.copy()
+    for j in range(2):                                  # columns: delta_j = max_i |p_ij|
+        d = np.abs(Pp[:, j]).max()
+        Pp[j, j] = Pp[j, j] * (1 + rho * d) + tp * alpha
+    for i in range(2):                                  # then rows
+        d = np.abs(Pp[i, :]).max()
+        Pp[i, i] = Pp[i, i] * (1 + rho * d) + tp * alpha
+    np.testing.assert_allclose(f.block(0)[6], np.linalg.inv(Pp), rtol=1e-12)
+    kappa = np.abs(Pp).sum(0).max() * np.abs(np.linalg.inv(Pp)).sum(0).max()
+    assert kappa < 1e12
+    g = oracle.factor(ip, ix, dv, [2], 0.0, aggregate=False, perturb=(PT[0], PT[1], 1e20))
+    assert g.n_perturbed == 0
+    np.testing.assert_allclose(g.block(0)[6], np.linalg.inv(A), rtol=1e-3)

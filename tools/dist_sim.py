@@ -79,11 +79,11 @@ out.update({"apply_begin_ms_per_rank": [round(v, 3) for v in tbeg], "apply_end_m
             "apply_single_gpu_ms": round(t_single_apply, 3)})
 if check:
     import oracle
-    from tests.parity import compare_present_blocks
+    from tests.parity import compare_present_blocks, oracle_replay
     exports = [g.export() for g in ctxs]
     near = {tuple(int(x) for x in row) for f in exports for row in np.asarray(f.near)}
     ip, ix, dv = oracle.permute_csr(P.indptr, P.indices, P.data, P.perm)
-    of = oracle.factor(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
+    of = oracle_replay(ip, ix, dv, P.block_sizes, P.tau, seg=owner, overrides=sorted(near))
     bst = np.concatenate([[0], np.cumsum(P.block_sizes)])
     worst, probs = 0.0, []
     for r, f in enumerate(exports):

@@ -5,7 +5,7 @@ sys.path.insert(0, "/root/repo")
 import oracle
 from inputs.configs import config1, config2, random_dd, dense_to_csr
 from paper_1908_10169_b200 import BILU
-from tests.parity import compare_factors, overrides_from_near
+from tests.parity import compare_factors, oracle_replay, overrides_from_near
 
 
 def run(name, ip, ix, dv, bs, tau, agg, perm=None):
@@ -19,7 +19,7 @@ def run(name, ip, ix, dv, bs, tau, agg, perm=None):
     else:
         pip, pix, pdv = ip, ix, dv
     ov = overrides_from_near(gf.near)
-    of = oracle.factor(pip, pix, pdv, bs, tau, aggregate=agg, overrides=ov)
+    of = oracle_replay(pip, pix, pdv, bs, tau, aggregate=agg, overrides=ov)
     r = compare_factors(gf, of)
     print("%-28s tau=%-6g agg=%d  blocks %5d->%5d  gpu %.3f ms  oracle %.3f s  flops g/o %.4g/%.4g  near %d  max_rel %.2e  %s" % (
         name, tau, agg, len(bs), gf.nblk, st["t_factor_ms"], of.t_factor_s, st["flops"], of.flops,
