@@ -33,8 +33,18 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False, def
         objdir = os.path.join(HERE, "build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
+    hdr_time = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS + []) if HEADERS else 0.0
+    hdr_time = max(hdr_time, os.path.getmtime(__file__))
+
+    def fresh(src, o):   # incremental: an object newer than its source and every header is kept
+        return (not force and os.path.exists(o) and
+                os.path.getmtime(o) >= max(os.path.getmtime(src), hdr_time))
+
     for f in CU_SOURCES:
         o = os.path.join(objdir, f + ".o")
+        objs.append(o)
+        if fresh(os.path.join(CSRC, f), o):
+            continue
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, f), "-o", o]
         if verbose:
@@ -44,12 +54,13 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False, def
         for d in defines:
             cmd.insert(1, "-D" + d)
         subprocess.check_call(cmd)
-        objs.append(o)
     for f in CPP_SOURCES:
         o = os.path.join(objdir, f + ".o")
+        objs.append(o)
+        if fresh(os.path.join(CSRC, f), o):
+            continue
         subprocess.check_call(["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-I/usr/local/cuda/include",
                                "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, f), "-o", o])
-        objs.append(o)
     tmp = lib + ".tmp%d" % os.getpid()
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
     os.replace(tmp, lib)
