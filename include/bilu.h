@@ -75,6 +75,14 @@ typedef struct {
   double  perturb_tau;   /* default 1e-2 (the paper's practice)                   */
   double  perturb_rho;   /* default 1e-1                                          */
   double  cond_max;      /* default 1e12                                          */
+  /* Dense trailing zone: the longest suffix of blocks, all at most 8 wide,
+   * whose dense panel buffers (2 x 64 B x blocks x unknowns of the suffix) fit this many
+   * bytes keeps its block columns / rows in those buffers; its contributors push their
+   * Schur updates there when they finish (same products, another summation order), so a
+   * ready block of the suffix (the top separators of a nested dissection) reads only its
+   * own panel.  0 = default budget (min(6 GiB, 1/4 of free memory)), < 0 = off.  Ignored
+   * by the distributed factorization. */
+  int64_t zone_bytes;
 } bilu_options;
 
 /* Fills *opt with the defaults (device 0, max_block 128, aggregate 1, near_rel
@@ -96,6 +104,8 @@ typedef struct {
   int64_t n_near;                /* of which |max/tau - 1| <= near_rel            */
   double  min_margin;            /* min |max/tau - 1| over all decisions (tau>0)  */
   int64_t n_perturbed;           /* pivot blocks modified by the Sec. 3.6 perturbation */
+  int32_t zone_blocks;           /* blocks of the dense trailing zone */
+  int32_t zone_unknowns;         /* ... and their unknowns                        */
 } bilu_factor_stats;
 
 /*
@@ -136,7 +146,8 @@ bilu_status bilu_set_values(bilu_ctx *h, const double *val, int32_t on_device);
  *   tau   drop tolerance >= 0 (0 keeps every row/column that is not exactly 0)
  *   st    optional statistics (may be NULL)
  * Returns BILU_ERR_BREAKDOWN (st->breakdown_block set) if a pivot block is
- * exactly singular; diagonal perturbation (Sec. 3.6) is not applied.
+ * exactly singular (or, with opt.perturb, still singular / ill-conditioned after the
+ * Sec. 3.6 perturbation).
  */
 bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *st);
 

@@ -39,7 +39,8 @@ class Options(ctypes.Structure):
                 ("near_rel", ctypes.c_double), ("arena_hint", ctypes.c_int64),
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("nccl_comm", ctypes.c_void_p), ("perturb", ctypes.c_int32), ("perturb_tau", ctypes.c_double),
-                ("perturb_rho", ctypes.c_double), ("cond_max", ctypes.c_double)]
+                ("perturb_rho", ctypes.c_double), ("cond_max", ctypes.c_double),
+                ("zone_bytes", ctypes.c_int64)]
 
 
 class FactorStats(ctypes.Structure):
@@ -50,7 +51,8 @@ class FactorStats(ctypes.Structure):
                 ("n_merges", ctypes.c_int32), ("breakdown_block", ctypes.c_int32),
                 ("n_retries", ctypes.c_int32), ("n_kernel_launches", ctypes.c_int32),
                 ("n_decisions", ctypes.c_int64), ("n_near", ctypes.c_int64),
-                ("min_margin", ctypes.c_double), ("n_perturbed", ctypes.c_int64)]
+                ("min_margin", ctypes.c_double), ("n_perturbed", ctypes.c_int64),
+                ("zone_blocks", ctypes.c_int32), ("zone_unknowns", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

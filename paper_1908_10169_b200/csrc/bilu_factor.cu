@@ -865,6 +865,23 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
                              const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops,
                              HeavyCtx *X = nullptr, int mode = 0);
 
+// a-1: release the blocks that wait for K (static adjacency of Ã + chain edges); K's writes
+// are fenced by the caller
+__device__ void release_block(const DevFactor &F, int K) {
+  const int tid = threadIdx.x;
+  const int a0 = F.adj_ptr[K], a1 = F.adj_ptr[K + 1];
+  const int nS = __ldcg(&F.succ.cnt[K]);
+  for (int x = tid; x < (a1 - a0) + nS; x += NT) {
+    int T = x < (a1 - a0) ? F.adj[a0 + x] : __ldcg(list_rec(F.succ, K, x - (a1 - a0)));
+    if (atomicSub(&F.pending[T], 1) == 1 && (F.owned == nullptr || F.owned[T])) {
+      unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
+      __threadfence();
+      st_vol(&F.queue[slot], T);
+    }
+  }
+  if (tid == 0) atomicAdd(&F.ctrl[CS * CTRL_DONE], 1ull);
+}
+
 // the destination line of every item of one side, into the global pool (split wide blocks)
 template <int SIDE>
 __device__ bool item_lines(const DevFactor &F, int K, int s, int e, const Contrib *C, int nc, int T, const LineMap &M,
@@ -1755,6 +1772,73 @@ scaled:
     if (j == 0 || cb[j] != cb[j - 1]) { cstart[run[mK + j] - nRr] = j; cblk[run[mK + j] - nRr] = cb[j]; }
   if (tid == 0) { rstart[nRr] = mK; cstart[nCr] = cK; }
   __syncthreads();
+  // ---------------- dense trailing zone: push K's Schur update into the
+  // panels of the zone blocks it feeds.  Every pair (i, j) of a kept row i and a kept column
+  // j, both in the zone, receives -L_K[i, :] Ũ_K[:, j] ("gather ... GEMM ... scatter",
+  // PAPER.md:371-374): in block column T = block(j) if T <= block(i), else in block row
+  // block(i) -- the same products the Crout path applies when T is processed (each pair once,
+  // at T = min(block(i), block(j))), in another summation order (R13).  Candidate bits: row
+  // i of every zone column block T < block(i) of K's columns, column j of every zone row
+  // block T < block(j) of K's rows (a-3: the union of the contributors' kept rows / columns).
+  if (F.nzb > 0) {
+    // K's kept rows / columns that are zone unknowns (with their zone numbers), and its
+    // row / column runs that are zone blocks
+    int *zx = (int *)balloc(A, (int64_t)(mK + cK + 2) * 4);
+    int *zi = (int *)balloc(A, (int64_t)(mK + cK + 2) * 4);
+    int *zrr = (int *)balloc(A, (int64_t)(nRr + nCr + 2) * 4);
+    OVF_CHECK();
+    if (tid == 0) { S.cnt[0] = 0; S.cnt[1] = 0; S.cnt[2] = 0; S.cnt[3] = 0; }
+    __syncthreads();
+    for (int x = tid; x < mK + cK; x += NT) {
+      const int u = x < mK ? R[x] : Cs[x - mK];
+      const int zl = F.zloc[u];
+      if (zl >= 0) {
+        const int q = atomicAdd(&S.cnt[x < mK ? 0 : 1], 1);
+        if (x < mK) { zx[q] = x; zi[q] = zl; }
+        else { zx[mK + q] = x - mK; zi[mK + q] = zl; }
+      }
+    }
+    for (int x = tid; x < nRr + nCr; x += NT) {
+      const int T = x < nRr ? rblk[x] : cblk[x - nRr];
+      if (F.zk[T] >= 0) {
+        const int q = atomicAdd(&S.cnt[x < nRr ? 2 : 3], 1);
+        if (x < nRr) zrr[q] = T; else zrr[nRr + q] = T;
+      }
+    }
+    __syncthreads();
+    const int nx = S.cnt[0], ny = S.cnt[1], nzr = S.cnt[2], nzc = S.cnt[3];
+    __syncthreads();
+    if (nx > 0 && ny > 0) {
+      // products, one per (zone row, zone column) pair
+      for (int p = tid; p < nx * ny; p += NT) {
+        const int px = p / ny, py = p - px * ny;
+        const int x = zx[px], y = zx[mK + py];
+        const double *l = b <= 16 ? WL + (int64_t)kr[ordR[x]] * b : Lsc + (int64_t)(kr[ordR[x]] - b) * b;
+        const double *u = WU + (int64_t)kc[ordC[y]] * b;
+        double d0 = 0.0, d1 = 0.0;
+        int t = 0;
+        for (; t + 1 < b; t += 2) { d0 = fma(l[t], u[t], d0); d1 = fma(l[t + 1], u[t + 1], d1); }
+        if (t < b) d0 = fma(l[t], u[t], d0);
+        const int Ti = rb[x], Tj = cb[y];
+        if (Tj <= Ti)
+          red_add_f64(F.SL + ((size_t)F.zk[Tj] * F.nz + zi[px]) * 8 + (Cs[y] - F.bstart[Tj]), -(d0 + d1));
+        else
+          red_add_f64(F.SU + ((size_t)F.zk[Ti] * F.nz + zi[mK + py]) * 8 + (R[x] - F.bstart[Ti]), -(d0 + d1));
+      }
+      // candidate bits: zone row i in every zone column block T < block(i) of K's columns,
+      // zone column j in every zone row block T < block(j) of K's rows (zone rows / columns
+      // only meet zone blocks: the zone is closed under etree ancestors)
+      for (int p = tid; p < nx * nzc; p += NT) {
+        const int px = p / nzc, T = zrr[nRr + (p - px * nzc)];
+        if (T < rb[zx[px]]) atomicOr(&F.BL[(size_t)F.zk[T] * F.nzw + (zi[px] >> 5)], 1u << (zi[px] & 31));
+      }
+      for (int p = tid; p < ny * nzr; p += NT) {
+        const int py = p / nzr, T = zrr[p - py * nzr];
+        if (T < cb[zx[mK + py]]) atomicOr(&F.BU[(size_t)F.zk[T] * F.nzw + (zi[mK + py] >> 5)], 1u << (zi[mK + py] & 31));
+      }
+      if (tid == 0) atomicAdd((double *)&F.ctrl[CS * CTRL_FLOPS], 2.0 * b * (double)nx * (double)ny);
+    }
+  }
   for (int x = tid; x < nRr; x += NT) {
     const int T = rblk[x];
     const int p = lbound(cblk, 0, nCr, T);
@@ -1777,13 +1861,17 @@ scaled:
   for (int x = tid; x < nRr + nCr + max(nN - 1, 0); x += NT) {
     if (x < nRr) {
       const int r0 = rstart[x], r1 = rstart[x + 1], T = rblk[x];
-      int rec[REC_INTS] = {K, r0, r1, lbound(Cs, 0, cK, F.bstart[T + 1]), 0, 0, 0, 0};
-      list_append(F, F.uc, T, rec);
+      if (F.nzb == 0 || F.zk[T] < 0) {   // zone targets read no contributor lists (their panels are pushed)
+        int rec[REC_INTS] = {K, r0, r1, lbound(Cs, 0, cK, F.bstart[T + 1]), 0, 0, 0, 0};
+        list_append(F, F.uc, T, rec);
+      }
     } else if (x < nRr + nCr) {
       const int y = x - nRr;
       const int c0 = cstart[y], c1 = cstart[y + 1], T = cblk[y];
-      int rec[REC_INTS] = {K, c0, c1, lbound(R, 0, mK, F.bstart[T]), lbound(R, 0, mK, F.bstart[T + 1]), 0, 0, 0};
-      list_append(F, F.lc, T, rec);
+      if (F.nzb == 0 || F.zk[T] < 0) {
+        int rec[REC_INTS] = {K, c0, c1, lbound(R, 0, mK, F.bstart[T]), lbound(R, 0, mK, F.bstart[T + 1]), 0, 0, 0};
+        list_append(F, F.lc, T, rec);
+      }
     } else {
       const int z = x - nRr - nCr;
       atomicAdd(&F.pending[nb[z + 1]], 1);
@@ -1797,20 +1885,305 @@ scaled:
   PROF(7);
 
   // ---------------- a-1: release successors (static adjacency of Ã + chain edges)
-  const int a0 = F.adj_ptr[K], a1 = F.adj_ptr[K + 1];
-  const int nS = __ldcg(&F.succ.cnt[K]);
-  for (int x = tid; x < (a1 - a0) + nS; x += NT) {
-    int T = x < (a1 - a0) ? F.adj[a0 + x] : __ldcg(list_rec(F.succ, K, x - (a1 - a0)));
-    if (atomicSub(&F.pending[T], 1) == 1 && (F.owned == nullptr || F.owned[T])) {
-      unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
-      __threadfence();
-      st_vol(&F.queue[slot], T);
-    }
-  }
-  if (tid == 0) atomicAdd(&F.ctrl[CS * CTRL_DONE], 1ull);
+  release_block(F, K);
   PROF(8);
   PROF_END(0, 0, nR, nC);
 #undef OVF_CHECK
+}
+
+// The whole step of a narrow zone block (b <= 8, no perturbation, at most ZL_MAXLINES
+// candidate lines) with few barriers and memory round trips: gather the panel (a-2..a-5,
+// pushed by the contributors), a-6 pivot inverse, a-7/a-8 scaling, dropping and
+// compaction, the push of K's own update into the zone, the chain edges of the readiness
+// rule and a-1 the release.  Same arithmetic as process_zone_block + finish_block.
+// Returns false (nothing consumed) if the block needs the general path.
+constexpr int ZL_MAXLINES = 1024;
+__device__ __forceinline__ int align16i(int x) { return (x + 15) & ~15; }
+
+__device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned char *smem) {
+  const int tid = threadIdx.x;
+  const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
+  if (b > 8 || F.perturb) return false;
+  const int k = F.zk[K];
+  const int le = F.zloc[s] + b;
+  const int w0 = le >> 5, nw = F.nzw - w0;
+  PROF_T0
+  unsigned char *sp = smem;
+  unsigned *bm = (unsigned *)sp; sp += align16i(2 * nw * 4);
+  int *pre = (int *)sp; sp += align16i((2 * nw + 1) * 4);
+  if ((int)(sp - smem) > F.smem_bytes) return false;
+  unsigned *gL = F.BL + (size_t)k * F.nzw + w0, *gU = F.BU + (size_t)k * F.nzw + w0;
+  for (int w = tid; w < 2 * nw; w += NT) {
+    const unsigned m = __ldcg(w < nw ? gL + w : gU + (w - nw));
+    bm[w] = m;
+    pre[w] = __popc(m);
+  }
+  __syncthreads();
+  const int tot = cta_scan(pre, 2 * nw, S.tmp);
+  const int nR = nw > 0 ? pre[nw] : 0, nC = tot - nR;
+  const int nL = b + nR, nl = nL + nC;
+  // shared-memory plan: lines (zone numbers), W (8 doubles per line), flags / positions, D
+  int *zl = (int *)sp; sp += align16i(nl * 4);
+  int *gb = (int *)sp; sp += align16i(nl * 4);                // block of every line
+  int *fl = (int *)sp; sp += align16i((nR + nC + 1) * 4);      // keep flags -> kept positions
+  int *kl = (int *)sp; sp += align16i((nR + nC + 1) * 4);      // kept lines (L then U)
+  int *run = (int *)sp; sp += align16i((nR + nC + 2) * 4);     // row / column runs
+  int *nb = (int *)sp; sp += align16i((nR + nC + 2) * 4);      // N(K)
+  double *D = (double *)sp; sp += 64 * 8;
+  int *ipiv = (int *)sp; sp += 64;
+  double *fcol = (double *)sp; sp += 24 * 8;
+  double *W = (double *)sp; sp += (size_t)nl * 64;
+  if (nl > ZL_MAXLINES || (int)(sp - smem) > F.smem_bytes) return false;
+  // committed: clear the bitmap words behind us
+  for (int w = tid; w < 2 * nw; w += NT)
+    if (bm[w]) *(w < nw ? gL + w : gU + (w - nw)) = 0u;
+  for (int x = tid; x < b; x += NT) zl[x] = le - b + x;
+  for (int w = tid; w < 2 * nw; w += NT) {
+    unsigned m = bm[w];
+    int at = w < nw ? b + pre[w] : nL + (pre[w] - nR);
+    const int base = (w0 + (w < nw ? w : w - nw)) << 5;
+    while (m) { const int bit = __ffs(m) - 1; zl[at++] = base + bit; m &= m - 1; }
+  }
+  __syncthreads();
+  // gather the lines (64 B each, 16-byte loads, all in flight) and zero them behind
+  for (int ln = tid; ln < nl; ln += NT) {
+    double2 *src = (double2 *)((ln < nL ? F.SL : F.SU) + ((size_t)k * F.nz + zl[ln]) * 8);
+    double2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __ldcg(src + q);
+    const int g = F.zblkof[zl[ln]];
+    double2 *dst = (double2 *)(W + (size_t)ln * 8);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { dst[q] = v[q]; src[q] = make_double2(0.0, 0.0); }
+    gb[ln] = g;
+  }
+  __syncthreads();
+  PROF(2);
+  // a-6: D_K = P_K^{-1} (P column-major from the pivot lines; gj_invert: warp 0, R6)
+  for (int x = tid; x < b * b; x += NT) D[x] = W[(x % b) * 8 + x / b];
+  __syncthreads();
+  if (gj_invert(D, b, ipiv, fcol, S)) { if (tid == 0) raise_abort(F, DEV_BREAKDOWN, K); return true; }
+  {
+    double *Dg = F.D + F.D_off[K];
+    for (int x = tid; x < b * b; x += NT) Dg[x] = D[x];
+  }
+  PROF(5);
+  // a-7/a-8: l = w D_K (kept iff max|l| > tau, stored scaled), u = D_K z (kept iff max|u| > tau,
+  // Ũ stores z); near-threshold decisions logged (R1-R3, R15)
+  const double tau = F.tau;
+  for (int x = tid; x < nR + nC; x += NT) {
+    const bool Lside = x < nR;
+    double *w = W + (size_t)(Lside ? b + x : nL + (x - nR)) * 8;
+    double wr[8], o[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) wr[t] = t < b ? w[t] : 0.0;
+    double mx = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (t < b && c < b) acc = fma(wr[t], Lside ? D[t + c * b] : D[c + t * b], acc);
+      o[c] = acc;
+      mx = fmax(mx, fabs(acc));
+    }
+    if (Lside) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) if (c < b) w[c] = o[c];
+    }
+    const int keep = mx > tau;
+    fl[x] = keep;
+    if (tau > 0.0) {
+      const double margin = fabs(mx / tau - 1.0);
+      if (margin <= F.near_rel) {
+        unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_NEAR], 1ull);
+        if (slot < (unsigned long long)F.near_cap) {
+          F.near_i[4 * slot] = K; F.near_i[4 * slot + 1] = Lside ? 0 : 1;
+          F.near_i[4 * slot + 2] = F.zglob[zl[Lside ? b + x : nL + (x - nR)]]; F.near_i[4 * slot + 3] = keep;
+          F.near_m[slot] = margin;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int nk = cta_scan(fl, nR + nC, S.tmp);
+  const int mK = nR > 0 ? (nC > 0 ? fl[nR] : nk) : 0, cK = nk - mK;
+  for (int x = tid; x < nR + nC; x += NT) {
+    const int nxt = x + 1 < nR + nC ? fl[x + 1] : nk;
+    if (nxt > fl[x]) kl[fl[x]] = x < nR ? b + x : nL + (x - nR);
+  }
+  if (tid < 5) {
+    const unsigned long long amt[5] = {((unsigned long long)mK + 31) & ~31ull, ((unsigned long long)mK * b + 15) & ~15ull,
+                                       ((unsigned long long)cK + 31) & ~31ull, ((unsigned long long)cK * b + 15) & ~15ull,
+                                       (unsigned long long)(nR + nC)};
+    const int which[5] = {CTRL_CUR_LIDX, CTRL_CUR_LVAL, CTRL_CUR_UIDX, CTRL_CUR_UVAL, CTRL_NDEC};
+    const unsigned long long o = atomicAdd(&F.ctrl[CS * which[tid]], amt[tid]);
+    if (tid < 4) S.off[tid] = o;
+  }
+  __syncthreads();
+  if (S.off[0] + mK > (unsigned long long)F.cap_Lidx || S.off[1] + (unsigned long long)mK * b > (unsigned long long)F.cap_Lval ||
+      S.off[2] + cK > (unsigned long long)F.cap_Uidx || S.off[3] + (unsigned long long)cK * b > (unsigned long long)F.cap_Uval) {
+    if (tid == 0) raise_abort(F, DEV_OVF_ARENA, K);
+    return true;
+  }
+  const int64_t oLi = (int64_t)S.off[0], oLv = (int64_t)S.off[1], oUi = (int64_t)S.off[2], oUv = (int64_t)S.off[3];
+  for (int x = tid; x < nk; x += NT) {
+    const int ln = kl[x], g = F.zglob[zl[ln]];
+    if (x < mK) F.Lidx[oLi + x] = g; else F.Uidx[oUi + (x - mK)] = g;
+  }
+  for (int it = tid; it < nk * b; it += NT) {
+    const int x = it / b, c = it - x * b;
+    const double v = W[(size_t)kl[x] * 8 + c];
+    if (x < mK) F.Lval[oLv + it] = v; else F.Uval[oUv + (it - mK * b)] = v;
+  }
+  if (tid == 0) {
+    F.Lrow_off[K] = oLi; F.Lm[K] = mK; F.Lval_off[K] = oLv;
+    F.Ucol_off[K] = oUi; F.Uc[K] = cK; F.Uval_off[K] = oUv;
+    F.blk_ncand[2 * K] = nR; F.blk_ncand[2 * K + 1] = nC;
+  }
+  PROF(6);
+  // push K's update into the zone (every kept row / column of a zone block is a zone unknown)
+  for (int p = tid; p < mK * cK; p += NT) {
+    const int x = p / cK, y = p - x * cK;
+    const int lx = kl[x], ly = kl[mK + y];
+    const double *l = W + (size_t)lx * 8, *u = W + (size_t)ly * 8;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      if (t < b) d0 = fma(l[t], u[t], d0);
+      if (t + 1 < b) d1 = fma(l[t + 1], u[t + 1], d1);
+    }
+    const int Ti = gb[lx], Tj = gb[ly];
+    if (Tj <= Ti)
+      red_add_f64(F.SL + ((size_t)F.zk[Tj] * F.nz + zl[lx]) * 8 + (F.zglob[zl[ly]] - F.bstart[Tj]), -(d0 + d1));
+    else
+      red_add_f64(F.SU + ((size_t)F.zk[Ti] * F.nz + zl[ly]) * 8 + (F.zglob[zl[lx]] - F.bstart[Ti]), -(d0 + d1));
+  }
+  // runs of the kept rows / columns by block (sorted): run[r] = start of run r
+  for (int x = tid; x < nk; x += NT) {
+    const bool first = (x == 0 || x == mK) ? true : gb[kl[x]] != gb[kl[x - 1]];
+    fl[x] = first ? 1 : 0;
+  }
+  __syncthreads();
+  const int nrun = cta_scan(fl, nk, S.tmp);
+  for (int x = tid; x < nk; x += NT) {
+    const bool first = (x == 0 || x == mK) ? true : gb[kl[x]] != gb[kl[x - 1]];
+    if (first) run[fl[x]] = x;
+  }
+  if (tid == 0) run[nrun] = nk;
+  __syncthreads();
+  const int nrr = mK > 0 ? (cK > 0 ? fl[mK] : nrun) : 0;     // row runs, then column runs
+  // candidate bits: zone row i of every column-run block T < block(i); zone column j of every
+  // row-run block T < block(j)
+  for (int p = tid; p < mK * (nrun - nrr); p += NT) {
+    const int x = p / (nrun - nrr), r = nrr + (p - x * (nrun - nrr));
+    const int T = gb[kl[run[r]]], zi = zl[kl[x]];
+    if (T < gb[kl[x]]) atomicOr(&F.BL[(size_t)F.zk[T] * F.nzw + (zi >> 5)], 1u << (zi & 31));
+  }
+  for (int p = tid; p < cK * nrr; p += NT) {
+    const int y = p / nrr, r = p - y * nrr;
+    const int T = gb[kl[run[r]]], zj = zl[kl[mK + y]];
+    if (T < gb[kl[mK + y]]) atomicOr(&F.BU[(size_t)F.zk[T] * F.nzw + (zj >> 5)], 1u << (zj & 31));
+  }
+  // N(K): sorted union of the row-run and column-run blocks; chain edges between neighbours
+  if (tid == 0) {
+    int i = 0, j = nrr, q = 0;
+    while (i < nrr || j < nrun) {
+      const int vi = i < nrr ? gb[kl[run[i]]] : INT_MAX, vj = j < nrun ? gb[kl[run[j]]] : INT_MAX;
+      const int v = min(vi, vj);
+      nb[q++] = v;
+      if (vi == v) ++i;
+      if (vj == v) ++j;
+    }
+    S.cnt[0] = q;
+    const double fl_ = 2.0 * b * b * (double)b + 2.0 * b * b * (double)(nR + nC) + 2.0 * b * (double)mK * (double)cK;
+    F.blk_flops[K] = fl_;
+    atomicAdd((double *)&F.ctrl[CS * CTRL_FLOPS], fl_);
+  }
+  __syncthreads();
+  const int nN = S.cnt[0];
+  for (int z = tid; z + 1 < nN; z += NT) {
+    atomicAdd(&F.pending[nb[z + 1]], 1);
+    int rec1 = nb[z + 1];
+    list_append(F, F.succ, nb[z], &rec1);
+  }
+  __threadfence();
+  __syncthreads();
+  PROF(7);
+  release_block(F, K);
+  PROF(8);
+  PROF_END(0, 0, nR, nC);
+  return true;
+}
+
+// a-2 .. a-5 of a block of the dense trailing zone: when the block is ready
+// every contributor has pushed its update into the block's panel (finish_block), so the
+// block gathers the candidate lines its bitmaps mark -- Ã's entries and the pushed
+// products already summed -- zeroes them behind it (the zone buffers are all zero whenever
+// no factorization runs), and continues with a-6 .. a-1.
+__device__ void process_zone_block(const DevFactor &F, int K, Shared &S, unsigned char *smem) {
+  const int tid = threadIdx.x;
+  const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
+  const int k = F.zk[K];
+  Bump A;
+  A.sbase = smem; A.sused = 0; A.scap = F.smem_bytes; A.stop = F.smem_bytes;
+  A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
+  A.ovf = false; A.bottom_global = false; A.pool = false;
+  PROF_T0
+  const int le = F.zloc[s] + b;                          // zone number of the first unknown >= e_K
+  const int w0 = le >> 5, nw = F.nzw - w0;                // bitmap words of the zone unknowns >= e_K
+  unsigned *bm = (unsigned *)balloc_top(A, (int64_t)(2 * nw + 2) * 4);
+  int *pre = (int *)balloc_top(A, (int64_t)(2 * nw + 2) * 4);
+  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
+  unsigned *gL = F.BL + (size_t)k * F.nzw + w0, *gU = F.BU + (size_t)k * F.nzw + w0;
+  for (int w = tid; w < 2 * nw; w += NT) {
+    unsigned *g = w < nw ? gL + w : gU + (w - nw);
+    const unsigned m = __ldcg(g);
+    bm[w] = m;
+    pre[w] = __popc(m);
+    if (m) *g = 0u;
+  }
+  __syncthreads();
+  const int tot = cta_scan(pre, 2 * nw, S.tmp);
+  const int nR = nw > 0 ? pre[nw] : 0, nC = tot - nR;
+  double *WL = (double *)balloc(A, (int64_t)(b + nR) * b * 8);
+  double *WU = (double *)balloc(A, (int64_t)nC * b * 8);
+  int *zlL = (int *)balloc(A, (int64_t)(b + nR + 1) * 4);      // zone numbers of the lines
+  int *zlU = (int *)balloc(A, (int64_t)(nC + 1) * 4);
+  int *lineL = (int *)balloc(A, (int64_t)(b + nR + 1) * 4);    // ... and the unknowns
+  int *lineU = (int *)balloc(A, (int64_t)(nC + 1) * 4);
+  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
+  for (int x = tid; x < b; x += NT) zlL[x] = le - b + x;
+  for (int w = tid; w < 2 * nw; w += NT) {
+    unsigned m = bm[w];
+    const bool u = w >= nw;
+    int at = pre[w] - (u ? nR : 0);
+    const int base = (w0 + (u ? w - nw : w)) << 5;
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      if (u) zlU[at++] = base + bit; else zlL[b + at++] = base + bit;
+      m &= m - 1;
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < b + nR + nC; x += NT) {
+    if (x < b + nR) lineL[x] = F.zglob[zlL[x]]; else lineU[x - b - nR] = F.zglob[zlU[x - b - nR]];
+  }
+  // the lines (64 B each in the zone buffers), zeroed behind
+  const int nl = (b + nR + nC) * b;
+  for (int it = tid; it < nl; it += NT) {
+    const int ln = it / b, c = it - ln * b;
+    double *src;
+    if (ln < b + nR) src = F.SL + ((size_t)k * F.nz + zlL[ln]) * 8 + c;
+    else src = F.SU + ((size_t)k * F.nz + zlU[ln - b - nR]) * 8 + c;
+    const double v = __ldcg(src);
+    if (ln < b + nR) WL[it] = v; else WU[it - (b + nR) * b] = v;
+    if (v != 0.0) *src = 0.0;
+  }
+  __syncthreads();
+  PROF(2);
+  A.stop = A.scap; A.gtop = A.gcap;   // release the bitmaps
+  finish_block(F, K, S, A, WL, WU, lineL, lineU, nR, nC, true, true, 0.0);
 }
 
 __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
@@ -1846,8 +2219,14 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
     if (K < 0) break;
     DBGK(K);
     __threadfence();
-    if (K < F.N) process_block(F, K, S, smem);
-    else run_part(F, K, S, smem);
+    if (K < F.N) {
+      if (F.nzb > 0 && F.zk[K] >= 0) {
+        if (!process_zone_lean(F, K, S, smem)) process_zone_block(F, K, S, smem);
+      }
+      else process_block(F, K, S, smem);
+    } else {
+      run_part(F, K, S, smem);
+    }
     __syncthreads();
   }
 }
@@ -2013,6 +2392,30 @@ extern "C" cudaError_t bilu_launch_pack(const DevFactor &F, const PackEntry *tab
 extern "C" cudaError_t bilu_launch_unpack(const DevFactor &F, const unsigned char *buf, const PackEntry *tab,
                                           int count, const int64_t *base, cudaStream_t st) {
   if (count > 0) unpack_kernel<<<count < 2048 ? count : 2048, 256, 0, st>>>(F, buf, tab, count, base);
+  return cudaGetLastError();
+}
+
+// Ã's entries inside the dense trailing zone into the zone panels, with their candidate
+// bits ("load the associated scalar sparse columns of A into block column buffer",
+// PAPER.md:370-371); the buffers are zero before (invariant kept by the zone blocks).
+__global__ void zone_init_kernel(DevFactor F, const int32_t *zblocks) {
+  for (int k = blockIdx.x; k < F.nzb; k += gridDim.x) {
+    const int K = zblocks[k], e = F.bstart[K + 1];
+    for (int64_t p = F.AL_ptr[K] + threadIdx.x; p < F.AL_ptr[K + 1]; p += blockDim.x) {
+      const int rc = F.AL_rc[p], i = rc >> 7, zi = F.zloc[i];
+      F.SL[((size_t)k * F.nz + zi) * 8 + (rc & 127)] = F.AL_val[p];
+      if (i >= e) atomicOr(&F.BL[(size_t)k * F.nzw + (zi >> 5)], 1u << (zi & 31));
+    }
+    for (int64_t p = F.AU_ptr[K] + threadIdx.x; p < F.AU_ptr[K + 1]; p += blockDim.x) {
+      const int rc = F.AU_rc[p], zj = F.zloc[rc >> 7];
+      F.SU[((size_t)k * F.nz + zj) * 8 + (rc & 127)] = F.AU_val[p];
+      atomicOr(&F.BU[(size_t)k * F.nzw + (zj >> 5)], 1u << (zj & 31));
+    }
+  }
+}
+
+extern "C" cudaError_t bilu_launch_zone_init(const DevFactor &F, const int32_t *zblocks, cudaStream_t st) {
+  if (F.nzb > 0) zone_init_kernel<<<F.nzb < 4096 ? F.nzb : 4096, 128, 0, st>>>(F, zblocks);
   return cudaGetLastError();
 }
 

@@ -29,6 +29,7 @@ using namespace bilu;
 
 namespace bilu {
 extern "C" cudaError_t bilu_launch_factor(const DevFactor &F, int grid, cudaStream_t st);
+extern "C" cudaError_t bilu_launch_zone_init(const DevFactor &F, const int32_t *zblocks, cudaStream_t st);
 extern "C" cudaError_t bilu_factor_occupancy(int smem_bytes, int *blocks_per_sm);
 extern "C" cudaError_t bilu_launch_gather(double *dst, const double *src, const int64_t *map,
                                           int64_t n, cudaStream_t st);
@@ -131,6 +132,10 @@ struct bilu_ctx {
   unsigned char *d_mhbig = nullptr; int64_t mhbig_cap = 0;   // merge test: per-CTA global tables
   double flops_local = 0.0, t_local_ms = 0.0;
   double *d_alpha = nullptr;
+  // dense trailing zone
+  bool zone_dirty = false;            // zone buffers may hold data (a launch did not complete)
+  int32_t *d_zblocks = nullptr;       // zone index -> block
+  size_t zone_val_bytes = 0, zone_bit_bytes = 0;
   // GMRES: A's CSR structure (original ordering) and the Krylov workspace
   int64_t *d_rp = nullptr; int32_t *d_ci = nullptr;
   double *d_kry = nullptr; int64_t kry_cap = 0;
@@ -538,6 +543,88 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   ALLOC(F.Lrow_off, n_blocks); ALLOC(F.Lm, n_blocks); ALLOC(F.Lval_off, n_blocks);
   ALLOC(F.Ucol_off, n_blocks); ALLOC(F.Uc, n_blocks); ALLOC(F.Uval_off, n_blocks);
   ALLOC(F.D, h->D_off[n_blocks]);
+  // ---- dense zone: the top of the block elimination tree of sym(Ã).  The
+  // exact-LU structure of a block column / row lies on its etree path to the root, so a set of
+  // blocks closed under etree ancestors holds every row / column its blocks can ever have.
+  // Blocks are taken by decreasing etree-subtree size (a parent's is larger than its child's,
+  // so every prefix is ancestor-closed) while they are at most 8 wide and the panel buffers
+  // (2 x 64 B x zone blocks x zone unknowns) fit the budget.
+  F.nzb = 0; F.nz = 0; F.nzw = 0;
+  F.zk = F.zloc = F.zglob = F.zblkof = nullptr;
+  F.SL = F.SU = nullptr; F.BL = F.BU = nullptr;
+  if (opt.zone_bytes >= 0 && n_blocks >= 2) {
+    std::vector<int32_t> par(n_blocks, -1), anc(n_blocks, -1);
+    {
+      // Liu's etree algorithm over the lower neighbours of every block (edges sorted by (a, b))
+      std::vector<int32_t> lp(n_blocks + 1, 0), lo;
+      for (uint64_t eg : edges) lp[(uint32_t)eg + 1]++;
+      for (int32_t K = 0; K < n_blocks; ++K) lp[K + 1] += lp[K];
+      lo.assign(edges.size(), 0);
+      std::vector<int32_t> fill(lp.begin(), lp.end() - 1);
+      for (uint64_t eg : edges) lo[fill[(uint32_t)eg]++] = (int32_t)(eg >> 32);
+      for (int32_t K = 0; K < n_blocks; ++K)
+        for (int32_t q = lp[K]; q < lp[K + 1]; ++q) {
+          int32_t r = lo[q];
+          while (anc[r] != -1 && anc[r] != K) { const int32_t nx = anc[r]; anc[r] = K; r = nx; }
+          if (anc[r] == -1) { anc[r] = K; par[r] = K; }
+        }
+    }
+    std::vector<int64_t> sub(n_blocks, 0);
+    for (int32_t K = 0; K < n_blocks; ++K) {
+      sub[K] += bstart[K + 1] - bstart[K];
+      if (par[K] >= 0) sub[par[K]] += sub[K];
+    }
+    std::vector<int32_t> order(n_blocks);
+    for (int32_t K = 0; K < n_blocks; ++K) order[K] = K;
+    std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return sub[x] != sub[y] ? sub[x] > sub[y] : x > y; });
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const double budget = opt.zone_bytes > 0 ? (double)opt.zone_bytes : std::min(6.0 * (1ull << 30), 0.25 * (double)fr);
+    int64_t nzb = 0, nz = 0;
+    for (int32_t x = 0; x < n_blocks; ++x) {
+      const int32_t K = order[x], bK = bstart[K + 1] - bstart[K];
+      if (bK > 8) break;
+      const double bytes = 2.0 * (nzb + 1) * (double)(nz + bK) * 64.0 + 2.0 * (nzb + 1) * (double)((nz + bK + 31) / 32) * 4.0;
+      if (bytes > budget) break;
+      nzb++; nz += bK;
+    }
+    if (nzb >= 2) {
+      std::vector<int32_t> zblocks(order.begin(), order.begin() + nzb);
+      std::sort(zblocks.begin(), zblocks.end());
+      std::vector<int32_t> zk(n_blocks, -1), zloc(n, -1), zglob;
+      zglob.reserve(nz);
+      for (int32_t k = 0; k < (int32_t)nzb; ++k) zk[zblocks[k]] = k;
+      for (int32_t K : zblocks)
+        for (int32_t i = bstart[K]; i < bstart[K + 1]; ++i) { zloc[i] = (int32_t)zglob.size(); zglob.push_back(i); }
+      const int64_t nzw = (nz + 31) / 32;
+      double *sl = nullptr, *su = nullptr;
+      unsigned *bl = nullptr, *bu = nullptr;
+      int32_t *dzk = nullptr, *dzl = nullptr, *dzg = nullptr, *dzb = nullptr, *dzo = nullptr;
+      if (dalloc(h, &sl, (size_t)(nzb * nz * 8)) == cudaSuccess && dalloc(h, &su, (size_t)(nzb * nz * 8)) == cudaSuccess &&
+          dalloc(h, &bl, (size_t)(nzb * nzw)) == cudaSuccess && dalloc(h, &bu, (size_t)(nzb * nzw)) == cudaSuccess &&
+          dalloc(h, &dzk, (size_t)n_blocks) == cudaSuccess && dalloc(h, &dzl, (size_t)n) == cudaSuccess &&
+          dalloc(h, &dzg, (size_t)nz) == cudaSuccess && dalloc(h, &dzb, (size_t)nzb) == cudaSuccess &&
+          dalloc(h, &dzo, (size_t)nz) == cudaSuccess) {
+        std::vector<int32_t> zbo(nz);
+        for (int64_t z = 0; z < nz; ++z) zbo[z] = block_of[zglob[z]];
+        cudaMemcpy(dzo, zbo.data(), nz * sizeof(int32_t), cudaMemcpyHostToDevice);
+        F.zblkof = dzo;
+        h->zone_val_bytes = (size_t)(nzb * nz * 8) * sizeof(double);
+        h->zone_bit_bytes = (size_t)(nzb * nzw) * sizeof(unsigned);
+        cudaMemset(sl, 0, h->zone_val_bytes); cudaMemset(su, 0, h->zone_val_bytes);
+        cudaMemset(bl, 0, h->zone_bit_bytes); cudaMemset(bu, 0, h->zone_bit_bytes);
+        cudaMemcpy(dzk, zk.data(), n_blocks * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(dzl, zloc.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(dzg, zglob.data(), nz * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(dzb, zblocks.data(), nzb * sizeof(int32_t), cudaMemcpyHostToDevice);
+        F.nzb = (int)nzb; F.nz = (int)nz; F.nzw = (int)nzw;
+        F.zk = dzk; F.zloc = dzl; F.zglob = dzg; h->d_zblocks = dzb;
+        F.SL = sl; F.SU = su; F.BL = bl; F.BU = bu;
+      } else {
+        cudaGetLastError();   // no zone if it does not fit (the buffers allocated so far stay owned)
+      }
+    }
+  }
   ALLOC(F.blk_flops, n_blocks);
   ALLOC(F.blk_ncand, 2 * (size_t)n_blocks);
   ALLOC(F.lc.cnt, n_blocks); ALLOC(F.uc.cnt, n_blocks); ALLOC(F.succ.cnt, n_blocks);
@@ -917,6 +1004,17 @@ static bilu_status run_phase(bilu_ctx *h, Phase ph, bilu_factor_stats &S, unsign
       CUDA_TRY(h, cudaMemsetAsync(F.hpool, 0, (size_t)std::min(h->hpool_dirty, F.hpool_cap) * 8, h->stream));
       h->hpool_dirty = 0;
     }
+    if (F.nzb > 0) {            // dense zone: Ã's entries in (zero buffers)
+      if (h->zone_dirty) {
+        CUDA_TRY(h, cudaMemsetAsync(F.SL, 0, h->zone_val_bytes, h->stream));
+        CUDA_TRY(h, cudaMemsetAsync(F.SU, 0, h->zone_val_bytes, h->stream));
+        CUDA_TRY(h, cudaMemsetAsync(F.BL, 0, h->zone_bit_bytes, h->stream));
+        CUDA_TRY(h, cudaMemsetAsync(F.BU, 0, h->zone_bit_bytes, h->stream));
+      }
+      CUDA_TRY(h, bilu_launch_zone_init(F, h->d_zblocks, h->stream));
+      launches += 1;
+      h->zone_dirty = true;
+    }
     CUDA_TRY(h, bilu_launch_factor(F, h->grid, h->stream));
     launches += 1;
     if (dbg_env) {
@@ -940,6 +1038,7 @@ static bilu_status run_phase(bilu_ctx *h, Phase ph, bilu_factor_stats &S, unsign
     h->hpool_dirty = std::min<int64_t>((int64_t)ctrl[CTRL_HPOOL], F.hpool_cap);
     const int code = (int)ctrl[CTRL_ABORT];
     if (code == DEV_OK) {
+      if (ctrl[CTRL_DONE] == (unsigned long long)F.n_target) h->zone_dirty = false;   // every zone block consumed its panel
       if (ctrl[CTRL_DONE] != (unsigned long long)F.n_target) {
         set_err(h, "bilu_factor: schedule finished %llu of %lld blocks", ctrl[CTRL_DONE], (long long)F.n_target);
         return BILU_ERR_STATE;
@@ -1028,6 +1127,8 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
   bilu_factor_stats S{};
   S.breakdown_block = -1;
   S.n_blocks_init = h->N;
+  S.zone_blocks = h->F.nzb;
+  S.zone_unknowns = h->F.nzb > 0 ? h->F.nz : 0;
   Events ev;
   for (auto &x : ev.e) CUDA_TRY(h, cudaEventCreate(&x));
   h->factored = false;
@@ -1048,6 +1149,7 @@ extern "C" bilu_status bilu_dist_setup(bilu_ctx *h, const int32_t *owner, int32_
   const int N = h->N;
   h->owner.assign(owner, owner + N);
   h->rank = rank;
+  h->F.nzb = 0;   // the distributed phases run the contributor-list path only
   h->own_list.clear(); h->sep_list.clear();
   for (int K = 0; K < N; ++K) {
     if (owner[K] < -1) { set_err(h, "bilu_dist_setup: owner[%d] = %d < -1", K, owner[K]); return BILU_ERR_ARG; }
@@ -1108,6 +1210,8 @@ extern "C" bilu_status bilu_factor_local(bilu_ctx *h, double tau, bilu_factor_st
   bilu_factor_stats S{};
   S.breakdown_block = -1;
   S.n_blocks_init = h->N;
+  S.zone_blocks = h->F.nzb;
+  S.zone_unknowns = h->F.nzb > 0 ? h->F.nz : 0;
   Events ev;
   for (auto &x : ev.e) CUDA_TRY(h, cudaEventCreate(&x));
   h->factored = false;
@@ -1273,6 +1377,8 @@ extern "C" bilu_status bilu_factor_separators(bilu_ctx *h, bilu_factor_stats *st
   bilu_factor_stats S{};
   S.breakdown_block = -1;
   S.n_blocks_init = h->N;
+  S.zone_blocks = h->F.nzb;
+  S.zone_unknowns = h->F.nzb > 0 ? h->F.nz : 0;
   Events ev;
   for (auto &x : ev.e) CUDA_TRY(h, cudaEventCreate(&x));
   int launches = 0;

@@ -118,6 +118,19 @@ struct DevFactor {
   int perturb; double ptau, prho, cond_max;
   const double *alpha;                  // device scalar: max |a_ij|
   int exp;                              // experiment switches (diagnostics only)
+  // dense zone: the top blocks of the block elimination tree (a set closed
+  // under ancestors, every block at most 8 wide) keep their panels in dense per-block
+  // buffers that their contributors update when THEY finish (a right-looking push), so a
+  // ready zone block only gathers its own panel.  The zone's nz unknowns are numbered
+  // 0..nz-1 in increasing order (zloc / zglob); nzb = 0: no zone.
+  //   zk[K]        zone index of block K, or -1
+  //   SL[(zk[K] * nz + zloc[i]) * 8 + c]  entry (i, s_K + c) of block column K (i >= s_K)
+  //   SU[(zk[K] * nz + zloc[j]) * 8 + r]  entry (s_K + r, j) of block row K    (j >= e_K)
+  //   BL / BU[zk[K] * nzw + w]            candidate rows / columns (bit = zone index)
+  int nzb, nz, nzw;
+  const int32_t *zk, *zloc, *zglob, *zblkof;   // zblkof[z] = block of zone unknown z
+  double *SL, *SU;
+  unsigned *BL, *BU;
 };
 
 struct MergeArgs {
