@@ -244,6 +244,7 @@ __device__ __forceinline__ void *balloc_top(Bump &A, int64_t bytes) {
 // --------------------------------------------------------------- the kernel
 struct Shared {
   int K;
+  int next;              // block made ready by this CTA, run next (release_block)
   int tmp[NW + 1];
   int piv;
   double pivd;
@@ -867,19 +868,45 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
 
 // a-1: release the blocks that wait for K (static adjacency of Ã + chain edges); K's writes
 // are fenced by the caller
-__device__ void release_block(const DevFactor &F, int K) {
+// The CTA keeps the first block it makes ready and runs it next (S.next), without a trip
+// through the queue: a dependency chain advances on one SM as soon as its predecessor is
+// done instead of waiting behind the blocks queued before it.
+// Among the blocks K makes ready, the CTA keeps the one with the largest etree subtree (the
+// one nearest the root: the long dependency chains run through the separators) and pushes
+// the others.
+__device__ void release_block(const DevFactor &F, int K, Shared &S) {
   const int tid = threadIdx.x;
   const int a0 = F.adj_ptr[K], a1 = F.adj_ptr[K + 1];
   const int nS = __ldcg(&F.succ.cnt[K]);
+  if (tid == 0) { S.cnt[0] = 0; S.off[0] = 0ull; }
+  __syncthreads();
+  int mine = -1;
   for (int x = tid; x < (a1 - a0) + nS; x += NT) {
     int T = x < (a1 - a0) ? F.adj[a0 + x] : __ldcg(list_rec(F.succ, K, x - (a1 - a0)));
     if (atomicSub(&F.pending[T], 1) == 1 && (F.owned == nullptr || F.owned[T])) {
-      unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
-      __threadfence();
-      st_vol(&F.queue[slot], T);
+      if (mine >= 0) {   // a thread that releases two keeps the better candidate, pushes the other
+        const int worse = F.prio[mine] >= F.prio[T] ? T : mine;
+        mine = worse == T ? mine : T;
+        unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
+        __threadfence();
+        st_vol(&F.queue[slot], worse);
+      } else {
+        mine = T;
+      }
     }
   }
-  if (tid == 0) atomicAdd(&F.ctrl[CS * CTRL_DONE], 1ull);
+  if (mine >= 0) atomicMax(&S.off[0], ((unsigned long long)(unsigned)F.prio[mine] << 32) | (unsigned)mine);
+  __syncthreads();
+  const unsigned long long best = S.off[0];
+  if (mine >= 0 && (best == 0ull || (int)(best & 0xffffffffu) != mine)) {
+    unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
+    __threadfence();
+    st_vol(&F.queue[slot], mine);
+  }
+  if (tid == 0) {
+    if (best != 0ull) S.next = (int)(best & 0xffffffffu);
+    atomicAdd(&F.ctrl[CS * CTRL_DONE], 1ull);
+  }
 }
 
 // the destination line of every item of one side, into the global pool (split wide blocks)
@@ -1885,7 +1912,7 @@ scaled:
   PROF(7);
 
   // ---------------- a-1: release successors (static adjacency of Ã + chain edges)
-  release_block(F, K);
+  release_block(F, K, S);
   PROF(8);
   PROF_END(0, 0, nR, nC);
 #undef OVF_CHECK
@@ -2110,7 +2137,7 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
   __threadfence();
   __syncthreads();
   PROF(7);
-  release_block(F, K);
+  release_block(F, K, S);
   PROF(8);
   PROF_END(0, 0, nR, nC);
   return true;
@@ -2189,6 +2216,7 @@ __device__ void process_zone_block(const DevFactor &F, int K, Shared &S, unsigne
 __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Shared S;
+  if (threadIdx.x == 0) S.next = -1;
   __syncthreads();
   while (true) {
     if (threadIdx.x == 0) {
@@ -2196,7 +2224,9 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
       long long _w0 = clock64();
 #endif
       int K = -1;
-      unsigned long long idx = aborted(F) ? ~0ull : atomicAdd(&F.ctrl[CS * CTRL_QTAIL], 1ull);
+      unsigned long long idx = ~0ull;
+      if (S.next >= 0) { K = S.next; S.next = -1; }                // continuation (release_block)
+      else idx = aborted(F) ? ~0ull : atomicAdd(&F.ctrl[CS * CTRL_QTAIL], 1ull);
       if (idx < (unsigned long long)F.qcap) {
         unsigned ns = 32, polls = 0;
         while (true) {

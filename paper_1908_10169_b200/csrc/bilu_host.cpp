@@ -543,6 +543,36 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   ALLOC(F.Lrow_off, n_blocks); ALLOC(F.Lm, n_blocks); ALLOC(F.Lval_off, n_blocks);
   ALLOC(F.Ucol_off, n_blocks); ALLOC(F.Uc, n_blocks); ALLOC(F.Uval_off, n_blocks);
   ALLOC(F.D, h->D_off[n_blocks]);
+  // ---- block elimination tree of sym(Ã) (Liu's algorithm over the lower neighbours of every
+  // block; edges are sorted by (a, b)) and the subtree sizes in unknowns
+  std::vector<int32_t> par(n_blocks, -1);
+  {
+    std::vector<int32_t> anc(n_blocks, -1), lp(n_blocks + 1, 0), lo(edges.size(), 0);
+    for (uint64_t eg : edges) lp[(uint32_t)eg + 1]++;
+    for (int32_t K = 0; K < n_blocks; ++K) lp[K + 1] += lp[K];
+    std::vector<int32_t> fill(lp.begin(), lp.end() - 1);
+    for (uint64_t eg : edges) lo[fill[(uint32_t)eg]++] = (int32_t)(eg >> 32);
+    for (int32_t K = 0; K < n_blocks; ++K)
+      for (int32_t q = lp[K]; q < lp[K + 1]; ++q) {
+        int32_t r = lo[q];
+        while (anc[r] != -1 && anc[r] != K) { const int32_t nx = anc[r]; anc[r] = K; r = nx; }
+        if (anc[r] == -1) { anc[r] = K; par[r] = K; }
+      }
+  }
+  std::vector<int64_t> sub(n_blocks, 0);
+  for (int32_t K = 0; K < n_blocks; ++K) {
+    sub[K] += bstart[K + 1] - bstart[K];
+    if (par[K] >= 0) sub[par[K]] += sub[K];
+  }
+  {
+    // continuation priority of release_block: the etree subtree size
+    std::vector<int32_t> pr(n_blocks);
+    for (int32_t K = 0; K < n_blocks; ++K) pr[K] = (int32_t)std::min<int64_t>(sub[K], INT32_MAX);
+    int32_t *dpr = nullptr;
+    ALLOC(dpr, n_blocks);
+    cudaMemcpy(dpr, pr.data(), n_blocks * sizeof(int32_t), cudaMemcpyHostToDevice);
+    F.prio = dpr;
+  }
   // ---- dense zone: the top of the block elimination tree of sym(Ã).  The
   // exact-LU structure of a block column / row lies on its etree path to the root, so a set of
   // blocks closed under etree ancestors holds every row / column its blocks can ever have.
@@ -553,27 +583,6 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   F.zk = F.zloc = F.zglob = F.zblkof = nullptr;
   F.SL = F.SU = nullptr; F.BL = F.BU = nullptr;
   if (opt.zone_bytes >= 0 && n_blocks >= 2) {
-    std::vector<int32_t> par(n_blocks, -1), anc(n_blocks, -1);
-    {
-      // Liu's etree algorithm over the lower neighbours of every block (edges sorted by (a, b))
-      std::vector<int32_t> lp(n_blocks + 1, 0), lo;
-      for (uint64_t eg : edges) lp[(uint32_t)eg + 1]++;
-      for (int32_t K = 0; K < n_blocks; ++K) lp[K + 1] += lp[K];
-      lo.assign(edges.size(), 0);
-      std::vector<int32_t> fill(lp.begin(), lp.end() - 1);
-      for (uint64_t eg : edges) lo[fill[(uint32_t)eg]++] = (int32_t)(eg >> 32);
-      for (int32_t K = 0; K < n_blocks; ++K)
-        for (int32_t q = lp[K]; q < lp[K + 1]; ++q) {
-          int32_t r = lo[q];
-          while (anc[r] != -1 && anc[r] != K) { const int32_t nx = anc[r]; anc[r] = K; r = nx; }
-          if (anc[r] == -1) { anc[r] = K; par[r] = K; }
-        }
-    }
-    std::vector<int64_t> sub(n_blocks, 0);
-    for (int32_t K = 0; K < n_blocks; ++K) {
-      sub[K] += bstart[K + 1] - bstart[K];
-      if (par[K] >= 0) sub[par[K]] += sub[K];
-    }
     std::vector<int32_t> order(n_blocks);
     for (int32_t K = 0; K < n_blocks; ++K) order[K] = K;
     std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return sub[x] != sub[y] ? sub[x] > sub[y] : x > y; });

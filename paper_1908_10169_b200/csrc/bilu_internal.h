@@ -79,6 +79,7 @@ struct DevFactor {
   const int32_t *adj_ptr; const int32_t *adj;
   int32_t *pending;          // [N]
   int32_t *queue;            // [qcap]: block ids (< N) and part tasks (>= N) of split heavy blocks
+  const int32_t *prio;       // [N] continuation priority: etree subtree size (unknowns), >= 1
   int64_t qcap;
   unsigned long long *ctrl;  // [CTRL_COUNT * CS]
   // factors (per original block)

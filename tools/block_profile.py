@@ -8,7 +8,8 @@ from paper_1908_10169_b200 import BILU
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 P = make_config(name)
 nct = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm, aggregate=0, n_ctas=nct)
+zb = int(float(sys.argv[3]) * (1 << 30)) if len(sys.argv) > 3 else 0
+g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm, aggregate=0, n_ctas=nct, zone_bytes=zb)
 N = len(P.block_sizes)
 buf = torch.zeros(N * 32, dtype=torch.int64, device="cuda")
 g.lib.bilu_prof_set_blk(ctypes.c_void_p(buf.data_ptr()))

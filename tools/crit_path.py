@@ -109,3 +109,14 @@ if len(sys.argv) > 4:
     names = ["contrib", "Lprep", "Uprep", "upd", "pivot", "drop", "reg", "release"]
     print("  zone path phases", {k: round(float(ph[path[mm], i].mean()), 1) for i, k in enumerate(names)})
     print("  non-zone path phases", {k: round(float(ph[path[~mm], i].mean()), 1) for i, k in enumerate(names)})
+if len(sys.argv) > 4:
+    g2 = np.concatenate([[0], gaps])
+    big = np.argsort(-g2)[:15]
+    print("  largest gaps on the path (start ms, gap us, zone?):", [(round(st[path[i]] / 1e3, 2), round(g2[i], 1), bool(z[path[i]])) for i in sorted(big)])
+    tt = st[path] / 1e3
+    for lo, hi in ((0, 10), (10, 20), (20, 30), (30, 60)):
+        m2 = (tt >= lo) & (tt < hi)
+        print("  path blocks starting in [%d, %d) ms: %d, gaps %.2f ms, block time %.2f ms" % (lo, hi, m2.sum(), g2[m2].sum() / 1e3, durs[m2].sum() / 1e3))
+    # concurrency over time
+    ts = np.linspace(0, en.max(), 12)
+    print("  active blocks:", [int(((st <= t) & (en > t)).sum()) for t in ts])
