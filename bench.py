@@ -199,6 +199,42 @@ def cpu_baseline(P, budget_s=30.0):
                       % (len(times), P.name, t, flops)}
 
 
+def time_config(name, steps, warmup, flush):
+    """Device time of the other BASELINE configs' factorizations at N = 1 (extra keys of the
+    bench line; c2 stays the headline): same protocol as the headline (warm-up, L2 flush,
+    CUDA events around bilu_factor), inputs resident in HBM."""
+    import torch
+    from inputs.configs import make_config
+    from paper_1908_10169_b200 import BILU
+    t0 = time.time()
+    P = make_config(name)
+    g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm)
+    prep_s = time.time() - t0
+    for _ in range(warmup):
+        g.factor(P.tau)
+    ms, kms = [], []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = g.factor(P.tau)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        kms.append(st["t_factor_ms"] - st["t_merge_ms"])
+    g.close()
+    t, tk = float(np.mean(ms)), float(np.mean(kms))
+    tf = st["flops"] / (tk * 1e-3) / 1e12
+    return {"ms_per_step": t, "factorizations_per_s": 1e3 / t, "steps": steps, "warmup": warmup,
+            "gflops": st["flops"] / (t * 1e-3) / 1e9, "flops_per_factorization": st["flops"],
+            "n": P.n, "nnz": P.nnz, "blocks_init": int(len(P.block_sizes)), "blocks_final": int(st["n_blocks_final"]),
+            "zone_blocks": int(st["zone_blocks"]),
+            "roofline": {"bound": "tensor", "kernel": "factor_kernel", "achieved": tf, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": tf / FP64_PEAK_TFLOPS, "kernel_ms": tk},
+            "generate_and_analyze_s": prep_s}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -209,6 +245,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the c3/c4/c5 factor timings (extra keys)")
     ap.add_argument("--dist", action="store_true",
                     help="use the distributed (subtree) path even at N=1 (checks its mechanics on one GPU)")
     args = ap.parse_args()
@@ -373,6 +410,8 @@ def main():
                             "apply_ms": ea0.elapsed_time(ea1) / 5}
         if dist_apply is not None:
             out["solve"] = dist_apply
+        if not use_dist and not args.no_extra:
+            out["extra_configs"] = {c: time_config(c, args.steps, args.warmup, flush) for c in ("c3", "c4", "c5")}
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(P)
         print(json.dumps(out), flush=True)

@@ -80,7 +80,7 @@ typedef struct {
    * bytes keeps its block columns / rows in those buffers; its contributors push their
    * Schur updates there when they finish (same products, another summation order), so a
    * ready block of the suffix (the top separators of a nested dissection) reads only its
-   * own panel.  0 = default budget (min(6 GiB, 1/4 of free memory)), < 0 = off.  Ignored
+   * own panel.  0 = default budget (min(24 GiB, 1/4 of free memory)), < 0 = off.  Ignored
    * by the distributed factorization. */
   int64_t zone_bytes;
 } bilu_options;
@@ -312,6 +312,28 @@ bilu_status bilu_ilu1_blocks(int32_t n, const int64_t *row_ptr, const int32_t *c
 bilu_status bilu_cosine_blocks(int32_t n, const int64_t *row_ptr, const int32_t *col_idx, double tau, int32_t max_size,
                                int32_t device, void *stream, int32_t *q, int32_t *block_sizes, int32_t *n_blocks,
                                int32_t *n_kernel_launches);
+
+/*
+ * bilu_mwm -- Sec. 3.1 preprocessing on the device (reading in DESIGN.md R22):
+ * the maximum product transversal of A and its scalings, so that D_l A D_r Pi has unit
+ * diagonal and off-diagonal entries of modulus at most 1 (the matching + scaling the paper
+ * applies before the reordering; MC64's column-normalised costs
+ * c_ij = log(max_k |a_kj|) - log|a_ij| on the stored nonzeros, explicit zeros excluded).
+ *   n, row_ptr, col_idx, val   HOST CSR of A as in bilu_analyze (values required)
+ *   device, stream   CUDA device ordinal and cudaStream_t (NULL = legacy default stream)
+ *   sigma       HOST int32[n]: sigma[i] = column matched to row i (a permutation)
+ *   dl, dr      HOST double[n]: row / column scalings, |dl_i a_ij dr_j| <= 1 (+ 1e-10 relative)
+ *               and = 1 on the matching
+ *   n_kernel_launches   optional (may be NULL)
+ * Parallel forward auction with eps-scaling down to 1e-10 (relative cost range) / n: the
+ * objective sum_i c_{i,sigma(i)} is optimal up to that margin (the oracle's Hungarian method
+ * finds the same transversal when the optimum is unique).  Synchronous; device memory
+ * allocated and freed inside.  Errors: BILU_ERR_ARG (bad CSR, or no perfect matching: an empty
+ * row / column or a structurally singular pattern), BILU_ERR_OOM, BILU_ERR_CUDA,
+ * BILU_ERR_NOT_BUILT.
+ */
+bilu_status bilu_mwm(int32_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *val, int32_t device,
+                     void *stream, int32_t *sigma, double *dl, double *dr, int32_t *n_kernel_launches);
 
 const char *bilu_last_error(const bilu_ctx *h);
 

@@ -4,6 +4,6 @@ The product path is libbilu.so (csrc/, include/bilu.h) driven through the thin
 ctypes binding in bilu.py.  Importing this package never falls back to a CPU
 implementation: a missing library raises at first use.
 """
-from .bilu import BILU, BiluError, Factor, default_options, load_library, ABI_SYMBOLS, ilu1_blocks, cosine_blocks  # noqa: F401
+from .bilu import BILU, BiluError, Factor, default_options, load_library, ABI_SYMBOLS, ilu1_blocks, cosine_blocks, mwm  # noqa: F401
 
-__all__ = ["BILU", "BiluError", "Factor", "default_options", "load_library", "ABI_SYMBOLS", "ilu1_blocks", "cosine_blocks"]
+__all__ = ["BILU", "BiluError", "Factor", "default_options", "load_library", "ABI_SYMBOLS", "ilu1_blocks", "cosine_blocks", "mwm"]

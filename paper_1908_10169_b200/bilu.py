@@ -23,7 +23,8 @@ ABI_SYMBOLS = ["bilu_options_default", "bilu_analyze", "bilu_set_values", "bilu_
                "bilu_status_string", "bilu_last_error", "bilu_kernel_launches", "bilu_diag_dgemm", "bilu_diag_tsgemm",
                "bilu_dist_setup", "bilu_factor_local", "bilu_interface_pack", "bilu_interface_unpack",
                "bilu_factor_separators", "bilu_gmres", "bilu_ilu1_blocks",
-               "bilu_cosine_blocks", "bilu_dist_separator_rows", "bilu_apply_dist_begin", "bilu_apply_dist_end"]
+               "bilu_cosine_blocks", "bilu_dist_separator_rows", "bilu_apply_dist_begin", "bilu_apply_dist_end",
+               "bilu_mwm"]
 
 
 class BiluError(RuntimeError):
@@ -139,6 +140,8 @@ def load_library():
     lib.bilu_ilu1_blocks.restype = ctypes.c_int
     lib.bilu_cosine_blocks.argtypes = [ctypes.c_int32, P, P, D, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P]
     lib.bilu_cosine_blocks.restype = ctypes.c_int
+    lib.bilu_mwm.argtypes = [ctypes.c_int32, P, P, P, ctypes.c_int32, P, P, P, P, P]
+    lib.bilu_mwm.restype = ctypes.c_int
     lib.bilu_dist_separator_rows.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
     lib.bilu_dist_separator_rows.restype = ctypes.c_int
     lib.bilu_apply_dist_begin.argtypes = [P, P, P, P]
@@ -392,6 +395,25 @@ def ilu1_blocks(indptr, indices, data, tau, max_size=8, perm=None, device=0, str
     if rc != 0:
         raise BiluError(rc, lib.bilu_last_error(None).decode())
     return out[: nb.value].copy(), nl.value
+
+
+def mwm(indptr, indices, data, device=0, stream=0):
+    """bilu_mwm: maximum product transversal + scalings of Sec. 3.1 on the device.
+    Returns (sigma int32 array: column matched to each row, dl, dr, kernels launched)."""
+    lib = load_library()
+    ip = _arr(indptr, np.int64)
+    ix = _arr(indices, np.int32)
+    dv = _arr(data, np.float64)
+    n = len(ip) - 1
+    sigma = np.zeros(max(n, 1), dtype=np.int32)
+    dl = np.zeros(max(n, 1))
+    dr = np.zeros(max(n, 1))
+    nl = ctypes.c_int32(0)
+    rc = lib.bilu_mwm(n, ip.ctypes.data, ix.ctypes.data, dv.ctypes.data, int(device), ctypes.c_void_p(stream),
+                      sigma.ctypes.data, dl.ctypes.data, dr.ctypes.data, ctypes.byref(nl))
+    if rc != 0:
+        raise BiluError(rc, lib.bilu_last_error(None).decode())
+    return sigma[:n].copy(), dl[:n].copy(), dr[:n].copy(), nl.value
 
 
 def cosine_blocks(indptr, indices, tau=0.8, max_size=128, device=0, stream=0):

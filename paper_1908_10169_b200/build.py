@@ -13,7 +13,8 @@ LIB = os.path.join(HERE, "libbilu.so")
 LIB_PROF = os.path.join(HERE, "libbilu_prof.so")   # diagnostic build with per-phase clock64 counters
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["bilu_factor.cu", "bilu_merge.cu", "bilu_apply.cu", "bilu_util.cu", "bilu_krylov.cu", "bilu_blocking.cu"]
+CU_SOURCES = ["bilu_factor.cu", "bilu_merge.cu", "bilu_apply.cu", "bilu_util.cu", "bilu_krylov.cu", "bilu_blocking.cu",
+              "bilu_matching.cu"]
 CPP_SOURCES = ["bilu_host.cpp"]
 HEADERS = ["bilu_internal.h", "dgemm_cta.cuh", os.path.join("..", "..", "include", "bilu.h")]
 

@@ -588,7 +588,7 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return sub[x] != sub[y] ? sub[x] > sub[y] : x > y; });
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    const double budget = opt.zone_bytes > 0 ? (double)opt.zone_bytes : std::min(6.0 * (1ull << 30), 0.25 * (double)fr);
+    const double budget = opt.zone_bytes > 0 ? (double)opt.zone_bytes : std::min(24.0 * (1ull << 30), 0.25 * (double)fr);
     int64_t nzb = 0, nz = 0;
     for (int32_t x = 0; x < n_blocks; ++x) {
       const int32_t K = order[x], bK = bstart[K + 1] - bstart[K];
@@ -1967,6 +1967,67 @@ extern "C" bilu_status bilu_cosine_blocks(int32_t n, const int64_t *row_ptr, con
   if (e != cudaSuccess) {
     set_err(nullptr, "bilu_cosine_blocks: %s", cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? BILU_ERR_OOM : BILU_ERR_CUDA;
+  }
+  return BILU_OK;
+}
+
+// ------------------------------------------------------------ Sec. 3.1 matching + scaling
+extern "C" int bilu_mwm_device(int n, const int64_t *rp, const int32_t *ci, const double *val, int32_t *assign,
+                               double *dl, double *dr, void *work, cudaStream_t st, int *launches, int *rounds);
+
+extern "C" bilu_status bilu_mwm(int32_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
+                                int32_t device, void *stream, int32_t *sigma, double *dl, double *dr,
+                                int32_t *n_kernel_launches) {
+  if (n < 1 || !row_ptr || !col_idx || !val || !sigma || !dl || !dr) {
+    set_err(nullptr, "bilu_mwm: null pointer or n < 1");
+    return BILU_ERR_ARG;
+  }
+  if (n >= (1 << 30)) { set_err(nullptr, "bilu_mwm: n must be < 2^30"); return BILU_ERR_ARG; }
+  std::vector<int32_t> pm, ipm;
+  bilu_status st = check_csr_perm("bilu_mwm", n, row_ptr, col_idx, nullptr, pm, ipm);
+  if (st != BILU_OK) return st;
+  const int64_t nnz = row_ptr[n];
+  if (cudaSetDevice(device) != cudaSuccess) {
+    set_err(nullptr, "bilu_mwm: cannot use CUDA device %d", device);
+    return BILU_ERR_NOT_BUILT;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t *d_rp = nullptr;
+  int32_t *d_ci = nullptr, *d_as = nullptr;
+  double *d_v = nullptr, *d_dl = nullptr, *d_dr = nullptr;
+  void *d_work = nullptr;
+  const size_t work_bytes = (size_t)n * (4 * 8 + 3 * 4) + 64 + 16 + (size_t)std::max<int64_t>(nnz, 1) * 8;
+  cudaError_t e = cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_v, sizeof(double) * std::max<int64_t>(nnz, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_as, sizeof(int32_t) * n);
+  if (e == cudaSuccess) e = cudaMalloc(&d_dl, sizeof(double) * n);
+  if (e == cudaSuccess) e = cudaMalloc(&d_dr, sizeof(double) * n);
+  if (e == cudaSuccess) e = cudaMalloc(&d_work, work_bytes);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(d_ci, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(d_v, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s);
+  int launches = 0, rounds = 0, rc = 0;
+  if (e == cudaSuccess) {
+    rc = bilu_mwm_device(n, d_rp, d_ci, d_v, d_as, d_dl, d_dr, d_work, s, &launches, &rounds);
+    if (rc > 0) e = (cudaError_t)rc;
+  }
+  if (e == cudaSuccess && rc == 0) {
+    e = cudaMemcpyAsync(sigma, d_as, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dl, d_dl, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dr, d_dr, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  }
+  if (getenv("BILU_VERBOSE")) fprintf(stderr, "[bilu] mwm: %d bidding rounds, %d launches\n", rounds, launches);
+  cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_v); cudaFree(d_as); cudaFree(d_dl); cudaFree(d_dr); cudaFree(d_work);
+  if (n_kernel_launches) *n_kernel_launches = launches;
+  if (e != cudaSuccess) {
+    set_err(nullptr, "bilu_mwm: %s", cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? BILU_ERR_OOM : BILU_ERR_CUDA;
+  }
+  if (rc == -2) {
+    set_err(nullptr, "bilu_mwm: the pattern has no perfect matching (structurally singular)");
+    return BILU_ERR_ARG;
   }
   return BILU_OK;
 }
