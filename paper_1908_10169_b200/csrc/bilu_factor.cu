@@ -1883,9 +1883,16 @@ scaled:
     nb[L + y - (L < nRr ? pdr[L] : ndup)] = v;
   }
   __syncthreads();
-  // one parallel pass: register K in Uc(T) / Lc(T) of every run, and the chain edges
-  // n_i -> n_{i+1} (n_{i+1} additionally waits for n_i)
-  for (int x = tid; x < nRr + nCr + max(nN - 1, 0); x += NT) {
+  // one parallel pass: register K in Uc(T) / Lc(T) of every run, and the readiness edges.
+  // K's update can only create entries of a block T1 in a block T2 > T1 when one of them is
+  // a row block and the other a column block of K (W_L[T2 rows, T1] -= L_K[T2 rows] Ũ_K[:, T1
+  // cols], W_U[T1, T2 cols] -= L_K[T1 rows] Ũ_K[:, T2 cols]), so the exact
+  // edges are the (row block, column block) pairs of N(K).  When there
+  // are few of them they are added as such; otherwise the chain n_i -> n_{i+1} over N(K) --
+  // whose transitive closure contains every pair -- keeps the edge count linear.
+  const bool pairs = nRr * nCr <= F.pair_cap;
+  const int nEdge = pairs ? nRr * nCr : max(nN - 1, 0);
+  for (int x = tid; x < nRr + nCr + nEdge; x += NT) {
     if (x < nRr) {
       const int r0 = rstart[x], r1 = rstart[x + 1], T = rblk[x];
       if (F.nzb == 0 || F.zk[T] < 0) {   // zone targets read no contributor lists (their panels are pushed)
@@ -1899,6 +1906,18 @@ scaled:
         int rec[REC_INTS] = {K, c0, c1, lbound(R, 0, mK, F.bstart[T]), lbound(R, 0, mK, F.bstart[T + 1]), 0, 0, 0};
         list_append(F, F.lc, T, rec);
       }
+    } else if (pairs) {
+      const int z = x - nRr - nCr, xr = z / nCr;
+      const int r = rblk[xr], c = cblk[z - xr * nCr];
+      if (r == c) continue;
+      // a pair of two blocks that are both row and column blocks appears twice: keep r < c
+      if (r > c) {
+        const int pc = lbound(cblk, 0, nCr, r), pr = lbound(rblk, 0, nRr, c);
+        if (pc < nCr && cblk[pc] == r && pr < nRr && rblk[pr] == c) continue;
+      }
+      const int lo = min(r, c), hi = max(r, c);
+      atomicAdd(&F.pending[hi], 1);
+      list_append(F, F.succ, lo, &hi);
     } else {
       const int z = x - nRr - nCr;
       atomicAdd(&F.pending[nb[z + 1]], 1);

@@ -526,6 +526,8 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     h->d_alpha = da;
   }
   F.heavy_T = 1024;
+  F.pair_cap = 128;
+  if (const char *pc = getenv("BILU_PAIR_CAP")) F.pair_cap = atoi(pc);
   if (const char *ht = getenv("BILU_HEAVY_T")) F.heavy_T = atoi(ht);
   F.heavy_idle = 8;
   F.part_items = 512;

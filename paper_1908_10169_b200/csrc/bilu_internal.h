@@ -107,6 +107,7 @@ struct DevFactor {
   HeavyCtx *hctx; int64_t hctx_cap;
   double *hpool; int64_t hpool_cap;     // doubles
   int heavy_T;                          // item count from which a block is split (0 = never)
+  int pair_cap;                         // readiness edges: (row, column) block pairs up to this many, else the chain
   int heavy_idle;                       // ... if at least this many CTAs are idle
   int part_items;                       // items per update-part task
   double wide_flops;                    // blocks wider than 16 are split from this many update flops
