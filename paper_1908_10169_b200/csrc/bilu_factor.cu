@@ -389,10 +389,16 @@ __device__ __forceinline__ int contrib_of(const Contrib *C, int nc, int t) {
 struct LineMap {
   const unsigned *bm; const int *pre; int words;   // bitmap path
   const int *pos;                                   // pos-map path (bm == nullptr)
+  const unsigned *l1; const int *pre1;              // two-level bitmap: pages of 1024 keys
   int e, base;
   __device__ __forceinline__ int operator()(int key) const {
     if (bm) {
-      const int r = key - e, w = r >> 5;
+      const int r = key - e;
+      int w = r >> 5;
+      if (l1) {                                     // page slot, then the word inside the page
+        const int p = r >> 10, w1 = p >> 5;
+        w = (pre1[w1] + __popc(l1[w1] & ((1u << (p & 31)) - 1u))) * 32 + (w & 31);
+      }
       return base + pre[w] + __popc(bm[w] & ((1u << (r & 31)) - 1u));
     }
     return pos[key];
@@ -407,6 +413,7 @@ struct SideState {
   bool sorted;     // lines in ascending index order (bitmap path)
   LineMap M;
   const unsigned *gbm; const int *gpre;   // global copies of the bitmap map (split blocks)
+  const unsigned *gl1; const int *gpre1;  // ... and of its page level (two-level maps)
 };
 
 constexpr int MAX_PARTS = 32;          // update parts per block (both sides)
@@ -455,7 +462,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
   const int words = (hi - e + 1 + 31) >> 5;
   const int base = SIDE == 0 ? b : 0;            // buffer line of the first candidate
   LineMap M;
-  M.e = e; M.base = base; M.bm = nullptr; M.pre = nullptr; M.words = words;
+  M.e = e; M.base = base; M.bm = nullptr; M.pre = nullptr; M.words = words; M.l1 = nullptr; M.pre1 = nullptr;
   M.pos = F.posmap + (size_t)blockIdx.x * F.n;
   int nU = 0;
   unsigned *bm = nullptr;
@@ -562,7 +569,7 @@ __device__ bool side_prepare(const DevFactor &F, int K, int s, int e, int b, con
       unsigned *gbm = (unsigned *)(W + wd + ld);
       int *gpre = (int *)(gbm + words + 1);
       for (int w = tid; w < words; w += NT) { gbm[w] = bm[w]; gpre[w] = pre[w]; }
-      R.gbm = gbm; R.gpre = gpre;
+      R.gbm = gbm; R.gpre = gpre; R.gl1 = nullptr; R.gpre1 = nullptr;
     }
   } else {
     W = (double *)balloc(A, (int64_t)nW * b * 8);
@@ -609,6 +616,33 @@ __device__ int prep_words(const Shared &S, int side, int e, const int32_t *arc, 
   return (hi - e + 1 + 31) >> 5;
 }
 
+// a-4: scatter Ã's block column (incl. the pivot block) into W_L and its block row into W_U
+// ("load the associated scalar sparse columns of A into block column buffer", PAPER.md:
+// 370-371); four entries in flight per thread.  CTA-wide, ends with a barrier.
+__device__ void scatter_A(const DevFactor &F, int s, int e, int b, int64_t aL0, int64_t aL1, int64_t aU0, int64_t aU1,
+                          const LineMap &ML, const LineMap &MU, double *WL, double *WU) {
+  const int nL0 = (int)(aL1 - aL0), nAU = (int)(aU1 - aU0);
+  for (int x0 = threadIdx.x; x0 < nL0 + nAU; x0 += 4 * NT) {
+    int rc4[4]; double v4[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int x = x0 + u * NT;
+      rc4[u] = -1; v4[u] = 0.0;
+      if (x < nL0) { rc4[u] = F.AL_rc[aL0 + x]; v4[u] = F.AL_val[aL0 + x]; }
+      else if (x < nL0 + nAU) { rc4[u] = F.AU_rc[aU0 + (x - nL0)]; v4[u] = F.AU_val[aU0 + (x - nL0)]; }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int x = x0 + u * NT;
+      if (rc4[u] < 0) continue;
+      const int key = rc4[u] >> 7;
+      if (x < nL0) WL[(int64_t)(key < e ? key - s : ML(key)) * b + (rc4[u] & 127)] = v4[u];
+      else WU[(int64_t)MU(key) * b + (rc4[u] & 127)] = v4[u];
+    }
+  }
+  __syncthreads();
+}
+
 __device__ bool prepare_both(const DevFactor &F, int K, int s, int e, int b, const Contrib *CL, int nLc, int TL,
                              const Contrib *CU, int nUc, int TU, int64_t aL0, int64_t aLe, int64_t aL1, int64_t aU0,
                              int64_t aU1, Bump &A, Shared &S, SideState &RL, SideState &RU, bool &ok) {
@@ -616,17 +650,20 @@ __device__ bool prepare_both(const DevFactor &F, int K, int s, int e, int b, con
   ok = true;
   const int wL = prep_words(S, 0, e, F.AL_rc, aLe, aL1), wU = prep_words(S, 1, e, F.AU_rc, aU0, aU1);
   if (wL > 8192 || wU > 8192) return false;
-  const int nAL = (int)(aL1 - aLe), nAU = (int)(aU1 - aU0);
   unsigned *bm = (unsigned *)balloc_top(A, (int64_t)(wL + wU + 2) * 4);
   int *pre = (int *)balloc_top(A, (int64_t)(wL + wU + 2) * 4);
   if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); ok = false; return true; }
   unsigned *bmL = bm, *bmU = bm + wL;
   for (int w = tid; w < wL + wU; w += NT) bm[w] = 0u;
   __syncthreads();
-  // Ã entries of both sides, then the items of both sides
-  for (int x = tid; x < nAL + nAU; x += NT) {
-    if (x < nAL) { const int r = (F.AL_rc[aLe + x] >> 7) - e; atomicOr(&bmL[r >> 5], 1u << (r & 31)); }
-    else { const int r = (F.AU_rc[aU0 + (x - nAL)] >> 7) - e; atomicOr(&bmU[r >> 5], 1u << (r & 31)); }
+  // Ã's distinct candidate keys of both sides, then the items of both sides
+  {
+    const int64_t kL0 = F.AKL_ptr[K], kU0 = F.AKU_ptr[K];
+    const int nKL = (int)(F.AKL_ptr[K + 1] - kL0), nKU = (int)(F.AKU_ptr[K + 1] - kU0);
+    for (int x = tid; x < nKL + nKU; x += NT) {
+      if (x < nKL) { const int r = F.AKL[kL0 + x] - e; atomicOr(&bmL[r >> 5], 1u << (r & 31)); }
+      else { const int r = F.AKU[kU0 + (x - nKL)] - e; atomicOr(&bmU[r >> 5], 1u << (r & 31)); }
+    }
   }
   {
     int aL = 0, aU = 0;
@@ -659,8 +696,8 @@ __device__ bool prepare_both(const DevFactor &F, int K, int s, int e, int b, con
   const int nUL = wU > 0 ? pre[wL] : tot, nUU = tot - nUL;
   // line maps: L lines start at b (pivot rows first); U prefix sums are offset by nUL
   LineMap ML, MU;
-  ML.e = e; ML.base = b; ML.bm = bmL; ML.pre = pre; ML.words = wL; ML.pos = nullptr;
-  MU.e = e; MU.base = -nUL; MU.bm = bmU; MU.pre = pre + wL; MU.words = wU; MU.pos = nullptr;
+  ML.e = e; ML.base = b; ML.bm = bmL; ML.pre = pre; ML.words = wL; ML.pos = nullptr; ML.l1 = nullptr; ML.pre1 = nullptr;
+  MU.e = e; MU.base = -nUL; MU.bm = bmU; MU.pre = pre + wL; MU.words = wU; MU.pos = nullptr; MU.l1 = nullptr; MU.pre1 = nullptr;
   const int nWL = b + nUL, nWU = nUU;
   double *WL, *WU;
   int *lineL, *lineU;
@@ -683,6 +720,7 @@ __device__ bool prepare_both(const DevFactor &F, int K, int s, int e, int b, con
     for (int w = tid; w < wL; w += NT) { gbmL[w] = bmL[w]; gpreL[w] = pre[w]; }
     for (int w = tid; w < wU; w += NT) { gbmU[w] = bmU[w]; gpreU[w] = pre[wL + w]; }
     RL.gbm = gbmL; RL.gpre = gpreL; RU.gbm = gbmU; RU.gpre = gpreU;   // global copies (same bases)
+    RL.gl1 = RU.gl1 = nullptr; RL.gpre1 = RU.gpre1 = nullptr;
   } else {
     WL = (double *)balloc(A, (int64_t)nWL * b * 8);
     lineL = (int *)balloc(A, (int64_t)(nWL + 1) * 4);
@@ -708,20 +746,159 @@ __device__ bool prepare_both(const DevFactor &F, int K, int s, int e, int b, con
     for (int x = tid; x < nWU * b; x += NT) WU[x] = 0.0;
   }
   __syncthreads();
-  // a-4: scatter Ã's block column (incl. the pivot block) and block row
-  const int nL0 = (int)(aL1 - aL0);
-  for (int x = tid; x < nL0 + nAU; x += NT) {
-    if (x < nL0) {
-      const int rc = F.AL_rc[aL0 + x], key = rc >> 7;
-      const int w = key < e ? key - s : ML(key);
-      WL[(int64_t)w * b + (rc & 127)] = F.AL_val[aL0 + x];
-    } else {
-      const int64_t p = aU0 + (x - nL0);
-      const int rc = F.AU_rc[p], key = rc >> 7;
-      WU[(int64_t)MU(key) * b + (rc & 127)] = F.AU_val[p];
+  scatter_A(F, s, e, b, aL0, aL1, aU0, aU1, ML, MU, WL, WU);
+  RL.W = WL; RL.lineOf = lineL; RL.nU = nUL; RL.M = ML; RL.sorted = true;
+  RU.W = WU; RU.lineOf = lineU; RU.nU = nUU; RU.M = MU; RU.sorted = true;
+  return true;
+}
+
+// a-3 / a-4 of both sides when a key range is too wide for the flat bitmap: a two-level
+// bitmap in shared memory -- a page bit per 1024 keys, then one 32-word bitmap per occupied
+// page -- so the candidate lines stay in ascending key order (sorted, no pos map) for any n.
+// Two passes over the occurrences (Ã's distinct candidate keys and the contributors' items), four loads in flight per thread.  Same result as side_prepare<0>
+// followed by side_prepare<1>.  Returns false (nothing done) if the occupied pages do not
+// fit in the shared-memory budget.
+__device__ bool prepare_both2(const DevFactor &F, int K, int s, int e, int b, const Contrib *CL, int nLc, int TL,
+                              const Contrib *CU, int nUc, int TU, int64_t aL0, int64_t aLe, int64_t aL1, int64_t aU0,
+                              int64_t aU1, Bump &A, Shared &S, SideState &RL, SideState &RU, bool &ok) {
+  const int tid = threadIdx.x;
+  ok = true;
+  const int hiL = max(max(e - 1, S.maxkey[0]), aL1 > aLe ? (F.AL_rc[aL1 - 1] >> 7) : e - 1);
+  const int hiU = max(max(e - 1, S.maxkey[1]), aU1 > aU0 ? (F.AU_rc[aU1 - 1] >> 7) : e - 1);
+  const int w1L = ((hiL - e + 1 + 1023) >> 10) / 32 + 1, w1U = ((hiU - e + 1 + 1023) >> 10) / 32 + 1;
+  const int64_t kL0 = F.AKL_ptr[K], kU0 = F.AKU_ptr[K];
+  const int nKL = (int)(F.AKL_ptr[K + 1] - kL0), nKU = (int)(F.AKU_ptr[K + 1] - kU0);
+  const int nocc = nKL + nKU + TL + TU;
+  const int stop0 = A.stop;
+  const int64_t gtop0 = A.gtop;
+  // level 1 (+ its prefix) and the slot -> page table
+  unsigned *l1 = (unsigned *)balloc_top(A, (int64_t)(w1L + w1U + 2) * 4);
+  int *pre1 = (int *)balloc_top(A, (int64_t)(w1L + w1U + 2) * 4);
+  if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); ok = false; return true; }
+  for (int w = tid; w < w1L + w1U; w += NT) l1[w] = 0u;
+  __syncthreads();
+  // the key of occurrence x (-1: not a candidate) and its side
+  auto occ = [&](int x, int &aL, int &aU, int &side) -> int {
+    if (x < nKL) { side = 0; return F.AKL[kL0 + x]; }
+    if (x < nKL + nKU) { side = 1; return F.AKU[kU0 + (x - nKL)]; }
+    int t = x - nKL - nKU;
+    if (t < TL) {
+      while (aL + 1 < nLc && CL[aL + 1].item_off <= t) ++aL;
+      const int i = t - CL[aL].item_off;
+      side = 0;
+      return i >= CL[aL].n_cand_skip ? F.Lidx[CL[aL].rows + i] : -1;   // pivot rows excluded
+    }
+    t -= TL;
+    while (aU + 1 < nUc && CU[aU + 1].item_off <= t) ++aU;
+    side = 1;
+    return F.Uidx[CU[aU].cols + (t - CU[aU].item_off)];
+  };
+  {   // pass A: occupied pages
+    int aL = 0, aU = 0;
+    for (int x0 = tid; x0 < nocc; x0 += 4 * NT) {
+      int k4[4], s4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const int x = x0 + u * NT; k4[u] = x < nocc ? occ(x, aL, aU, s4[u]) : -1; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k4[u] >= 0) { const int pg = (k4[u] - e) >> 10; atomicOr(&l1[(s4[u] ? w1L : 0) + (pg >> 5)], 1u << (pg & 31)); }
     }
   }
   __syncthreads();
+  for (int w = tid; w < w1L + w1U; w += NT) pre1[w] = __popc(l1[w]);
+  __syncthreads();
+  const int npu = cta_scan(pre1, w1L + w1U, S.tmp);
+  const int npuL = pre1[w1L];
+  // page bitmaps: budget -- fall back to the pos map beyond it
+  const int64_t need = (int64_t)npu * 32 * 8 + (int64_t)npu * 4 + 64;
+  if (need > (int64_t)(A.stop - A.sused) - 16 * 1024) {
+    A.stop = stop0; A.gtop = gtop0;       // release l1 / pre1
+    __syncthreads();
+    return false;
+  }
+  unsigned *bm = (unsigned *)balloc_top(A, (int64_t)npu * 32 * 4 + 4);
+  int *pre = (int *)balloc_top(A, (int64_t)npu * 32 * 4 + 4);
+  int *pg = (int *)balloc_top(A, (int64_t)npu * 4 + 4);
+  for (int w = tid; w < npu * 32; w += NT) bm[w] = 0u;
+  for (int w = tid; w < w1L + w1U; w += NT) {
+    unsigned m = l1[w];
+    int at = pre1[w];
+    const int pb = (w < w1L ? w : w - w1L) << 5;
+    while (m) { const int bit = __ffs(m) - 1; pg[at++] = pb + bit; m &= m - 1; }
+  }
+  __syncthreads();
+  {   // pass B: key bits inside the pages
+    int aL = 0, aU = 0;
+    for (int x0 = tid; x0 < nocc; x0 += 4 * NT) {
+      int k4[4], s4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const int x = x0 + u * NT; k4[u] = x < nocc ? occ(x, aL, aU, s4[u]) : -1; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k4[u] >= 0) {
+          const int r = k4[u] - e, p = r >> 10, w1 = (s4[u] ? w1L : 0) + (p >> 5);
+          const int slot = pre1[w1] + __popc(l1[w1] & ((1u << (p & 31)) - 1u));
+          atomicOr(&bm[slot * 32 + ((r >> 5) & 31)], 1u << (r & 31));
+        }
+    }
+  }
+  __syncthreads();
+  for (int w = tid; w < npu * 32; w += NT) pre[w] = __popc(bm[w]);
+  __syncthreads();
+  const int tot = cta_scan(pre, npu * 32, S.tmp);
+  const int nUL = npuL < npu ? pre[npuL * 32] : tot, nUU = tot - nUL;
+  LineMap ML, MU;
+  ML.e = e; ML.base = b; ML.bm = bm; ML.pre = pre; ML.words = npu * 32; ML.pos = nullptr; ML.l1 = l1; ML.pre1 = pre1;
+  MU.e = e; MU.base = -nUL; MU.bm = bm; MU.pre = pre; MU.words = npu * 32; MU.pos = nullptr; MU.l1 = l1 + w1L;
+  MU.pre1 = pre1 + w1L;
+  const int nWL = b + nUL, nWU = nUU;
+  double *WL, *WU;
+  int *lineL, *lineU;
+  if (A.pool) {
+    const int64_t wdL = (int64_t)nWL * b, ldL = ((int64_t)nWL + 2) / 2 + 1;
+    const int64_t wdU = (int64_t)nWU * b, ldU = ((int64_t)nWU + 2) / 2 + 1;
+    const int64_t md = ((int64_t)npu * 64 + 2 * (w1L + w1U) + 8) / 2 + 2;      // bm, pre, l1, pre1 (ints)
+    const int64_t d = wdL + ldL + wdU + ldU + md;
+    if (tid == 0) S.off[3] = atomicAdd(&F.ctrl[CS * CTRL_HPOOL], (unsigned long long)d);
+    __syncthreads();
+    const unsigned long long o = S.off[3];
+    __syncthreads();
+    if (o + d > (unsigned long long)F.hpool_cap) { if (tid == 0) raise_abort(F, DEV_OVF_HPOOL, K); ok = false; return true; }
+    WL = F.hpool + o;
+    lineL = (int *)(WL + wdL);
+    WU = WL + wdL + ldL;
+    lineU = (int *)(WU + wdU);
+    unsigned *gbm = (unsigned *)(WU + wdU + ldU);
+    int *gpre = (int *)(gbm + npu * 32);
+    unsigned *gl1 = (unsigned *)(gpre + npu * 32);
+    int *gpre1 = (int *)(gl1 + w1L + w1U);
+    for (int w = tid; w < npu * 32; w += NT) { gbm[w] = bm[w]; gpre[w] = pre[w]; }
+    for (int w = tid; w < w1L + w1U; w += NT) { gl1[w] = l1[w]; gpre1[w] = pre1[w]; }
+    RL.gbm = gbm; RL.gpre = gpre; RU.gbm = gbm; RU.gpre = gpre;
+    RL.gl1 = gl1; RL.gpre1 = gpre1; RU.gl1 = gl1 + w1L; RU.gpre1 = gpre1 + w1L;
+  } else {
+    WL = (double *)balloc(A, (int64_t)nWL * b * 8);
+    lineL = (int *)balloc(A, (int64_t)(nWL + 1) * 4);
+    WU = (double *)balloc(A, (int64_t)nWU * b * 8);
+    lineU = (int *)balloc(A, (int64_t)(nWU + 1) * 4);
+    if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); ok = false; return true; }
+  }
+  for (int x = tid; x < b; x += NT) lineL[x] = s + x;
+  for (int w = tid; w < npu * 32; w += NT) {
+    const int sl = w >> 5;
+    const bool u = sl >= npuL;
+    unsigned m = bm[w];
+    int at = u ? pre[w] - nUL : b + pre[w];
+    int *lo = u ? lineU : lineL;
+    const int kb = e + (pg[sl] << 10) + ((w & 31) << 5);
+    while (m) { const int bit = __ffs(m) - 1; lo[at++] = kb + bit; m &= m - 1; }
+  }
+  if (!A.pool) {
+    for (int x = tid; x < nWL * b; x += NT) WL[x] = 0.0;
+    for (int x = tid; x < nWU * b; x += NT) WU[x] = 0.0;
+  }
+  __syncthreads();
+  scatter_A(F, s, e, b, aL0, aL1, aU0, aU1, ML, MU, WL, WU);
   RL.W = WL; RL.lineOf = lineL; RL.nU = nUL; RL.M = ML; RL.sorted = true;
   RU.W = WU; RU.lineOf = lineU; RU.nU = nUU; RU.M = MU; RU.sorted = true;
   return true;
@@ -978,6 +1155,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
 
   // ---------------- a-3 / a-4 for both sides
   SideState RL, RU;
+  RL.gbm = RU.gbm = nullptr; RL.gpre = RU.gpre = nullptr; RL.gl1 = RU.gl1 = nullptr; RL.gpre1 = RU.gpre1 = nullptr;
   const bool wide = b > 16 || maxbJ > 16;
   double *gs = nullptr;
   if (wide) {   // staging of the contributors' B operands (b_J <= 128 rows of TsB<128>::LDB)
@@ -985,9 +1163,13 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     OVF_CHECK();
   }
   bool both_ok = true;
-  const bool both = !(F.exp & 4) &&
-                    prepare_both(F, K, s, e, b, CL, nLc, TL, CU, nUc, TU, aL0, aLe, aL1, aU0, aU1, A, S, RL, RU, both_ok);
+  bool both = !(F.exp & 4) &&
+              prepare_both(F, K, s, e, b, CL, nLc, TL, CU, nUc, TU, aL0, aLe, aL1, aU0, aU1, A, S, RL, RU, both_ok);
   if (!both_ok) return;
+  if (!both && !(F.exp & 8)) {
+    both = prepare_both2(F, K, s, e, b, CL, nLc, TL, CU, nUc, TU, aL0, aLe, aL1, aU0, aU1, A, S, RL, RU, both_ok);
+    if (!both_ok) return;
+  }
   if (!both && !side_prepare<0>(F, K, s, e, b, CL, nLc, TL, aL0, aLe, aL1, A, S, RL)) return;
   PROF(2);
   int *ilineL = nullptr, *ilineU = nullptr;
@@ -1041,6 +1223,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
         X.K = K; X.nc[0] = nLc; X.nc[1] = nUc; X.T[0] = TL; X.T[1] = TU; X.np[0] = pL; X.np[1] = pU;
         X.C[0] = gCL; X.C[1] = gCU; X.R[0] = RL; X.R[1] = RU; X.flops = flops;
         X.R[0].M.bm = RL.gbm; X.R[0].M.pre = RL.gpre; X.R[1].M.bm = RU.gbm; X.R[1].M.pre = RU.gpre;
+        X.R[0].M.l1 = RL.gl1; X.R[0].M.pre1 = RL.gpre1; X.R[1].M.l1 = RU.gl1; X.R[1].M.pre1 = RU.gpre1;
         X.wide = wide ? 1 : 0;
         X.iline[0] = ilineL; X.iline[1] = ilineU;
         if (wide) {
@@ -1255,10 +1438,130 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
   finish_block(F, K, S, A, WL, WU, rowOf, colOf, nR, nC, X.R[0].sorted, X.R[1].sorted, X.flops, &X, fmode);
 }
 
+// Gauss-Jordan inverse for 8 < b <= BR with P_K held in registers: the first BR * G threads
+// take part (G = 4 column groups, named barrier 1); thread t owns row i = t % BR and the
+// columns g*RP .. g*RP+RP-1 of it (g = t / BR), so lanes run over rows and every shared-memory
+// access is conflict-free (column-major P) or a broadcast (a row).  Each step k reads the
+// matrix of step k-1 from one of two shared copies (P and P + b^2, ping-pong) and writes its
+// updated entries to the other, so one barrier per step suffices; the update is branch-free
+// (rows k and bi, swapped, are patched afterwards).  The pivot of step k (argmax_{i>=k}
+// |a_ik|, ties -> lowest row, R6) comes from the per-warp maxima (signed value, row) that the
+// owners of column k reduced with shuffles at the end of step k-1.  Same arithmetic as the
+// shared-memory version below.  P: 2 b^2 doubles; pv: >= 8 doubles.
+template <int BR, int RP>
+__device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double *pv, Shared &S) {
+  constexpr int G = 4, NTH = BR * G, NWS = BR / 32;   // warps per column group
+  static_assert(G * RP >= BR && NTH <= NT && BR % 32 == 0, "shape");
+  const int tid = threadIdx.x, i = tid % BR, g = tid / BR, c0 = g * RP, lane = tid & 31;
+  const int64_t bb = (int64_t)b * b;
+  if (tid < NTH) {
+    const bool act = i < b;
+    double x[RP];
+#pragma unroll
+    for (int u = 0; u < RP; ++u) x[u] = (act && c0 + u < b) ? P[i + (int64_t)(c0 + u) * b] : 0.0;
+    // warp maxima of column col over rows >= from (owners of col only; whole warps)
+    auto publish = [&](int col, int from) {
+      double v = 0.0;
+#pragma unroll
+      for (int u = 0; u < RP; ++u) if (c0 + u == col) v = x[u];
+      double a = (act && i >= from) ? fabs(v) : -1.0;
+      int r = i;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {        // lower row wins ties
+        const double ao = __shfl_xor_sync(0xffffffffu, a, o), vo = __shfl_xor_sync(0xffffffffu, v, o);
+        const int ro = __shfl_xor_sync(0xffffffffu, r, o);
+        if (ao > a || (ao == a && ro < r)) { a = ao; v = vo; r = ro; }
+      }
+      if (lane == 0) {
+        double *slot = pv + (col & 1) * 2 * NWS;
+        slot[i / 32] = a < 0.0 ? 0.0 : v;
+        ((int *)(slot + NWS))[i / 32] = a < 0.0 ? INT_MAX : r;
+      }
+    };
+    if (g == 0) publish(0, 0);
+    asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
+    bool sing = false;
+    for (int k = 0; k < b; ++k) {
+      const double *cur = (k & 1) ? P + bb : P;
+      double *nxt = (k & 1) ? P : P + bb;
+      const double *slot = pv + (k & 1) * 2 * NWS;
+      double vb = slot[0], best = fabs(vb);
+      int bi = ((const int *)(slot + NWS))[0];
+#pragma unroll
+      for (int q = 1; q < NWS; ++q) {           // warps in row order: the first maximum wins
+        const double vq = slot[q];
+        if (fabs(vq) > best) { best = fabs(vq); vb = vq; bi = ((const int *)(slot + NWS))[q]; }
+      }
+      if (!(best > 0.0)) { sing = true; break; }   // identical decision in every thread
+      // every shared-memory read of the step before any write
+      double pr[RP];
+#pragma unroll
+      for (int u = 0; u < RP; ++u) pr[u] = cur[bi + (int64_t)min(c0 + u, b - 1) * b];   // old row bi
+      const double aik = act ? cur[i + (int64_t)k * b] : 0.0;
+      const double d = 1.0 / vb;
+#pragma unroll
+      for (int u = 0; u < RP; ++u) pr[u] *= d;  // the new pivot row, scaled
+      const bool kin = k / RP == g;             // this column group owns column k (warp-uniform)
+      if (i == bi && i != k) {                  // row bi takes old row k (one lane)
+        const double ckk = cur[k + (int64_t)k * b];
+#pragma unroll
+        for (int u = 0; u < RP; ++u) {
+          const int c = min(c0 + u, b - 1);
+          x[u] = (c0 + u == k) ? -ckk * d : fma(-ckk, pr[u], cur[k + (int64_t)c * b]);
+        }
+      } else if (i == k) {                      // the pivot row (one lane)
+#pragma unroll
+        for (int u = 0; u < RP; ++u) x[u] = (c0 + u == k) ? d : pr[u];
+      } else if (kin) {
+#pragma unroll
+        for (int u = 0; u < RP; ++u) x[u] = (c0 + u == k) ? -aik * d : fma(-aik, pr[u], x[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < RP; ++u) x[u] = fma(-aik, pr[u], x[u]);
+      }
+      if (act) {
+#pragma unroll
+        for (int u = 0; u < RP; ++u)
+          if (c0 + u < b) nxt[i + (int64_t)(c0 + u) * b] = x[u];
+      }
+      if (k + 1 < b && (k + 1) / RP == g) publish(k + 1, k + 1);
+      if (tid == 0) ipiv[k] = bi;
+      asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
+    }
+    if (!sing) {
+      // undo the row interchanges as column interchanges, in reverse order: composite map
+      if (tid == 0) {
+        for (int jj = 0; jj < b; ++jj) fcol[2 * b + jj] = jj;
+        for (int k = b - 1; k >= 0; --k) {
+          const int pvk = ipiv[k];
+          if (pvk != k) { const double t = fcol[2 * b + k]; fcol[2 * b + k] = fcol[2 * b + pvk]; fcol[2 * b + pvk] = t; }
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
+      // column jd of the result = column fcol[2b + jd] of the eliminated matrix: the
+      // eliminated matrix sits in the ping-pong copy written last; gather from it
+      const double *fin = (b & 1) ? P + bb : P;
+      if (act)
+        for (int jd = g; jd < b; jd += G) P[i + (int64_t)jd * b + (fin == P ? bb : 0)] = fin[i + (int64_t)(int)fcol[2 * b + jd] * b];
+      asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
+      if (fin == P)
+        for (int e = tid; e < (int)bb; e += NTH) P[e] = P[bb + e];
+    }
+    if (tid == 0) S.piv = sing ? 1 : 0;
+  }
+  __syncthreads();
+  return S.piv != 0;
+}
+
 // D_K = P_K^{-1} in place (P column-major b x b in shared memory; b > 8 needs 2 b^2 doubles
 // of P and 3 b of fcol), Gauss-Jordan with partial pivoting inside the block
 // (ties -> lowest row, R6).  CTA-wide; returns true if a pivot is exactly 0.
-__device__ bool gj_invert(double *P, int b, int *ipiv, double *fcol, Shared &S) {
+__device__ __noinline__ bool gj_invert(double *P, int b, int *ipiv, double *fcol, Shared &S, bool reg = true) {
+  if (reg && b > 8 && b <= 64) {
+    __shared__ double pvbuf[8];
+    if (b <= 32) return gj_invert_reg<32, 8>(P, b, ipiv, fcol, pvbuf, S);
+    return gj_invert_reg<64, 16>(P, b, ipiv, fcol, pvbuf, S);
+  }
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   bool singular = false;
   if (b <= 8) {

@@ -150,6 +150,8 @@ struct bilu_ctx {
   double *d_val_orig = nullptr;
   int64_t *d_AL_ptr = nullptr, *d_AL_ge = nullptr, *d_AU_ptr = nullptr;
   int32_t *d_AL_rc = nullptr, *d_AU_rc = nullptr;
+  int64_t *d_AKL_ptr = nullptr, *d_AKU_ptr = nullptr;
+  int32_t *d_AKL = nullptr, *d_AKU = nullptr;
   double *d_AL_val = nullptr, *d_AU_val = nullptr;
   int64_t *d_AL_map = nullptr, *d_AU_map = nullptr;
   int64_t nAL = 0, nAU = 0;
@@ -451,6 +453,17 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     }
   }
   h->nAL = AL_ptr[n_blocks]; h->nAU = AU_ptr[n_blocks];
+  // distinct candidate keys of Ã per block (rows >= e_K of AL, columns of AU): the a-3 passes
+  // read these instead of every entry
+  std::vector<int64_t> AKL_ptr(n_blocks + 1, 0), AKU_ptr(n_blocks + 1, 0);
+  std::vector<int32_t> AKL, AKU;
+  for (int32_t K = 0; K < n_blocks; ++K) {
+    for (int64_t q = AL_ge[K]; q < AL_ptr[K + 1]; ++q)
+      if (q == AL_ge[K] || (AL_rc[q] >> 7) != (AL_rc[q - 1] >> 7)) AKL.push_back(AL_rc[q] >> 7);
+    for (int64_t q = AU_ptr[K]; q < AU_ptr[K + 1]; ++q)
+      if (q == AU_ptr[K] || (AU_rc[q] >> 7) != (AU_rc[q - 1] >> 7)) AKU.push_back(AU_rc[q] >> 7);
+    AKL_ptr[K + 1] = (int64_t)AKL.size(); AKU_ptr[K + 1] = (int64_t)AKU.size();
+  }
   std::vector<int32_t> adj_ptr(n_blocks + 1, 0), adj(edges.size()), pending0(n_blocks, 0);
   for (uint64_t eg : edges) { adj_ptr[(eg >> 32) + 1]++; pending0[(uint32_t)eg]++; }
   for (int32_t K = 0; K < n_blocks; ++K) adj_ptr[K + 1] += adj_ptr[K];
@@ -476,6 +489,10 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   ALLOC(h->d_AL_rc, h->nAL); if (h->nAL) H2D(h->d_AL_rc, AL_rc.data(), h->nAL);
   ALLOC(h->d_AU_rc, h->nAU); if (h->nAU) H2D(h->d_AU_rc, AU_rc.data(), h->nAU);
   ALLOC(h->d_AL_map, h->nAL); if (h->nAL) H2D(h->d_AL_map, AL_map.data(), h->nAL);
+  ALLOC(h->d_AKL_ptr, n_blocks + 1); H2D(h->d_AKL_ptr, AKL_ptr.data(), n_blocks + 1);
+  ALLOC(h->d_AKU_ptr, n_blocks + 1); H2D(h->d_AKU_ptr, AKU_ptr.data(), n_blocks + 1);
+  ALLOC(h->d_AKL, std::max<size_t>(AKL.size(), 1)); if (!AKL.empty()) H2D(h->d_AKL, AKL.data(), AKL.size());
+  ALLOC(h->d_AKU, std::max<size_t>(AKU.size(), 1)); if (!AKU.empty()) H2D(h->d_AKU, AKU.data(), AKU.size());
   ALLOC(h->d_AU_map, h->nAU); if (h->nAU) H2D(h->d_AU_map, AU_map.data(), h->nAU);
   ALLOC(h->d_AL_val, h->nAL); ALLOC(h->d_AU_val, h->nAU); ALLOC(h->d_val_orig, nnz);
   ALLOC(h->d_adj_ptr, n_blocks + 1); H2D(h->d_adj_ptr, adj_ptr.data(), n_blocks + 1);
@@ -499,6 +516,7 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   F.bstart = h->d_bstart; F.block_of = h->d_block_of;
   F.AL_ptr = h->d_AL_ptr; F.AL_ge = h->d_AL_ge; F.AL_rc = h->d_AL_rc; F.AL_val = h->d_AL_val;
   F.AU_ptr = h->d_AU_ptr; F.AU_rc = h->d_AU_rc; F.AU_val = h->d_AU_val;
+  F.AKL_ptr = h->d_AKL_ptr; F.AKL = h->d_AKL; F.AKU_ptr = h->d_AKU_ptr; F.AKU = h->d_AKU;
   F.adj_ptr = h->d_adj_ptr; F.adj = h->d_adj;
   ALLOC(F.pending, n_blocks);
   // heavy-block splitting: contexts, part tasks in the queue

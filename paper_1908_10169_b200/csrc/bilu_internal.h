@@ -74,6 +74,8 @@ struct DevFactor {
   // packed rc = row << 7 | (col - s_K); AU = entries of block row K with col >= e_K,
   // rc = col << 7 | (row - s_K).  AL_ge[K] = first AL entry with row >= e_K.
   const int64_t *AL_ptr; const int64_t *AL_ge; const int32_t *AL_rc; const double *AL_val;
+  const int64_t *AKL_ptr; const int32_t *AKL;   // distinct candidate keys of Ã per block (AL rows >= e_K)
+  const int64_t *AKU_ptr; const int32_t *AKU;   // ... (AU columns)
   const int64_t *AU_ptr; const int32_t *AU_rc; const double *AU_val;
   // static schedule: block adjacency of sym(Ã), successors > J
   const int32_t *adj_ptr; const int32_t *adj;
