@@ -11,6 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbilu.so")
 LIB_PROF = os.path.join(HERE, "libbilu_prof.so")   # diagnostic build with per-phase clock64 counters
+LIB_TUNE = os.path.join(HERE, "libbilu_tune.so")   # tools/ build that reads the BILU_* tuning switches
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["bilu_factor.cu", "bilu_merge.cu", "bilu_apply.cu", "bilu_util.cu", "bilu_krylov.cu", "bilu_blocking.cu",
@@ -24,8 +25,12 @@ def _newest_source() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False, defines=(), out=None) -> str:
-    """Compile and link libbilu.so (or a variant: `defines` extra -D flags, `out` library path)."""
+def build(force: bool = False, verbose: bool = False, profile: bool = False, defines=(), out=None,
+          tuning: bool = False) -> str:
+    """Compile and link libbilu.so (or a variant: `defines` extra -D flags, `out` library path;
+    `tuning`: libbilu_tune.so, which reads the BILU_* tuning/diagnostic environment switches)."""
+    if tuning:
+        defines, out = tuple(defines) + ("BILU_TUNING",), out or LIB_TUNE
     lib = out or (LIB_PROF if profile else LIB)
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= _newest_source():
         return lib
@@ -72,4 +77,4 @@ if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv,
-                defines=defs, out=os.path.join(HERE, outs[0]) if outs else None))
+                defines=defs, out=os.path.join(HERE, outs[0]) if outs else None, tuning="--tuning" in sys.argv))

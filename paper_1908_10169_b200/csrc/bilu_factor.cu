@@ -1144,7 +1144,7 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     const bool big = F.heavy_T > 0 && (wide_ ? (S.sflops[0] + S.sflops[1] >= F.wide_flops) : (TL + TU >= F.heavy_T));
     // big blocks keep W in global memory (native fp64 reductions); they are split into
     // parts only when CTAs are idle, else this CTA applies every part itself
-    S.cnt[3] = big ? ((idle >= F.heavy_idle ? 2 : 0) | (!(F.exp & 2) || idle >= F.heavy_idle ? 1 : 0)) : 0;
+    S.cnt[3] = big ? ((idle >= F.heavy_idle ? 2 : 0) | 1) : 0;
   }
   __syncthreads();
   const bool heavy = (S.cnt[3] & 1) != 0;
@@ -1163,10 +1163,9 @@ __device__ void process_block(const DevFactor &F, int K, Shared &S, unsigned cha
     OVF_CHECK();
   }
   bool both_ok = true;
-  bool both = !(F.exp & 4) &&
-              prepare_both(F, K, s, e, b, CL, nLc, TL, CU, nUc, TU, aL0, aLe, aL1, aU0, aU1, A, S, RL, RU, both_ok);
+  bool both = prepare_both(F, K, s, e, b, CL, nLc, TL, CU, nUc, TU, aL0, aLe, aL1, aU0, aU1, A, S, RL, RU, both_ok);
   if (!both_ok) return;
-  if (!both && !(F.exp & 8)) {
+  if (!both) {
     both = prepare_both2(F, K, s, e, b, CL, nLc, TL, CU, nUc, TU, aL0, aLe, aL1, aU0, aU1, A, S, RL, RU, both_ok);
     if (!both_ok) return;
   }
@@ -2779,7 +2778,7 @@ extern "C" cudaError_t bilu_launch_factor(const DevFactor &F, int grid, cudaStre
   // (the Schur updates read contributor panels through L1)
   {
     int carve = 50;
-    if (const char *cv = getenv("BILU_CARVEOUT")) carve = atoi(cv);
+    if (const char *cv = tune_env("BILU_CARVEOUT")) carve = atoi(cv);
     cudaFuncSetAttribute(factor_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
   }
   factor_kernel<<<grid, NT, F.smem_bytes, st>>>(F);

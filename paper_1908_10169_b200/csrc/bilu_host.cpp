@@ -545,20 +545,20 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   }
   F.heavy_T = 1024;
   F.pair_cap = 128;
-  if (const char *pc = getenv("BILU_PAIR_CAP")) F.pair_cap = atoi(pc);
-  if (const char *ht = getenv("BILU_HEAVY_T")) F.heavy_T = atoi(ht);
+  if (const char *pc = tune_env("BILU_PAIR_CAP")) F.pair_cap = atoi(pc);
+  if (const char *ht = tune_env("BILU_HEAVY_T")) F.heavy_T = atoi(ht);
   F.heavy_idle = 8;
   F.part_items = 512;
   F.wide_flops = 4e6;
   F.scale_split = 1024;
   F.scale_rows = 384;
-  if (const char *ss = getenv("BILU_SCALE_SPLIT")) F.scale_split = atoi(ss);
-  if (const char *sr = getenv("BILU_SCALE_ROWS")) F.scale_rows = std::max(32, atoi(sr));
+  if (const char *ss = tune_env("BILU_SCALE_SPLIT")) F.scale_split = atoi(ss);
+  if (const char *sr = tune_env("BILU_SCALE_ROWS")) F.scale_rows = std::max(32, atoi(sr));
   F.wide_part_flops = 2e6;
-  if (const char *wf = getenv("BILU_WIDE_FLOPS")) F.wide_flops = atof(wf);
-  if (const char *wp = getenv("BILU_WIDE_PART_FLOPS")) F.wide_part_flops = atof(wp);
-  if (const char *pi = getenv("BILU_PART_ITEMS")) F.part_items = std::max(64, atoi(pi));
-  if (const char *hi = getenv("BILU_HEAVY_IDLE")) F.heavy_idle = atoi(hi);
+  if (const char *wf = tune_env("BILU_WIDE_FLOPS")) F.wide_flops = atof(wf);
+  if (const char *wp = tune_env("BILU_WIDE_PART_FLOPS")) F.wide_part_flops = atof(wp);
+  if (const char *pi = tune_env("BILU_PART_ITEMS")) F.part_items = std::max(64, atoi(pi));
+  if (const char *hi = tune_env("BILU_HEAVY_IDLE")) F.heavy_idle = atoi(hi);
   ALLOC(F.ctrl, CTRL_COUNT * CS);
   ALLOC(F.Lrow_off, n_blocks); ALLOC(F.Lm, n_blocks); ALLOC(F.Lval_off, n_blocks);
   ALLOC(F.Ucol_off, n_blocks); ALLOC(F.Uc, n_blocks); ALLOC(F.Uval_off, n_blocks);
@@ -668,12 +668,12 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
 
   // launch geometry: persistent CTAs, all co-resident
   F.smem_bytes = 110 * 1024;
-  if (const char *sk = getenv("BILU_SMEM_KB")) F.smem_bytes = std::max(16, std::min(220, atoi(sk))) * 1024;
+  if (const char *sk = tune_env("BILU_SMEM_KB")) F.smem_bytes = std::max(16, std::min(220, atoi(sk))) * 1024;
   int per_sm = 0;
   if (bilu_factor_occupancy(F.smem_bytes, &per_sm) != cudaSuccess || per_sm < 1) per_sm = 1;
   const int occ = per_sm;
   per_sm = 1;   // one CTA per SM: the rest of the unified L1/shared array caches panels
-  if (const char *cp = getenv("BILU_CTAS_PER_SM")) per_sm = std::max(1, std::min(occ, atoi(cp)));
+  if (const char *cp = tune_env("BILU_CTAS_PER_SM")) per_sm = std::max(1, std::min(occ, atoi(cp)));
   h->grid = opt.n_ctas > 0 ? opt.n_ctas : h->sms * per_sm;
 
   // initial capacities (grown on overflow)
@@ -1020,7 +1020,7 @@ static bilu_status run_phase(bilu_ctx *h, Phase ph, bilu_factor_stats &S, unsign
       bs = prepare_separators(h);
     }
     if (bs != BILU_OK) return bs;
-    const char *dbg_env = getenv("BILU_DEBUG_TIMEOUT");
+    const char *dbg_env = tune_env("BILU_DEBUG_TIMEOUT");
     if (dbg_env && !F.dbg) {
       void *hp = nullptr, *dp = nullptr;
       CUDA_TRY(h, cudaHostAlloc(&hp, 4 * sizeof(int) * h->grid, cudaHostAllocMapped));
@@ -1079,7 +1079,7 @@ static bilu_status run_phase(bilu_ctx *h, Phase ph, bilu_factor_stats &S, unsign
       set_err(h, "bilu_factor: pivot block %d is exactly singular", S.breakdown_block);
       return BILU_ERR_BREAKDOWN;
     }
-    if (getenv("BILU_VERBOSE"))
+    if (tune_env("BILU_VERBOSE"))
       fprintf(stderr, "bilu_factor retry %d (phase %d): code %d block %llu hpool %lld/%lld hctx %llu/%lld work %lld\n",
               attempt, (int)ph, code, ctrl[CTRL_ERRBLK], (long long)ctrl[CTRL_HPOOL], (long long)h->hpool_cap,
               ctrl[CTRL_HCTX], (long long)F.hctx_cap, (long long)h->work_per_cta);
@@ -1113,7 +1113,6 @@ static void factor_setup(bilu_ctx *h, double tau) {
   DevFactor &F = h->F;
   F.tau = tau;
   F.near_rel = h->opt.near_rel;
-  F.exp = getenv("BILU_EXP") ? atoi(getenv("BILU_EXP")) : 0;
 }
 
 // finalize (aggregation post-pass) + statistics shared by bilu_factor and the separator phase
@@ -1794,7 +1793,7 @@ static bilu_status run_sweep(bilu_ctx *h, const int32_t *cnt0, const int32_t *q0
   if (nq) CUDA_TRY(h, cudaMemcpyAsync(A.queue, q0, nq * 4, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(A.ctrl, 0, 4 * sizeof(unsigned long long), st));
   CUDA_TRY(h, cudaMemcpyAsync(A.ctrl, nq_ull, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
-  const char *prof_path = getenv("BILU_APPLY_PROF");   // diagnostics: per-block times to <path>.<sweep>
+  const char *prof_path = tune_env("BILU_APPLY_PROF");   // diagnostics: per-block times to <path>.<sweep>
   unsigned long long *d_prof = nullptr;
   if (prof_path) {
     CUDA_TRY(h, cudaMalloc(&d_prof, sizeof(unsigned long long) * 3 * nF));
@@ -1827,7 +1826,7 @@ extern "C" bilu_status bilu_apply(bilu_ctx *h, const double *x, double *y, void 
   if (!h->apply_ready) { bilu_status s = build_apply(h); if (s != BILU_OK) return s; }
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
   CUDA_TRY(h, bilu_launch_permute(h->d_w, x, h->d_perm, h->n, 0, st));
-  const int only = getenv("BILU_APPLY_ONLY") ? atoi(getenv("BILU_APPLY_ONLY")) : -1;   // diagnostics
+  const int only = tune_env("BILU_APPLY_ONLY") ? atoi(tune_env("BILU_APPLY_ONLY")) : -1;   // diagnostics
   bilu_status s;
   if (only != 1 && (s = run_sweep(h, h->d_cnt_f0, h->d_q_f0, h->nq_f0, &h->nq_f0_ull, h->nt_f0, 0, st)) != BILU_OK)
     return s;
@@ -1932,7 +1931,7 @@ extern "C" bilu_status bilu_ilu1_blocks(int32_t n, const int64_t *row_ptr, const
   if (e == cudaSuccess)
     e = bilu_ilu1_run(n, d_rp, d_ci, d_v, d_pm, d_ipm, tau, max_size, sms, s, block_sizes, n_blocks, &launches);
   cudaStreamSynchronize(s);
-  if (getenv("BILU_VERBOSE")) {
+  if (tune_env("BILU_VERBOSE")) {
     const auto t_dev1 = std::chrono::steady_clock::now();
     fprintf(stderr, "[bilu] ilu1_blocks: host validate+upload %.2f ms, device permute+estimate %.2f ms (%d launches)\n",
             std::chrono::duration<double, std::milli>(t_dev0 - t_host0).count(),
@@ -1982,7 +1981,7 @@ extern "C" bilu_status bilu_cosine_blocks(int32_t n, const int64_t *row_ptr, con
   if (e == cudaSuccess) e = bilu_cosine_run(n, d_rp, d_ci, tau, max_size, sms, s, q, block_sizes, n_blocks, &launches, &rounds);
   cudaStreamSynchronize(s);
   cudaFree(d_rp); cudaFree(d_ci);
-  if (getenv("BILU_VERBOSE")) fprintf(stderr, "[bilu] cosine_blocks: %d launches, %d greedy rounds\n", launches, rounds);
+  if (tune_env("BILU_VERBOSE")) fprintf(stderr, "[bilu] cosine_blocks: %d launches, %d greedy rounds\n", launches, rounds);
   if (n_kernel_launches) *n_kernel_launches = launches;
   if (e != cudaSuccess) {
     set_err(nullptr, "bilu_cosine_blocks: %s", cudaGetErrorString(e));
@@ -2038,7 +2037,7 @@ extern "C" bilu_status bilu_mwm(int32_t n, const int64_t *row_ptr, const int32_t
     if (e == cudaSuccess) e = cudaMemcpyAsync(dr, d_dr, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   }
-  if (getenv("BILU_VERBOSE")) fprintf(stderr, "[bilu] mwm: %d bidding rounds, %d launches\n", rounds, launches);
+  if (tune_env("BILU_VERBOSE")) fprintf(stderr, "[bilu] mwm: %d bidding rounds, %d launches\n", rounds, launches);
   cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_v); cudaFree(d_as); cudaFree(d_dl); cudaFree(d_dr); cudaFree(d_work);
   if (n_kernel_launches) *n_kernel_launches = launches;
   if (e != cudaSuccess) {

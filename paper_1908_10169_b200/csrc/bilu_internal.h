@@ -2,6 +2,19 @@
 // the sm_100a kernels (bilu_kernels.cu).  Not part of the public ABI.
 #pragma once
 #include <stdint.h>
+#include <stdlib.h>
+
+// Tuning and diagnostic switches (BILU_HEAVY_T, BILU_SMEM_KB, BILU_DEBUG_TIMEOUT, ...) are
+// read from the environment only in the builds of tools/ (-DBILU_TUNING, or the per-phase
+// profiling build -DBILU_PROFILE).  The product library ignores the environment.
+static inline const char *tune_env(const char *name) {
+#if defined(BILU_TUNING) || defined(BILU_PROFILE)
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 namespace bilu {
 
@@ -121,7 +134,6 @@ struct DevFactor {
   // Sec. 3.6 perturbation of singular / ill-conditioned pivot blocks (R19)
   int perturb; double ptau, prho, cond_max;
   const double *alpha;                  // device scalar: max |a_ij|
-  int exp;                              // experiment switches (diagnostics only)
   // dense zone: the top blocks of the block elimination tree (a set closed
   // under ancestors, every block at most 8 wide) keep their panels in dense per-block
   // buffers that their contributors update when THEY finish (a right-looking push), so a

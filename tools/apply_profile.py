@@ -8,6 +8,8 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1908_10169_b200.build import build  # noqa: E402
+os.environ["BILU_LIB"] = build(tuning=True)   # BILU_APPLY_PROF is read by the tuning build only
 import torch  # noqa: E402
 from inputs.configs import make_config  # noqa: E402
 from paper_1908_10169_b200 import BILU  # noqa: E402
