@@ -44,7 +44,7 @@ def load_peaks():
 
 def load_traffic(config):
     """DRAM bytes per factor_kernel launch from the committed ncu --set full capture (or None)."""
-    p = os.path.join(ROOT, "profiles", "r01_factor_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r02_factor_traffic.json")
     try:
         d = json.load(open(p))
         if not d["workload"].startswith(config):
@@ -380,7 +380,7 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "factor_kernel (persistent, all of a-1..a-8)",
                          "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": load_traffic(args.config),
-                         "traffic_source": "profiles/r01_factor_traffic.json (ncu --set full, DRAM read+write bytes "
+                         "traffic_source": "profiles/r02_factor_traffic.json (ncu --set full, DRAM read+write bytes "
                                            "per factor_kernel launch)",
                          "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_fp64_peak.md)",
                          "kernel_ms": t_kern,
