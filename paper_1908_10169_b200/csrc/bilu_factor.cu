@@ -1039,6 +1039,19 @@ __device__ void side_gemms(const DevFactor &F, int s, int e, int b, const Contri
 // part runs a-6..a-1 (finish_block).  Same values as the one-CTA path up to the
 // summation order (R13).
 
+// zone panels: unknown with path coordinate zdv in zone block T's panel
+__device__ __forceinline__ int zone_loc(const DevFactor &F, int T, int zdv) { return F.zA[T] - zdv; }
+__device__ __forceinline__ void zone_bit(unsigned *B, const DevFactor &F, int T, int zdv) {
+  const int loc = zone_loc(F, T, zdv);
+  atomicOr(&B[F.zwb[T] + (loc >> 5)], 1u << (loc & 31));
+}
+// local panel index -> unknown, from the run table of the block's path (shared memory)
+__device__ __forceinline__ int zone_unknown(const int2 *runs, int nr, int z) {
+  int r = nr - 1;
+  while (r > 0 && runs[r].x > z) --r;
+  return runs[r].y + (z - runs[r].x);
+}
+
 __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, double *WL, double *WU, const int *rowOf,
                              const int *colOf, int nR, int nC, bool sortedR, bool sortedC, double flops,
                              HeavyCtx *X = nullptr, int mode = 0);
@@ -2110,8 +2123,8 @@ scaled:
   // i of every zone column block T < block(i) of K's columns, column j of every zone row
   // block T < block(j) of K's rows (a-3: the union of the contributors' kept rows / columns).
   if (F.nzb > 0) {
-    // K's kept rows / columns that are zone unknowns (with their zone numbers), and its
-    // row / column runs that are zone blocks
+    // K's kept rows / columns that are zone unknowns (with their path coordinates zd), and
+    // its row / column runs that are zone blocks
     int *zx = (int *)balloc(A, (int64_t)(mK + cK + 2) * 4);
     int *zi = (int *)balloc(A, (int64_t)(mK + cK + 2) * 4);
     int *zrr = (int *)balloc(A, (int64_t)(nRr + nCr + 2) * 4);
@@ -2120,7 +2133,7 @@ scaled:
     __syncthreads();
     for (int x = tid; x < mK + cK; x += NT) {
       const int u = x < mK ? R[x] : Cs[x - mK];
-      const int zl = F.zloc[u];
+      const int zl = F.zd[u];
       if (zl >= 0) {
         const int q = atomicAdd(&S.cnt[x < mK ? 0 : 1], 1);
         if (x < mK) { zx[q] = x; zi[q] = zl; }
@@ -2150,20 +2163,20 @@ scaled:
         if (t < b) d0 = fma(l[t], u[t], d0);
         const int Ti = rb[x], Tj = cb[y];
         if (Tj <= Ti)
-          red_add_f64(F.SL + ((size_t)F.zk[Tj] * F.nz + zi[px]) * 8 + (Cs[y] - F.bstart[Tj]), -(d0 + d1));
+          red_add_f64(F.SL + (size_t)(F.zpb[Tj] + F.zA[Tj] - zi[px]) * 8 + (Cs[y] - F.bstart[Tj]), -(d0 + d1));
         else
-          red_add_f64(F.SU + ((size_t)F.zk[Ti] * F.nz + zi[mK + py]) * 8 + (R[x] - F.bstart[Ti]), -(d0 + d1));
+          red_add_f64(F.SU + (size_t)(F.zpb[Ti] + F.zA[Ti] - zi[mK + py]) * 8 + (R[x] - F.bstart[Ti]), -(d0 + d1));
       }
       // candidate bits: zone row i in every zone column block T < block(i) of K's columns,
       // zone column j in every zone row block T < block(j) of K's rows (zone rows / columns
       // only meet zone blocks: the zone is closed under etree ancestors)
       for (int p = tid; p < nx * nzc; p += NT) {
         const int px = p / nzc, T = zrr[nRr + (p - px * nzc)];
-        if (T < rb[zx[px]]) atomicOr(&F.BL[(size_t)F.zk[T] * F.nzw + (zi[px] >> 5)], 1u << (zi[px] & 31));
+        if (T < rb[zx[px]]) zone_bit(F.BL, F, T, zi[px]);
       }
       for (int p = tid; p < ny * nzr; p += NT) {
         const int py = p / nzr, T = zrr[p - py * nzr];
-        if (T < cb[zx[mK + py]]) atomicOr(&F.BU[(size_t)F.zk[T] * F.nzw + (zi[mK + py] >> 5)], 1u << (zi[mK + py] & 31));
+        if (T < cb[zx[mK + py]]) zone_bit(F.BU, F, T, zi[mK + py]);
       }
       if (tid == 0) atomicAdd((double *)&F.ctrl[CS * CTRL_FLOPS], 2.0 * b * (double)nx * (double)ny);
     }
@@ -2253,25 +2266,30 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
   const int s = F.bstart[K], e = F.bstart[K + 1], b = e - s;
   if (b > 8 || F.perturb) return false;
   const int k = F.zk[K];
-  const int le = F.zloc[s] + b;
-  const int w0 = le >> 5, nw = F.nzw - w0;
+  const int le = b;                                       // panel index of the first unknown >= e_K
+  const int w0 = le >> 5, nw = ((F.zA[K] + 31) >> 5) - w0;
+  const int rr0 = F.zrp[k], nrn = F.zrp[k + 1] - rr0;      // runs of K's etree path
   PROF_T0
   unsigned char *sp = smem;
+  int2 *zr = (int2 *)sp; sp += align16i(nrn * 8);
   unsigned *bm = (unsigned *)sp; sp += align16i(2 * nw * 4);
   int *pre = (int *)sp; sp += align16i((2 * nw + 1) * 4);
   if ((int)(sp - smem) > F.smem_bytes) return false;
-  unsigned *gL = F.BL + (size_t)k * F.nzw + w0, *gU = F.BU + (size_t)k * F.nzw + w0;
+  unsigned *gL = F.BL + F.zwb[K] + w0, *gU = F.BU + F.zwb[K] + w0;
   for (int w = tid; w < 2 * nw; w += NT) {
     const unsigned m = __ldcg(w < nw ? gL + w : gU + (w - nw));
     bm[w] = m;
     pre[w] = __popc(m);
   }
+  for (int x = tid; x < nrn; x += NT) zr[x] = F.zrun[rr0 + x];
   __syncthreads();
   const int tot = cta_scan(pre, 2 * nw, S.tmp);
   const int nR = nw > 0 ? pre[nw] : 0, nC = tot - nR;
   const int nL = b + nR, nl = nL + nC;
-  // shared-memory plan: lines (zone numbers), W (8 doubles per line), flags / positions, D
+  // shared-memory plan: lines (panel indices, then unknowns), their path coordinates, W (8
+  // doubles per line), flags / positions, D
   int *zl = (int *)sp; sp += align16i(nl * 4);
+  int *zq = (int *)sp; sp += align16i(nl * 4);
   int *gb = (int *)sp; sp += align16i(nl * 4);                // block of every line
   int *fl = (int *)sp; sp += align16i((nR + nC + 1) * 4);      // keep flags -> kept positions
   int *kl = (int *)sp; sp += align16i((nR + nC + 1) * 4);      // kept lines (L then U)
@@ -2295,11 +2313,14 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
   __syncthreads();
   // gather the lines (64 B each, 16-byte loads, all in flight) and zero them behind
   for (int ln = tid; ln < nl; ln += NT) {
-    double2 *src = (double2 *)((ln < nL ? F.SL : F.SU) + ((size_t)k * F.nz + zl[ln]) * 8);
+    double2 *src = (double2 *)((ln < nL ? F.SL : F.SU) + (size_t)(F.zpb[K] + zl[ln]) * 8);
     double2 v[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) v[q] = __ldcg(src + q);
-    const int g = F.zblkof[zl[ln]];
+    const int u = zone_unknown(zr, nrn, zl[ln]);
+    const int g = F.block_of[u];
+    zl[ln] = u;
+    zq[ln] = F.zd[u];
     double2 *dst = (double2 *)(W + (size_t)ln * 8);
 #pragma unroll
     for (int q = 0; q < 4; ++q) { dst[q] = v[q]; src[q] = make_double2(0.0, 0.0); }
@@ -2347,7 +2368,7 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
         unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_NEAR], 1ull);
         if (slot < (unsigned long long)F.near_cap) {
           F.near_i[4 * slot] = K; F.near_i[4 * slot + 1] = Lside ? 0 : 1;
-          F.near_i[4 * slot + 2] = F.zglob[zl[Lside ? b + x : nL + (x - nR)]]; F.near_i[4 * slot + 3] = keep;
+          F.near_i[4 * slot + 2] = zl[Lside ? b + x : nL + (x - nR)]; F.near_i[4 * slot + 3] = keep;
           F.near_m[slot] = margin;
         }
       }
@@ -2376,7 +2397,7 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
   }
   const int64_t oLi = (int64_t)S.off[0], oLv = (int64_t)S.off[1], oUi = (int64_t)S.off[2], oUv = (int64_t)S.off[3];
   for (int x = tid; x < nk; x += NT) {
-    const int ln = kl[x], g = F.zglob[zl[ln]];
+    const int ln = kl[x], g = zl[ln];
     if (x < mK) F.Lidx[oLi + x] = g; else F.Uidx[oUi + (x - mK)] = g;
   }
   for (int it = tid; it < nk * b; it += NT) {
@@ -2403,9 +2424,9 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
     }
     const int Ti = gb[lx], Tj = gb[ly];
     if (Tj <= Ti)
-      red_add_f64(F.SL + ((size_t)F.zk[Tj] * F.nz + zl[lx]) * 8 + (F.zglob[zl[ly]] - F.bstart[Tj]), -(d0 + d1));
+      red_add_f64(F.SL + (size_t)(F.zpb[Tj] + F.zA[Tj] - zq[lx]) * 8 + (zl[ly] - F.bstart[Tj]), -(d0 + d1));
     else
-      red_add_f64(F.SU + ((size_t)F.zk[Ti] * F.nz + zl[ly]) * 8 + (F.zglob[zl[lx]] - F.bstart[Ti]), -(d0 + d1));
+      red_add_f64(F.SU + (size_t)(F.zpb[Ti] + F.zA[Ti] - zq[ly]) * 8 + (zl[lx] - F.bstart[Ti]), -(d0 + d1));
   }
   // runs of the kept rows / columns by block (sorted): run[r] = start of run r
   for (int x = tid; x < nk; x += NT) {
@@ -2425,13 +2446,13 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
   // row-run block T < block(j)
   for (int p = tid; p < mK * (nrun - nrr); p += NT) {
     const int x = p / (nrun - nrr), r = nrr + (p - x * (nrun - nrr));
-    const int T = gb[kl[run[r]]], zi = zl[kl[x]];
-    if (T < gb[kl[x]]) atomicOr(&F.BL[(size_t)F.zk[T] * F.nzw + (zi >> 5)], 1u << (zi & 31));
+    const int T = gb[kl[run[r]]];
+    if (T < gb[kl[x]]) zone_bit(F.BL, F, T, zq[kl[x]]);
   }
   for (int p = tid; p < cK * nrr; p += NT) {
     const int y = p / nrr, r = p - y * nrr;
-    const int T = gb[kl[run[r]]], zj = zl[kl[mK + y]];
-    if (T < gb[kl[mK + y]]) atomicOr(&F.BU[(size_t)F.zk[T] * F.nzw + (zj >> 5)], 1u << (zj & 31));
+    const int T = gb[kl[run[r]]];
+    if (T < gb[kl[mK + y]]) zone_bit(F.BU, F, T, zq[kl[mK + y]]);
   }
   // N(K): sorted union of the row-run and column-run blocks; chain edges between neighbours
   if (tid == 0) {
@@ -2478,12 +2499,15 @@ __device__ void process_zone_block(const DevFactor &F, int K, Shared &S, unsigne
   A.gbase = F.work + (size_t)blockIdx.x * F.work_per_cta; A.gused = 0; A.gcap = F.work_per_cta; A.gtop = F.work_per_cta;
   A.ovf = false; A.bottom_global = false; A.pool = false;
   PROF_T0
-  const int le = F.zloc[s] + b;                          // zone number of the first unknown >= e_K
-  const int w0 = le >> 5, nw = F.nzw - w0;                // bitmap words of the zone unknowns >= e_K
+  const int le = b;                                      // panel index of the first unknown >= e_K
+  const int w0 = le >> 5, nw = ((F.zA[K] + 31) >> 5) - w0; // bitmap words of the path unknowns >= e_K
+  const int rr0 = F.zrp[k], nrn = F.zrp[k + 1] - rr0;      // runs of K's etree path
   unsigned *bm = (unsigned *)balloc_top(A, (int64_t)(2 * nw + 2) * 4);
   int *pre = (int *)balloc_top(A, (int64_t)(2 * nw + 2) * 4);
+  int2 *zr = (int2 *)balloc_top(A, (int64_t)(nrn + 1) * 8);
   if (A.ovf) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
-  unsigned *gL = F.BL + (size_t)k * F.nzw + w0, *gU = F.BU + (size_t)k * F.nzw + w0;
+  unsigned *gL = F.BL + F.zwb[K] + w0, *gU = F.BU + F.zwb[K] + w0;
+  for (int x = tid; x < nrn; x += NT) zr[x] = F.zrun[rr0 + x];
   for (int w = tid; w < 2 * nw; w += NT) {
     unsigned *g = w < nw ? gL + w : gU + (w - nw);
     const unsigned m = __ldcg(g);
@@ -2496,7 +2520,7 @@ __device__ void process_zone_block(const DevFactor &F, int K, Shared &S, unsigne
   const int nR = nw > 0 ? pre[nw] : 0, nC = tot - nR;
   double *WL = (double *)balloc(A, (int64_t)(b + nR) * b * 8);
   double *WU = (double *)balloc(A, (int64_t)nC * b * 8);
-  int *zlL = (int *)balloc(A, (int64_t)(b + nR + 1) * 4);      // zone numbers of the lines
+  int *zlL = (int *)balloc(A, (int64_t)(b + nR + 1) * 4);      // panel indices of the lines
   int *zlU = (int *)balloc(A, (int64_t)(nC + 1) * 4);
   int *lineL = (int *)balloc(A, (int64_t)(b + nR + 1) * 4);    // ... and the unknowns
   int *lineU = (int *)balloc(A, (int64_t)(nC + 1) * 4);
@@ -2515,15 +2539,15 @@ __device__ void process_zone_block(const DevFactor &F, int K, Shared &S, unsigne
   }
   __syncthreads();
   for (int x = tid; x < b + nR + nC; x += NT) {
-    if (x < b + nR) lineL[x] = F.zglob[zlL[x]]; else lineU[x - b - nR] = F.zglob[zlU[x - b - nR]];
+    if (x < b + nR) lineL[x] = zone_unknown(zr, nrn, zlL[x]); else lineU[x - b - nR] = zone_unknown(zr, nrn, zlU[x - b - nR]);
   }
   // the lines (64 B each in the zone buffers), zeroed behind
   const int nl = (b + nR + nC) * b;
   for (int it = tid; it < nl; it += NT) {
     const int ln = it / b, c = it - ln * b;
     double *src;
-    if (ln < b + nR) src = F.SL + ((size_t)k * F.nz + zlL[ln]) * 8 + c;
-    else src = F.SU + ((size_t)k * F.nz + zlU[ln - b - nR]) * 8 + c;
+    if (ln < b + nR) src = F.SL + (size_t)(F.zpb[K] + zlL[ln]) * 8 + c;
+    else src = F.SU + (size_t)(F.zpb[K] + zlU[ln - b - nR]) * 8 + c;
     const double v = __ldcg(src);
     if (ln < b + nR) WL[it] = v; else WU[it - (b + nR) * b] = v;
     if (v != 0.0) *src = 0.0;
@@ -2753,14 +2777,14 @@ __global__ void zone_init_kernel(DevFactor F, const int32_t *zblocks) {
   for (int k = blockIdx.x; k < F.nzb; k += gridDim.x) {
     const int K = zblocks[k], e = F.bstart[K + 1];
     for (int64_t p = F.AL_ptr[K] + threadIdx.x; p < F.AL_ptr[K + 1]; p += blockDim.x) {
-      const int rc = F.AL_rc[p], i = rc >> 7, zi = F.zloc[i];
-      F.SL[((size_t)k * F.nz + zi) * 8 + (rc & 127)] = F.AL_val[p];
-      if (i >= e) atomicOr(&F.BL[(size_t)k * F.nzw + (zi >> 5)], 1u << (zi & 31));
+      const int rc = F.AL_rc[p], i = rc >> 7, zi = F.zd[i];
+      F.SL[(size_t)(F.zpb[K] + zone_loc(F, K, zi)) * 8 + (rc & 127)] = F.AL_val[p];
+      if (i >= e) zone_bit(F.BL, F, K, zi);
     }
     for (int64_t p = F.AU_ptr[K] + threadIdx.x; p < F.AU_ptr[K + 1]; p += blockDim.x) {
-      const int rc = F.AU_rc[p], zj = F.zloc[rc >> 7];
-      F.SU[((size_t)k * F.nz + zj) * 8 + (rc & 127)] = F.AU_val[p];
-      atomicOr(&F.BU[(size_t)k * F.nzw + (zj >> 5)], 1u << (zj & 31));
+      const int rc = F.AU_rc[p], zj = F.zd[rc >> 7];
+      F.SU[(size_t)(F.zpb[K] + zone_loc(F, K, zj)) * 8 + (rc & 127)] = F.AU_val[p];
+      zone_bit(F.BU, F, K, zj);
     }
   }
 }

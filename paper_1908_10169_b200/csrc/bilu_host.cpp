@@ -136,6 +136,7 @@ struct bilu_ctx {
   bool zone_dirty = false;            // zone buffers may hold data (a launch did not complete)
   int32_t *d_zblocks = nullptr;       // zone index -> block
   size_t zone_val_bytes = 0, zone_bit_bytes = 0;
+  int64_t zone_unknowns = 0;
   // GMRES: A's CSR structure (original ordering) and the Krylov workspace
   int64_t *d_rp = nullptr; int32_t *d_ci = nullptr;
   double *d_kry = nullptr; int64_t kry_cap = 0;
@@ -594,60 +595,94 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
     F.prio = dpr;
   }
   // ---- dense zone: the top of the block elimination tree of sym(Ã).  The
-  // exact-LU structure of a block column / row lies on its etree path to the root, so a set of
-  // blocks closed under etree ancestors holds every row / column its blocks can ever have.
-  // Blocks are taken by decreasing etree-subtree size (a parent's is larger than its child's,
-  // so every prefix is ancestor-closed) while they are at most 8 wide and the panel buffers
-  // (2 x 64 B x zone blocks x zone unknowns) fit the budget.
-  F.nzb = 0; F.nz = 0; F.nzw = 0;
-  F.zk = F.zloc = F.zglob = F.zblkof = nullptr;
+  // exact-LU structure of a block column / row lies on its etree path to the root (and the
+  // ILU structure inside it), so block T's panel has one row per unknown of that path.  A set
+  // closed under etree ancestors is taken by decreasing etree-subtree size (a parent's is
+  // larger than its child's, so every prefix is ancestor-closed) while the blocks are at most
+  // 8 wide and the panels (2 x 64 B per path unknown) and bitmaps fit the budget.
+  F.nzb = 0;
+  F.zk = F.zA = F.zd = F.zrp = nullptr;
+  F.zpb = F.zwb = nullptr;
+  F.zrun = nullptr;
   F.SL = F.SU = nullptr; F.BL = F.BU = nullptr;
+  h->zone_unknowns = 0;
   if (opt.zone_bytes >= 0 && n_blocks >= 2) {
+    // path lengths A(K) = b_K + A(par K), parents first (par K > K)
+    std::vector<int64_t> pathA(n_blocks, 0);
+    for (int32_t K = n_blocks - 1; K >= 0; --K)
+      pathA[K] = (bstart[K + 1] - bstart[K]) + (par[K] >= 0 ? pathA[par[K]] : 0);
     std::vector<int32_t> order(n_blocks);
     for (int32_t K = 0; K < n_blocks; ++K) order[K] = K;
     std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return sub[x] != sub[y] ? sub[x] > sub[y] : x > y; });
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    const double budget = opt.zone_bytes > 0 ? (double)opt.zone_bytes : std::min(24.0 * (1ull << 30), 0.25 * (double)fr);
-    int64_t nzb = 0, nz = 0;
+    const double budget = opt.zone_bytes > 0 ? (double)opt.zone_bytes : std::min(64.0 * (1ull << 30), 0.45 * (double)fr);
+    int64_t nzb = 0, rows = 0, words = 0;
+    double bytes = 0.0;
     for (int32_t x = 0; x < n_blocks; ++x) {
       const int32_t K = order[x], bK = bstart[K + 1] - bstart[K];
-      if (bK > 8) break;
-      const double bytes = 2.0 * (nzb + 1) * (double)(nz + bK) * 64.0 + 2.0 * (nzb + 1) * (double)((nz + bK + 31) / 32) * 4.0;
-      if (bytes > budget) break;
-      nzb++; nz += bK;
+      if (bK > 8 || pathA[K] > INT32_MAX / 2) break;
+      const int64_t wK = (pathA[K] + 31) / 32;
+      const double add = 2.0 * (double)pathA[K] * 64.0 + 2.0 * (double)wK * 4.0;
+      if (bytes + add > budget) break;
+      bytes += add; nzb++; rows += pathA[K]; words += wK;
     }
     if (nzb >= 2) {
       std::vector<int32_t> zblocks(order.begin(), order.begin() + nzb);
       std::sort(zblocks.begin(), zblocks.end());
-      std::vector<int32_t> zk(n_blocks, -1), zloc(n, -1), zglob;
-      zglob.reserve(nz);
-      for (int32_t k = 0; k < (int32_t)nzb; ++k) zk[zblocks[k]] = k;
-      for (int32_t K : zblocks)
-        for (int32_t i = bstart[K]; i < bstart[K + 1]; ++i) { zloc[i] = (int32_t)zglob.size(); zglob.push_back(i); }
-      const int64_t nzw = (nz + 31) / 32;
+      std::vector<int32_t> zk(n_blocks, -1), zA(n_blocks, 0), zd(n, -1), zrp(nzb + 1, 0);
+      std::vector<int64_t> zpb(n_blocks, -1), zwb(n_blocks, -1);
+      int64_t pr = 0, pw = 0, nzu = 0;
+      for (int64_t k = 0; k < nzb; ++k) {
+        const int32_t K = zblocks[k];
+        zk[K] = (int32_t)k; zA[K] = (int32_t)pathA[K];
+        zpb[K] = pr; zwb[K] = pw;
+        pr += pathA[K]; pw += (pathA[K] + 31) / 32;
+        for (int32_t i = bstart[K]; i < bstart[K + 1]; ++i) zd[i] = (int32_t)(pathA[K] - (i - bstart[K]));
+        nzu += bstart[K + 1] - bstart[K];
+      }
+      // run tables, parents first: runs(K) = [(0, s_K)] + runs(par K) shifted by b_K, the
+      // parent's first run merged into K's when par K = K + 1 (consecutive unknowns)
+      std::vector<std::vector<int2>> runs(nzb);
+      for (int64_t k = nzb - 1; k >= 0; --k) {
+        const int32_t K = zblocks[k], bK = bstart[K + 1] - bstart[K];
+        std::vector<int2> &r = runs[k];
+        r.push_back(make_int2(0, bstart[K]));
+        if (par[K] >= 0) {
+          const std::vector<int2> &rp = runs[zk[par[K]]];
+          for (size_t q = (par[K] == K + 1 ? 1 : 0); q < rp.size(); ++q) r.push_back(make_int2(rp[q].x + bK, rp[q].y));
+        }
+      }
+      std::vector<int2> zrun;
+      for (int64_t k = 0; k < nzb; ++k) { zrp[k] = (int32_t)zrun.size(); zrun.insert(zrun.end(), runs[k].begin(), runs[k].end()); }
+      zrp[nzb] = (int32_t)zrun.size();
       double *sl = nullptr, *su = nullptr;
       unsigned *bl = nullptr, *bu = nullptr;
-      int32_t *dzk = nullptr, *dzl = nullptr, *dzg = nullptr, *dzb = nullptr, *dzo = nullptr;
-      if (dalloc(h, &sl, (size_t)(nzb * nz * 8)) == cudaSuccess && dalloc(h, &su, (size_t)(nzb * nz * 8)) == cudaSuccess &&
-          dalloc(h, &bl, (size_t)(nzb * nzw)) == cudaSuccess && dalloc(h, &bu, (size_t)(nzb * nzw)) == cudaSuccess &&
-          dalloc(h, &dzk, (size_t)n_blocks) == cudaSuccess && dalloc(h, &dzl, (size_t)n) == cudaSuccess &&
-          dalloc(h, &dzg, (size_t)nz) == cudaSuccess && dalloc(h, &dzb, (size_t)nzb) == cudaSuccess &&
-          dalloc(h, &dzo, (size_t)nz) == cudaSuccess) {
-        std::vector<int32_t> zbo(nz);
-        for (int64_t z = 0; z < nz; ++z) zbo[z] = block_of[zglob[z]];
-        cudaMemcpy(dzo, zbo.data(), nz * sizeof(int32_t), cudaMemcpyHostToDevice);
-        F.zblkof = dzo;
-        h->zone_val_bytes = (size_t)(nzb * nz * 8) * sizeof(double);
-        h->zone_bit_bytes = (size_t)(nzb * nzw) * sizeof(unsigned);
+      int32_t *dzk = nullptr, *dzA = nullptr, *dzd = nullptr, *dzrp = nullptr, *dzb = nullptr;
+      int64_t *dpb = nullptr, *dwb = nullptr;
+      int2 *drun = nullptr;
+      if (dalloc(h, &sl, (size_t)(pr * 8)) == cudaSuccess && dalloc(h, &su, (size_t)(pr * 8)) == cudaSuccess &&
+          dalloc(h, &bl, (size_t)pw) == cudaSuccess && dalloc(h, &bu, (size_t)pw) == cudaSuccess &&
+          dalloc(h, &dzk, (size_t)n_blocks) == cudaSuccess && dalloc(h, &dzA, (size_t)n_blocks) == cudaSuccess &&
+          dalloc(h, &dzd, (size_t)n) == cudaSuccess && dalloc(h, &dzrp, (size_t)(nzb + 1)) == cudaSuccess &&
+          dalloc(h, &dzb, (size_t)nzb) == cudaSuccess && dalloc(h, &dpb, (size_t)n_blocks) == cudaSuccess &&
+          dalloc(h, &dwb, (size_t)n_blocks) == cudaSuccess && dalloc(h, &drun, zrun.size()) == cudaSuccess) {
+        h->zone_val_bytes = (size_t)pr * 8 * sizeof(double);
+        h->zone_bit_bytes = (size_t)pw * sizeof(unsigned);
         cudaMemset(sl, 0, h->zone_val_bytes); cudaMemset(su, 0, h->zone_val_bytes);
         cudaMemset(bl, 0, h->zone_bit_bytes); cudaMemset(bu, 0, h->zone_bit_bytes);
         cudaMemcpy(dzk, zk.data(), n_blocks * sizeof(int32_t), cudaMemcpyHostToDevice);
-        cudaMemcpy(dzl, zloc.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice);
-        cudaMemcpy(dzg, zglob.data(), nz * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(dzA, zA.data(), n_blocks * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(dzd, zd.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(dzrp, zrp.data(), (nzb + 1) * sizeof(int32_t), cudaMemcpyHostToDevice);
         cudaMemcpy(dzb, zblocks.data(), nzb * sizeof(int32_t), cudaMemcpyHostToDevice);
-        F.nzb = (int)nzb; F.nz = (int)nz; F.nzw = (int)nzw;
-        F.zk = dzk; F.zloc = dzl; F.zglob = dzg; h->d_zblocks = dzb;
+        cudaMemcpy(dpb, zpb.data(), n_blocks * sizeof(int64_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(dwb, zwb.data(), n_blocks * sizeof(int64_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(drun, zrun.data(), zrun.size() * sizeof(int2), cudaMemcpyHostToDevice);
+        F.nzb = (int)nzb;
+        F.zk = dzk; F.zA = dzA; F.zd = dzd; F.zrp = dzrp; F.zpb = dpb; F.zwb = dwb; F.zrun = drun;
+        h->d_zblocks = dzb;
+        h->zone_unknowns = nzu;
         F.SL = sl; F.SU = su; F.BL = bl; F.BU = bu;
       } else {
         cudaGetLastError();   // no zone if it does not fit (the buffers allocated so far stay owned)
@@ -1156,7 +1191,7 @@ extern "C" bilu_status bilu_factor(bilu_ctx *h, double tau, bilu_factor_stats *s
   S.breakdown_block = -1;
   S.n_blocks_init = h->N;
   S.zone_blocks = h->F.nzb;
-  S.zone_unknowns = h->F.nzb > 0 ? h->F.nz : 0;
+  S.zone_unknowns = h->F.nzb > 0 ? (int32_t)h->zone_unknowns : 0;
   Events ev;
   for (auto &x : ev.e) CUDA_TRY(h, cudaEventCreate(&x));
   h->factored = false;
@@ -1239,7 +1274,7 @@ extern "C" bilu_status bilu_factor_local(bilu_ctx *h, double tau, bilu_factor_st
   S.breakdown_block = -1;
   S.n_blocks_init = h->N;
   S.zone_blocks = h->F.nzb;
-  S.zone_unknowns = h->F.nzb > 0 ? h->F.nz : 0;
+  S.zone_unknowns = h->F.nzb > 0 ? (int32_t)h->zone_unknowns : 0;
   Events ev;
   for (auto &x : ev.e) CUDA_TRY(h, cudaEventCreate(&x));
   h->factored = false;
@@ -1406,7 +1441,7 @@ extern "C" bilu_status bilu_factor_separators(bilu_ctx *h, bilu_factor_stats *st
   S.breakdown_block = -1;
   S.n_blocks_init = h->N;
   S.zone_blocks = h->F.nzb;
-  S.zone_unknowns = h->F.nzb > 0 ? h->F.nz : 0;
+  S.zone_unknowns = h->F.nzb > 0 ? (int32_t)h->zone_unknowns : 0;
   Events ev;
   for (auto &x : ev.e) CUDA_TRY(h, cudaEventCreate(&x));
   int launches = 0;

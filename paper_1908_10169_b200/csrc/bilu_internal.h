@@ -3,6 +3,7 @@
 #pragma once
 #include <stdint.h>
 #include <stdlib.h>
+#include <vector_types.h>
 
 // Tuning and diagnostic switches (BILU_HEAVY_T, BILU_SMEM_KB, BILU_DEBUG_TIMEOUT, ...) are
 // read from the environment only in the builds of tools/ (-DBILU_TUNING, or the per-phase
@@ -137,14 +138,22 @@ struct DevFactor {
   // dense zone: the top blocks of the block elimination tree (a set closed
   // under ancestors, every block at most 8 wide) keep their panels in dense per-block
   // buffers that their contributors update when THEY finish (a right-looking push), so a
-  // ready zone block only gathers its own panel.  The zone's nz unknowns are numbered
-  // 0..nz-1 in increasing order (zloc / zglob); nzb = 0: no zone.
-  //   zk[K]        zone index of block K, or -1
-  //   SL[(zk[K] * nz + zloc[i]) * 8 + c]  entry (i, s_K + c) of block column K (i >= s_K)
-  //   SU[(zk[K] * nz + zloc[j]) * 8 + r]  entry (s_K + r, j) of block row K    (j >= e_K)
-  //   BL / BU[zk[K] * nzw + w]            candidate rows / columns (bit = zone index)
-  int nzb, nz, nzw;
-  const int32_t *zk, *zloc, *zglob, *zblkof;   // zblkof[z] = block of zone unknown z
+  // ready zone block only gathers its own panel.  Panel rows of block T are the unknowns on
+  // T's etree path to the root (the only rows / columns T can have), in increasing order:
+  // unknown i has the path coordinate zd[i] = A(B) - (i - s_B) (B = block of i, A(X) = the
+  // unknowns from X up to the root), and sits at local index zA[T] - zd[i] in T's panel.
+  //   SL[(zpb[T] + loc) * 8 + c]   entry (i, s_T + c) of block column T (i >= s_T)
+  //   SU[(zpb[T] + loc) * 8 + r]   entry (s_T + r, j) of block row T    (j >= e_T)
+  //   BL / BU[zwb[T] + (loc >> 5)]  candidate rows / columns (bit loc & 31)
+  //   zrun[zrp[zk[T]] ..]          runs (first local index, first unknown) of T's path
+  // nzb = 0: no zone.
+  int nzb;
+  const int32_t *zk;                    // [N] zone index of block K, or -1
+  const int32_t *zA;                    // [N] unknowns on the etree path from K to the root
+  const int64_t *zpb, *zwb;             // [N] first panel row / first bitmap word of zone block K
+  const int32_t *zd;                    // [n] path coordinate of zone unknown i, -1 outside the zone
+  const int32_t *zrp;                   // [nzb + 1] run table offsets (by zone index)
+  const int2 *zrun;                     // runs of the paths
   double *SL, *SU;
   unsigned *BL, *BU;
 };

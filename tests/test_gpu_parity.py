@@ -250,6 +250,32 @@ def test_c5_reduced_parity_and_gmres():
     assert ok_g and ok_o and abs(it_g - it_o) <= 1
 
 
+@pytest.mark.parametrize("zone", ["none", "partial", "full"])
+@pytest.mark.parametrize("cfg", ["c2r", "c5r"])
+def test_zone_coverage_parity(cfg, zone):
+    """Dense zone: the factors must not depend on how much of the block
+    elimination tree keeps pushed per-block panels -- none (contributor lists only), a
+    budget-limited top of the tree, or every block (panels over each block's etree path)."""
+    from inputs.configs import config5
+    P = config2(N=24, leaf=128) if cfg == "c2r" else config5(N=20, top_levels=1)
+    nb = len(P.block_sizes)
+    zb = {"none": -1, "partial": 6 << 20, "full": 0}[zone]
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm, zone_bytes=zb)
+    assert_parity(gf, of)
+    assert st["n_merges"] == of.n_merges
+    if zone == "none":
+        assert st["zone_blocks"] == 0
+    elif zone == "full":
+        assert st["zone_blocks"] == nb and st["zone_unknowns"] == P.n
+    else:
+        assert 2 <= st["zone_blocks"] < nb
+    # refactor with new values: the zone buffers are all zero again after a factorization
+    st2 = g.factor(P.tau)
+    gf2 = g.export()
+    assert st2["n_blocks_final"] == st["n_blocks_final"]
+    assert np.array_equal(np.asarray(gf2.Lv), np.asarray(gf.Lv)) or compare_factors(gf2, of, TOL)["problems"] == []
+
+
 @pytest.mark.parametrize("agg", [False, True])
 def test_edge_wide_key_range_posmap(agg):
     """Candidate key ranges wider than 2^18 unknowns (the per-CTA pos-map path of a-3
