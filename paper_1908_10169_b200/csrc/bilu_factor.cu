@@ -1064,17 +1064,26 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
 // Among the blocks K makes ready, the CTA keeps the one with the largest etree subtree (the
 // one nearest the root: the long dependency chains run through the separators) and pushes
 // the others.
-__device__ void release_block(const DevFactor &F, int K, Shared &S) {
+// own: K's static adjacency and chain successors; extra[0 .. nex): further blocks whose
+// pending count K holds (the early-release edges of process_zone_lean); last: K is done (the
+// CTA keeps the best ready block as its continuation, K counts as finished), else every
+// ready block goes to the queue (the CTA still has work for K)
+__device__ void release_block(const DevFactor &F, int K, Shared &S, bool own = true, const int *extra = nullptr,
+                              int nex = 0, bool last = true) {
   const int tid = threadIdx.x;
-  const int a0 = F.adj_ptr[K], a1 = F.adj_ptr[K + 1];
-  const int nS = __ldcg(&F.succ.cnt[K]);
+  const int a0 = F.adj_ptr[K], a1 = own ? F.adj_ptr[K + 1] : a0;
+  const int nS = own ? __ldcg(&F.succ.cnt[K]) : 0;
   if (tid == 0) { S.cnt[0] = 0; S.off[0] = 0ull; }
   __syncthreads();
   int mine = -1;
-  for (int x = tid; x < (a1 - a0) + nS; x += NT) {
-    int T = x < (a1 - a0) ? F.adj[a0 + x] : __ldcg(list_rec(F.succ, K, x - (a1 - a0)));
+  for (int x = tid; x < (a1 - a0) + nS + nex; x += NT) {
+    int T = x < (a1 - a0) ? F.adj[a0 + x] : x < (a1 - a0) + nS ? __ldcg(list_rec(F.succ, K, x - (a1 - a0))) : extra[x - (a1 - a0) - nS];
     if (atomicSub(&F.pending[T], 1) == 1 && (F.owned == nullptr || F.owned[T])) {
-      if (mine >= 0) {   // a thread that releases two keeps the better candidate, pushes the other
+      if (!last) {
+        unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
+        __threadfence();
+        st_vol(&F.queue[slot], T);
+      } else if (mine >= 0) {   // a thread that releases two keeps the better candidate, pushes the other
         const int worse = F.prio[mine] >= F.prio[T] ? T : mine;
         mine = worse == T ? mine : T;
         unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
@@ -1093,10 +1102,11 @@ __device__ void release_block(const DevFactor &F, int K, Shared &S) {
     __threadfence();
     st_vol(&F.queue[slot], mine);
   }
-  if (tid == 0) {
+  if (tid == 0 && last) {
     if (best != 0ull) S.next = (int)(best & 0xffffffffu);
     atomicAdd(&F.ctrl[CS * CTRL_DONE], 1ull);
   }
+  __syncthreads();
 }
 
 // the destination line of every item of one side, into the global pool (split wide blocks)
@@ -2411,23 +2421,6 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
     F.blk_ncand[2 * K] = nR; F.blk_ncand[2 * K + 1] = nC;
   }
   PROF(6);
-  // push K's update into the zone (every kept row / column of a zone block is a zone unknown)
-  for (int p = tid; p < mK * cK; p += NT) {
-    const int x = p / cK, y = p - x * cK;
-    const int lx = kl[x], ly = kl[mK + y];
-    const double *l = W + (size_t)lx * 8, *u = W + (size_t)ly * 8;
-    double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; t += 2) {
-      if (t < b) d0 = fma(l[t], u[t], d0);
-      if (t + 1 < b) d1 = fma(l[t + 1], u[t + 1], d1);
-    }
-    const int Ti = gb[lx], Tj = gb[ly];
-    if (Tj <= Ti)
-      red_add_f64(F.SL + (size_t)(F.zpb[Tj] + F.zA[Tj] - zq[lx]) * 8 + (zl[ly] - F.bstart[Tj]), -(d0 + d1));
-    else
-      red_add_f64(F.SU + (size_t)(F.zpb[Ti] + F.zA[Ti] - zq[ly]) * 8 + (zl[lx] - F.bstart[Ti]), -(d0 + d1));
-  }
   // runs of the kept rows / columns by block (sorted): run[r] = start of run r
   for (int x = tid; x < nk; x += NT) {
     const bool first = (x == 0 || x == mK) ? true : gb[kl[x]] != gb[kl[x - 1]];
@@ -2442,19 +2435,7 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
   if (tid == 0) run[nrun] = nk;
   __syncthreads();
   const int nrr = mK > 0 ? (cK > 0 ? fl[mK] : nrun) : 0;     // row runs, then column runs
-  // candidate bits: zone row i of every column-run block T < block(i); zone column j of every
-  // row-run block T < block(j)
-  for (int p = tid; p < mK * (nrun - nrr); p += NT) {
-    const int x = p / (nrun - nrr), r = nrr + (p - x * (nrun - nrr));
-    const int T = gb[kl[run[r]]];
-    if (T < gb[kl[x]]) zone_bit(F.BL, F, T, zq[kl[x]]);
-  }
-  for (int p = tid; p < cK * nrr; p += NT) {
-    const int y = p / nrr, r = p - y * nrr;
-    const int T = gb[kl[run[r]]];
-    if (T < gb[kl[mK + y]]) zone_bit(F.BU, F, T, zq[kl[mK + y]]);
-  }
-  // N(K): sorted union of the row-run and column-run blocks; chain edges between neighbours
+  // N(K): sorted union of the row-run and column-run blocks
   if (tid == 0) {
     int i = 0, j = nrr, q = 0;
     while (i < nrr || j < nrun) {
@@ -2471,15 +2452,79 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
   }
   __syncthreads();
   const int nN = S.cnt[0];
-  for (int z = tid; z + 1 < nN; z += NT) {
-    atomicAdd(&F.pending[nb[z + 1]], 1);
-    int rec1 = nb[z + 1];
-    list_append(F, F.succ, nb[z], &rec1);
+  // readiness: the chain edges n_z -> n_{z+1} of the readiness rule, and an edge K -> n_z for
+  // every target, released below as soon as K's push into n_z is complete (every n_z waits
+  // for K's release, so its pending count is > 0 here)
+  for (int z = tid; z < nN; z += NT) {
+    atomicAdd(&F.pending[nb[z]], 1);
+    if (z + 1 < nN) {
+      atomicAdd(&F.pending[nb[z + 1]], 1);
+      int rec1 = nb[z + 1];
+      list_append(F, F.succ, nb[z], &rec1);
+    }
+  }
+  // push K's update into the zone (every kept row / column of a zone block is a zone unknown):
+  // pair (x, y) goes to block column Tj if Tj <= Ti, else to block row Ti.  The pairs of the
+  // first target n0 = min N(K) -- the rows in n0 times every column and the columns in n0
+  // times every row -- go first, and n0 is released before the rest: n0 is the next block of
+  // the dependency chain ("early release")
+  auto push = [&](int x, int y) {
+    const int lx = kl[x], ly = kl[mK + y];
+    const double *l = W + (size_t)lx * 8, *u = W + (size_t)ly * 8;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      if (t < b) d0 = fma(l[t], u[t], d0);
+      if (t + 1 < b) d1 = fma(l[t + 1], u[t + 1], d1);
+    }
+    const int Ti = gb[lx], Tj = gb[ly];
+    if (Tj <= Ti)
+      red_add_f64(F.SL + (size_t)(F.zpb[Tj] + F.zA[Tj] - zq[lx]) * 8 + (zl[ly] - F.bstart[Tj]), -(d0 + d1));
+    else
+      red_add_f64(F.SU + (size_t)(F.zpb[Ti] + F.zA[Ti] - zq[ly]) * 8 + (zl[lx] - F.bstart[Ti]), -(d0 + d1));
+  };
+  const int n0 = nN > 0 ? nb[0] : -1;
+  const int r0 = (nrr > 0 && gb[kl[run[0]]] == n0) ? run[1] : 0;                // kept rows in n0
+  const int c0 = (nrun > nrr && gb[kl[run[nrr]]] == n0) ? run[nrr + 1] - mK : 0;  // kept columns in n0
+  {
+    const int p1a = r0 * cK, p1 = p1a + (mK - r0) * c0;
+    for (int p = tid; p < p1; p += NT) {
+      if (p < p1a) { const int x = p / cK; push(x, p - x * cK); }
+      else { const int q = p - p1a, x = q / c0; push(r0 + x, q - x * c0); }
+    }
+    // candidate bits of n0: the rows below n0 if n0 is a column block, the columns after n0
+    // if n0 is a row block
+    if (c0 > 0) for (int x = r0 + tid; x < mK; x += NT) zone_bit(F.BL, F, n0, zq[kl[x]]);
+    if (r0 > 0) for (int y = c0 + tid; y < cK; y += NT) zone_bit(F.BU, F, n0, zq[kl[mK + y]]);
+  }
+  __threadfence();
+  __syncthreads();
+  // K's own edges (static adjacency, chain successors) and n0's: every block K pushes into
+  // also waits for its explicit edge, so nothing else of K is needed by the successors
+  release_block(F, K, S, true, nb, nN > 0 ? 1 : 0, false);
+  {
+    const int q1 = cK - c0;
+    for (int p = tid; p < (mK - r0) * q1; p += NT) { const int x = p / q1; push(r0 + x, c0 + (p - x * q1)); }
+  }
+  // candidate bits: zone row i of every column-run block T < block(i); zone column j of every
+  // row-run block T < block(j) (n0's were set above)
+  {
+    const int cr0 = nrr + (c0 > 0 ? 1 : 0), ncr = nrun - cr0, rr0_ = r0 > 0 ? 1 : 0, nrr2 = nrr - rr0_;
+    for (int p = tid; p < mK * ncr; p += NT) {
+      const int x = p / ncr, r = cr0 + (p - x * ncr);
+      const int T = gb[kl[run[r]]];
+      if (T < gb[kl[x]]) zone_bit(F.BL, F, T, zq[kl[x]]);
+    }
+    for (int p = tid; p < cK * nrr2; p += NT) {
+      const int y = p / nrr2, r = rr0_ + (p - y * nrr2);
+      const int T = gb[kl[run[r]]];
+      if (T < gb[kl[mK + y]]) zone_bit(F.BU, F, T, zq[kl[mK + y]]);
+    }
   }
   __threadfence();
   __syncthreads();
   PROF(7);
-  release_block(F, K, S);
+  release_block(F, K, S, false, nb + 1, nN > 0 ? nN - 1 : 0, true);
   PROF(8);
   PROF_END(0, 0, nR, nC);
   return true;
