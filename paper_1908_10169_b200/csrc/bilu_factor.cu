@@ -55,7 +55,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PROF_END(a, b_, c, d) do { if (threadIdx.x == 0 && g_blkprof) { g_blkprof[32 * (size_t)K + 10] = gtimer(); \
   g_blkprof[32 * (size_t)K + 11] = (a); g_blkprof[32 * (size_t)K + 12] = (b_); g_blkprof[32 * (size_t)K + 13] = (c); \
   g_blkprof[32 * (size_t)K + 14] = (d); g_blkprof[32 * (size_t)K + 15] = blockIdx.x; } } while (0)
+// the time block T became ready and the block whose release did it (profile slots 18, 26)
+#define READY_MARK(T, K) do { if (g_blkprof) { g_blkprof[32 * (size_t)(T) + 18] = gtimer(); \
+  g_blkprof[32 * (size_t)(T) + 26] = (unsigned long long)(K); } } while (0)
 #else
+#define READY_MARK(T, K) do {} while (0)
 #define PROF_END(a, b_, c, d) do {} while (0)
 #define SUBP(i) do {} while (0)
 #define SUBP_T0
@@ -71,6 +75,28 @@ __device__ __forceinline__ unsigned long long ld_vol64(const unsigned long long 
 }
 __device__ __forceinline__ void st_vol(int *p, int v) { *(volatile int *)p = v; }
 
+// high-priority queue: push tasks and the blocks they release (the dependency chains of the
+// zone) are taken before the main queue's backlog
+__device__ __forceinline__ void enqueue_hi(const DevFactor &F, int item) {
+  const unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_HQHEAD], 1ull);
+  __threadfence();
+  if (slot < (unsigned long long)F.hqcap) { st_vol(&F.hq[slot], item); return; }
+  const unsigned long long s2 = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);   // full: main queue
+  st_vol(&F.queue[s2], item);
+}
+__device__ __forceinline__ bool try_dequeue_hi(const DevFactor &F, int &item) {
+  while (true) {
+    const unsigned long long t = ld_vol64(&F.ctrl[CS * CTRL_HQTAIL]);
+    const unsigned long long h = min(ld_vol64(&F.ctrl[CS * CTRL_HQHEAD]), (unsigned long long)F.hqcap);
+    if (t >= h) return false;
+    if (atomicCAS(&F.ctrl[CS * CTRL_HQTAIL], t, t + 1) == t) {
+      int v;
+      while ((v = ld_vol(&F.hq[t])) == -1) __nanosleep(32);   // producer between its ticket and its store
+      item = v;
+      return true;
+    }
+  }
+}
 __device__ __forceinline__ void raise_abort(const DevFactor &F, int code, int blk) {
   if (atomicCAS(&F.ctrl[CS * CTRL_ABORT], 0ull, (unsigned long long)code) == 0ull)
     atomicExch(&F.ctrl[CS * CTRL_ERRBLK], (unsigned long long)blk);
@@ -245,6 +271,7 @@ __device__ __forceinline__ void *balloc_top(Bump &A, int64_t bytes) {
 struct Shared {
   int K;
   int next;              // block made ready by this CTA, run next (release_block)
+  unsigned long long ticket;   // main-queue slot this CTA holds (~0: none)
   int tmp[NW + 1];
   int piv;
   double pivd;
@@ -1079,6 +1106,7 @@ __device__ void release_block(const DevFactor &F, int K, Shared &S, bool own = t
   for (int x = tid; x < (a1 - a0) + nS + nex; x += NT) {
     int T = x < (a1 - a0) ? F.adj[a0 + x] : x < (a1 - a0) + nS ? __ldcg(list_rec(F.succ, K, x - (a1 - a0))) : extra[x - (a1 - a0) - nS];
     if (atomicSub(&F.pending[T], 1) == 1 && (F.owned == nullptr || F.owned[T])) {
+      READY_MARK(T, K);
       if (!last) {
         unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
         __threadfence();
@@ -2464,70 +2492,182 @@ __device__ bool process_zone_lean(const DevFactor &F, int K, Shared &S, unsigned
     }
   }
   // push K's update into the zone (every kept row / column of a zone block is a zone unknown):
-  // pair (x, y) goes to block column Tj if Tj <= Ti, else to block row Ti.  The pairs of the
-  // first target n0 = min N(K) -- the rows in n0 times every column and the columns in n0
-  // times every row -- go first, and n0 is released before the rest: n0 is the next block of
-  // the dependency chain ("early release")
-  auto push = [&](int x, int y) {
-    const int lx = kl[x], ly = kl[mK + y];
-    const double *l = W + (size_t)lx * 8, *u = W + (size_t)ly * 8;
-    double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; t += 2) {
-      if (t < b) d0 = fma(l[t], u[t], d0);
-      if (t + 1 < b) d1 = fma(l[t + 1], u[t + 1], d1);
-    }
-    const int Ti = gb[lx], Tj = gb[ly];
-    if (Tj <= Ti)
-      red_add_f64(F.SL + (size_t)(F.zpb[Tj] + F.zA[Tj] - zq[lx]) * 8 + (zl[ly] - F.bstart[Tj]), -(d0 + d1));
-    else
-      red_add_f64(F.SU + (size_t)(F.zpb[Ti] + F.zA[Ti] - zq[ly]) * 8 + (zl[lx] - F.bstart[Ti]), -(d0 + d1));
-  };
+  // pair (x, y) goes to block column Tj if Tj <= Ti, else to block row Ti, i.e. to the target
+  // min(Ti, Tj).  Every block K pushes into waits for its explicit edge K -> n_z.  The first
+  // target n0 = min N(K) -- the next block of the dependency chain -- is pushed here by the
+  // whole CTA (the rows in n0 times every column, every row times the columns in n0) and
+  // released together with K's own edges (static adjacency, chain successors: they need
+  // nothing more from K); the other targets go to a push task that any idle CTA runs from
+  // K's stored factors (run_push_task), releasing each target when its pairs are complete.
+  // This CTA continues with the next ready block ("early release").
   const int n0 = nN > 0 ? nb[0] : -1;
   const int r0 = (nrr > 0 && gb[kl[run[0]]] == n0) ? run[1] : 0;                // kept rows in n0
   const int c0 = (nrun > nrr && gb[kl[run[nrr]]] == n0) ? run[nrr + 1] - mK : 0;  // kept columns in n0
   {
     const int p1a = r0 * cK, p1 = p1a + (mK - r0) * c0;
     for (int p = tid; p < p1; p += NT) {
-      if (p < p1a) { const int x = p / cK; push(x, p - x * cK); }
-      else { const int q = p - p1a, x = q / c0; push(r0 + x, q - x * c0); }
+      int x, y;
+      if (p < p1a) { x = p / cK; y = p - x * cK; }
+      else { const int q = p - p1a; x = q / c0; y = q - x * c0; x += r0; }
+      const int lx = kl[x], ly = kl[mK + y];
+      const double *l = W + (size_t)lx * 8, *u = W + (size_t)ly * 8;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < 8; t += 2) {
+        if (t < b) d0 = fma(l[t], u[t], d0);
+        if (t + 1 < b) d1 = fma(l[t + 1], u[t + 1], d1);
+      }
+      const int Ti = gb[lx], Tj = gb[ly];
+      if (Tj <= Ti)
+        red_add_f64(F.SL + (size_t)(F.zpb[Tj] + F.zA[Tj] - zq[lx]) * 8 + (zl[ly] - F.bstart[Tj]), -(d0 + d1));
+      else
+        red_add_f64(F.SU + (size_t)(F.zpb[Ti] + F.zA[Ti] - zq[ly]) * 8 + (zl[lx] - F.bstart[Ti]), -(d0 + d1));
     }
-    // candidate bits of n0: the rows below n0 if n0 is a column block, the columns after n0
-    // if n0 is a row block
+    // candidate bits of n0: the rows after n0 if n0 is a column block, the columns after n0
+    // if n0 is a row block (a-3: the union of the contributors' kept rows / columns)
     if (c0 > 0) for (int x = r0 + tid; x < mK; x += NT) zone_bit(F.BL, F, n0, zq[kl[x]]);
     if (r0 > 0) for (int y = c0 + tid; y < cK; y += NT) zone_bit(F.BU, F, n0, zq[kl[mK + y]]);
   }
   __threadfence();
   __syncthreads();
-  // K's own edges (static adjacency, chain successors) and n0's: every block K pushes into
-  // also waits for its explicit edge, so nothing else of K is needed by the successors
-  release_block(F, K, S, true, nb, nN > 0 ? 1 : 0, false);
-  {
-    const int q1 = cK - c0;
-    for (int p = tid; p < (mK - r0) * q1; p += NT) { const int x = p / q1; push(r0 + x, c0 + (p - x * q1)); }
-  }
-  // candidate bits: zone row i of every column-run block T < block(i); zone column j of every
-  // row-run block T < block(j) (n0's were set above)
-  {
-    const int cr0 = nrr + (c0 > 0 ? 1 : 0), ncr = nrun - cr0, rr0_ = r0 > 0 ? 1 : 0, nrr2 = nrr - rr0_;
-    for (int p = tid; p < mK * ncr; p += NT) {
-      const int x = p / ncr, r = cr0 + (p - x * ncr);
-      const int T = gb[kl[run[r]]];
-      if (T < gb[kl[x]]) zone_bit(F.BL, F, T, zq[kl[x]]);
+  // the other targets: a push task (push_mode 1: high-priority queue, 2: main queue; 3: only if
+  // CTAs are idle), else (push_mode 0) this CTA pushes them after releasing n0
+  if (tid == 0) {
+    bool task = nN > 1 && F.push_mode != 0;
+    if (task && F.push_mode == 3)
+      task = (long long)ld_vol64(&F.ctrl[CS * CTRL_QTAIL]) - (long long)ld_vol64(&F.ctrl[CS * CTRL_QHEAD]) >= 1;
+    if (task) {   // published before any release
+      if (F.push_mode == 1) enqueue_hi(F, -2 - K);
+      else {
+        const unsigned long long slot = atomicAdd(&F.ctrl[CS * CTRL_QHEAD], 1ull);
+        __threadfence();
+        st_vol(&F.queue[slot], -2 - K);
+      }
     }
-    for (int p = tid; p < cK * nrr2; p += NT) {
-      const int y = p / nrr2, r = rr0_ + (p - y * nrr2);
-      const int T = gb[kl[run[r]]];
-      if (T < gb[kl[mK + y]]) zone_bit(F.BU, F, T, zq[kl[mK + y]]);
-    }
+    S.cnt[2] = (nN > 1 && !task) ? 1 : 0;
   }
-  __threadfence();
   __syncthreads();
-  PROF(7);
-  release_block(F, K, S, false, nb + 1, nN > 0 ? nN - 1 : 0, true);
+  if (S.cnt[2]) {
+    release_block(F, K, S, true, nb, 1, false);
+    const int q1 = cK - c0;
+    for (int p = tid; p < (mK - r0) * q1; p += NT) {
+      const int x = r0 + p / q1, y = c0 + (p - (p / q1) * q1);
+      const int lx = kl[x], ly = kl[mK + y];
+      const double *l = W + (size_t)lx * 8, *u = W + (size_t)ly * 8;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < 8; t += 2) {
+        if (t < b) d0 = fma(l[t], u[t], d0);
+        if (t + 1 < b) d1 = fma(l[t + 1], u[t + 1], d1);
+      }
+      const int Ti = gb[lx], Tj = gb[ly];
+      if (Tj <= Ti)
+        red_add_f64(F.SL + (size_t)(F.zpb[Tj] + F.zA[Tj] - zq[lx]) * 8 + (zl[ly] - F.bstart[Tj]), -(d0 + d1));
+      else
+        red_add_f64(F.SU + (size_t)(F.zpb[Ti] + F.zA[Ti] - zq[ly]) * 8 + (zl[lx] - F.bstart[Ti]), -(d0 + d1));
+    }
+    // candidate bits of the other targets: zone row i in every column-run block T (after n0)
+    // with T < block(i); zone column j in every row-run block T (after n0) with T < block(j)
+    {
+      const int cr0 = nrr + (c0 > 0 ? 1 : 0), ncr = nrun - cr0, rb0 = r0 > 0 ? 1 : 0, nrb = nrr - rb0;
+      for (int p = tid; p < mK * ncr; p += NT) {
+        const int x = p / ncr, T = gb[kl[run[cr0 + (p - x * ncr)]]];
+        if (T < gb[kl[x]]) zone_bit(F.BL, F, T, zq[kl[x]]);
+      }
+      for (int p = tid; p < cK * nrb; p += NT) {
+        const int y = p / nrb, T = gb[kl[run[rb0 + (p - y * nrb)]]];
+        if (T < gb[kl[mK + y]]) zone_bit(F.BU, F, T, zq[kl[mK + y]]);
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    PROF(7);
+    release_block(F, K, S, false, nb + 1, nN - 1, true);
+  } else {
+    PROF(7);
+    release_block(F, K, S, true, nb, nN > 0 ? 1 : 0, true);
+  }
   PROF(8);
   PROF_END(0, 0, nR, nC);
   return true;
+}
+
+// The push of a finished zone block K into its targets n_1 .. n_{|N(K)|-1} (n_0 was pushed and
+// released by K's own CTA, process_zone_lean): the same products, from K's stored factors --
+// the kept rows of L_K (scaled, row-major) and the kept columns of Ũ_K -- each target pushed by
+// one warp (n_z by warp z mod NW) and released by it when its pairs and candidate bits are
+// complete (explicit edge K -> n_z).  No CTA barrier between targets.
+__device__ void run_push_task(const DevFactor &F, int K, Shared &S, unsigned char *smem) {
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int s = F.bstart[K], b = F.bstart[K + 1] - s;
+  const int mK = F.Lm[K], cK = F.Uc[K], nk = mK + cK;
+  const int64_t oLi = F.Lrow_off[K], oLv = F.Lval_off[K], oUi = F.Ucol_off[K], oUv = F.Uval_off[K];
+  int *gu = (int *)smem;            // unknown of kept row x / kept column mK + y
+  int *gbk = gu + nk;               // ... its block
+  int *gq = gbk + nk;               // ... its path coordinate
+  int *fl = gq + nk;                // run-start flags -> run numbers
+  int *run = fl + nk + 1;           // run starts (row runs, then column runs)
+  int *nb = run + nk + 2;           // N(K)
+  if ((int64_t)(6 * nk + 8) * 4 > F.smem_bytes) { if (tid == 0) raise_abort(F, DEV_OVF_WORK, K); return; }
+  for (int x = tid; x < nk; x += NT) {
+    const int u = x < mK ? F.Lidx[oLi + x] : F.Uidx[oUi + (x - mK)];
+    gu[x] = u; gbk[x] = F.block_of[u]; gq[x] = F.zd[u];
+  }
+  __syncthreads();
+  for (int x = tid; x < nk; x += NT) fl[x] = (x == 0 || x == mK || gbk[x] != gbk[x - 1]) ? 1 : 0;
+  __syncthreads();
+  const int nrun = cta_scan(fl, nk, S.tmp);
+  for (int x = tid; x < nk; x += NT)
+    if (x == 0 || x == mK || gbk[x] != gbk[x - 1]) run[fl[x]] = x;
+  if (tid == 0) run[nrun] = nk;
+  __syncthreads();
+  const int nrr = mK > 0 ? (cK > 0 ? fl[mK] : nrun) : 0;
+  if (tid == 0) {
+    int i = 0, j = nrr, q = 0;
+    while (i < nrr || j < nrun) {
+      const int vi = i < nrr ? gbk[run[i]] : INT_MAX, vj = j < nrun ? gbk[run[j]] : INT_MAX;
+      const int v = min(vi, vj);
+      nb[q++] = v;
+      if (vi == v) ++i;
+      if (vj == v) ++j;
+    }
+    S.cnt[0] = q;
+  }
+  __syncthreads();
+  const int nN = S.cnt[0];
+  const double *Lv = F.Lval + oLv, *Uv = F.Uval + oUv;
+  auto rows_below = [&](int v) { int lo = 0, hi = mK; while (lo < hi) { const int m = (lo + hi) >> 1; if (gbk[m] < v) lo = m + 1; else hi = m; } return lo; };
+  auto cols_below = [&](int v) { int lo = 0, hi = cK; while (lo < hi) { const int m = (lo + hi) >> 1; if (gbk[mK + m] < v) lo = m + 1; else hi = m; } return lo; };
+  for (int z = 1 + wid; z < nN; z += NW) {
+    const int T = nb[z];
+    const int ra = rows_below(T), rb2 = rows_below(T + 1), ca = cols_below(T), cb2 = cols_below(T + 1);
+    // pairs: rows in T x columns >= T, then rows after T x columns in T
+    const int P1 = (rb2 - ra) * (cK - ca), P2 = (mK - rb2) * (cb2 - ca);
+    for (int p = lane; p < P1 + P2; p += 32) {
+      int x, y;
+      if (p < P1) { const int w = cK - ca; x = p / w; y = ca + (p - x * w); x += ra; }
+      else { const int q = p - P1, w = cb2 - ca; x = q / w; y = ca + (q - x * w); x += rb2; }
+      const double *l = Lv + (int64_t)x * b, *u = Uv + (int64_t)y * b;
+      double d0 = 0.0, d1 = 0.0;
+      int t = 0;
+      for (; t + 1 < b; t += 2) { d0 = fma(l[t], u[t], d0); d1 = fma(l[t + 1], u[t + 1], d1); }
+      if (t < b) d0 = fma(l[t], u[t], d0);
+      const int Ti = gbk[x], Tj = gbk[mK + y];
+      if (Tj <= Ti)
+        red_add_f64(F.SL + (size_t)(F.zpb[Tj] + F.zA[Tj] - gq[x]) * 8 + (gu[mK + y] - F.bstart[Tj]), -(d0 + d1));
+      else
+        red_add_f64(F.SU + (size_t)(F.zpb[Ti] + F.zA[Ti] - gq[mK + y]) * 8 + (gu[x] - F.bstart[Ti]), -(d0 + d1));
+    }
+    if (cb2 > ca) for (int x = rb2 + lane; x < mK; x += 32) zone_bit(F.BL, F, T, gq[x]);
+    if (rb2 > ra) for (int y = cb2 + lane; y < cK; y += 32) zone_bit(F.BU, F, T, gq[mK + y]);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0 && atomicSub(&F.pending[T], 1) == 1) {
+      READY_MARK(T, K);
+      enqueue_hi(F, T);
+    }
+  }
+  __syncthreads();
 }
 
 // a-2 .. a-5 of a block of the dense trailing zone: when the block is ready
@@ -2606,7 +2746,7 @@ __device__ void process_zone_block(const DevFactor &F, int K, Shared &S, unsigne
 __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Shared S;
-  if (threadIdx.x == 0) S.next = -1;
+  if (threadIdx.x == 0) { S.next = -1; S.ticket = ~0ull; }
   __syncthreads();
   while (true) {
     if (threadIdx.x == 0) {
@@ -2614,18 +2754,23 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
       long long _w0 = clock64();
 #endif
       int K = -1;
-      unsigned long long idx = ~0ull;
       if (S.next >= 0) { K = S.next; S.next = -1; }                // continuation (release_block)
-      else idx = aborted(F) ? ~0ull : atomicAdd(&F.ctrl[CS * CTRL_QTAIL], 1ull);
-      if (idx < (unsigned long long)F.qcap) {
-        unsigned ns = 32, polls = 0;
-        while (true) {
-          K = ld_vol(&F.queue[idx]);
-          if (K >= 0) break;
-          if ((++polls & 15u) == 0 &&
-              (aborted(F) || ld_vol64(&F.ctrl[CS * CTRL_DONE]) >= (unsigned long long)F.n_target)) { K = -1; break; }
-          __nanosleep(ns);
-          if (ns < 256) ns <<= 1;
+      else if (!try_dequeue_hi(F, K)) {
+        // the main queue: hold a ticket (kept across high-priority items taken meanwhile)
+        if (S.ticket == ~0ull && !aborted(F)) S.ticket = atomicAdd(&F.ctrl[CS * CTRL_QTAIL], 1ull);
+        if (S.ticket < (unsigned long long)F.qcap) {
+          unsigned ns = 32, polls = 0;
+          while (true) {
+            K = ld_vol(&F.queue[S.ticket]);
+            if (K != -1) { S.ticket = ~0ull; break; }          // a block, a part task or a push task (<= -2)
+            if (try_dequeue_hi(F, K)) break;
+            if ((++polls & 15u) == 0 &&
+                (aborted(F) || ld_vol64(&F.ctrl[CS * CTRL_DONE]) >= (unsigned long long)F.n_target)) { K = -1; break; }
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+          }
+        } else {
+          K = -1;
         }
       }
       S.K = K;
@@ -2636,10 +2781,12 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(DevFactor F) {
     }
     __syncthreads();
     const int K = S.K;
-    if (K < 0) break;
+    if (K == -1) break;
     DBGK(K);
     __threadfence();
-    if (K < F.N) {
+    if (K <= -2) {
+      run_push_task(F, -2 - K, S, smem);
+    } else if (K < F.N) {
       if (F.nzb > 0 && F.zk[K] >= 0) {
         if (!process_zone_lean(F, K, S, smem)) process_zone_block(F, K, S, smem);
       }

@@ -522,8 +522,12 @@ extern "C" bilu_status bilu_analyze(int32_t n, const int64_t *row_ptr, const int
   ALLOC(F.pending, n_blocks);
   // heavy-block splitting: contexts, part tasks in the queue
   F.hctx_cap = std::max<int64_t>(256, n_blocks);          // a block is split at most once
-  F.qcap = (int64_t)n_blocks + F.hctx_cap * bilu_max_parts();
+  F.qcap = 2 * (int64_t)n_blocks + F.hctx_cap * bilu_max_parts();   // blocks, push tasks, part tasks
   ALLOC(F.queue, F.qcap);
+  F.hqcap = 2 * (int64_t)n_blocks + 64;
+  F.push_mode = 0;   // 0: the CTA pushes every target (n0 first, released early); 1-3: push tasks (tools/ builds)
+  if (const char *pm = tune_env("BILU_PUSH_MODE")) F.push_mode = atoi(pm);
+  ALLOC(F.hq, F.hqcap);
   {
     void *hc = nullptr;
     if (cudaMalloc(&hc, (size_t)F.hctx_cap * bilu_heavyctx_size()) != cudaSuccess) {
@@ -819,6 +823,7 @@ static bilu_status reset_schedule(bilu_ctx *h, const int32_t *d_ready, int32_t n
   h->qhead0 = (unsigned long long)nready;
   CUDA_TRY(h, cudaMemcpyAsync(F.pending, h->d_pending0, N * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(F.queue, 0xFF, F.qcap * sizeof(int32_t), st));
+  CUDA_TRY(h, cudaMemsetAsync(F.hq, 0xFF, F.hqcap * sizeof(int32_t), st));
   if (nready)
     CUDA_TRY(h, cudaMemcpyAsync(F.queue, d_ready, nready * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(F.ctrl, 0, CTRL_COUNT * CS * sizeof(unsigned long long), st));
@@ -1419,6 +1424,7 @@ static bilu_status prepare_separators(bilu_ctx *h) {
   h->ctrl_init[CS * CTRL_DONE] = (unsigned long long)(h->N - nsep);
   CUDA_TRY(h, cudaMemcpyAsync(F.ctrl, h->ctrl_init, sizeof(h->ctrl_init), cudaMemcpyHostToDevice, st));
   CUDA_TRY(h, cudaMemsetAsync(F.queue, 0xFF, F.qcap * sizeof(int32_t), st));
+  CUDA_TRY(h, cudaMemsetAsync(F.hq, 0xFF, F.hqcap * sizeof(int32_t), st));
   std::vector<int32_t> ifc(h->own_ifc);
   ifc.insert(ifc.end(), h->remote_ifc.begin(), h->remote_ifc.end());
   if ((int64_t)ifc.size() > h->ifc_cap) {

@@ -64,6 +64,8 @@ enum : int {
   CTRL_HPOOL,      // doubles used in the heavy-block pool
   CTRL_HCTX,       // heavy contexts used
   CTRL_NPERT,      // pivot blocks perturbed (Sec. 3.6)
+  CTRL_HQHEAD,     // high-priority queue (push tasks and the blocks they release)
+  CTRL_HQTAIL,
   CTRL_COUNT = 24
 };
 constexpr int CS = 16;   // ctrl stride: every control word on its own 128-byte line
@@ -98,6 +100,8 @@ struct DevFactor {
   const int32_t *prio;       // [N] continuation priority: etree subtree size (unknowns), >= 1
   int64_t qcap;
   unsigned long long *ctrl;  // [CTRL_COUNT * CS]
+  int32_t *hq; int64_t hqcap;  // high-priority queue (-1 = empty slot)
+  int push_mode;               // zone push of the targets after n0
   // factors (per original block)
   int64_t *Lrow_off; int32_t *Lm; int64_t *Lval_off;
   int64_t *Ucol_off; int32_t *Uc; int64_t *Uval_off;
