@@ -1514,18 +1514,20 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
       double v = 0.0;
 #pragma unroll
       for (int u = 0; u < RP; ++u) if (c0 + u == col) v = x[u];
-      double a = (act && i >= from) ? fabs(v) : -1.0;
-      int r = i;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {        // lower row wins ties
-        const double ao = __shfl_xor_sync(0xffffffffu, a, o), vo = __shfl_xor_sync(0xffffffffu, v, o);
-        const int ro = __shfl_xor_sync(0xffffffffu, r, o);
-        if (ao > a || (ao == a && ro < r)) { a = ao; v = vo; r = ro; }
-      }
+      // exact argmax of |v| over the warp's rows >= from, lowest row on ties, by two integer
+      // max-reductions of the 64-bit key bits(|v|) + 1 (0: not a candidate; the bit pattern of
+      // a non-negative double orders like its value) -- instead of five shuffle rounds
+      const unsigned long long key = (act && i >= from) ? (unsigned long long)__double_as_longlong(fabs(v)) + 1ull : 0ull;
+      const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+      const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      const int w = __ffs(__ballot_sync(0xffffffffu, hi == mh && lo == ml)) - 1;
+      const double vw = __shfl_sync(0xffffffffu, v, w);
       if (lane == 0) {
+        const bool none = (mh | ml) == 0u;
         double *slot = pv + (col & 1) * 2 * NWS;
-        slot[i / 32] = a < 0.0 ? 0.0 : v;
-        ((int *)(slot + NWS))[i / 32] = a < 0.0 ? INT_MAX : r;
+        slot[i / 32] = none ? 0.0 : vw;
+        ((int *)(slot + NWS))[i / 32] = none ? INT_MAX : i + w;
       }
     };
     if (g == 0) publish(0, 0);
