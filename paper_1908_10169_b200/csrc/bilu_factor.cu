@@ -1500,23 +1500,29 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
 // shared-memory version below.  P: 2 b^2 doubles; pv: >= 8 doubles.
 template <int BR, int RP>
 __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double *pv, Shared &S) {
+  // P and pv are in shared memory (checked by the caller): 32-bit shared addresses and
+  // ld/st.shared instead of generic 64-bit pointer arithmetic on every access
   constexpr int G = 4, NTH = BR * G, NWS = BR / 32;   // warps per column group
   static_assert(G * RP >= BR && NTH <= NT && BR % 32 == 0, "shape");
   const int tid = threadIdx.x, i = tid % BR, g = tid / BR, c0 = g * RP, lane = tid & 31;
-  const int64_t bb = (int64_t)b * b;
+  const int bb = b * b;
+  const unsigned sP = (unsigned)__cvta_generic_to_shared(P), sV = (unsigned)__cvta_generic_to_shared(pv);
+  auto lds = [](unsigned a) { double v; asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory"); return v; };
+  auto sts = [](unsigned a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory"); };
+  auto ldsi = [](unsigned a) { int v; asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory"); return v; };
+  auto stsi = [](unsigned a, int v) { asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); };
   if (tid < NTH) {
     const bool act = i < b;
     double x[RP];
 #pragma unroll
-    for (int u = 0; u < RP; ++u) x[u] = (act && c0 + u < b) ? P[i + (int64_t)(c0 + u) * b] : 0.0;
-    // warp maxima of column col over rows >= from (owners of col only; whole warps)
+    for (int u = 0; u < RP; ++u) x[u] = (act && c0 + u < b) ? lds(sP + 8u * (unsigned)(i + (c0 + u) * b)) : 0.0;
+    // warp maxima of column col over rows >= from (owners of col only; whole warps): exact
+    // argmax of |v|, lowest row on ties, by two integer max-reductions of the 64-bit key
+    // bits(|v|) + 1 (0: not a candidate; the bits of a non-negative double order like its value)
     auto publish = [&](int col, int from) {
       double v = 0.0;
 #pragma unroll
       for (int u = 0; u < RP; ++u) if (c0 + u == col) v = x[u];
-      // exact argmax of |v| over the warp's rows >= from, lowest row on ties, by two integer
-      // max-reductions of the 64-bit key bits(|v|) + 1 (0: not a candidate; the bit pattern of
-      // a non-negative double orders like its value) -- instead of five shuffle rounds
       const unsigned long long key = (act && i >= from) ? (unsigned long long)__double_as_longlong(fabs(v)) + 1ull : 0ull;
       const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
       const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
@@ -1525,41 +1531,41 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
       const double vw = __shfl_sync(0xffffffffu, v, w);
       if (lane == 0) {
         const bool none = (mh | ml) == 0u;
-        double *slot = pv + (col & 1) * 2 * NWS;
-        slot[i / 32] = none ? 0.0 : vw;
-        ((int *)(slot + NWS))[i / 32] = none ? INT_MAX : i + w;
+        const unsigned slot = sV + 8u * (unsigned)((col & 1) * 2 * NWS);
+        sts(slot + 8u * (i / 32), none ? 0.0 : vw);
+        stsi(slot + 8u * NWS + 4u * (i / 32), none ? INT_MAX : i + w);
       }
     };
     if (g == 0) publish(0, 0);
     asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
     bool sing = false;
     for (int k = 0; k < b; ++k) {
-      const double *cur = (k & 1) ? P + bb : P;
-      double *nxt = (k & 1) ? P : P + bb;
-      const double *slot = pv + (k & 1) * 2 * NWS;
-      double vb = slot[0], best = fabs(vb);
-      int bi = ((const int *)(slot + NWS))[0];
+      const unsigned cur = (k & 1) ? sP + 8u * bb : sP;
+      const unsigned nxt = (k & 1) ? sP : sP + 8u * bb;
+      const unsigned slot = sV + 8u * (unsigned)((k & 1) * 2 * NWS);
+      double vb = lds(slot), best = fabs(vb);
+      int bi = ldsi(slot + 8u * NWS);
 #pragma unroll
       for (int q = 1; q < NWS; ++q) {           // warps in row order: the first maximum wins
-        const double vq = slot[q];
-        if (fabs(vq) > best) { best = fabs(vq); vb = vq; bi = ((const int *)(slot + NWS))[q]; }
+        const double vq = lds(slot + 8u * q);
+        if (fabs(vq) > best) { best = fabs(vq); vb = vq; bi = ldsi(slot + 8u * NWS + 4u * q); }
       }
       if (!(best > 0.0)) { sing = true; break; }   // identical decision in every thread
       // every shared-memory read of the step before any write
       double pr[RP];
 #pragma unroll
-      for (int u = 0; u < RP; ++u) pr[u] = cur[bi + (int64_t)min(c0 + u, b - 1) * b];   // old row bi
-      const double aik = act ? cur[i + (int64_t)k * b] : 0.0;
+      for (int u = 0; u < RP; ++u) pr[u] = lds(cur + 8u * (unsigned)(bi + min(c0 + u, b - 1) * b));   // old row bi
+      const double aik = act ? lds(cur + 8u * (unsigned)(i + k * b)) : 0.0;
       const double d = 1.0 / vb;
 #pragma unroll
       for (int u = 0; u < RP; ++u) pr[u] *= d;  // the new pivot row, scaled
       const bool kin = k / RP == g;             // this column group owns column k (warp-uniform)
       if (i == bi && i != k) {                  // row bi takes old row k (one lane)
-        const double ckk = cur[k + (int64_t)k * b];
+        const double ckk = lds(cur + 8u * (unsigned)(k + k * b));
 #pragma unroll
         for (int u = 0; u < RP; ++u) {
           const int c = min(c0 + u, b - 1);
-          x[u] = (c0 + u == k) ? -ckk * d : fma(-ckk, pr[u], cur[k + (int64_t)c * b]);
+          x[u] = (c0 + u == k) ? -ckk * d : fma(-ckk, pr[u], lds(cur + 8u * (unsigned)(k + c * b)));
         }
       } else if (i == k) {                      // the pivot row (one lane)
 #pragma unroll
@@ -1574,7 +1580,7 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
       if (act) {
 #pragma unroll
         for (int u = 0; u < RP; ++u)
-          if (c0 + u < b) nxt[i + (int64_t)(c0 + u) * b] = x[u];
+          if (c0 + u < b) sts(nxt + 8u * (unsigned)(i + (c0 + u) * b), x[u]);
       }
       if (k + 1 < b && (k + 1) / RP == g) publish(k + 1, k + 1);
       if (tid == 0) ipiv[k] = bi;
@@ -1592,12 +1598,13 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
       asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
       // column jd of the result = column fcol[2b + jd] of the eliminated matrix: the
       // eliminated matrix sits in the ping-pong copy written last; gather from it
-      const double *fin = (b & 1) ? P + bb : P;
+      const bool fin0 = (b & 1) == 0;           // the last copy written is P itself
+      const unsigned fin = fin0 ? sP : sP + 8u * bb, dst = fin0 ? sP + 8u * bb : sP;
       if (act)
-        for (int jd = g; jd < b; jd += G) P[i + (int64_t)jd * b + (fin == P ? bb : 0)] = fin[i + (int64_t)(int)fcol[2 * b + jd] * b];
+        for (int jd = g; jd < b; jd += G) sts(dst + 8u * (unsigned)(i + jd * b), lds(fin + 8u * (unsigned)(i + (int)fcol[2 * b + jd] * b)));
       asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
-      if (fin == P)
-        for (int e = tid; e < (int)bb; e += NTH) P[e] = P[bb + e];
+      if (fin0)
+        for (int e = tid; e < bb; e += NTH) sts(sP + 8u * e, lds(sP + 8u * (bb + e)));
     }
     if (tid == 0) S.piv = sing ? 1 : 0;
   }
@@ -1609,7 +1616,7 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
 // of P and 3 b of fcol), Gauss-Jordan with partial pivoting inside the block
 // (ties -> lowest row, R6).  CTA-wide; returns true if a pivot is exactly 0.
 __device__ __noinline__ bool gj_invert(double *P, int b, int *ipiv, double *fcol, Shared &S, bool reg = true) {
-  if (reg && b > 8 && b <= 64) {
+  if (reg && b > 8 && b <= 64 && __isShared(P)) {
     __shared__ double pvbuf[8];
     if (b <= 32) return gj_invert_reg<32, 8>(P, b, ipiv, fcol, pvbuf, S);
     return gj_invert_reg<64, 16>(P, b, ipiv, fcol, pvbuf, S);

@@ -18,6 +18,15 @@
 
 namespace bilu {
 
+// dynamic shared memory of the calling kernel: a generic pointer into it, re-derived from this
+// array, lets the compiler emit 32-bit ld/st.shared instead of generic 64-bit accesses
+extern __shared__ double dyn_sm[];
+template <class T>
+__device__ __forceinline__ T *as_shared(T *p) {
+  const unsigned off = (unsigned)__cvta_generic_to_shared(p) - (unsigned)__cvta_generic_to_shared(dyn_sm);
+  return (T *)((char *)dyn_sm + off);
+}
+
 struct DMat {
   const double *p;
   int64_t rs, cs;   // element (i, j) at p[i * rs + j * cs]
@@ -38,7 +47,7 @@ constexpr int DGEMM_SMEM_DOUBLES = 2 * GT * GS;
 // Ends with __syncthreads().  C may alias neither A nor B.
 // Epilogue functor: epi(i, j, acc) receives every output element (i < M, j < N) once.
 template <int NTH, class Epi>
-__device__ void cta_dgemm_epi(int M, int N, int K, DMat A, DMat B, Epi epi, double *smem) {
+__device__ __forceinline__ void cta_dgemm_epi_impl(int M, int N, int K, DMat A, DMat B, Epi epi, double *smem) {
   constexpr int NWARP = NTH / 32;
   constexpr int WN = NWARP >= 4 ? 4 : NWARP;          // warps along n
   constexpr int WM = NWARP / WN;                       // warps along m
@@ -116,6 +125,12 @@ __device__ void cta_dgemm_epi(int M, int N, int K, DMat A, DMat B, Epi epi, doub
   __syncthreads();
 }
 
+template <int NTH, class Epi>
+__device__ void cta_dgemm_epi(int M, int N, int K, DMat A, DMat B, Epi epi, double *smem) {
+  if (__isShared(smem)) cta_dgemm_epi_impl<NTH>(M, N, K, A, B, epi, as_shared(smem));
+  else cta_dgemm_epi_impl<NTH>(M, N, K, A, B, epi, smem);
+}
+
 // Tall-skinny product C[M x N] = A[M x K] * B[K x N] with K, N <= NMAX: B is staged once
 // in shared memory (Bs, K rows of ldb = NMAX + 4 doubles, zero-padded to NMAX columns) and
 // every warp streams its own 8-row tiles of A from global memory (one m8n8k4 A fragment
@@ -141,7 +156,7 @@ __device__ void tsgemm_stage_b(int K, int N, DMat B, double *Bs) {
 // rmax (optional): rmax[i] = max_j |C(i, j)| (every tile spans all N columns, so a 4-lane
 // shuffle reduction gives complete row maxima)
 template <int NTH, int NMAX, class Epi>
-__device__ void cta_tsgemm(int M, int N, int K, DMat A, const double *Bs, Epi epi, double *rmax = nullptr) {
+__device__ __forceinline__ void cta_tsgemm_impl(int M, int N, int K, DMat A, const double *Bs, Epi epi, double *rmax) {
   constexpr int NWARP = NTH / 32, NF = NMAX / 8, LDB = TsB<NMAX>::LDB;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -190,6 +205,12 @@ __device__ void cta_tsgemm(int M, int N, int K, DMat A, const double *Bs, Epi ep
       if (rv && q == 0) rmax[row] = mx;
     }
   }
+}
+
+template <int NTH, int NMAX, class Epi>
+__device__ void cta_tsgemm(int M, int N, int K, DMat A, const double *Bs, Epi epi, double *rmax = nullptr) {
+  if (__isShared(Bs)) cta_tsgemm_impl<NTH, NMAX>(M, N, K, A, as_shared(Bs), epi, rmax);
+  else cta_tsgemm_impl<NTH, NMAX>(M, N, K, A, Bs, epi, rmax);
 }
 
 struct EpiAxpby {

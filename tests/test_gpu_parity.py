@@ -310,6 +310,18 @@ def test_c5_full_parity_and_gmres():
     assert ok_g and ok_o and abs(it_g - it_o) <= 1
 
 
+def test_c4_full_parity():
+    """BASELINE configs[3] at full size (20,000 dense blocks of 16-64, n = 802,382, 422M nnz),
+    in the bench.py launch configuration; the oracle takes a few minutes single-threaded."""
+    from inputs.configs import config4
+    P = config4()
+    assert P.nnz == 422328517
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    assert st["n_blocks_init"] == 20000 and st["n_blocks_final"] == of.nblk
+    r = assert_parity(gf, of)
+    assert r["max_rel"] <= TOL
+
+
 def test_c4_2000_blocks_parity():
     """BASELINE configs[3] recipe with 2,000 of its 20,000 blocks (n ~ 80k, nnz ~ 43M): the
     split wide-block path (contributor-range GEMM parts, scaling parts) at scale."""
