@@ -1500,13 +1500,17 @@ __device__ void run_part(const DevFactor &F, int task, Shared &S, unsigned char 
 // shared-memory version below.  P: 2 b^2 doubles; pv: >= 8 doubles.
 template <int BR, int RP>
 __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double *pv, Shared &S) {
-  // P and pv are in shared memory (checked by the caller): 32-bit shared addresses and
-  // ld/st.shared instead of generic 64-bit pointer arithmetic on every access
+  // P and pv are in shared memory (checked by the caller), P with room for 2 BR^2 doubles: the
+  // elimination runs on diag(P_K, I) padded to BR x BR (leading dimension BR), so every shared
+  // access has a compile-time offset from one per-thread base and needs no bounds check (the
+  // identity part never changes: its rows are 0 in the pivot columns and the pivot rows are 0
+  // in its columns); 32-bit ld/st.shared instead of generic 64-bit pointer arithmetic
   constexpr int G = 4, NTH = BR * G, NWS = BR / 32;   // warps per column group
-  static_assert(G * RP >= BR && NTH <= NT && BR % 32 == 0, "shape");
+  constexpr unsigned CST = 8u * BR;                     // bytes between columns
+  static_assert(G * RP == BR && NTH <= NT && BR % 32 == 0, "shape");
   const int tid = threadIdx.x, i = tid % BR, g = tid / BR, c0 = g * RP, lane = tid & 31;
-  const int bb = b * b;
   const unsigned sP = (unsigned)__cvta_generic_to_shared(P), sV = (unsigned)__cvta_generic_to_shared(pv);
+  const unsigned buf1 = sP + 8u * BR * BR;
   auto lds = [](unsigned a) { double v; asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory"); return v; };
   auto sts = [](unsigned a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory"); };
   auto ldsi = [](unsigned a) { int v; asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory"); return v; };
@@ -1515,7 +1519,8 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
     const bool act = i < b;
     double x[RP];
 #pragma unroll
-    for (int u = 0; u < RP; ++u) x[u] = (act && c0 + u < b) ? lds(sP + 8u * (unsigned)(i + (c0 + u) * b)) : 0.0;
+    for (int u = 0; u < RP; ++u)
+      x[u] = (act && c0 + u < b) ? lds(sP + 8u * (unsigned)(i + (c0 + u) * b)) : (i == c0 + u ? 1.0 : 0.0);
     // warp maxima of column col over rows >= from (owners of col only; whole warps): exact
     // argmax of |v|, lowest row on ties, by two integer max-reductions of the 64-bit key
     // bits(|v|) + 1 (0: not a candidate; the bits of a non-negative double order like its value)
@@ -1536,12 +1541,18 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
         stsi(slot + 8u * NWS + 4u * (i / 32), none ? INT_MAX : i + w);
       }
     };
+    asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");   // P read into registers before the padded copy
+    {
+      const unsigned my = sP + 8u * i + CST * c0;
+#pragma unroll
+      for (int u = 0; u < RP; ++u) sts(my + CST * u, x[u]);
+    }
     if (g == 0) publish(0, 0);
     asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
     bool sing = false;
     for (int k = 0; k < b; ++k) {
-      const unsigned cur = (k & 1) ? sP + 8u * bb : sP;
-      const unsigned nxt = (k & 1) ? sP : sP + 8u * bb;
+      const unsigned cur = (k & 1) ? buf1 : sP;
+      const unsigned nxt = (k & 1) ? sP : buf1;
       const unsigned slot = sV + 8u * (unsigned)((k & 1) * 2 * NWS);
       double vb = lds(slot), best = fabs(vb);
       int bi = ldsi(slot + 8u * NWS);
@@ -1553,34 +1564,36 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
       if (!(best > 0.0)) { sing = true; break; }   // identical decision in every thread
       // every shared-memory read of the step before any write
       double pr[RP];
+      {
+        const unsigned rowbi = cur + 8u * bi + CST * c0;
 #pragma unroll
-      for (int u = 0; u < RP; ++u) pr[u] = lds(cur + 8u * (unsigned)(bi + min(c0 + u, b - 1) * b));   // old row bi
-      const double aik = act ? lds(cur + 8u * (unsigned)(i + k * b)) : 0.0;
+        for (int u = 0; u < RP; ++u) pr[u] = lds(rowbi + CST * u);   // old row bi
+      }
+      const double aik = lds(cur + 8u * i + CST * k);
       const double d = 1.0 / vb;
 #pragma unroll
       for (int u = 0; u < RP; ++u) pr[u] *= d;  // the new pivot row, scaled
       const bool kin = k / RP == g;             // this column group owns column k (warp-uniform)
       if (i == bi && i != k) {                  // row bi takes old row k (one lane)
-        const double ckk = lds(cur + 8u * (unsigned)(k + k * b));
+        const double ckk = lds(cur + 8u * k + CST * k);
+        const unsigned rowk = cur + 8u * k + CST * c0;
 #pragma unroll
-        for (int u = 0; u < RP; ++u) {
-          const int c = min(c0 + u, b - 1);
-          x[u] = (c0 + u == k) ? -ckk * d : fma(-ckk, pr[u], lds(cur + 8u * (unsigned)(k + c * b)));
-        }
+        for (int u = 0; u < RP; ++u) x[u] = (c0 + u == k) ? -ckk * d : fma(-ckk, pr[u], lds(rowk + CST * u));
       } else if (i == k) {                      // the pivot row (one lane)
 #pragma unroll
         for (int u = 0; u < RP; ++u) x[u] = (c0 + u == k) ? d : pr[u];
-      } else if (kin) {
-#pragma unroll
-        for (int u = 0; u < RP; ++u) x[u] = (c0 + u == k) ? -aik * d : fma(-aik, pr[u], x[u]);
       } else {
 #pragma unroll
         for (int u = 0; u < RP; ++u) x[u] = fma(-aik, pr[u], x[u]);
-      }
-      if (act) {
+        if (kin) {
 #pragma unroll
-        for (int u = 0; u < RP; ++u)
-          if (c0 + u < b) sts(nxt + 8u * (unsigned)(i + (c0 + u) * b), x[u]);
+          for (int u = 0; u < RP; ++u) if (c0 + u == k) x[u] = -aik * d;
+        }
+      }
+      {
+        const unsigned my = nxt + 8u * i + CST * c0;
+#pragma unroll
+        for (int u = 0; u < RP; ++u) sts(my + CST * u, x[u]);
       }
       if (k + 1 < b && (k + 1) / RP == g) publish(k + 1, k + 1);
       if (tid == 0) ipiv[k] = bi;
@@ -1596,15 +1609,21 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
         }
       }
       asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
-      // column jd of the result = column fcol[2b + jd] of the eliminated matrix: the
-      // eliminated matrix sits in the ping-pong copy written last; gather from it
-      const bool fin0 = (b & 1) == 0;           // the last copy written is P itself
-      const unsigned fin = fin0 ? sP : sP + 8u * bb, dst = fin0 ? sP + 8u * bb : sP;
-      if (act)
-        for (int jd = g; jd < b; jd += G) sts(dst + 8u * (unsigned)(i + jd * b), lds(fin + 8u * (unsigned)(i + (int)fcol[2 * b + jd] * b)));
+      // column jd of the result = column fcol[2b + jd] of the eliminated matrix (in the copy
+      // written last), back to P with leading dimension b: read into registers, then write
+      const unsigned fin = (b & 1) ? buf1 : sP;
+      double o[RP];
+#pragma unroll
+      for (int u = 0; u < RP; ++u) {
+        const int jd = g + G * u;
+        o[u] = (act && jd < b) ? lds(fin + 8u * i + CST * (unsigned)(int)fcol[2 * b + jd]) : 0.0;
+      }
       asm volatile("bar.sync 1, %0;" ::"r"(NTH) : "memory");
-      if (fin0)
-        for (int e = tid; e < bb; e += NTH) sts(sP + 8u * e, lds(sP + 8u * (bb + e)));
+#pragma unroll
+      for (int u = 0; u < RP; ++u) {
+        const int jd = g + G * u;
+        if (act && jd < b) sts(sP + 8u * (unsigned)(i + jd * b), o[u]);
+      }
     }
     if (tid == 0) S.piv = sing ? 1 : 0;
   }
@@ -1835,7 +1854,8 @@ __device__ void finish_block(const DevFactor &F, int K, Shared &S, Bump &A, doub
   if (mode == 2) goto scaled;
   {
   // ---------------- a-6: D_K = P_K^{-1}, Gauss-Jordan with partial pivoting (column-major P)
-  P = (double *)balloc(A, (int64_t)b * b * 8 * (b > 8 ? 2 : 1));
+  // b in (8, 64]: room for the padded ping-pong copies of the register Gauss-Jordan
+  P = (double *)balloc(A, (b <= 8 ? (int64_t)b * b : b <= 32 ? 2 * 32 * 32 : b <= 64 ? 2 * 64 * 64 : 2 * (int64_t)b * b) * 8);
   int *ipiv = (int *)balloc(A, (int64_t)b * 4);
   double *fcol = (double *)balloc(A, (int64_t)b * 8 * 3);
   OVF_CHECK();

@@ -10,7 +10,7 @@ using namespace bilu;
 __global__ void __launch_bounds__(NT, 1) gjk(const double *A, int b, int variant, double *out, long long *cyc) {
   extern __shared__ double sm[];
   __shared__ Shared S;
-  double *P = sm, *fcol = sm + 2 * b * b;
+  double *P = sm, *fcol = sm + 2 * 64 * 64;   // room for the padded copies (b <= 64)
   int *ipiv = (int *)(fcol + 3 * b);
   for (int i = threadIdx.x; i < b * b; i += NT) P[i] = A[i];
   __syncthreads();
