@@ -235,6 +235,45 @@ def time_config(name, steps, warmup, flush):
             "generate_and_analyze_s": prep_s}
 
 
+def time_config_dist(name, world, steps, warmup, flush):
+    """N > 1: the distributed factorization (phase A, NCCL exchange, phase B) of another
+    BASELINE config -- c5 is the 1/2/4/8-GPU config -- timed like the headline (device events,
+    L2 flush, max over ranks).  Every rank takes part; rank 0 reports (extra key)."""
+    import torch
+    from paper_1908_10169_b200 import BILU
+    from paper_1908_10169_b200.dist import factor_distributed, partition_owner
+    rank = int(os.environ.get("RANK", "0"))
+    t0 = time.time()
+    P = make_problem(name, max(world, 2))
+    g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm, device=torch.cuda.current_device())
+    g.dist_setup(partition_owner(P.block_part, world), rank)
+    prep_s = time.time() - t0
+    for _ in range(warmup):
+        factor_distributed(g, P.tau)
+    ms = []
+    for _ in range(steps):
+        flush.zero_()
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st, sent, recv = factor_distributed(g, P.tau)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    local = g.local_stats["flops"]
+    flops = allreduce_sum(local, world) + (st["flops"] - local)
+    t = allreduce_max(float(np.mean(ms)), world)
+    g.close()
+    return {"ms_per_step": t, "factorizations_per_s": 1e3 / t, "steps": steps, "warmup": warmup,
+            "gflops": flops / (t * 1e-3) / 1e9, "flops_per_factorization": flops,
+            "fp64_peak_fraction": flops / (t * 1e-3) / 1e12 / (FP64_PEAK_TFLOPS * world),
+            "n": P.n, "nnz": P.nnz, "blocks_init": int(len(P.block_sizes)),
+            "exchange_bytes_rank0": {"sent": sent, "received": recv},
+            "parallelism": "ND subtrees over %d GPUs, interface panels over NCCL, separators replicated" % world,
+            "generate_and_analyze_s": prep_s}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -355,6 +394,10 @@ def main():
                "d2h_bytes_per_step": int(16 * 8 + (16 * 8 + 4 + 8 + 4 if g.opt.aggregate else 0)),
                "ms_per_step": t_e2e * 1e3}
 
+    extra_dist = None
+    if use_dist and not args.no_extra:
+        extra_dist = {"c5": time_config_dist("c5", world, args.steps, args.warmup, flush)}
+
     if rank == 0:
         hbm_peak, hbm_src = load_peaks()
         achieved_tf = st["flops"] / (t_kern * 1e-3) / 1e12
@@ -412,6 +455,8 @@ def main():
             out["solve"] = dist_apply
         if not use_dist and not args.no_extra:
             out["extra_configs"] = {c: time_config(c, args.steps, args.warmup, flush) for c in ("c3", "c4", "c5")}
+        if extra_dist is not None:
+            out["extra_configs"] = extra_dist
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(P)
         print(json.dumps(out), flush=True)

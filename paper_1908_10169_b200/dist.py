@@ -45,6 +45,10 @@ def exchange_variable(local, group=None):
     import torch.distributed as dist
     world = dist.get_world_size(group)
     me = dist.get_rank(group)
+    if local.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves CPU tensors only (all_gather): stage the payloads through host memory
+        return [b.to(local.device) if r != me else local
+                for r, b in enumerate(exchange_variable(local.cpu(), group))]
     n = torch.tensor([local.numel()], dtype=torch.int64, device=local.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
@@ -90,7 +94,18 @@ def apply_distributed(g, x, group=None):
     the forward sweep, and the assembly of y from the ranks' disjoint shares."""
     import torch.distributed as dist
     contrib = g.apply_dist_begin(x)
-    dist.all_reduce(contrib, group=group)
+    _all_reduce(contrib, group)
     y = g.apply_dist_end(contrib, write_separators=dist.get_rank(group) == 0)
-    dist.all_reduce(y, group=group)
+    _all_reduce(y, group)
     return y
+
+
+def _all_reduce(t, group=None):
+    """Sum over the ranks in place (NCCL on CUDA tensors; gloo stages through host memory)."""
+    import torch.distributed as dist
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
