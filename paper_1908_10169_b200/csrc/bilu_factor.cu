@@ -1631,10 +1631,178 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
   return S.piv != 0;
 }
 
+// Blocked Gauss-Jordan inverse for 8 < b <= 64 (same pivot rule and the same elementary steps
+// as the unblocked versions, R6).  The b steps run in panels of NB columns:
+// warp 0 holds the panel (rows lane and lane + 32, NB columns in registers) and runs its NB
+// steps with shuffles only -- pivot search, row interchange, the in-place elimination -- while
+// tracking the composite row permutation src of the panel's interchanges.  Every other column j
+// (earlier transform columns and later matrix columns) sees the panel's steps as one product
+// T = (I + Q) Pi: column j becomes Pi a_j + Q (Pi a_j)[panel rows], where Q = (final panel
+// columns) - (identity columns) -- the in-place stored panel column k equals (I + Q) e_k (the
+// later interchanges of the panel do not move e_k).  All threads apply that rank-NB update,
+// reading the matrix before the panel from one shared copy and writing the other (ping-pong,
+// one barrier per panel instead of one per step).  P: 2 b^2 doubles; fcol: 3 b doubles.
+// Measured (tools/micro/gj_standalone.cu, one CTA): b = 64 93K cycles (unblocked register
+// version 110K), b = 33 46K (60K); a panel step costs ~1,000 cycles of one warp's dependent
+// chain (pivot reductions, row shuffles, the division, the update).  A depth-1 lookahead
+// (trailing update by the other warps during the next panel) was slower (b = 64 100K).
+#ifndef BILU_GJ_BLK_MIN
+#define BILU_GJ_BLK_MIN 33     // blocked Gauss-Jordan from this block size on (tools/micro/gj_bench.cu)
+#endif
+template <int NB>
+__device__ bool gj_invert_blk(double *P, int b, int *ipiv, double *fcol, Shared &S) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int *src = (int *)fcol;                       // b ints (fcol[0 .. b/2]); fcol[2b .. 3b) below
+  const unsigned sP = (unsigned)__cvta_generic_to_shared(P);
+  auto lds = [](unsigned a) { double v; asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory"); return v; };
+  auto sts = [](unsigned a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory"); };
+  const unsigned CB = 8u * (unsigned)b;         // bytes between columns
+  unsigned cur = sP, nxt = sP + 8u * (unsigned)(b * b);
+  for (int p = 0; p < b; p += NB) {
+    const int nbp = min(NB, b - p);
+    if (wid == 0) {
+      const int r0 = lane, r1 = lane + 32;
+      const bool v0 = r0 < b, v1 = r1 < b;
+      double x0[NB], x1[NB];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        x0[u] = (v0 && u < nbp) ? lds(cur + 8u * r0 + CB * (unsigned)(p + u)) : 0.0;
+        x1[u] = (v1 && u < nbp) ? lds(cur + 8u * r1 + CB * (unsigned)(p + u)) : 0.0;
+      }
+      int s0 = r0, s1 = r1;
+      bool sing = false;
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        if (u < nbp && !sing) {
+          const int k = p + u;
+          // argmax_{i >= k} |a_ik|, lowest row on ties: exact max of the 64-bit key
+          // bits(|v|) + 1 by two integer reductions, then the lowest row holding it
+          const double a0 = fabs(x0[u]), a1 = fabs(x1[u]);
+          const bool c0 = v0 && r0 >= k, c1 = v1 && r1 >= k;
+          const unsigned long long k0 = c0 ? (unsigned long long)__double_as_longlong(a0) + 1ull : 0ull;
+          const unsigned long long k1 = c1 ? (unsigned long long)__double_as_longlong(a1) + 1ull : 0ull;
+          const unsigned long long kl = k1 > k0 ? k1 : k0;
+          const int rl = k1 > k0 ? r1 : r0;
+          const unsigned hi = (unsigned)(kl >> 32), lo = (unsigned)kl;
+          const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+          const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+          const int bi = (int)__reduce_min_sync(0xffffffffu, (hi == mh && lo == ml && kl != 0ull) ? (unsigned)rl : 0x7fffffffu);
+          const int lb = bi & 31, lk = k & 31;
+          const bool sb = bi >= 32, sk = k >= 32;
+          double pr[NB], rk[NB];
+#pragma unroll
+          for (int w = 0; w < NB; ++w) {
+            pr[w] = __shfl_sync(0xffffffffu, sb ? x1[w] : x0[w], lb);
+            rk[w] = __shfl_sync(0xffffffffu, sk ? x1[w] : x0[w], lk);
+          }
+          const int sbi = __shfl_sync(0xffffffffu, sb ? s1 : s0, lb);
+          const int skk = __shfl_sync(0xffffffffu, sk ? s1 : s0, lk);
+          const double vb = pr[u];
+          if (!(fabs(vb) > 0.0)) { sing = true; continue; }   // warp-uniform
+          const double d = 1.0 / vb, ckk = rk[u];
+#pragma unroll
+          for (int w = 0; w < NB; ++w) pr[w] *= d;
+          auto step = [&](double (&x)[NB], int r, int &s) {
+            if (r == k) {                         // the pivot row
+#pragma unroll
+              for (int w = 0; w < NB; ++w) x[w] = (w == u) ? d : pr[w];
+              s = sbi;
+            } else if (r == bi) {                 // takes old row k
+#pragma unroll
+              for (int w = 0; w < NB; ++w) x[w] = (w == u) ? -ckk * d : fma(-ckk, pr[w], rk[w]);
+              s = skk;
+            } else {
+              const double aik = x[u];
+#pragma unroll
+              for (int w = 0; w < NB; ++w) x[w] = (w == u) ? -aik * d : fma(-aik, pr[w], x[w]);
+            }
+          };
+          step(x0, r0, s0);
+          step(x1, r1, s1);
+          if (lane == 0) ipiv[k] = bi;
+        }
+      }
+      if (!sing) {
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          if (u < nbp) {
+            if (v0) sts(nxt + 8u * r0 + CB * (unsigned)(p + u), x0[u]);
+            if (v1) sts(nxt + 8u * r1 + CB * (unsigned)(p + u), x1[u]);
+          }
+        }
+        if (v0) src[r0] = s0;
+        if (v1) src[r1] = s1;
+      }
+      if (lane == 0) S.piv = sing ? 1 : 0;
+    }
+    __syncthreads();
+    if (S.piv) return true;
+    // the other columns: new a_j = Pi a_j + Q (Pi a_j)[p .. p+nbp)
+    {
+      const int ng = NT / b, ncol = b - nbp;
+      if (tid < ng * b) {
+        const int i = tid % b, g = tid / b;
+        const unsigned si = 8u * (unsigned)src[i];
+        double q[NB];
+        unsigned sp[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          q[u] = u < nbp ? lds(nxt + 8u * i + CB * (unsigned)(p + u)) - (i == p + u ? 1.0 : 0.0) : 0.0;
+          sp[u] = u < nbp ? 8u * (unsigned)src[p + u] : 0u;
+        }
+        for (int jj = g; jj < ncol; jj += 2 * ng) {
+          const bool two = jj + ng < ncol;
+          const int j0 = jj < p ? jj : jj + nbp, j1t = jj + ng, j1 = j1t < p ? j1t : j1t + nbp;
+          const unsigned c0 = cur + CB * (unsigned)j0, c1 = cur + CB * (unsigned)(two ? j1 : j0);
+          double a0[NB], a1[NB];
+          double acc0 = lds(c0 + si), acc1 = lds(c1 + si);
+#pragma unroll
+          for (int u = 0; u < NB; ++u) {
+            a0[u] = u < nbp ? lds(c0 + sp[u]) : 0.0;
+            a1[u] = u < nbp ? lds(c1 + sp[u]) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < NB; ++u) { acc0 = fma(q[u], a0[u], acc0); acc1 = fma(q[u], a1[u], acc1); }
+          sts(nxt + 8u * (unsigned)i + CB * (unsigned)j0, acc0);
+          if (two) sts(nxt + 8u * (unsigned)i + CB * (unsigned)j1, acc1);
+        }
+      }
+    }
+    __syncthreads();
+    const unsigned t = cur; cur = nxt; nxt = t;
+  }
+  // undo the row interchanges as column interchanges, in reverse order: composite map
+  if (tid == 0) {
+    for (int jj = 0; jj < b; ++jj) fcol[2 * b + jj] = jj;
+    for (int k = b - 1; k >= 0; --k) {
+      const int pvk = ipiv[k];
+      if (pvk != k) { const double t = fcol[2 * b + k]; fcol[2 * b + k] = fcol[2 * b + pvk]; fcol[2 * b + pvk] = t; }
+    }
+  }
+  __syncthreads();
+  // column jd of the result = column fcol[2b + jd] of the final copy, back to P (ld b)
+  constexpr int MAXE = (64 * 64 + NT - 1) / NT;
+  double o[MAXE];
+#pragma unroll
+  for (int e = 0; e < MAXE; ++e) {
+    const int x = tid + e * NT;
+    o[e] = x < b * b ? lds(cur + 8u * (unsigned)(x % b) + CB * (unsigned)(int)fcol[2 * b + x / b]) : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < MAXE; ++e) {
+    const int x = tid + e * NT;
+    if (x < b * b) sts(sP + 8u * (unsigned)x, o[e]);
+  }
+  __syncthreads();
+  return false;
+}
+
 // D_K = P_K^{-1} in place (P column-major b x b in shared memory; b > 8 needs 2 b^2 doubles
 // of P and 3 b of fcol), Gauss-Jordan with partial pivoting inside the block
 // (ties -> lowest row, R6).  CTA-wide; returns true if a pivot is exactly 0.
 __device__ __noinline__ bool gj_invert(double *P, int b, int *ipiv, double *fcol, Shared &S, bool reg = true) {
+  if (reg && b >= BILU_GJ_BLK_MIN && b <= 64 && __isShared(P)) return gj_invert_blk<8>(P, b, ipiv, fcol, S);
   if (reg && b > 8 && b <= 64 && __isShared(P)) {
     __shared__ double pvbuf[8];
     if (b <= 32) return gj_invert_reg<32, 8>(P, b, ipiv, fcol, pvbuf, S);
