@@ -1646,8 +1646,11 @@ __device__ bool gj_invert_reg(double *P, int b, int *ipiv, double *fcol, double 
 // version 110K), b = 33 46K (60K); a panel step costs ~1,000 cycles of one warp's dependent
 // chain (pivot reductions, row shuffles, the division, the update).  A depth-1 lookahead
 // (trailing update by the other warps during the next panel) was slower (b = 64 100K).
+// Off by default: faster alone (above) but slower inside factor_kernel -- c4 136.5 -> 143.4 ms
+// in an interleaved A/B (tools/ab_cfg.sh, profiles/r02_gj_blocked.md).  -DBILU_GJ_BLK_MIN=33
+// switches it on for b >= 33.
 #ifndef BILU_GJ_BLK_MIN
-#define BILU_GJ_BLK_MIN 33     // blocked Gauss-Jordan from this block size on (tools/micro/gj_bench.cu)
+#define BILU_GJ_BLK_MIN 1000
 #endif
 template <int NB>
 __device__ bool gj_invert_blk(double *P, int b, int *ipiv, double *fcol, Shared &S) {

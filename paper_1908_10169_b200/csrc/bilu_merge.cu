@@ -660,9 +660,10 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
           const double *Lv = M.Lval + M.Lval_off[j];
           const int mj = M.Lm[j];
           const int mi = s_mi[x];
-          for (int it = mi * bj + tid; it < mj * bj; it += MT) {
-            const int p = it / bj, t = it - p * bj;
-            G[(size_t)m_lbound(Rl, 0, u, rows[p]) * P + oj + t] = Lv[it];
+          for (int p = mi + tid; p < mj; p += MT) {     // one search per row, then its b_j values
+            double *g = G + (size_t)m_lbound(Rl, 0, u, rows[p]) * P + oj;
+            const double *lv = Lv + (size_t)p * bj;
+            for (int t = 0; t < bj; ++t) g[t] = lv[t];
           }
         }
         __syncthreads();
@@ -687,9 +688,10 @@ __global__ void __launch_bounds__(MT) merge_arith_kernel(MergeArgs M, double *dw
           const double *Uv = M.Uval + M.Uval_off[j];
           const int cj = M.Uc[j];
           const int ci = s_ci[x];
-          for (int it = ci * bj + tid; it < cj * bj; it += MT) {
-            const int q = it / bj, t = it - q * bj;
-            G[(size_t)m_lbound(Cl, 0, v, cols[q]) * P + oj + t] = Uv[it];
+          for (int q = ci + tid; q < cj; q += MT) {     // one search per column, then its b_j values
+            double *g = G + (size_t)m_lbound(Cl, 0, v, cols[q]) * P + oj;
+            const double *uv = Uv + (size_t)q * bj;
+            for (int t = 0; t < bj; ++t) g[t] = uv[t];
           }
         }
         __syncthreads();
