@@ -1,4 +1,4 @@
-"""Factor time vs dense-trailing-zone budget: python tools/zone_probe.py c2 [reps]"""
+"""Factor time vs dense-trailing-zone budget: python tools/zone_probe.py c5 [reps] [GiB,GiB,...]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from inputs.configs import make_config
@@ -7,7 +7,11 @@ name = sys.argv[1]; reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 P = make_config(name)
 zbs = [int(float(x) * (1 << 30)) for x in sys.argv[3].split(',')] if len(sys.argv) > 3 else [-1, 64 << 20, 256 << 20, 1 << 30, 4 << 30, 0]
 for zb in zbs:
-    g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm, zone_bytes=zb)
+    try:
+        g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm, zone_bytes=zb)
+    except Exception as e:   # e.g. the budget does not fit the free HBM
+        print("%s zone_bytes=%d: %s" % (name, zb, e), flush=True)
+        continue
     ts = []
     for _ in range(reps):
         st = g.factor(P.tau)
