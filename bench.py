@@ -199,6 +199,12 @@ def cpu_baseline(P, budget_s=30.0):
                       % (len(times), P.name, t, flops)}
 
 
+# Dense-zone budgets (bilu_options.zone_bytes, DESIGN 5b) of the extra configs where the
+# library default (min(64 GiB, 45% of the free HBM)) is not the fastest measured one
+# (profiles/r02_zone_sweep.log: c3 52.5 ms at 64 GiB, 49.3 at 96, 46.3 at 128; c5 flat beyond 64).
+ZONE_GIB = {"c3": 120}
+
+
 def time_config(name, steps, warmup, flush):
     """Device time of the other BASELINE configs' factorizations at N = 1 (extra keys of the
     bench line; c2 stays the headline): same protocol as the headline (warm-up, L2 flush,
@@ -208,7 +214,11 @@ def time_config(name, steps, warmup, flush):
     from paper_1908_10169_b200 import BILU
     t0 = time.time()
     P = make_config(name)
-    g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm)
+    opts = {}
+    free = torch.cuda.mem_get_info()[0]
+    if name in ZONE_GIB and free >= (ZONE_GIB[name] + 40) << 30:   # leave 40 GiB for the factors
+        opts["zone_bytes"] = ZONE_GIB[name] << 30
+    g = BILU(P.indptr, P.indices, P.data, P.block_sizes, perm=P.perm, **opts)
     prep_s = time.time() - t0
     for _ in range(warmup):
         g.factor(P.tau)
@@ -230,6 +240,7 @@ def time_config(name, steps, warmup, flush):
             "gflops": st["flops"] / (t * 1e-3) / 1e9, "flops_per_factorization": st["flops"],
             "n": P.n, "nnz": P.nnz, "blocks_init": int(len(P.block_sizes)), "blocks_final": int(st["n_blocks_final"]),
             "zone_blocks": int(st["zone_blocks"]),
+            "zone_bytes": opts.get("zone_bytes", "library default"),
             "roofline": {"bound": "tensor", "kernel": "factor_kernel", "achieved": tf, "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": tf / FP64_PEAK_TFLOPS, "kernel_ms": tk},
             "generate_and_analyze_s": prep_s}
@@ -392,7 +403,9 @@ def main():
         e2e = {"value": (world if world == 1 else 1) / t_e2e, "unit": "factorizations/s",
                "h2d_bytes_per_step": int(P.nnz * 8),
                "d2h_bytes_per_step": int(16 * 8 + (16 * 8 + 4 + 8 + 4 if g.opt.aggregate else 0)),
-               "ms_per_step": t_e2e * 1e3}
+               "ms_per_step": t_e2e * 1e3,
+               "note": "bilu_set_values from pinned host values + bilu_factor + its device->host statistics "
+                       "read; the factors stay in HBM (they are a preconditioner, applied by bilu_apply)"}
 
     extra_dist = None
     if use_dist and not args.no_extra:
@@ -454,6 +467,7 @@ def main():
         if dist_apply is not None:
             out["solve"] = dist_apply
         if not use_dist and not args.no_extra:
+            g.close()   # c2's zone panels (38 GB) go back before the other configs are set up
             out["extra_configs"] = {c: time_config(c, args.steps, args.warmup, flush) for c in ("c3", "c4", "c5")}
         if extra_dist is not None:
             out["extra_configs"] = extra_dist

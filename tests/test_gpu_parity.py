@@ -288,11 +288,21 @@ def test_edge_wide_key_range_posmap(agg):
     assert_parity(gf, of)
 
 
-def test_c3_full_parity():
-    """BASELINE configs[2] at full size (48^3 nodes x 3 dof, n = 331,776, 25.8M nnz)."""
+@pytest.mark.parametrize("zone_gib", [None, 120])
+def test_c3_full_parity(zone_gib):
+    """BASELINE configs[2] at full size (48^3 nodes x 3 dof, n = 331,776, 25.8M nnz), with the
+    library's default dense-zone budget and with the one bench.py passes for c3 (ZONE_GIB)."""
+    import torch
+    opts = {}
+    if zone_gib is not None:
+        if torch.cuda.mem_get_info()[0] < (zone_gib + 40) << 30:
+            pytest.skip("needs %d GiB of free HBM" % (zone_gib + 40))
+        opts["zone_bytes"] = zone_gib << 30
     P = config3()
-    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm)
+    g, st, gf, of = run_pair(P.indptr, P.indices, P.data, P.block_sizes, P.tau, True, P.perm, **opts)
     assert st["n_blocks_init"] == 110592
+    if zone_gib is not None:
+        assert st["zone_blocks"] > 60000
     assert_parity(gf, of)
     assert st["n_merges"] == of.n_merges
 
